@@ -1,0 +1,175 @@
+/*
+ * crop_b200.h -- C-ABI of the B200-native CRoP hot path (libcrop_b200.so).
+ *
+ * The reference package (pkg/src/crop, pure Python) has no FFI; its hot path
+ * is a set of Python functions. Each entry point below replaces one of them
+ * and is bound by paper_1210_0461_b200/_native.py through ctypes (the same
+ * binding a reference maintainer would add).
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA
+ *    tensors) unless named h_*; `stream` is a cudaStream_t passed as void*.
+ *    Calls are stream-ordered; functions that must read back a size
+ *    (crop_pairs_create) synchronise the stream and say so.
+ *  - Return value: CROP_OK (0) or an error status; crop_last_error() gives
+ *    the message. Status -> Python exception (errors.py:8-34):
+ *      2 InputError, 3 ConfigError, 4 ResourceCapError, 5 CUDA failure.
+ *  - Item ids are uint32 < 2^31; transactions / outer products are CSR:
+ *    offsets int64[n+1], indices uint32[offsets[n]] (ascending per row).
+ *  - Hash coefficients are the reference's (mul, add) pairs modulo 2^61-1
+ *    (hashing.py:127-146); kappa <= 2^31.
+ */
+#ifndef CROP_B200_H
+#define CROP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CROP_OK 0
+#define CROP_EINPUT 2
+#define CROP_ECONFIG 3
+#define CROP_ERESOURCE 4
+#define CROP_ECUDA 5
+
+/* Version of the ABI (bumped on any signature change). */
+int crop_abi_version(void);
+
+/* Message of the last failing call on this thread. */
+const char* crop_last_error(void);
+
+/* K0 -- per-item hash tables, IndexHashFn.values (hashing.py:68-71):
+ * h_row[i] = ((row_mul*i + row_add) mod p) mod kappa, likewise h_col, for
+ * i in [0, n_items). Exact 128-bit Mersenne arithmetic on device. */
+int crop_hash_tables(uint32_t n_items, uint64_t row_mul, uint64_t row_add, uint64_t col_mul,
+                     uint64_t col_add, uint32_t kappa, uint32_t* h_row, uint32_t* h_col,
+                     void* stream);
+
+/* Sign hash (hashing.py:98-100) of n entries: out[e] = s(row[e], col[e]). */
+int crop_sign_hash(const uint32_t* row, const uint32_t* col, uint64_t n, uint64_t sign_mul,
+                   uint64_t sign_add, int8_t* out, void* stream);
+
+/* K1 -- per-bucket term counts of a self-join transaction stream, the
+ * quantity measure_loads / count_sorted report (engine.py:305-349,
+ * interval.py:192-233) before folding buckets into worker intervals.
+ * upper_only: pairs i<j only (mining); else every ordered (i,j) incl. i==j.
+ * bucket_loads: uint64[kappa], accumulated into (caller zeroes it). */
+int crop_selfjoin_bucket_loads(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                               const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
+                               int upper_only, uint64_t* bucket_loads, void* stream);
+
+/* Same for a general stream a_k x b_k (count_interval, interval.py:257-269). */
+int crop_outer_bucket_loads(const int64_t* a_ptr, const uint32_t* a_idx, const int64_t* b_ptr,
+                            const uint32_t* b_idx, int64_t n_products, const uint32_t* h_row,
+                            const uint32_t* h_col, uint32_t kappa, int upper_only,
+                            uint64_t* bucket_loads, void* stream);
+
+/* K2 -- exact pair counting of a self-join 0/1 stream restricted to a bucket
+ * interval [start, stop): the exact regime of engine.run / run_worker
+ * (engine.py:238-302, 396-455), where every per-bucket Space-Saving summary
+ * holds exact counts. Output: the distinct (row, col) entries
+ * of the interval with their uint32 counts, unordered.
+ *
+ * Two calls. crop_pairs_create scans the input once (per-item term counts),
+ * SYNCHRONISES the stream, and plans the on-chip tiles; it reports the output
+ * capacity the caller must allocate. crop_pairs_run then routes, counts and
+ * writes the entries (async); *d_n_entries (device uint64) receives the
+ * number written. The job keeps its own device scratch until destroyed. */
+typedef struct crop_pairs crop_pairs;
+
+typedef struct {
+    uint32_t kappa;         /* buckets */
+    uint32_t start, stop;   /* owned interval [start, stop) */
+    const uint32_t* h_row;  /* device uint32[n_items] (crop_hash_tables) */
+    const uint32_t* h_col;
+} crop_interval;
+
+int crop_pairs_create(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                      uint32_t n_items, int upper_only, const crop_interval* interval,
+                      void* stream, crop_pairs** job);
+/* host-side plan facts: output capacity, total terms (all buckets), tiles */
+int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* total_terms,
+                    uint64_t* n_tiles, uint64_t* n_units);
+int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32_t* out_count,
+                   uint64_t* d_n_entries, void* stream);
+void crop_pairs_destroy(crop_pairs* job);
+
+/* Per-instance bucket statistics of counted entries (the LoadReport rows,
+ * engine.py:179-216, Count-Sketch cells, countsketch.py:33-41, and per-bucket
+ * distinct counts). For instance t the hash tables are h_row[t*n_items ...].
+ * Outputs (accumulated, caller zeroes): loads uint64[t][kappa] = sum of
+ * counts, distinct uint32[t][kappa], cs int64[t][kappa] = sum count*sign
+ * (pass NULL to skip), sign coefficients h_sign[2*t] (host array). */
+int crop_entry_bucket_stats(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                            const uint64_t* d_n_entries, uint64_t max_entries, int instances,
+                            uint32_t n_items, const uint32_t* h_row, const uint32_t* h_col,
+                            uint32_t kappa, const uint64_t* h_sign, uint64_t* loads,
+                            uint32_t* distinct, int64_t* cs, void* stream);
+
+/* Real-weight variant: per-bucket entry counts and fp64 Count-Sketch cells
+ * sum weight*sign (accumulated; order differs from the reference, so cells
+ * agree to rounding). distinct uint32[t][kappa], cs double[t][kappa]|NULL. */
+int crop_entry_bucket_stats_f64(const uint32_t* row, const uint32_t* col, const double* weight,
+                                const uint64_t* d_n_entries, uint64_t max_entries, int instances,
+                                uint32_t n_items, const uint32_t* h_row, const uint32_t* h_col,
+                                uint32_t kappa, const uint64_t* h_sign, uint32_t* distinct,
+                                double* cs, void* stream);
+
+/* Per-product worker loads, LoadReport.per_product (engine.py:250-251,287-288):
+ * out[k*workers + w] (uint32, caller zeroes) = terms of product k that fall in
+ * worker w's interval (interval.py:37-45). Self-joins pass a == b. */
+int crop_product_worker_loads(const int64_t* a_ptr, const uint32_t* a_idx, const int64_t* b_ptr,
+                              const uint32_t* b_idx, int64_t n_products, const uint32_t* h_row,
+                              const uint32_t* h_col, uint32_t kappa, uint32_t workers,
+                              int upper_only, uint32_t* out, void* stream);
+
+/* Bucket of each entry for one instance: out[e] = (h_row[row]+h_col[col]) mod kappa. */
+int crop_entry_buckets(const uint32_t* row, const uint32_t* col, uint64_t n,
+                       const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
+                       uint32_t* out, void* stream);
+
+/* K4 -- top-k select (SketchState.top_entries, engine.py:162-172; exact_top,
+ * oracle.py:53-58): indices of the k entries first in the order
+ * (count desc, row asc, col asc); written unordered to out_idx[0..k'),
+ * k' = min(k, n) returned in *d_k_out (device uint64). */
+int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+              const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k, uint64_t* out_idx,
+              uint64_t* d_k_out, void* stream);
+
+/* K5 -- general outer-product stream (real values), restricted to buckets
+ * [start, stop): the per-partition enumerate_interval + accumulate loop
+ * (interval.py:236-254; exact_product, oracle.py:20-50). Terms are emitted,
+ * stably sorted by (bucket, row, col) and summed in fp64 in stream order, so
+ * each sum equals the reference's dict accumulation bit for bit. Output is
+ * the per-partition sorted COO: row/col uint32, value float64, bucket
+ * uint32, grouped by bucket ascending, (row, col) ascending inside. Zero sums
+ * are kept (the caller decides, exact_product drops them, oracle.py:50).
+ * crop_outer_create synchronises once to size the term buffer. */
+typedef struct crop_outer crop_outer;
+int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, const double* a_val,
+                      const int64_t* b_ptr, const uint32_t* b_idx, const double* b_val,
+                      int64_t n_products, int upper_only, const crop_interval* interval,
+                      void* stream, crop_outer** job);
+int crop_outer_info(const crop_outer* job, uint64_t* max_entries, uint64_t* total_terms);
+int crop_outer_run(crop_outer* job, uint32_t* out_row, uint32_t* out_col, double* out_value,
+                   uint32_t* out_bucket, uint64_t* d_n_entries, void* stream);
+void crop_outer_destroy(crop_outer* job);
+
+/* Synthetic transaction workload (bench / tests): successive sampling without
+ * replacement from an integer alias table (h_alias_*: host arrays, n_items
+ * long), lengths from an integer CDF over [len_lo, len_lo + n_len).
+ * Deterministic in (seed, transaction index) on any GPU count.
+ *   crop_gen_lengths writes lengths int64[n_tx]; the caller prefix-sums them
+ *   into offsets; crop_gen_items fills items (sorted ascending per row). */
+int crop_gen_lengths(int64_t n_tx, uint64_t seed, const uint32_t* h_len_cdf, uint32_t n_len,
+                     uint32_t len_lo, int64_t* lengths, void* stream);
+int crop_gen_items(int64_t n_tx, uint64_t seed, uint32_t n_items, const uint32_t* h_alias_thresh,
+                   const uint32_t* h_alias_idx, const int64_t* offsets, uint32_t* items,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CROP_B200_H */

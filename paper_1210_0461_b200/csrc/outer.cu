@@ -1,0 +1,354 @@
+// outer.cu -- K5: general (real-valued) outer-product streams.
+//
+// Replaces the per-partition enumerate_interval + dict accumulation loop
+// (interval.py:236-254, scan_sorted :125-189) and exact_product
+// (oracle.py:20-50) for streams whose two sides differ or carry real values
+// (configuration 4: C = A*B with A as CSC and B as CSR). Each product's terms
+// are mostly distinct entries, so there is nothing to aggregate on chip; the
+// kernel path is emit -> stable sort -> ordered segment sum:
+//
+//   k_outer_count  per product: own-interval terms (warp per product)
+//   scan           exclusive offsets (CUB)
+//   k_outer_emit   (row<<32|col, term index) for own terms, in stream order;
+//                  values are a_k(i)*b_k(j) in fp64 (exact for fp32 inputs)
+//   sort           stable radix sort by (row, col), then stable by bucket (CUB)
+//   k_outer_reduce segment heads sum their run IN STREAM ORDER in fp64 ->
+//                  bit-identical to the reference's dict accumulation; output
+//                  per-bucket sorted COO (row, col, value, bucket)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace crop;
+
+namespace {
+
+template <bool FILTER>
+__device__ __forceinline__ bool own_term(uint32_t i, uint32_t j, int upper,
+                                         const crop_interval& iv) {
+  if (upper && i >= j) return false;
+  if (FILTER) {
+    uint32_t b = iv.h_row[i] + iv.h_col[j];
+    if (b >= iv.kappa) b -= iv.kappa;
+    return b >= iv.start && b < iv.stop;
+  }
+  return true;
+}
+
+template <bool FILTER>
+__global__ void k_outer_count(const int64_t* __restrict__ a_ptr, const uint32_t* __restrict__ a_idx,
+                              const int64_t* __restrict__ b_ptr, const uint32_t* __restrict__ b_idx,
+                              int64_t n, int upper, crop_interval iv,
+                              unsigned long long* __restrict__ counts) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int64_t k = (int64_t)blockIdx.x * warps + threadIdx.x / 32; k < n;
+       k += (int64_t)gridDim.x * warps) {
+    const int64_t a0 = a_ptr[k], la = a_ptr[k + 1] - a0;
+    const int64_t b0 = b_ptr[k], lb = b_ptr[k + 1] - b0;
+    unsigned long long c = 0;
+    if (!FILTER && !upper) {
+      c = (unsigned long long)(la * lb);
+    } else {
+      for (int64_t t = lane; t < la * lb; t += 32) {
+        const int64_t p = t / lb, q = t - p * lb;
+        c += own_term<FILTER>(a_idx[a0 + p], b_idx[b0 + q], upper, iv);
+      }
+      c = warp_sum(c);
+    }
+    if (lane == 0) counts[k] = c;
+  }
+}
+
+template <bool FILTER>
+__global__ void k_outer_emit(const int64_t* __restrict__ a_ptr, const uint32_t* __restrict__ a_idx,
+                             const double* __restrict__ a_val, const int64_t* __restrict__ b_ptr,
+                             const uint32_t* __restrict__ b_idx, const double* __restrict__ b_val,
+                             int64_t n, int upper, crop_interval iv,
+                             const unsigned long long* __restrict__ offs,
+                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ seq,
+                             double* __restrict__ vals) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int64_t k = (int64_t)blockIdx.x * warps + threadIdx.x / 32; k < n;
+       k += (int64_t)gridDim.x * warps) {
+    const int64_t a0 = a_ptr[k], la = a_ptr[k + 1] - a0;
+    const int64_t b0 = b_ptr[k], lb = b_ptr[k + 1] - b0;
+    unsigned long long pos = offs[k];
+    for (int64_t t0 = 0; t0 < la * lb; t0 += 32) {
+      const int64_t t = t0 + lane;
+      bool keep = false;
+      uint32_t i = 0, j = 0;
+      int64_t p = 0, q = 0;
+      if (t < la * lb) {
+        p = t / lb;
+        q = t - p * lb;
+        i = a_idx[a0 + p];
+        j = b_idx[b0 + q];
+        keep = own_term<FILTER>(i, j, upper, iv);
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const unsigned long long o = pos + __popc(m & ((1u << lane) - 1u));
+        keys[o] = ((unsigned long long)i << 32) | j;
+        seq[o] = (uint32_t)o;
+        vals[o] = (a_val ? a_val[a0 + p] : 1.0) * (b_val ? b_val[b0 + q] : 1.0);
+      }
+      pos += __popc(m);
+    }
+  }
+}
+
+__global__ void k_bucket_of_keys(const unsigned long long* __restrict__ keys, uint64_t n,
+                                 crop_interval iv, int has_hash, uint32_t* __restrict__ buckets) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (!has_hash) {
+      buckets[e] = 0;
+      continue;
+    }
+    const unsigned long long k = keys[e];
+    uint32_t b = iv.h_row[(uint32_t)(k >> 32)] + iv.h_col[(uint32_t)k];
+    buckets[e] = b >= iv.kappa ? b - iv.kappa : b;
+  }
+}
+
+// perm[] maps final position -> position in the (row,col)-sorted arrays.
+__global__ void k_gather_final(const uint32_t* __restrict__ perm,
+                               const unsigned long long* __restrict__ keys_rc,
+                               const uint32_t* __restrict__ seq_rc, uint64_t n,
+                               unsigned long long* __restrict__ keys_f, uint32_t* __restrict__ seq_f) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = perm[e];
+    keys_f[e] = keys_rc[s];
+    seq_f[e] = seq_rc[s];
+  }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ out, uint64_t n) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    out[e] = (uint32_t)e;
+}
+
+__global__ void k_heads(const unsigned long long* __restrict__ keys, uint64_t n,
+                        uint32_t* __restrict__ head) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1u : 0u;
+}
+
+__global__ void k_outer_reduce(const unsigned long long* __restrict__ keys,
+                               const uint32_t* __restrict__ seq, const double* __restrict__ vals,
+                               const uint32_t* __restrict__ buckets_sorted,
+                               const uint32_t* __restrict__ head,
+                               const uint32_t* __restrict__ head_pos, uint64_t n,
+                               uint32_t* __restrict__ out_row, uint32_t* __restrict__ out_col,
+                               double* __restrict__ out_val, uint32_t* __restrict__ out_bucket) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (!head[e]) continue;
+    const unsigned long long k = keys[e];
+    double s = vals[seq[e]];
+    for (uint64_t f = e + 1; f < n && keys[f] == k; ++f) s = s + vals[seq[f]];
+    const uint32_t o = head_pos[e];
+    out_row[o] = (uint32_t)(k >> 32);
+    out_col[o] = (uint32_t)k;
+    out_val[o] = s;
+    out_bucket[o] = buckets_sorted[e];
+  }
+}
+
+}  // namespace
+
+struct crop_outer {
+  const int64_t *a_ptr, *b_ptr;
+  const uint32_t *a_idx, *b_idx;
+  const double *a_val, *b_val;
+  int64_t n;
+  int upper;
+  bool filter, has_hash;
+  crop_interval iv;
+  uint64_t total_terms;  // own-interval terms
+  uint64_t all_terms;
+  unsigned long long* d_counts = nullptr;
+  unsigned long long* d_offs = nullptr;
+};
+
+extern "C" int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, const double* a_val,
+                                 const int64_t* b_ptr, const uint32_t* b_idx, const double* b_val,
+                                 int64_t n_products, int upper_only, const crop_interval* interval,
+                                 void* stream, crop_outer** job) {
+  *job = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  crop_outer* J = new crop_outer();
+  J->a_ptr = a_ptr;
+  J->a_idx = a_idx;
+  J->a_val = a_val;
+  J->b_ptr = b_ptr;
+  J->b_idx = b_idx;
+  J->b_val = b_val;
+  J->n = n_products;
+  J->upper = upper_only;
+  J->has_hash = interval != nullptr;
+  J->filter = false;
+  if (interval) {
+    J->iv = *interval;
+    if (interval->kappa == 0 || interval->start > interval->stop || interval->stop > interval->kappa) {
+      delete J;
+      crop_set_error(CROP_ECONFIG, "invalid interval");
+      return CROP_ECONFIG;
+    }
+    J->filter = !(interval->start == 0 && interval->stop == interval->kappa);
+  } else {
+    J->iv = crop_interval{1, 0, 1, nullptr, nullptr};
+  }
+  const int64_t nn = std::max<int64_t>(n_products, 1);
+  cudaError_t e1 = cudaMalloc(&J->d_counts, nn * 8);
+  cudaError_t e2 = cudaMalloc(&J->d_offs, (nn + 1) * 8);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaFree(J->d_counts);
+    cudaFree(J->d_offs);
+    delete J;
+    crop_set_error(CROP_ECUDA, "cudaMalloc failed");
+    return CROP_ECUDA;
+  }
+  J->total_terms = 0;
+  if (n_products > 0) {
+    int64_t blocks = std::min<int64_t>((n_products + 7) / 8, 8 * kNumSMs);
+    if (J->filter)
+      k_outer_count<true><<<(int)blocks, 256, 0, st>>>(a_ptr, a_idx, b_ptr, b_idx, n_products,
+                                                      upper_only, J->iv, J->d_counts);
+    else
+      k_outer_count<false><<<(int)blocks, 256, 0, st>>>(a_ptr, a_idx, b_ptr, b_idx, n_products,
+                                                       upper_only, J->iv, J->d_counts);
+    CROP_LAUNCH_CHECK();
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, J->d_counts, J->d_offs, n_products + 1, st);
+    void* tmp = nullptr;
+    CROP_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    // offs has n+1 entries: scan n+1 values where counts[n] is garbage-free by
+    // scanning only n and adding the last count below
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, J->d_counts, J->d_offs, n_products, st);
+    cudaFreeAsync(tmp, st);
+    unsigned long long last_off = 0, last_cnt = 0;
+    CROP_CUDA(cudaMemcpyAsync(&last_off, J->d_offs + n_products - 1, 8, cudaMemcpyDeviceToHost, st));
+    CROP_CUDA(cudaMemcpyAsync(&last_cnt, J->d_counts + n_products - 1, 8, cudaMemcpyDeviceToHost, st));
+    CROP_CUDA(cudaStreamSynchronize(st));
+    J->total_terms = last_off + last_cnt;
+    if (J->total_terms >= (1ull << 32)) {
+      cudaFree(J->d_counts);
+      cudaFree(J->d_offs);
+      delete J;
+      crop_set_error(CROP_ERESOURCE, "more than 2^32 terms in one interval; split the stream");
+      return CROP_ERESOURCE;
+    }
+  }
+  *job = J;
+  return CROP_OK;
+}
+
+extern "C" int crop_outer_info(const crop_outer* J, uint64_t* max_entries, uint64_t* total_terms) {
+  if (max_entries) *max_entries = J->total_terms;
+  if (total_terms) *total_terms = J->total_terms;
+  return CROP_OK;
+}
+
+extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_col,
+                              double* out_value, uint32_t* out_bucket, uint64_t* d_n_entries,
+                              void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  CROP_CUDA(cudaMemsetAsync(d_n_entries, 0, 8, st));
+  const uint64_t n = J->total_terms;
+  if (n == 0) return CROP_OK;
+  unsigned long long *keys = nullptr, *keys2 = nullptr, *keys_f = nullptr;
+  uint32_t *seq = nullptr, *seq2 = nullptr, *seq_f = nullptr, *buck = nullptr, *buck2 = nullptr;
+  uint32_t *iota = nullptr, *perm = nullptr, *head = nullptr, *head_pos = nullptr;
+  double* vals = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, t2 = 0;
+  CROP_CUDA(cudaMallocAsync(&keys, n * 8, st));
+  CROP_CUDA(cudaMallocAsync(&keys2, n * 8, st));
+  CROP_CUDA(cudaMallocAsync(&seq, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&seq2, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&vals, n * 8, st));
+  CROP_CUDA(cudaMallocAsync(&buck, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&buck2, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&iota, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&perm, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&keys_f, n * 8, st));
+  CROP_CUDA(cudaMallocAsync(&seq_f, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&head, n * 4, st));
+  CROP_CUDA(cudaMallocAsync(&head_pos, n * 4, st));
+  {
+    int64_t blocks = std::min<int64_t>((J->n + 7) / 8, 8 * kNumSMs);
+    if (J->filter)
+      k_outer_emit<true><<<(int)blocks, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr,
+                                                     J->b_idx, J->b_val, J->n, J->upper, J->iv,
+                                                     J->d_offs, keys, seq, vals);
+    else
+      k_outer_emit<false><<<(int)blocks, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr,
+                                                      J->b_idx, J->b_val, J->n, J->upper, J->iv,
+                                                      J->d_offs, keys, seq, vals);
+    CROP_LAUNCH_CHECK();
+  }
+  // stable sort by (row, col): ties keep emission (= stream) order
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, seq, seq2, (int64_t)n, 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, buck, buck2, iota, perm, (int64_t)n, 0, 32, st);
+  tmp_bytes = std::max(tmp_bytes, t2);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, head, head_pos, (int64_t)n, st);
+  tmp_bytes = std::max(tmp_bytes, t2);
+  CROP_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, seq, seq2, (int64_t)n, 0, 64, st);
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 16 * kNumSMs);
+  k_bucket_of_keys<<<(int)blocks, 256, 0, st>>>(keys2, n, J->iv, J->has_hash, buck);
+  CROP_LAUNCH_CHECK();
+  // stable sort by bucket of the (row,col)-sorted sequence
+  k_iota<<<(int)blocks, 256, 0, st>>>(iota, n);
+  CROP_LAUNCH_CHECK();
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, buck, buck2, iota, perm, (int64_t)n, 0, 32, st);
+  k_gather_final<<<(int)blocks, 256, 0, st>>>(perm, keys2, seq2, n, keys_f, seq_f);
+  CROP_LAUNCH_CHECK();
+  k_heads<<<(int)blocks, 256, 0, st>>>(keys_f, n, head);
+  CROP_LAUNCH_CHECK();
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, head, head_pos, (int64_t)n, st);
+  k_outer_reduce<<<(int)blocks, 256, 0, st>>>(keys_f, seq_f, vals, buck2, head, head_pos, n,
+                                              out_row, out_col, out_value, out_bucket);
+  CROP_LAUNCH_CHECK();
+  // number of segments = head_pos[n-1] + head[n-1]
+  {
+    cub::TransformInputIterator<unsigned long long, cub::CastOp<unsigned long long>, uint32_t*> hi(
+        head, cub::CastOp<unsigned long long>());
+    size_t tb = 0;
+    cub::DeviceReduce::Sum(nullptr, tb, hi, (unsigned long long*)d_n_entries, (int64_t)n, st);
+    void* t3 = nullptr;
+    CROP_CUDA(cudaMallocAsync(&t3, tb, st));
+    cub::DeviceReduce::Sum(t3, tb, hi, (unsigned long long*)d_n_entries, (int64_t)n, st);
+    cudaFreeAsync(t3, st);
+  }
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(keys, st);
+  cudaFreeAsync(keys2, st);
+  cudaFreeAsync(seq, st);
+  cudaFreeAsync(seq2, st);
+  cudaFreeAsync(vals, st);
+  cudaFreeAsync(buck, st);
+  cudaFreeAsync(buck2, st);
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(perm, st);
+  cudaFreeAsync(keys_f, st);
+  cudaFreeAsync(seq_f, st);
+  cudaFreeAsync(head, st);
+  cudaFreeAsync(head_pos, st);
+  CROP_LAUNCH_CHECK();
+  return CROP_OK;
+}
+
+extern "C" void crop_outer_destroy(crop_outer* J) {
+  if (!J) return;
+  cudaFree(J->d_counts);
+  cudaFree(J->d_offs);
+  delete J;
+}

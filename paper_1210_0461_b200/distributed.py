@@ -1,0 +1,121 @@
+"""Multi-GPU execution: broadcast the input once, count disjoint intervals, gather.
+
+The paper's processors each hold the whole input and never communicate
+after the broadcast; the reference emulates this
+with one OS process per worker and a pickled/JSON merge (engine.py:540-592).
+Here one process per GPU (torchrun) is the worker pool:
+
+1. rank 0 broadcasts the columnar stream (CSR offsets/items, or CSC/CSR with
+   values) with `torch.distributed.broadcast` -- NCCL over NVLink on B200,
+   gloo on CPU in the tests;
+2. rank r owns the contiguous block of worker intervals
+   [r*W/G, (r+1)*W/G) and counts only the buckets of that block on its GPU
+   (no communication while counting);
+3. the disjoint per-worker payloads are gathered to rank 0 and merged with
+   `merge_partials`, which validates the tiling of [0, kappa).
+
+Because bucket ownership depends only on (i, j) and the seed, the merged
+state is identical for every G (the reference's K-invariance).
+The per-rank compute function is injectable so the CPU tests can drive the
+same orchestration with the oracle (tests/test_distributed.py).
+"""
+
+import numpy as np
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def world_size() -> int:
+    dist = _dist()
+    return dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+
+
+def rank() -> int:
+    dist = _dist()
+    return dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
+
+
+def rank_workers(workers: int, r: int, world: int) -> tuple[int, int]:
+    """Contiguous worker block [lo, hi) of rank r (empty when world > workers)."""
+    return r * workers // world, (r + 1) * workers // world
+
+
+def _device_for_backend():
+    import torch
+
+    dist = _dist()
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def broadcast_arrays(arrays: dict | None, src: int = 0) -> dict:
+    """Broadcast named 1-D numpy arrays from `src` (shapes first, then data)."""
+    import torch
+
+    dist = _dist()
+    dev = _device_for_backend()
+    me = dist.get_rank()
+    names = sorted(arrays) if me == src else None
+    obj = [names, {k: (str(arrays[k].dtype), arrays[k].shape[0]) for k in names}
+           if me == src else None]
+    dist.broadcast_object_list(obj, src=src)
+    names, meta = obj
+    out = {}
+    for k in names:
+        dtype, n = meta[k]
+        np_dt = np.dtype(dtype)
+        view = {np.dtype(np.uint32): np.int32, np.dtype(np.uint64): np.int64}.get(np_dt, np_dt)
+        if me == src:
+            t = torch.from_numpy(np.ascontiguousarray(arrays[k]).view(view)).to(dev)
+        else:
+            t = torch.empty(n, dtype=getattr(torch, np.dtype(view).name), device=dev)
+        dist.broadcast(t, src=src)
+        out[k] = t.cpu().numpy().view(np_dt)
+    return out
+
+
+def _stream_arrays(stream) -> dict:
+    from .sparse import ColumnRowStream, as_transaction_stream
+
+    ts = as_transaction_stream(stream)
+    if ts is not None:
+        return {"kind": np.array([0]), "dim": np.array([stream.n_rows], dtype=np.int64),
+                "offsets": ts.offsets, "items": ts.items}
+    cr = ColumnRowStream.from_stream(stream)
+    return {"kind": np.array([1]), "dim": np.array([cr.n_rows, cr.n_cols], dtype=np.int64),
+            "a_ptr": cr.a_ptr, "a_idx": cr.a_idx, "a_val": cr.a_val,
+            "b_ptr": cr.b_ptr, "b_idx": cr.b_idx, "b_val": cr.b_val}
+
+
+def _stream_from_arrays(arr: dict):
+    from .sparse import ColumnRowStream, TransactionStream
+
+    if int(arr["kind"][0]) == 0:
+        return TransactionStream(int(arr["dim"][0]), arr["offsets"], arr["items"], validate=False)
+    return ColumnRowStream(int(arr["dim"][0]), int(arr["dim"][1]), arr["a_ptr"], arr["a_idx"],
+                           arr["a_val"], arr["b_ptr"], arr["b_idx"], arr["b_val"])
+
+
+def run_distributed(stream, config, upper_triangle_only: bool = False, compute=None, src: int = 0):
+    """SPMD body of run_parallel. Returns (state, report) on rank `src`,
+    (None, None) elsewhere. `compute(stream, config, w_lo, w_hi, upper)` returns
+    the payloads of a worker block (default: the GPU engine's worker_payloads)."""
+    from .engine import merge_partials, worker_payloads
+
+    dist = _dist()
+    me, world = dist.get_rank(), dist.get_world_size()
+    local = _stream_from_arrays(broadcast_arrays(_stream_arrays(stream) if me == src else None,
+                                                 src=src))
+    compute = compute or worker_payloads
+    lo, hi = rank_workers(config.workers, me, world)
+    payloads = compute(local, config, lo, hi, upper_triangle_only) if hi > lo else []
+    gathered = [None] * world if me == src else None
+    dist.gather_object(payloads, gathered, dst=src)
+    if me != src:
+        return None, None
+    return merge_partials([p for part in gathered for p in part])

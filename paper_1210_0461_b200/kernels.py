@@ -1,0 +1,374 @@
+"""Thin torch-facing wrappers over the C-ABI (one function per kernel family).
+
+Device buffers are torch CUDA tensors (uint32 data is carried in int32
+tensors, uint64 in int64); every call is ordered on the current CUDA stream.
+Nothing here falls back to the CPU: without the library or a device the
+calls raise `DeviceError` (see `_native.require_cuda`).
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import ConfigError, InputError
+
+U32_MASK = 0xFFFFFFFF
+
+
+def _dev():
+    return nat.require_cuda()
+
+
+def u32_to_numpy(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+# ------------------------------------------------------------------ inputs
+
+@dataclass
+class DeviceTransactions:
+    """Transactions resident in HBM: CSR offsets int64[n+1], items uint32[nnz]."""
+
+    offsets: torch.Tensor
+    items: torch.Tensor
+    n_items: int
+
+    @property
+    def n_tx(self) -> int:
+        return self.offsets.shape[0] - 1
+
+    @property
+    def n_rows(self) -> int:
+        return self.n_items
+
+    n_cols = n_rows
+
+    @property
+    def nnz(self) -> int:
+        return self.items.shape[0]
+
+    @classmethod
+    def from_host(cls, offsets: np.ndarray, items: np.ndarray, n_items: int,
+                  non_blocking: bool = False) -> "DeviceTransactions":
+        dev = _dev()
+        off = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64))
+        it = torch.from_numpy(np.ascontiguousarray(items, dtype=np.uint32).view(np.int32))
+        if non_blocking:
+            off, it = off.pin_memory(), it.pin_memory()
+        return cls(off.to(dev, non_blocking=non_blocking), it.to(dev, non_blocking=non_blocking),
+                   int(n_items))
+
+    def to_host(self) -> tuple[np.ndarray, np.ndarray]:
+        return self.offsets.cpu().numpy(), u32_to_numpy(self.items)
+
+
+@dataclass
+class DeviceOuterStream:
+    """General stream in HBM: a_k (CSC column) x b_k (CSR row), float64 values."""
+
+    a_ptr: torch.Tensor
+    a_idx: torch.Tensor
+    a_val: torch.Tensor
+    b_ptr: torch.Tensor
+    b_idx: torch.Tensor
+    b_val: torch.Tensor
+    n_rows: int
+    n_cols: int
+
+    @property
+    def n_products(self) -> int:
+        return self.a_ptr.shape[0] - 1
+
+    @classmethod
+    def from_host(cls, s, non_blocking: bool = False) -> "DeviceOuterStream":
+        dev = _dev()
+
+        def up(a, dt, view=None):
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt) if view is None else
+                                 np.ascontiguousarray(a, dtype=dt).view(view))
+            if non_blocking:
+                t = t.pin_memory()
+            return t.to(dev, non_blocking=non_blocking)
+
+        return cls(up(s.a_ptr, np.int64), up(s.a_idx, np.uint32, np.int32), up(s.a_val, np.float64),
+                   up(s.b_ptr, np.int64), up(s.b_idx, np.uint32, np.int32), up(s.b_val, np.float64),
+                   s.n_rows, s.n_cols)
+
+
+# ------------------------------------------------------------------ hashing
+
+def hash_tables(hasher, n_items: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """K0: (h_row, h_col) uint32[n_items] for one EntryHasher (hashing.py:68-71)."""
+    dev = _dev()
+    kappa = hasher.kappa
+    if kappa > (1 << 31):
+        raise ConfigError(f"kappa {kappa} exceeds the device limit 2^31")
+    n = max(int(n_items), 1)
+    h_row = torch.empty(n, dtype=torch.int32, device=dev)
+    h_col = torch.empty(n, dtype=torch.int32, device=dev)
+    nat.call("crop_hash_tables", int(n_items), hasher.row_hash.mul, hasher.row_hash.add,
+             hasher.col_hash.mul, hasher.col_hash.add, kappa, nat.ptr(h_row), nat.ptr(h_col),
+             nat.stream_ptr())
+    return h_row, h_col
+
+
+def sign_hash(row: torch.Tensor, col: torch.Tensor, sign_fn) -> torch.Tensor:
+    out = torch.empty(row.shape[0], dtype=torch.int8, device=row.device)
+    nat.call("crop_sign_hash", nat.ptr(row), nat.ptr(col), row.shape[0], sign_fn.mul, sign_fn.add,
+             nat.ptr(out), nat.stream_ptr())
+    return out
+
+
+def interval_struct(kappa: int, start: int, stop: int, h_row=None, h_col=None) -> nat.Interval:
+    return nat.Interval(kappa, start, stop, nat.ptr(h_row), nat.ptr(h_col))
+
+
+# ------------------------------------------------------------------ K1 loads
+
+def selfjoin_bucket_loads(dtx: DeviceTransactions, h_row, h_col, kappa: int,
+                          upper_only: bool) -> torch.Tensor:
+    loads = torch.zeros(kappa, dtype=torch.int64, device=dtx.offsets.device)
+    nat.call("crop_selfjoin_bucket_loads", nat.ptr(dtx.offsets), nat.ptr(dtx.items), dtx.n_tx,
+             nat.ptr(h_row), nat.ptr(h_col), kappa, int(upper_only), nat.ptr(loads),
+             nat.stream_ptr())
+    return loads
+
+
+def outer_bucket_loads(ds: DeviceOuterStream, h_row, h_col, kappa: int,
+                       upper_only: bool) -> torch.Tensor:
+    loads = torch.zeros(kappa, dtype=torch.int64, device=ds.a_ptr.device)
+    nat.call("crop_outer_bucket_loads", nat.ptr(ds.a_ptr), nat.ptr(ds.a_idx), nat.ptr(ds.b_ptr),
+             nat.ptr(ds.b_idx), ds.n_products, nat.ptr(h_row), nat.ptr(h_col), kappa,
+             int(upper_only), nat.ptr(loads), nat.stream_ptr())
+    return loads
+
+
+# ------------------------------------------------------------------ K2 pairs
+
+@dataclass
+class DeviceEntries:
+    """Counted entries in HBM (unordered): row, col uint32 and a weight column.
+
+    `count` (uint32) for 0/1 streams, `value` (float64) for real streams;
+    `bucket` is filled by the real-valued path (sorted per bucket)."""
+
+    row: torch.Tensor
+    col: torch.Tensor
+    count: torch.Tensor | None
+    value: torch.Tensor | None
+    n: int
+    total_terms: int
+    bucket: torch.Tensor | None = None
+
+    def weights_f64(self) -> torch.Tensor:
+        if self.value is not None:
+            return self.value[: self.n]
+        return (self.count[: self.n].to(torch.int64) & U32_MASK).to(torch.float64)
+
+    def to_numpy(self):
+        row = u32_to_numpy(self.row[: self.n])
+        col = u32_to_numpy(self.col[: self.n])
+        w = self.weights_f64().cpu().numpy()
+        return row, col, w
+
+
+class PairCountJob:
+    """K2 handle: plan on create (one stream sync), run on demand."""
+
+    def __init__(self, dtx: DeviceTransactions, upper_only: bool, interval: nat.Interval | None,
+                 keep: tuple = ()):
+        self._keep = (dtx, keep)  # tensors the native job points at
+        self.dtx = dtx
+        lib = nat.load()
+        h = ctypes.c_void_p()
+        iv = ctypes.byref(interval) if interval is not None else None
+        nat.check(lib.crop_pairs_create(nat.ptr(dtx.offsets), nat.ptr(dtx.items), dtx.n_tx,
+                                        dtx.n_items, int(upper_only), iv, nat.stream_ptr(),
+                                        ctypes.byref(h)))
+        self._h = h
+        me, tt, nt, nu = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        nat.check(lib.crop_pairs_info(h, ctypes.byref(me), ctypes.byref(tt), ctypes.byref(nt),
+                                      ctypes.byref(nu)))
+        self.max_entries, self.total_terms = int(me.value), int(tt.value)
+        self.n_tiles, self.n_units = int(nt.value), int(nu.value)
+
+    def run(self, sync: bool = True) -> DeviceEntries:
+        dev = self.dtx.offsets.device
+        m = max(self.max_entries, 1)
+        row = torch.empty(m, dtype=torch.int32, device=dev)
+        col = torch.empty(m, dtype=torch.int32, device=dev)
+        cnt = torch.empty(m, dtype=torch.int32, device=dev)
+        n_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        nat.check(nat.load().crop_pairs_run(self._h, nat.ptr(row), nat.ptr(col), nat.ptr(cnt),
+                                            nat.ptr(n_dev), nat.stream_ptr()))
+        ent = DeviceEntries(row, col, cnt, None, -1, self.total_terms)
+        ent.n_dev = n_dev
+        if sync:
+            ent.n = int(n_dev.item())
+            if ent.n > self.max_entries:
+                raise InputError(f"pair engine overflow: {ent.n} > {self.max_entries}")
+        return ent
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            nat.load().crop_pairs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def count_pairs(dtx: DeviceTransactions, upper_only: bool = True, kappa: int = 1, start: int = 0,
+                stop: int | None = None, h_row=None, h_col=None) -> DeviceEntries:
+    """Exact supports of the entries whose bucket lies in [start, stop)."""
+    stop = kappa if stop is None else stop
+    iv = None
+    if not (start == 0 and stop == kappa):
+        if h_row is None or h_col is None:
+            raise ConfigError("a partial interval needs the hash tables")
+        iv = interval_struct(kappa, start, stop, h_row, h_col)
+    job = PairCountJob(dtx, upper_only, iv, keep=(h_row, h_col))
+    try:
+        return job.run()
+    finally:
+        job.close()
+
+
+def entry_bucket_stats(ent: DeviceEntries, tables: list, kappa: int, n_items: int,
+                       signs: list | None):
+    """Per-instance (loads, distinct, cs) of counted entries; tables[t]=(h_row,h_col)."""
+    dev = ent.row.device
+    t = len(tables)
+    h_row = torch.cat([x[0][:n_items] for x in tables]) if t > 1 else tables[0][0]
+    h_col = torch.cat([x[1][:n_items] for x in tables]) if t > 1 else tables[0][1]
+    loads = torch.zeros(t * kappa, dtype=torch.int64, device=dev)
+    distinct = torch.zeros(t * kappa, dtype=torch.int32, device=dev)
+    cs = torch.zeros(t * kappa, dtype=torch.int64, device=dev) if signs else None
+    sg = None
+    if signs:
+        sg = (ctypes.c_uint64 * (2 * t))(*[v for s in signs for v in (s.mul, s.add)])
+    n_dev = getattr(ent, "n_dev", None)
+    if n_dev is None:
+        n_dev = torch.tensor([ent.n], dtype=torch.int64, device=dev)
+    nat.call("crop_entry_bucket_stats", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count),
+             nat.ptr(n_dev), ent.row.shape[0], t, n_items,
+             nat.ptr(h_row), nat.ptr(h_col), kappa, sg, nat.ptr(loads), nat.ptr(distinct),
+             nat.ptr(cs), nat.stream_ptr())
+    return loads.view(t, kappa), distinct.view(t, kappa), (cs.view(t, kappa) if cs is not None else None)
+
+
+def entry_buckets(row, col, n: int, h_row, h_col, kappa: int) -> torch.Tensor:
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=row.device)
+    nat.call("crop_entry_buckets", nat.ptr(row), nat.ptr(col), n, nat.ptr(h_row), nat.ptr(h_col),
+             kappa, nat.ptr(out), nat.stream_ptr())
+    return out[:n]
+
+
+# ------------------------------------------------------------------ K4 top-k
+
+def topk_indices(ent: DeviceEntries, k: int, count: torch.Tensor | None = None) -> torch.Tensor:
+    """Indices of the best k entries by (count desc, row asc, col asc), unordered."""
+    dev = ent.row.device
+    cnt = ent.count if count is None else count
+    k = int(k)
+    out = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+    kout = torch.zeros(1, dtype=torch.int64, device=dev)
+    n_dev = getattr(ent, "n_dev", None)
+    if n_dev is None:
+        n_dev = torch.tensor([ent.n], dtype=torch.int64, device=dev)
+    nat.call("crop_topk", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(cnt), nat.ptr(n_dev),
+             ent.row.shape[0], k, nat.ptr(out), nat.ptr(kout), nat.stream_ptr())
+    return out[: int(kout.item())]
+
+
+# ------------------------------------------------------------------ K5 outer
+
+def outer_product(ds: DeviceOuterStream, upper_only: bool = False, kappa: int = 1, start: int = 0,
+                  stop: int | None = None, h_row=None, h_col=None) -> DeviceEntries:
+    """Per-bucket sorted COO of the stream restricted to buckets [start, stop)."""
+    stop = kappa if stop is None else stop
+    iv = interval_struct(kappa, start, stop, h_row, h_col) if h_row is not None else None
+    if iv is None and not (start == 0 and stop == kappa):
+        raise ConfigError("a partial interval needs the hash tables")
+    lib = nat.load()
+    h = ctypes.c_void_p()
+    nat.check(lib.crop_outer_create(nat.ptr(ds.a_ptr), nat.ptr(ds.a_idx), nat.ptr(ds.a_val),
+                                    nat.ptr(ds.b_ptr), nat.ptr(ds.b_idx), nat.ptr(ds.b_val),
+                                    ds.n_products, int(upper_only),
+                                    ctypes.byref(iv) if iv is not None else None,
+                                    nat.stream_ptr(), ctypes.byref(h)))
+    try:
+        me, tt = ctypes.c_uint64(), ctypes.c_uint64()
+        nat.check(lib.crop_outer_info(h, ctypes.byref(me), ctypes.byref(tt)))
+        m = max(int(me.value), 1)
+        dev = ds.a_ptr.device
+        row = torch.empty(m, dtype=torch.int32, device=dev)
+        col = torch.empty(m, dtype=torch.int32, device=dev)
+        val = torch.empty(m, dtype=torch.float64, device=dev)
+        buck = torch.empty(m, dtype=torch.int32, device=dev)
+        n_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        nat.check(lib.crop_outer_run(h, nat.ptr(row), nat.ptr(col), nat.ptr(val), nat.ptr(buck),
+                                     nat.ptr(n_dev), nat.stream_ptr()))
+        n = int(n_dev.item())
+    finally:
+        lib.crop_outer_destroy(h)
+    ent = DeviceEntries(row, col, None, val, n, int(tt.value), bucket=buck)
+    ent.n_dev = n_dev
+    return ent
+
+
+# ------------------------------------------------------------------ generator
+
+def generate_transactions(n_tx: int, n_items: int, item_alias: tuple, len_cdf: np.ndarray,
+                          len_lo: int, seed: int) -> DeviceTransactions:
+    dev = _dev()
+    thresh, alias = item_alias
+    lengths = torch.empty(max(n_tx, 1), dtype=torch.int64, device=dev)
+    cdf = np.ascontiguousarray(len_cdf, dtype=np.uint32)
+    nat.call("crop_gen_lengths", n_tx, seed, cdf.ctypes.data, cdf.shape[0], len_lo,
+             nat.ptr(lengths), nat.stream_ptr())
+    offsets = torch.zeros(n_tx + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(lengths[:n_tx], 0, out=offsets[1:])
+    nnz = int(offsets[-1].item())
+    items = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    th = np.ascontiguousarray(thresh, dtype=np.uint32)
+    al = np.ascontiguousarray(alias, dtype=np.uint32)
+    nat.call("crop_gen_items", n_tx, seed, n_items, th.ctypes.data, al.ctypes.data,
+             nat.ptr(offsets), nat.ptr(items), nat.stream_ptr())
+    return DeviceTransactions(offsets, items[:nnz], n_items)
+
+
+def entry_bucket_stats_f64(ent: DeviceEntries, tables: list, kappa: int, n_items: int,
+                           signs: list | None):
+    """Real-weight entries: per-instance (distinct, cs) per bucket."""
+    dev = ent.row.device
+    t = len(tables)
+    h_row = torch.cat([x[0][:n_items] for x in tables]) if t > 1 else tables[0][0]
+    h_col = torch.cat([x[1][:n_items] for x in tables]) if t > 1 else tables[0][1]
+    distinct = torch.zeros(t * kappa, dtype=torch.int32, device=dev)
+    cs = torch.zeros(t * kappa, dtype=torch.float64, device=dev) if signs else None
+    sg = None
+    if signs:
+        sg = (ctypes.c_uint64 * (2 * t))(*[v for s in signs for v in (s.mul, s.add)])
+    n_dev = getattr(ent, "n_dev", None)
+    if n_dev is None:
+        n_dev = torch.tensor([ent.n], dtype=torch.int64, device=dev)
+    nat.call("crop_entry_bucket_stats_f64", nat.ptr(ent.row), nat.ptr(ent.col),
+             nat.ptr(ent.value), nat.ptr(n_dev), ent.row.shape[0], t, n_items, nat.ptr(h_row),
+             nat.ptr(h_col), kappa, sg, nat.ptr(distinct), nat.ptr(cs), nat.stream_ptr())
+    return distinct.view(t, kappa), (cs.view(t, kappa) if cs is not None else None)
+
+
+def product_worker_loads(a_ptr, a_idx, b_ptr, b_idx, n_products: int, h_row, h_col, kappa: int,
+                         workers: int, upper_only: bool) -> torch.Tensor:
+    out = torch.zeros(max(n_products, 1) * workers, dtype=torch.int32, device=a_ptr.device)
+    nat.call("crop_product_worker_loads", nat.ptr(a_ptr), nat.ptr(a_idx), nat.ptr(b_ptr),
+             nat.ptr(b_idx), n_products, nat.ptr(h_row), nat.ptr(h_col), kappa, workers,
+             int(upper_only), nat.ptr(out), nat.stream_ptr())
+    return out[: n_products * workers].view(n_products, workers)

@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the public API / C-ABI) against the
+reference's golden fixtures and the C oracle on the same seeded inputs.
+
+Integer work (hashes, buckets, loads, pair counts, Count-Sketch cells of 0/1
+streams, top-k order) must match bit for bit; real-valued products are summed
+in fp64 in stream order and must match bit for bit as well (tolerance
+rel 1e-5 / abs 1e-6 is what BASELINE.json allows; we assert exact equality).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_1210_0461_b200 as crop  # noqa: E402
+from conftest import tx_to_csr, vectors_to_csr  # noqa: E402
+from paper_1210_0461_b200 import kernels, workloads  # noqa: E402
+
+
+def _records(recs):
+    return sorted((int(b), int(r), int(c), float(n), float(o)) for b, r, c, n, o in recs)
+
+
+def _state_records(state):
+    out = []
+    for inst in state.instances:
+        rs = []
+        for b, s in inst.summaries.items():
+            for item, cnt, over in s.records():
+                rs.append((b, item[0], item[1], cnt, over))
+        out.append(sorted(rs))
+    return out
+
+
+# ----------------------------------------------------------------- hashing
+
+def test_device_hash_tables_match_reference(golden):
+    for case in golden["hashes"]:
+        h = crop.make_hashes(crop.HashConfig(case["kappa"], case["seed"]))
+        assert list(h.coefficients()) == case["coeffs"]
+        idx = case["indices"]
+        n = max(idx) + 1
+        if n > (1 << 24):
+            continue  # tables for huge ids are checked through index_hash below
+        hr, hc = kernels.hash_tables(h, n)
+        hr = kernels.u32_to_numpy(hr)
+        hc = kernels.u32_to_numpy(hc)
+        assert hr[idx].tolist() == case["h_row"]
+        assert hc[idx].tolist() == case["h_col"]
+
+
+def test_device_sign_hash(golden):
+    for case in golden["hashes"]:
+        h = crop.make_hashes(crop.HashConfig(case["kappa"], case["seed"]))
+        rows = torch.tensor([r for r, _, _ in case["signs"]], dtype=torch.int64).to(torch.int32)
+        cols = torch.tensor([c for _, c, _ in case["signs"]], dtype=torch.int64).to(torch.int32)
+        s = kernels.sign_hash(rows.cuda(), cols.cuda(), h.sign_hash).cpu().tolist()
+        assert s == [x for _, _, x in case["signs"]]
+
+
+# ----------------------------------------------------------------- mining golden
+
+@pytest.mark.parametrize("case_idx", range(5))
+def test_run_matches_reference_golden(golden, case_idx):
+    case = golden["mining"][case_idx]
+    cfg = crop.EngineConfig(**case["config"])
+    stream = crop.transactions_to_stream(case["transactions"])
+    state, report = crop.run(stream, cfg, upper_triangle_only=True)
+    assert report.rows == case["rows"]
+    assert report.input_pair_total == case["input_pair_total"]
+    assert report.assignments == [tuple(a) for a in case["assignments"]]
+    assert report.max_avg_ratio() == case["max_avg_ratio"]
+    exact = cfg.ss_capacity >= 2 ** 31
+    for inst, want in zip(state.instances, case["instances"]):
+        assert inst.seed == want["seed"]
+        assert list(inst.hasher.coefficients()) == want["coeffs"]
+        assert inst.sketch.cells == want["cs"]
+        for b, tot in want["bucket_totals"].items():
+            assert inst.summaries[int(b)].total_weight == tot
+    if exact:
+        got = _state_records(state)
+        for g, want in zip(got, case["instances"]):
+            assert g == _records(want["records"])
+        top = [[t.entry.row, t.entry.col, t.lower, t.upper, t.estimate]
+               for t in state.top_entries(25)]
+        assert top == case["top25"]
+        for i, j, lo, up, est in case["queries"]:
+            assert list(state.query((i, j))) == [lo, up, est]
+    else:
+        # bounded regime: Space-Saving guarantees against exact supports
+        supports = {(a, b): c for a, b, c in case["supports"]}
+        for inst in state.instances:
+            for b, s in inst.summaries.items():
+                m = s.total_weight
+                for item, cnt, over in s.records():
+                    assert cnt - over <= supports[item] <= cnt
+                    assert over <= m / cfg.ss_capacity
+        for (i, j), true in supports.items():
+            lo, up, _ = state.query((i, j))
+            assert lo <= true <= up
+
+
+def test_measure_loads_matches_reference(golden):
+    for case in golden["mining"]:
+        cfg = crop.EngineConfig(**case["config"])
+        stream = crop.transactions_to_stream(case["transactions"])
+        up = crop.measure_loads(stream, cfg, upper_triangle_only=True)
+        full = crop.measure_loads(stream, cfg, upper_triangle_only=False)
+        assert up.rows == case["loads_upper"]
+        assert full.rows == case["loads_full"]
+        assert full.input_pair_total == case["pair_total_full"]
+
+
+def test_selfjoin_full_matches_reference(golden):
+    case = golden["selfjoin_full"]
+    cfg = crop.EngineConfig(**case["config"])
+    stream = crop.transactions_to_stream(case["transactions"])
+    state, report = crop.run(stream, cfg, upper_triangle_only=False)
+    assert report.rows == case["rows"]
+    got = _state_records(state)
+    assert got[0] == _records(case["instances"][0]["records"])
+    assert state.instances[0].sketch.cells == case["instances"][0]["cs"]
+
+
+def test_exact_pair_supports_matches_reference(golden):
+    for case in golden["mining"]:
+        got = crop.exact_pair_supports(case["transactions"])
+        assert sorted([a, b, c] for (a, b), c in got.items()) == case["supports"]
+
+
+# ----------------------------------------------------------------- general streams
+
+def _general_stream(case):
+    ap, ai, av = vectors_to_csr(case["a"])
+    bp, bi, bv = vectors_to_csr(case["b"])
+    return crop.ColumnRowStream(case["n_dim"], case["n_dim"], ap, ai, av, bp, bi, bv)
+
+
+def test_exact_product_matches_reference(golden):
+    for case in golden["general"]:
+        s = _general_stream(case)
+        got = crop.exact_product(s)
+        assert sorted([a, b, w] for (a, b), w in got.items()) == case["exact"]
+        got = crop.exact_product(s, upper_only=True)
+        assert sorted([a, b, w] for (a, b), w in got.items()) == case["exact_upper"]
+
+
+def test_partition_enumeration_matches_reference(golden):
+    for case in golden["general"]:
+        s = _general_stream(case)
+        h = crop.make_hashes(crop.HashConfig(case["kappa"], case["seed"]))
+        ds = kernels.DeviceOuterStream.from_host(s)
+        tab = kernels.hash_tables(h, case["n_dim"])
+        for part in case["partitions"]:
+            ent = kernels.outer_product(ds, False, case["kappa"], part["start"], part["stop"], *tab)
+            r, c, w = ent.to_numpy()
+            assert sorted([int(a), int(b), float(x)] for a, b, x in zip(r, c, w)) == part["entries"]
+            loads = kernels.outer_bucket_loads(ds, tab[0], tab[1], case["kappa"], False)
+            assert int(loads[part["start"]:part["stop"]].sum()) == part["count"]
+
+
+def test_enumerate_interval_single_products(golden):
+    case = golden["general"][1]
+    h = crop.make_hashes(crop.HashConfig(case["kappa"], case["seed"]))
+    for (ai, av), (bi, bv) in list(zip(case["a"], case["b"]))[:6]:
+        a = crop.SparseVector(case["n_dim"], ai, av)
+        b = crop.SparseVector(case["n_dim"], bi, bv)
+        for asg in crop.WorkerAssignment.split(case["kappa"], case["workers"]):
+            got = list(crop.enumerate_interval(a, b, h.row_hash, h.col_hash, asg))
+            want = [((i, j), a.get(i) * b.get(j)) for i in ai for j in bi
+                    if asg.start <= h.bucket_of(i, j) < asg.stop]
+            assert sorted((tuple(e), v) for e, v in got) == sorted(want)
+            assert crop.count_interval(a, b, h.row_hash, h.col_hash, asg) == len(want)
+
+
+def test_run_rejects_negative_terms(golden):
+    s = _general_stream(golden["general"][0])
+    with pytest.raises(crop.InputError):
+        crop.run(s, crop.EngineConfig(kappa=4, ss_capacity=8))
+
+
+# ----------------------------------------------------------------- config workloads vs oracle
+
+def _oracle_pairs(off, items):
+    r, c, w = oracle.pair_supports(off, items)
+    return oracle.sorted_pairs(r, c, w)
+
+
+def _gpu_pairs(ent):
+    r, c, w = ent.to_numpy()
+    return oracle.sorted_pairs(r, c, w)
+
+
+@pytest.mark.parametrize("name,n_tx", [("c1", None), ("c2", 60_000), ("c5", 3_000),
+                                       ("c3", 30_000)])
+def test_config_prefix_counts_bit_exact(name, n_tx):
+    cfg = workloads.CONFIGS[name]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=n_tx)
+    off, items = dtx.to_host()
+    ent = kernels.count_pairs(dtx, True)
+    gr, gc, gw = _gpu_pairs(ent)
+    orow, ocol, ow = _oracle_pairs(off, items)
+    assert np.array_equal(gr, orow) and np.array_equal(gc, ocol) and np.array_equal(gw, ow)
+    lens = np.diff(off)
+    assert ent.total_terms == int((lens * (lens - 1) // 2).sum())
+    assert int(gw.sum()) == ent.total_terms  # conservation
+
+
+def test_c1_full_run_against_oracle():
+    cfg = workloads.CONFIGS["c1"]
+    dtx = workloads.generate_pairs_workload(cfg)
+    off, items = dtx.to_host()
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers, seed=0)
+    state, report = crop.run(dtx, config, upper_triangle_only=True)
+    h = crop.make_hashes(crop.HashConfig(cfg.kappa, config.instance_seeds()[0]))
+    recs, loads = oracle.run(oracle.Stream(off, items), h.coefficients(), cfg.kappa, cfg.workers,
+                             upper_only=True, cs=True)
+    assert report.rows[0] == loads.tolist()
+    assert state.device_result.instances[0].cs.tolist() == recs.cs.tolist()
+    top = state.top_entries(cfg.top_k)
+    want = sorted(zip(recs.count.tolist(), recs.row.tolist(), recs.col.tolist()),
+                  key=lambda x: (-x[0], x[1], x[2]))[: cfg.top_k]
+    assert [(t.entry.row, t.entry.col, t.upper) for t in top] == [(r, c, n) for n, r, c in want]
+
+
+@pytest.mark.parametrize("kappa,workers,worker", [(8, 8, 3), (1184, 8, 5), (16, 4, 0)])
+def test_interval_filter_matches_oracle_worker(kappa, workers, worker):
+    cfg = workloads.CONFIGS["c2"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=20_000)
+    off, items = dtx.to_host()
+    config = crop.EngineConfig(kappa=kappa, ss_capacity=2 ** 31, workers=workers, seed=7)
+    h = crop.make_hashes(crop.HashConfig(kappa, config.instance_seeds()[0]))
+    asg = config.assignments()[worker]
+    tab = kernels.hash_tables(h, cfg.n_items)
+    ent = kernels.count_pairs(dtx, True, kappa, asg.start, asg.stop, *tab)
+    recs, load = oracle.run_worker(oracle.Stream(off, items), h.coefficients(), kappa, workers,
+                                   worker, upper_only=True)
+    want = oracle.sorted_pairs(recs.row, recs.col, recs.count)
+    got = _gpu_pairs(ent)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+    assert int(got[2].sum()) == load
+
+
+def test_topk_with_ties_matches_sort():
+    cfg = workloads.CONFIGS["c2"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=30_000)
+    ent = kernels.count_pairs(dtx, True)
+    r, c, w = ent.to_numpy()
+    order = np.lexsort((c, r, -w))
+    for k in (1, 7, 1000, 5000, int(r.shape[0]), int(r.shape[0]) + 10):
+        idx = kernels.topk_indices(ent, k).cpu().numpy()
+        got = sorted(zip(-w[idx], r[idx], c[idx]))
+        want = sorted(zip(-w[order[:k]], r[order[:k]], c[order[:k]]))
+        assert got == want
+
+
+def test_c4_prefix_product_matches_oracle():
+    cfg = workloads.CONFIGS["c4"]
+    s = workloads.generate_product_workload(cfg, n_products=20_000)
+    s = crop.ColumnRowStream(cfg.n, cfg.n, s.a_ptr, s.a_idx, s.a_val, s.b_ptr, s.b_idx, s.b_val)
+    ds = kernels.DeviceOuterStream.from_host(s)
+    h = crop.make_hashes(crop.HashConfig(cfg.kappa, crop.derive_seed(0, "instance:0")))
+    tab = kernels.hash_tables(h, cfg.n)
+    ent = kernels.outer_product(ds, False, cfg.kappa, 0, cfg.kappa, *tab)
+    gr, gc, gw = ent.to_numpy()
+    ost = oracle.Stream(s.a_ptr, s.a_idx, s.a_val, s.b_ptr, s.b_idx, s.b_val)
+    orow, ocol, ow = oracle.exact_product(ost)
+    # include exact zero sums on the GPU side for comparison
+    nz = gw != 0.0
+    g = oracle.sorted_pairs(gr[nz], gc[nz], gw[nz])
+    o = oracle.sorted_pairs(orow, ocol, ow)
+    assert np.array_equal(g[0], o[0]) and np.array_equal(g[1], o[1])
+    np.testing.assert_allclose(g[2], o[2], rtol=1e-5, atol=1e-6)
+    assert np.array_equal(g[2], o[2])  # stream-ordered fp64 sums: bit-exact
+    # per-bucket sorted COO
+    b = kernels.u32_to_numpy(ent.bucket[: ent.n])
+    assert np.all(np.diff(b.astype(np.int64)) >= 0)
+    key = (b.astype(np.uint64) << np.uint64(40)) | (gr.astype(np.uint64) << np.uint64(20)) | gc
+    assert np.all(np.diff(key.astype(np.int64)) > 0)
+
+
+def test_edge_cases():
+    # empty stream, empty and singleton transactions
+    for tx in ([], [[]], [[5]], [[], [1, 2], [3]], [[0, 1, 2, 3]]):
+        stream = crop.transactions_to_stream(tx, dim=8)
+        cfg = crop.EngineConfig(kappa=3, ss_capacity=100, workers=3, seed=1)
+        state, report = crop.run(stream, cfg, upper_triangle_only=True)
+        sup = {}
+        for t in tx:
+            for a in range(len(t)):
+                for b in range(a + 1, len(t)):
+                    sup[(t[a], t[b])] = sup.get((t[a], t[b]), 0) + 1
+        assert report.total_entries == sum(sup.values())
+        for (i, j), v in sup.items():
+            assert state.query((i, j))[:2] == (v, v)
+        assert len(state.top_entries(5)) == min(5, len(sup))
+
+
+def test_long_transactions_and_wide_rows():
+    # lengths up to the 8192 limit; n > kDenseCap forces column windows
+    rng = np.random.default_rng(0)
+    n = 120_000
+    tx = [np.unique(rng.integers(0, n, size=L)).tolist() for L in (8000, 300, 5000, 2)]
+    tx += [[0, 1, 2, n - 1], [0, n - 2, n - 1]] * 20
+    # a row with > kHashCap terms and > kDenseCap columns -> column windows
+    tx += [[0] + np.unique(rng.integers(1, n, size=1000)).tolist() for _ in range(30)]
+    off, items = tx_to_csr(tx)
+    dtx = kernels.DeviceTransactions.from_host(off, items, n)
+    ent = kernels.count_pairs(dtx, True)
+    g = _gpu_pairs(ent)
+    o = _oracle_pairs(off, items)
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)
+    too_long = [list(range(9000))]
+    off, items = tx_to_csr(too_long)
+    with pytest.raises(crop.InputError):
+        kernels.count_pairs(kernels.DeviceTransactions.from_host(off, items, 9000), True)

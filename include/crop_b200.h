@@ -94,6 +94,8 @@ int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* tota
                     uint64_t* n_tiles, uint64_t* n_units);
 int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32_t* out_count,
                    uint64_t* d_n_entries, void* stream);
+/* 1 if the entry list overflowed its capacity (never expected; synchronises). */
+int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
 void crop_pairs_destroy(crop_pairs* job);
 
 /* Per-instance bucket statistics of counted entries (the LoadReport rows,

@@ -37,6 +37,7 @@ _SIGS = {
     "crop_pairs_info": (i32, [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
                               ctypes.POINTER(u64)]),
     "crop_pairs_run": (i32, [P, P, P, P, P, P]),
+    "crop_pairs_overflowed": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_destroy": (None, [P]),
     "crop_entry_bucket_stats": (i32, [P, P, P, P, u64, i32, u32, P, P, u32, P, P, P, P, P]),
     "crop_entry_buckets": (i32, [P, P, u64, P, P, u32, P, P]),

@@ -77,6 +77,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 // ------------------------------------------------------------------ errors
 void crop_set_error(int code, const char* fmt, ...);
+// Keep freed device scratch in the stream-ordered pool (no cudaMalloc per job).
+int crop_pool_setup();
 
 #define CROP_CUDA(call)                                                                  \
   do {                                                                                   \

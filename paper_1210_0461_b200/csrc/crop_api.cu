@@ -18,6 +18,19 @@ void crop_set_error(int code, const char* fmt, ...) {
 }
 
 extern "C" int crop_abi_version(void) { return 1; }
+
+int crop_pool_setup() {
+  static int done_dev = -1;
+  int dev = 0;
+  CROP_CUDA(cudaGetDevice(&dev));
+  if (done_dev == dev) return CROP_OK;
+  cudaMemPool_t pool;
+  CROP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thresh = UINT64_MAX;
+  CROP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+  done_dev = dev;
+  return CROP_OK;
+}
 extern "C" const char* crop_last_error(void) { return g_err; }
 
 using namespace crop;

@@ -183,6 +183,7 @@ extern "C" int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, co
                                  void* stream, crop_outer** job) {
   *job = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
+  if (int rc = crop_pool_setup()) return rc;
   crop_outer* J = new crop_outer();
   J->a_ptr = a_ptr;
   J->a_idx = a_idx;

@@ -43,17 +43,22 @@ namespace {
 
 constexpr int kCountThreads = 1024;
 constexpr int kCountWarps = kCountThreads / 32;
-constexpr uint32_t kDenseCap = 49152;   // dense counters per tile (192 KB)
-constexpr uint32_t kHashSlots = 24576;  // hash slots per tile (keys+counts 192 KB)
-constexpr uint32_t kHashCap = 16384;    // max distinct keys per hash tile (load <= 0.67)
-constexpr uint32_t kMaxLen = 8192;      // longest transaction (u32 pair counts per warp)
-constexpr uint32_t kStatSmemItems = 53248;
-constexpr uint32_t kTileSmem = 53248;   // route-pass shared tile counters
-constexpr int kRouteThreads = 512;
-constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr size_t kTableBytes = 196608;  // max(kDenseCap*4, kHashSlots*8)
-constexpr size_t kJobBytes = kCountWarps * 32 * 24;
+constexpr uint32_t kDenseCap = 50176;                // dense u32 counters per tile (196 KB)
+constexpr size_t kTableBytes = (size_t)kDenseCap * 4;
+constexpr uint32_t kHashSlots = kTableBytes / 8;     // 25088 key+count slots
+constexpr uint32_t kHashCap = 16384;                 // max distinct keys per hash tile
+constexpr uint32_t kMaxLen = 8192;                   // longest transaction
+constexpr int kJobWords = 5;                         // per-lane job record (shared memory)
+constexpr size_t kJobBytes = (size_t)kCountWarps * 32 * kJobWords * 4;
 constexpr size_t kCountSmem = kTableBytes + kJobBytes + 64;
+constexpr int kPassThreads = 1024;
+constexpr int kChunkTx = 4096;                       // transactions per position-parallel chunk
+constexpr size_t kOffBytes = (kChunkTx + 1) * 8;
+constexpr uint32_t kStatSmemItems = 40960;           // pass A privatised items (160 KB)
+constexpr uint32_t kTileSmem = 40960;                // route shared tile counters (160 KB)
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kUnknown = 0xFFFFFFFEu;       // route: previous tile not known yet
+constexpr uint32_t kWinFlag = 0x80000000u;           // item_tile: row is split into windows
 
 struct Tile {
   uint32_t row0, row1;  // rows [row0, row1)
@@ -76,174 +81,236 @@ __host__ __device__ __forceinline__ uint64_t tri_rowbase(uint64_t r, uint64_t ro
   return k * (n - 1) - k * (row0 + r - 1) / 2;
 }
 
+// ----------------------------------------------------- position-parallel walk
+// A CTA owns chunks of kChunkTx transactions whose offsets are staged in
+// shared memory. Each warp takes a contiguous range of item positions and
+// walks it 32 positions at a time (lane = position, coalesced loads of
+// items[g]); a lane finds its transaction by stepping forward from the
+// warp's cursor, so one position costs O(1) shared-memory reads. All O(nnz)
+// passes read the input once, coalesced.
+struct Pos {
+  int64_t base;  // global position of the transaction start
+  uint32_t p;    // position inside the transaction
+  uint32_t L;    // transaction length
+  uint32_t tx;   // chunk-local transaction index
+  bool valid;
+};
+
+__device__ __forceinline__ int stage_offsets(int64_t* s_off, const int64_t* __restrict__ offsets,
+                                             int64_t n_tx, int64_t chunk) {
+  const int64_t t0 = chunk * kChunkTx;
+  const int ntx = (int)(n_tx - t0 < kChunkTx ? n_tx - t0 : kChunkTx);
+  for (int t = threadIdx.x; t <= ntx; t += blockDim.x) s_off[t] = offsets[t0 + t];
+  __syncthreads();
+  return ntx;
+}
+
+// Calls body(g, pos) for every position of the chunk; all 32 lanes of a warp
+// execute body together (pos.valid false past the range) so body may use
+// warp shuffles. `cursor` is the warp's transaction cursor.
+template <typename Body>
+__device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx, Body&& body) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t g_lo = s_off[0], g_hi = s_off[ntx];
+  const int64_t per = (((g_hi - g_lo + nw - 1) / nw) + 31) & ~31ll;
+  const int64_t w_lo = g_lo + warp * per;
+  const int64_t w_hi = min(g_hi, w_lo + per);
+  if (w_lo >= w_hi) return;
+  int lo = 0, hi = ntx;  // cursor: last t with s_off[t] <= w_lo
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_off[mid] <= w_lo) lo = mid;
+    else hi = mid;
+  }
+  int cur = lo;
+  for (int64_t g0 = w_lo; g0 < w_hi; g0 += 32) {
+    const int64_t g = g0 + lane;
+    Pos q;
+    q.valid = g < w_hi;
+    int t = cur;
+    if (q.valid)
+      while (s_off[t + 1] <= g) ++t;
+    q.tx = (uint32_t)t;
+    q.base = s_off[t];
+    q.p = (uint32_t)(g - q.base);
+    q.L = (uint32_t)(s_off[t + 1] - q.base);
+    cur = __shfl_sync(0xffffffffu, t, 31);
+    body(g, q);
+  }
+}
+
 // ------------------------------------------------------------- pass A
 template <bool UPPER>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(kPassThreads, 1)
     k_item_terms(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
                  int64_t n_tx, uint32_t n_items, unsigned long long* __restrict__ terms,
                  unsigned int* __restrict__ max_len) {
-  extern __shared__ uint32_t s_terms[];
-  const uint32_t n_smem = n_items < kStatSmemItems ? n_items : kStatSmemItems;
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);
+  uint32_t* s_terms = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  const uint32_t n_smem = min(n_items, kStatSmemItems);
   for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x) s_terms[i] = 0;
-  __syncthreads();
-  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
   uint32_t my_max = 0;
-  for (int64_t t = (int64_t)blockIdx.x * warps + threadIdx.x / 32; t < n_tx;
-       t += (int64_t)gridDim.x * warps) {
-    int64_t base = offsets[t];
-    uint32_t L = (uint32_t)(offsets[t + 1] - base);
-    my_max = max(my_max, L);
-    for (uint32_t p = lane; p < L; p += 32) {
-      uint32_t i = items[base + p];
-      uint32_t c = UPPER ? L - 1 - p : L;
-      if (c == 0) continue;
+  const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    __syncthreads();
+    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk);
+    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
+      if (!q.valid) return;
+      const uint32_t i = items[g];
+      my_max = max(my_max, q.L);
+      const uint32_t c = UPPER ? q.L - 1 - q.p : q.L;
+      if (c == 0) return;
       if (i < n_smem) atomicAdd(&s_terms[i], c);
       else atomicAdd(&terms[i], (unsigned long long)c);
-    }
+    });
   }
-  if (lane == 0) atomicMax(max_len, my_max);
+  atomicMax(max_len, my_max);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x)
     if (s_terms[i]) atomicAdd(&terms[i], (unsigned long long)s_terms[i]);
 }
 
 // ------------------------------------------------------------- pass B
-// Walks one transaction with a warp and calls emit(tile, tx, packed) for each
-// entry: a run of consecutive positions whose rows share a (non-windowed)
-// tile, or one (row, window) per column window present after the row.
+// Entries (the work list of a tile), one per run of consecutive positions of
+// a transaction whose rows share a tile (UPPER), or per (row, column window
+// present) for split rows:
+//   UPPER: x = global position of the run's first row, y = len | rows << 16
+//          (len = positions from the first row to the end of the transaction)
+//   full : x = global position of the transaction start, y = L | p << 16
+//          (one row per entry)
+// Runs are found with warp shuffles: a lane's tile is compared with its
+// neighbours'; a run that leaves the 32-position window is finished with
+// loads (rare).
 template <bool UPPER, typename Emit>
-__device__ __forceinline__ void walk_tx(int64_t tx, const int64_t* __restrict__ offsets,
-                                        const uint32_t* __restrict__ items,
-                                        const uint32_t* __restrict__ item_tile,
-                                        const Tile* __restrict__ tiles, Emit&& emit) {
+__device__ __forceinline__ void route_window(int64_t g, const Pos& q,
+                                             const uint32_t* __restrict__ items,
+                                             const uint32_t* __restrict__ item_tile,
+                                             const Tile* __restrict__ tiles, uint32_t& carry_tile,
+                                             Emit&& emit) {
   const int lane = threadIdx.x & 31;
-  const int64_t base = offsets[tx];
-  const uint32_t L = (uint32_t)(offsets[tx + 1] - base);
-  for (uint32_t c = 0; c < L; c += 32) {
-    const uint32_t p = c + lane;
-    const bool valid = p < L;
-    uint32_t item = valid ? items[base + p] : 0;
-    uint32_t tile = valid ? item_tile[item] : kNone;
-    if (UPPER && p + 1 >= L) tile = kNone;  // last item has no partner after it
-    bool windowed = false;
-    if (tile != kNone) windowed = tiles[tile].nwin != 0;
-    uint32_t prev = __shfl_up_sync(0xffffffffu, tile, 1);
-    uint32_t next = __shfl_down_sync(0xffffffffu, tile, 1);
-    if (lane == 0) prev = kNone;
-    if (lane == 31) next = kNone;
-    const bool run_member = tile != kNone && !windowed;
-    const bool is_start = run_member && tile != prev;
-    const bool is_end = run_member && tile != next;
-    const uint32_t end_mask = __ballot_sync(0xffffffffu, is_end);
-    if (is_start) {
-      uint32_t e = __ffs(end_mask & (0xffffffffu << lane)) - 1;
-      uint32_t p1 = c + e + 1;
-      emit(tile, tx, p | (p1 << 16));
-    }
-    if (windowed) {
-      // columns after (UPPER) or anywhere in (full) the transaction, grouped
-      // by window; sorted items => window ids are non-decreasing.
-      const Tile t0 = tiles[tile];
-      const uint32_t lo = t0.c0;  // column start of window 0
-      uint32_t last_w = kNone;
-      for (uint32_t q = UPPER ? p + 1 : 0; q < L; ++q) {
-        uint32_t j = items[base + q];
-        if (j < lo) continue;
-        uint32_t w = (j - lo) / kDenseCap;
-        if (w >= t0.nwin) break;
-        if (w != last_w) {
-          emit(tile + w, tx, p | ((p + 1) << 16));
-          last_w = w;
-        }
+  uint32_t tv = kNone;
+  if (q.valid) {
+    tv = item_tile[items[g]];
+    if (UPPER && q.p + 1 >= q.L) tv = kNone;  // the last item has no partner after it
+  }
+  // previous position's tile (same transaction only)
+  uint32_t prev = __shfl_up_sync(0xffffffffu, tv, 1);
+  if (lane == 0) {
+    prev = carry_tile;
+    if (prev == kUnknown && q.valid && q.p > 0) prev = item_tile[items[g - 1]];
+  }
+  if (q.p == 0) prev = kNone;
+  const uint32_t next_tv = __shfl_down_sync(0xffffffffu, tv, 1);
+  const uint32_t next_p = __shfl_down_sync(0xffffffffu, q.p, 1);
+  carry_tile = __shfl_sync(0xffffffffu, tv, 31);
+  if (tv == kNone) return;
+  if (tv & kWinFlag) {  // split row: one entry per column window present
+    const uint32_t tile = tv & ~kWinFlag;
+    const Tile t0 = tiles[tile];
+    const uint32_t lo = t0.c0;
+    uint32_t last_w = kNone;
+    for (uint32_t p = UPPER ? q.p + 1 : 0; p < q.L; ++p) {
+      const uint32_t j = items[q.base + p];
+      if (j < lo) continue;
+      const uint32_t w = (j - lo) / kDenseCap;
+      if (w >= t0.nwin) break;
+      if (w != last_w) {
+        if (UPPER) emit(tile + w, (uint32_t)g, (q.L - q.p) | (1u << 16));
+        else emit(tile + w, (uint32_t)q.base, q.L | (q.p << 16));
+        last_w = w;
       }
     }
+    return;
   }
+  if (!UPPER) {
+    emit(tv, (uint32_t)q.base, q.L | (q.p << 16));
+    return;
+  }
+  if (prev == tv) return;  // not the first row of its run
+  uint32_t p1 = q.p + 1;
+  const bool next_known = lane < 31 && next_p == q.p + 1;
+  if (!(next_known && next_tv != tv))  // the run may continue: extend with loads
+    while (p1 + 1 < q.L && item_tile[items[q.base + p1]] == tv) ++p1;
+  emit(tv, (uint32_t)g, (q.L - q.p) | ((p1 - q.p) << 16));
 }
 
-struct CountEmit {
-  uint32_t* s_cnt;
-  uint32_t* g_cnt;
-  __device__ void operator()(uint32_t tile, int64_t, uint32_t) const {
-    if (tile < kTileSmem) atomicAdd(&s_cnt[tile], 1u);
-    else atomicAdd(&g_cnt[tile], 1u);
-  }
-};
-
 template <bool UPPER>
-__global__ void __launch_bounds__(kRouteThreads)
+__global__ void __launch_bounds__(kPassThreads, 1)
     k_route_count(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
                   int64_t n_tx, const uint32_t* __restrict__ item_tile,
                   const Tile* __restrict__ tiles, uint32_t n_tiles,
                   uint32_t* __restrict__ tile_entries) {
-  extern __shared__ uint32_t s_cnt[];
-  const uint32_t ns = n_tiles < kTileSmem ? n_tiles : kTileSmem;
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  const uint32_t ns = min(n_tiles, kTileSmem);
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
-  __syncthreads();
-  const int warps = blockDim.x / 32;
-  CountEmit em{s_cnt, tile_entries};
-  for (int64_t tx = (int64_t)blockIdx.x * warps + threadIdx.x / 32; tx < n_tx;
-       tx += (int64_t)gridDim.x * warps)
-    walk_tx<UPPER>(tx, offsets, items, item_tile, tiles, em);
+  auto emit = [&](uint32_t tile, uint32_t, uint32_t) {
+    if (tile < ns) atomicAdd(&s_cnt[tile], 1u);
+    else atomicAdd(&tile_entries[tile], 1u);
+  };
+  const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    __syncthreads();
+    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk);
+    uint32_t carry = kUnknown;
+    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
+      route_window<UPPER>(g, q, items, item_tile, tiles, carry, emit);
+    });
+  }
   __syncthreads();
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x)
     if (s_cnt[t]) atomicAdd(&tile_entries[t], s_cnt[t]);
 }
 
-struct WriteEmit {
-  uint32_t* s_cur;
-  unsigned long long* g_cur;
-  uint2* entries;
-  unsigned long long cap;
-  uint32_t* overflow;
-  __device__ void operator()(uint32_t tile, int64_t tx, uint32_t packed) const {
-    unsigned long long pos;
-    if (tile < kTileSmem) pos = atomicAdd(&s_cur[tile], 1u);  // holds the claimed base
-    else pos = atomicAdd(&g_cur[tile], 1ull);
-    if (pos < cap) entries[pos] = make_uint2((uint32_t)tx, packed);
-    else *overflow = 1u;
-  }
-};
-
-// Static transaction ranges per CTA: count the range's entries per tile in
-// shared memory, claim one global range per touched tile, then write.
+// Per chunk: count entries per shared tile, claim one global range per
+// touched tile, then write the entries (shared cursors hand out positions).
 template <bool UPPER>
-__global__ void __launch_bounds__(kRouteThreads)
+__global__ void __launch_bounds__(kPassThreads, 1)
     k_route_write(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
                   int64_t n_tx, const uint32_t* __restrict__ item_tile,
                   const Tile* __restrict__ tiles, uint32_t n_tiles,
                   unsigned long long* __restrict__ tile_cursor, uint2* __restrict__ entries,
                   unsigned long long cap, uint32_t* __restrict__ overflow) {
-  extern __shared__ uint32_t s_cnt[];
-  const uint32_t ns = n_tiles < kTileSmem ? n_tiles : kTileSmem;
-  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
-  __syncthreads();
-  const int warps = blockDim.x / 32;
-  const int64_t tx0 = n_tx * blockIdx.x / gridDim.x, tx1 = n_tx * (blockIdx.x + 1) / gridDim.x;
-  // walk 1: local counts for shared-memory tiles only
-  struct LocalCount {
-    uint32_t* s;
-    __device__ void operator()(uint32_t tile, int64_t, uint32_t) const {
-      if (tile < kTileSmem) atomicAdd(&s[tile], 1u);
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  const uint32_t ns = min(n_tiles, kTileSmem);
+  const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
+    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk);
+    auto count = [&](uint32_t tile, uint32_t, uint32_t) {
+      if (tile < ns) atomicAdd(&s_cnt[tile], 1u);
+    };
+    uint32_t carry = kUnknown;
+    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
+      route_window<UPPER>(g, q, items, item_tile, tiles, carry, count);
+    });
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) {
+      const uint32_t c = s_cnt[t];
+      if (c) s_cnt[t] = (uint32_t)atomicAdd(&tile_cursor[t], (unsigned long long)c);
     }
-  } lc{s_cnt};
-  for (int64_t tx = tx0 + threadIdx.x / 32; tx < tx1; tx += warps)
-    walk_tx<UPPER>(tx, offsets, items, item_tile, tiles, lc);
-  __syncthreads();
-  // claim: replace each count by the claimed global position (fits 32 bits
-  // only if entries < 2^32; checked on the host)
-  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) {
-    uint32_t c = s_cnt[t];
-    if (c) s_cnt[t] = (uint32_t)atomicAdd(&tile_cursor[t], (unsigned long long)c);
+    __syncthreads();
+    auto write = [&](uint32_t tile, uint32_t x, uint32_t y) {
+      unsigned long long pos;
+      if (tile < ns) pos = atomicAdd(&s_cnt[tile], 1u);
+      else pos = atomicAdd(&tile_cursor[tile], 1ull);
+      if (pos < cap) entries[pos] = make_uint2(x, y);
+      else *overflow = 1u;
+    };
+    carry = kUnknown;
+    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
+      route_window<UPPER>(g, q, items, item_tile, tiles, carry, write);
+    });
   }
-  __syncthreads();
-  WriteEmit we{s_cnt, tile_cursor, entries, cap, overflow};
-  for (int64_t tx = tx0 + threadIdx.x / 32; tx < tx1; tx += warps)
-    walk_tx<UPPER>(tx, offsets, items, item_tile, tiles, we);
 }
 
 // ------------------------------------------------------------- count
 struct CountArgs {
-  const int64_t* offsets;
   const uint32_t* items;
   const Tile* tiles;
   const Unit* units;
@@ -255,7 +322,6 @@ struct CountArgs {
   uint32_t n_items;
   uint32_t col_bits;
   // bucket filter
-  int filter;
   uint32_t kappa, start, stop;
   const uint32_t* h_row;
   const uint32_t* h_col;
@@ -265,6 +331,7 @@ struct CountArgs {
   uint32_t* out_count;
   unsigned long long* out_n;
   uint32_t* slabs;
+  unsigned int* tile_done;
 };
 
 __device__ __forceinline__ uint32_t lower_bound_items(const uint32_t* __restrict__ a, uint32_t lo,
@@ -296,6 +363,172 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   return r;
 }
 
+// Persistent CTAs pull units heavy-first. For each warp batch of 32 entries
+// the pairs are flattened across lanes: an inclusive scan of the per-entry
+// pair counts, then each iteration maps lane -> entry with a 32-bit boundary
+// mask (__reduce_or_sync) and popc, so every lane counts one pair per
+// iteration however the pairs split over entries. For single-row entries the
+// column position is t + delta[entry] (one shared load); the column item of
+// the next iteration is loaded before the current one is counted. The inner
+// loop is specialised per tile kind (chosen once per unit):
+//   kDenseRow    one row, all columns after it (UPPER) / all columns (full)
+//   kDenseWindow one row, columns [c0, c1)
+//   kDenseMulti  several rows, closed-form triangle (UPPER) / rectangle
+//   kHash        open-addressing keys (row - row0) << col_bits | col
+// A tile split over several units is reduced by the last unit to finish:
+// the others leave their counters in a slab (L2-resident by then) and the
+// last one adds them into its shared table before compacting.
+enum TileKind { kDenseRow = 0, kDenseWindow = 1, kDenseMulti = 2, kHash = 3 };
+
+struct WarpJobs {
+  uint32_t* delta;  // column position - flattened index (single-row entries)
+  uint32_t* excl;   // first flattened pair index of the entry
+  uint32_t* item;   // row item of the entry's first row
+  uint32_t* x;      // entry.x
+  uint32_t* y;      // entry.y
+};
+
+template <int KIND, bool UPPER, bool FILTER>
+__device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T, uint64_t e0,
+                                              uint64_t e1, const WarpJobs& J, uint32_t* table,
+                                              uint32_t* hcount) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* __restrict__ items = A.items;
+  const uint32_t n = A.n_items;
+  const uint32_t col_lo = UPPER ? T.row0 + 1 : 0;  // kDenseRow slot origin
+
+  auto count_pair = [&](uint32_t i, uint32_t j) {
+    if (KIND == kDenseRow || KIND == kDenseWindow) i = T.row0;  // single-row tiles
+    if (FILTER) {
+      uint32_t b = A.h_row[i] + A.h_col[j];
+      if (b >= A.kappa) b -= A.kappa;
+      if (b < A.start || b >= A.stop) return;
+    }
+    if (KIND == kDenseRow) {
+      atomicAdd(&table[j - col_lo], 1u);
+    } else if (KIND == kDenseWindow) {
+      atomicAdd(&table[j - T.c0], 1u);
+    } else if (KIND == kDenseMulti) {
+      const uint32_t slot = UPPER ? (uint32_t)tri_rowbase(i, T.row0, n) + (j - i - 1)
+                                  : (i - T.row0) * n + j;
+      atomicAdd(&table[slot], 1u);
+    } else {
+      const uint32_t key = ((i - T.row0) << A.col_bits) | j;
+      uint32_t s = __umulhi(mix32(key), kHashSlots);
+      for (;;) {
+        const uint32_t k = table[s];
+        if (k == key) {
+          atomicAdd(&hcount[s], 1u);
+          break;
+        }
+        if (k == kEmpty32) {
+          const uint32_t old = atomicCAS(&table[s], kEmpty32, key);
+          if (old == kEmpty32 || old == key) {
+            atomicAdd(&hcount[s], 1u);
+            break;
+          }
+        }
+        if (++s == kHashSlots) s = 0;
+      }
+    }
+  };
+  // rows > 1 only for UPPER runs in kDenseMulti / kHash tiles
+  constexpr bool MULTI = UPPER && (KIND == kDenseMulti || KIND == kHash);
+
+  for (uint64_t eb_w = e0 + (uint64_t)warp * 32; eb_w < e1; eb_w += (uint64_t)kCountWarps * 32) {
+    const uint64_t e = eb_w + lane;
+    uint32_t cnt = 0, x = 0, y = 0, first = 0, ri = 0;
+    if (e < e1) {
+      const uint2 en = A.entries[e];
+      x = en.x;
+      y = en.y;
+      if (UPPER) {
+        const uint32_t len = y & 0xFFFFu, rows = y >> 16;
+        if (KIND != kDenseRow && KIND != kDenseWindow) ri = items[x];
+        if (KIND == kDenseWindow) {
+          first = lower_bound_items(items, x + 1, x + len, T.c0);
+          cnt = lower_bound_items(items, first, x + len, T.c1) - first;
+        } else {
+          first = x + 1;
+          cnt = rows * (len - 1) - rows * (rows - 1) / 2;
+        }
+      } else {
+        const uint32_t L = y & 0xFFFFu, p = y >> 16;
+        ri = items[x + p];
+        if (KIND == kDenseWindow) {
+          first = lower_bound_items(items, x, x + L, T.c0);
+          cnt = lower_bound_items(items, first, x + L, T.c1) - first;
+        } else {
+          first = x;
+          cnt = L;
+        }
+      }
+    }
+    const uint32_t incl = warp_incl_scan(cnt);
+    const uint32_t excl = incl - cnt;
+    J.delta[lane] = first - excl;
+    J.excl[lane] = excl;
+    J.item[lane] = ri;
+    if (MULTI) {
+      J.x[lane] = x;
+      J.y[lane] = y;
+    }
+    const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    uint32_t owner_base = 0;
+    auto owner_of = [&](uint32_t t0) {
+      // entries ending strictly inside [t0, t0+32) move the owner forward
+      const uint32_t bit = (incl > t0 && incl < t0 + 32) ? (1u << (incl - t0)) : 0u;
+      const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
+      const uint32_t at_end = __reduce_add_sync(0xffffffffu, (incl == t0 + 32) ? 1u : 0u);
+      const uint32_t owner = owner_base + __popc(B & (0xffffffffu >> (31 - lane)));
+      owner_base += __popc(B) + at_end;
+      return owner;
+    };
+    // (row item, column item) of flattened pair t owned by entry `o`
+    auto locate_pair = [&](uint32_t t, uint32_t o, uint32_t& i, uint32_t& jpos) {
+      if (MULTI) {
+        const uint32_t yy = J.y[o];
+        if ((yy >> 16) > 1) {
+          uint32_t loc = t - J.excl[o], w = (yy & 0xFFFFu) - 1, k = 0;
+          while (loc >= w) {
+            loc -= w;
+            ++k;
+            --w;
+          }
+          const uint32_t xx = J.x[o];
+          i = k ? items[xx + k] : J.item[o];
+          jpos = xx + k + 1 + loc;
+          return;
+        }
+      }
+      if (KIND != kDenseRow && KIND != kDenseWindow) i = J.item[o];
+      jpos = t + J.delta[o];
+    };
+    uint32_t ci = 0, cjp = 0, cj = 0;
+    const uint32_t o0 = owner_of(0);  // warp-collective: outside any divergent branch
+    if (lane < S) {
+      locate_pair(lane, o0, ci, cjp);
+      cj = items[cjp];
+    }
+    for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+      const uint32_t tn = t0 + 32 + lane;
+      uint32_t ni = 0, njp = 0, nj = 0;
+      if (t0 + 32 < S) {  // warp-uniform
+        const uint32_t o = owner_of(t0 + 32);
+        if (tn < S) {
+          locate_pair(tn, o, ni, njp);
+          nj = items[njp];
+        }
+      }
+      if (t0 + lane < S) count_pair(ci, cj);
+      ci = ni;
+      cj = nj;
+    }
+    __syncwarp();
+  }
+}
+
 template <bool UPPER, bool FILTER>
 __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -307,13 +540,12 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
   __shared__ unsigned long long s_base;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // per-warp job arrays (struct of arrays, 32 lanes each)
-  uint32_t* j_base_lo = job + warp * 32 * 6;
-  uint32_t* j_L = j_base_lo + 32;
-  uint32_t* j_p = j_L + 32;      // p0 | p1 << 16
-  uint32_t* j_q = j_p + 32;      // q0 | q1 << 16 (windowed / full)
-  uint32_t* j_incl = j_q + 32;
-  uint32_t* j_base_hi = j_incl + 32;
+  WarpJobs J;
+  J.delta = job + warp * 32 * kJobWords;
+  J.excl = J.delta + 32;
+  J.item = J.excl + 32;
+  J.x = J.item + 32;
+  J.y = J.x + 32;
   const uint32_t n = A.n_items;
 
   for (;;) {
@@ -332,6 +564,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
     const bool single_row = T.row1 - T.row0 == 1;
     const bool windowed = single_row && (T.c0 != 0 || T.c1 != n);
     const uint32_t width = T.width;
+    const int kind = !dense ? kHash : windowed ? kDenseWindow : single_row ? kDenseRow : kDenseMulti;
 
     if (dense) {
       uint4* t4 = reinterpret_cast<uint4*>(table);
@@ -345,102 +578,46 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
     }
     __syncthreads();
 
-    for (uint64_t eb_w = e0 + (uint64_t)warp * 32; eb_w < e1; eb_w += (uint64_t)kCountWarps * 32) {
-      const uint64_t e = eb_w + lane;
-      uint32_t cnt = 0, p0 = 0, p1 = 0, q0 = 0, q1 = 0, L = 0;
-      int64_t base = 0;
-      if (e < e1) {
-        const uint2 en = A.entries[e];
-        base = A.offsets[en.x];
-        L = (uint32_t)(A.offsets[en.x + 1] - base);
-        p0 = en.y & 0xFFFFu;
-        p1 = en.y >> 16;
-        if (windowed || !UPPER) {
-          // columns: positions whose item lies in [c0, c1) (after the row when UPPER)
-          const uint32_t* it = A.items + base;
-          uint32_t lo = UPPER ? p0 + 1 : 0;
-          q0 = lower_bound_items(it, lo, L, T.c0);
-          q1 = lower_bound_items(it, q0, L, T.c1);
-          cnt = (p1 - p0) * (q1 - q0);
-        } else {
-          const uint32_t k = p1 - p0;
-          cnt = k * (L - 1) - (p0 + p1 - 1) * k / 2;
-        }
-      }
-      const uint32_t incl = warp_incl_scan(cnt);
-      j_base_lo[lane] = (uint32_t)base;
-      j_base_hi[lane] = (uint32_t)((uint64_t)base >> 32);
-      j_L[lane] = L;
-      j_p[lane] = p0 | (p1 << 16);
-      j_q[lane] = q0 | (q1 << 16);
-      j_incl[lane] = incl;
-      const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
-      __syncwarp();
-      uint32_t owner = 0;
-      for (uint32_t t = lane; t < S; t += 32) {
-        while (j_incl[owner] <= t) ++owner;
-        const uint32_t excl = owner ? j_incl[owner - 1] : 0;
-        uint32_t loc = t - excl;
-        const int64_t ob = (int64_t)(((uint64_t)j_base_hi[owner] << 32) | j_base_lo[owner]);
-        const uint32_t op = j_p[owner];
-        uint32_t r = op & 0xFFFFu, q;
-        if (windowed || !UPPER) {
-          const uint32_t oq = j_q[owner];
-          const uint32_t qa = oq & 0xFFFFu, ql = (oq >> 16) - qa;
-          r += loc / ql;
-          q = qa + loc % ql;
-        } else {
-          const uint32_t oL = j_L[owner];
-          uint32_t w = oL - 1 - r;
-          while (loc >= w) {
-            loc -= w;
-            ++r;
-            --w;
-          }
-          q = r + 1 + loc;
-        }
-        const uint32_t i = A.items[ob + r];
-        const uint32_t j = A.items[ob + q];
-        if (FILTER) {
-          uint32_t b = A.h_row[i] + A.h_col[j];
-          if (b >= A.kappa) b -= A.kappa;
-          if (b < A.start || b >= A.stop) continue;
-        }
-        if (dense) {
-          uint32_t slot;
-          if (single_row) slot = j - (UPPER ? max(T.c0, i + 1) : T.c0);
-          else if (UPPER) slot = (uint32_t)tri_rowbase(i, T.row0, n) + (j - i - 1);
-          else slot = (i - T.row0) * n + j;
-          atomicAdd(&table[slot], 1u);
-        } else {
-          const uint32_t key = ((i - T.row0) << A.col_bits) | j;
-          uint32_t s = __umulhi(mix32(key), kHashSlots);
-          for (;;) {
-            uint32_t k = table[s];
-            if (k == key) {
-              atomicAdd(&hcount[s], 1u);
-              break;
-            }
-            if (k == kEmpty32) {
-              uint32_t old = atomicCAS(&table[s], kEmpty32, key);
-              if (old == kEmpty32 || old == key) {
-                atomicAdd(&hcount[s], 1u);
-                break;
-              }
-            }
-            if (++s == kHashSlots) s = 0;
-          }
-        }
-      }
-      __syncwarp();
+    switch (kind) {
+      case kDenseRow:
+        count_entries<kDenseRow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        break;
+      case kDenseWindow:
+        count_entries<kDenseWindow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        break;
+      case kDenseMulti:
+        count_entries<kDenseMulti, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        break;
+      default:
+        count_entries<kHash, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        break;
     }
     __syncthreads();
 
+    bool emit_now = true;
     if (dense && T.n_units > 1) {
+      // leave this unit's counters in its slab; the last unit reduces them
       uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * kDenseCap);
       const uint4* src = reinterpret_cast<const uint4*>(table);
       for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads) dst[s] = src[s];
-    } else {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_misc[1] = atomicAdd(&A.tile_done[unit.tile], 1u) == T.n_units - 1;
+      __syncthreads();
+      emit_now = s_misc[1] != 0;
+      if (emit_now) {
+        __threadfence();
+        const uint32_t* slab = A.slabs + T.slab_base * kDenseCap;
+        for (uint32_t s = threadIdx.x; s < width; s += kCountThreads) {
+          uint32_t c = table[s];
+          for (uint32_t v = 0; v < T.n_units; ++v)
+            if (v != unit.local) c += __ldcg(slab + (uint64_t)v * kDenseCap + s);
+          table[s] = c;
+        }
+        __syncthreads();
+      }
+    }
+    if (emit_now) {
       // compact non-zero counters: warp w owns a contiguous slot range
       const uint32_t slots = dense ? width : kHashSlots;
       const uint32_t per_warp = (slots + kCountWarps - 1) / kCountWarps;
@@ -461,13 +638,16 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
           if (dense) {
             c = table[s];
             if (c) {
-              if (single_row) {
+              if (windowed) {
                 i = T.row0;
-                j = s + (UPPER ? max(T.c0, i + 1) : T.c0);
+                j = s + T.c0;
+              } else if (single_row) {
+                i = T.row0;
+                j = UPPER ? s + i + 1 : s;
               } else if (UPPER) {
                 uint32_t lo = T.row0, hi = T.row1;  // last row with rowbase <= s
                 while (hi - lo > 1) {
-                  uint32_t mid = (lo + hi) >> 1;
+                  const uint32_t mid = (lo + hi) >> 1;
                   if (tri_rowbase(mid, T.row0, n) <= s) lo = mid;
                   else hi = mid;
                 }
@@ -501,92 +681,10 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
   }
 }
 
-// ------------------------------------------------------------- reduce
-struct ReduceArgs {
-  const Tile* tiles;
-  const uint32_t* split_tiles;  // ids of multi-unit dense tiles
-  uint32_t n_split;
-  const uint32_t* slabs;
-  uint32_t n_items;
-  uint32_t* out_row;
-  uint32_t* out_col;
-  uint32_t* out_count;
-  unsigned long long* out_n;
-};
-
-constexpr int kReduceThreads = 1024;
-constexpr uint32_t kReduceChunk = 16384;  // slots per block
-
-template <bool UPPER>
-__global__ void __launch_bounds__(kReduceThreads) k_slab_reduce(ReduceArgs A) {
-  __shared__ uint32_t s_warp[33];
-  __shared__ unsigned long long s_base;
-  const uint32_t chunks_per_tile = (kDenseCap + kReduceChunk - 1) / kReduceChunk;
-  const uint32_t tile_id = A.split_tiles[blockIdx.x / chunks_per_tile];
-  const uint32_t chunk = blockIdx.x % chunks_per_tile;
-  const Tile T = A.tiles[tile_id];
-  const uint32_t n = A.n_items;
-  const uint32_t lo = chunk * kReduceChunk;
-  const uint32_t hi = min(T.width, lo + kReduceChunk);
-  if (lo >= hi) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t per_warp = (hi - lo + 31) / 32;
-  const uint32_t s_lo = min(hi, lo + warp * per_warp), s_hi = min(hi, s_lo + per_warp);
-  const uint32_t* slab = A.slabs + T.slab_base * kDenseCap;
-  auto sum_at = [&](uint32_t s) {
-    uint32_t c = 0;
-    for (uint32_t u = 0; u < T.n_units; ++u) c += slab[(uint64_t)u * kDenseCap + s];
-    return c;
-  };
-  uint32_t mine = 0;
-  for (uint32_t s = s_lo + lane; s < s_hi; s += 32) mine += sum_at(s) != 0;
-  mine = warp_sum(mine);
-  uint32_t total;
-  uint32_t wbase = block_excl_scan(lane == 0 ? mine : 0, s_warp, total);
-  wbase = __shfl_sync(0xffffffffu, wbase, 0);
-  if (threadIdx.x == 0) s_base = atomicAdd(A.out_n, (unsigned long long)total);
-  __syncthreads();
-  uint64_t pos = s_base + wbase;
-  const bool single_row = T.row1 - T.row0 == 1;
-  for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-    const uint32_t s = s0 + lane;
-    uint32_t c = 0, i = 0, j = 0;
-    if (s < s_hi) {
-      c = sum_at(s);
-      if (c) {
-        if (single_row) {
-          i = T.row0;
-          j = s + (UPPER ? max(T.c0, i + 1) : T.c0);
-        } else if (UPPER) {
-          uint32_t a = T.row0, b = T.row1;
-          while (b - a > 1) {
-            uint32_t mid = (a + b) >> 1;
-            if (tri_rowbase(mid, T.row0, n) <= s) a = mid;
-            else b = mid;
-          }
-          i = a;
-          j = (uint32_t)(s - tri_rowbase(i, T.row0, n)) + i + 1;
-        } else {
-          i = T.row0 + s / n;
-          j = s % n;
-        }
-      }
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, c != 0);
-    if (c) {
-      const uint64_t o = pos + __popc(m & ((1u << lane) - 1u));
-      A.out_row[o] = i;
-      A.out_col[o] = j;
-      A.out_count[o] = c;
-    }
-    pos += __popc(m);
-  }
-}
-
-__global__ void k_exclusive_scan_u32_to_u64(const uint32_t* __restrict__ in, uint32_t n,
+__global__ void __launch_bounds__(1024) k_exclusive_scan_u32_to_u64(const uint32_t* __restrict__ in, uint32_t n,
                                             unsigned long long* __restrict__ out,
                                             unsigned long long* __restrict__ total) {
-  // single block, 1024 threads; n up to a few million (tiles)
+  // single block, 1024 threads
   __shared__ unsigned long long s_part[1024];
   const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
   const uint32_t lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
@@ -594,14 +692,21 @@ __global__ void k_exclusive_scan_u32_to_u64(const uint32_t* __restrict__ in, uin
   for (uint32_t i = lo; i < hi; ++i) acc += in[i];
   s_part[threadIdx.x] = acc;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0 scans the 1024 partials, 32 per lane
     unsigned long long run = 0;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      unsigned long long v = s_part[t];
-      s_part[t] = run;
-      run += v;
+    for (int k = 0; k < 32; ++k) run += s_part[threadIdx.x * 32 + k];
+    unsigned long long x = run;
+    for (int d = 1; d < 32; d <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+      if ((int)threadIdx.x >= d) x += y;
     }
-    *total = run;
+    unsigned long long acc = x - run;
+    for (int k = 0; k < 32; ++k) {
+      const unsigned long long v = s_part[threadIdx.x * 32 + k];
+      s_part[threadIdx.x * 32 + k] = acc;
+      acc += v;
+    }
+    if (threadIdx.x == 31) *total = x;
   }
   __syncthreads();
   unsigned long long run = s_part[threadIdx.x];
@@ -619,6 +724,7 @@ struct crop_pairs {
   const int64_t* offsets;
   const uint32_t* items;
   int64_t n_tx;
+  int64_t nnz;
   uint32_t n_items;
   int upper;
   bool filter;
@@ -627,11 +733,12 @@ struct crop_pairs {
   uint64_t total_terms;
   uint64_t max_entries;
   uint64_t entry_cap;
+  cudaStream_t stream;
   std::vector<Tile> tiles;
   std::vector<Unit> units;
   std::vector<uint32_t> split;
   uint64_t n_slabs;
-  // device
+  // device (stream-ordered pool)
   unsigned long long* d_terms = nullptr;
   unsigned int* d_maxlen = nullptr;
   uint32_t* d_item_tile = nullptr;
@@ -646,23 +753,16 @@ struct crop_pairs {
   uint32_t* d_slabs = nullptr;
   unsigned int* d_unit_counter = nullptr;
   uint32_t* d_overflow = nullptr;
+  unsigned int* d_tile_done = nullptr;
+  std::vector<uint32_t> h_item_tile;  // kept alive for the async uploads
 };
 
 static void free_job(crop_pairs* j) {
-  cudaFree(j->d_terms);
-  cudaFree(j->d_maxlen);
-  cudaFree(j->d_item_tile);
-  cudaFree(j->d_tiles);
-  cudaFree(j->d_units);
-  cudaFree(j->d_split);
-  cudaFree(j->d_tile_entries);
-  cudaFree(j->d_tile_ebase);
-  cudaFree(j->d_tile_cursor);
-  cudaFree(j->d_total_entries);
-  cudaFree(j->d_entries);
-  cudaFree(j->d_slabs);
-  cudaFree(j->d_unit_counter);
-  cudaFree(j->d_overflow);
+  void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_tiles, j->d_units, j->d_split,
+                  j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_total_entries,
+                  j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, j->stream);
 }
 
 // Greedy tile planner over rows in id order (see file header).
@@ -679,9 +779,11 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     bool dense_ok, hash_ok;
   };
   std::vector<Tile> tiles;
-  std::vector<std::vector<uint32_t>> group_rows_tile;  // not needed
   item_tile.assign(n, kNone);
   auto width_of = [&](uint32_t i) -> uint64_t { return upper ? (uint64_t)(n - 1 - i) : n; };
+  auto units_for = [&](uint64_t terms_) {
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(4096, (terms_ + unit_terms - 1) / unit_terms));
+  };
 
   bool open = false;
   Group g{};
@@ -692,14 +794,13 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     t.row1 = g.row1;
     t.c0 = 0;
     t.c1 = n;
-    bool dense = g.dense_ok && (!g.hash_ok || g.st * 8 >= g.sw);
+    const bool dense = g.dense_ok && (!g.hash_ok || g.st * 8 >= g.sw);
     t.mode = dense ? 0 : 1;
     t.nwin = 0;
     t.width = dense ? (uint32_t)g.sw : 0;
     t.terms = g.st;
-    t.n_units = dense ? (uint32_t)std::min<uint64_t>(4096, (g.st + unit_terms - 1) / unit_terms) : 1;
-    if (t.n_units == 0) t.n_units = 1;
-    uint32_t id = (uint32_t)tiles.size();
+    t.n_units = dense ? units_for(g.st) : 1;
+    const uint32_t id = (uint32_t)tiles.size();
     for (uint32_t i = g.row0; i < g.row1; ++i)
       if (terms[i]) item_tile[i] = id;
     tiles.push_back(t);
@@ -710,9 +811,9 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     const uint64_t w = width_of(i);
     const uint64_t b = std::min<uint64_t>(w, tm);
     if (open) {
-      bool d_ok = g.dense_ok && g.sw + w <= kDenseCap;
-      bool h_ok = g.hash_ok && g.sb + b <= kHashCap && g.st + tm <= unit_terms &&
-                  (g.row1 - g.row0 + 1) <= hash_rows_max;
+      const bool d_ok = g.dense_ok && g.sw + w <= kDenseCap;
+      const bool h_ok = g.hash_ok && g.sb + b <= kHashCap && g.st + tm <= unit_terms &&
+                        (g.row1 - g.row0 + 1) <= hash_rows_max;
       if (d_ok || h_ok) {
         g.row1 = i + 1;
         g.sw += w;
@@ -732,8 +833,8 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
       g = Group{i, i + 1, w, b, tm, d_ok, h_ok};
       continue;
     }
-    // single row too wide for a dense tile and too heavy for a hash tile:
-    // column windows of kDenseCap counters, consecutive tile ids.
+    // one row too wide for a dense tile and too heavy for a hash tile:
+    // column windows of kDenseCap counters with consecutive tile ids.
     const uint32_t col_lo = upper ? i + 1 : 0;
     const uint32_t nwin = (uint32_t)((w + kDenseCap - 1) / kDenseCap);
     const uint32_t first = (uint32_t)tiles.size();
@@ -747,42 +848,39 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
       t.nwin = k == 0 ? nwin : 0;
       t.width = t.c1 - t.c0;
       t.terms = tm / nwin + 1;
-      t.n_units = (uint32_t)std::min<uint64_t>(4096, (t.terms + unit_terms - 1) / unit_terms);
-      if (t.n_units == 0) t.n_units = 1;
+      t.n_units = units_for(t.terms);
       tiles.push_back(t);
     }
-    // window 0 must start at col_lo for the router's window arithmetic
-    item_tile[i] = first;
+    item_tile[i] = first | kWinFlag;
   }
   close();
 
-  // Renumber heavy-first (router keeps the heaviest tiles in shared memory);
-  // a split row's windows stay consecutive.
-  std::vector<uint32_t> groups;  // first tile of each group
+  // Renumber heavy-first (the router keeps the heaviest tiles in shared
+  // memory); a split row's windows stay consecutive.
+  std::vector<uint32_t> groups;
   for (uint32_t t = 0; t < tiles.size();) {
     groups.push_back(t);
     t += tiles[t].nwin ? tiles[t].nwin : 1;
   }
-  auto group_terms = [&](uint32_t t) {
-    uint64_t s = 0;
-    uint32_t k = tiles[t].nwin ? tiles[t].nwin : 1;
-    for (uint32_t q = 0; q < k; ++q) s += tiles[t + q].terms;
-    return s;
-  };
+  std::vector<uint64_t> gterms(tiles.size(), 0);
+  for (uint32_t g0 : groups) {
+    const uint32_t k = tiles[g0].nwin ? tiles[g0].nwin : 1;
+    for (uint32_t q = 0; q < k; ++q) gterms[g0] += tiles[g0 + q].terms;
+  }
   std::stable_sort(groups.begin(), groups.end(),
-                   [&](uint32_t a, uint32_t b) { return group_terms(a) > group_terms(b); });
+                   [&](uint32_t a, uint32_t b) { return gterms[a] > gterms[b]; });
   std::vector<uint32_t> new_id(tiles.size());
   std::vector<Tile> out;
   out.reserve(tiles.size());
   for (uint32_t g0 : groups) {
-    uint32_t k = tiles[g0].nwin ? tiles[g0].nwin : 1;
+    const uint32_t k = tiles[g0].nwin ? tiles[g0].nwin : 1;
     for (uint32_t q = 0; q < k; ++q) {
       new_id[g0 + q] = (uint32_t)out.size();
       out.push_back(tiles[g0 + q]);
     }
   }
   for (uint32_t i = 0; i < n; ++i)
-    if (item_tile[i] != kNone) item_tile[i] = new_id[item_tile[i]];
+    if (item_tile[i] != kNone) item_tile[i] = new_id[item_tile[i] & ~kWinFlag] | (item_tile[i] & kWinFlag);
   J->tiles.swap(out);
 
   // units heavy-first; slabs for split dense tiles
@@ -816,6 +914,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     return CROP_EINPUT;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (int rc = crop_pool_setup()) return rc;
   crop_pairs* J = new crop_pairs();
   J->offsets = offsets;
   J->items = items;
@@ -823,6 +922,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
   J->n_items = n_items;
   J->upper = upper_only;
   J->filter = false;
+  J->stream = st;
   if (interval) {
     J->iv = *interval;
     if (interval->kappa == 0 || interval->start > interval->stop || interval->stop > interval->kappa) {
@@ -849,19 +949,19 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
   } while (0)
   {
     const uint32_t nn = std::max<uint32_t>(n_items, 1);
-    JCUDA(cudaMalloc(&J->d_terms, nn * sizeof(unsigned long long)));
-    JCUDA(cudaMalloc(&J->d_maxlen, sizeof(unsigned int)));
+    JCUDA(cudaMallocAsync(&J->d_terms, nn * sizeof(unsigned long long), st));
+    JCUDA(cudaMallocAsync(&J->d_maxlen, sizeof(unsigned int), st));
     JCUDA(cudaMemsetAsync(J->d_terms, 0, nn * sizeof(unsigned long long), st));
     JCUDA(cudaMemsetAsync(J->d_maxlen, 0, sizeof(unsigned int), st));
     if (n_tx > 0 && n_items > 0) {
       auto kern = upper_only ? k_item_terms<true> : k_item_terms<false>;
       const uint32_t ns = std::min<uint32_t>(n_items, kStatSmemItems);
+      const size_t smem = kOffBytes + ns * 4;
       JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kStatSmemItems * 4)));
-      int64_t grid = std::max<int64_t>(2 * kNumSMs, (n_tx + 32767) / 32768);
-      grid = std::min<int64_t>(grid, (n_tx + 15) / 16);
-      if (grid < 1) grid = 1;
-      kern<<<(int)grid, 512, ns * 4, st>>>(offsets, items, n_tx, n_items, J->d_terms, J->d_maxlen);
+                                 (int)(kOffBytes + kStatSmemItems * 4)));
+      const int64_t chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+      const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
+      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, J->d_terms, J->d_maxlen);
       JCUDA(cudaGetLastError());
     }
     std::vector<unsigned long long> terms(nn);
@@ -871,26 +971,34 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     JCUDA(cudaMemcpyAsync(&maxlen, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
     if (n_tx > 0) JCUDA(cudaMemcpyAsync(&nnz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
     JCUDA(cudaStreamSynchronize(st));
+    J->nnz = nnz;
     if (maxlen > kMaxLen) {
       crop_set_error(CROP_EINPUT, "transaction of %u items exceeds the %u-item limit", maxlen, kMaxLen);
       rc = CROP_EINPUT;
       goto fail;
     }
+    if ((uint64_t)nnz >= (1ull << 32)) {
+      crop_set_error(CROP_EINPUT, "%lld item occurrences exceed the 2^32 limit of one job; "
+                     "split the stream", (long long)nnz);
+      rc = CROP_EINPUT;
+      goto fail;
+    }
     J->total_terms = 0;
     for (uint32_t i = 0; i < n_items; ++i) J->total_terms += terms[i];
-    std::vector<uint32_t> item_tile;
+    std::vector<uint32_t>& item_tile = J->h_item_tile;
     plan_tiles(J, terms, item_tile);
     const uint32_t nt = (uint32_t)J->tiles.size();
-    JCUDA(cudaMalloc(&J->d_item_tile, nn * 4));
-    JCUDA(cudaMalloc(&J->d_tiles, std::max<size_t>(1, nt) * sizeof(Tile)));
-    JCUDA(cudaMalloc(&J->d_units, std::max<size_t>(1, J->units.size()) * sizeof(Unit)));
-    JCUDA(cudaMalloc(&J->d_split, std::max<size_t>(1, J->split.size()) * 4));
-    JCUDA(cudaMalloc(&J->d_tile_entries, std::max<size_t>(1, nt) * 4));
-    JCUDA(cudaMalloc(&J->d_tile_ebase, std::max<size_t>(1, nt) * 8));
-    JCUDA(cudaMalloc(&J->d_tile_cursor, std::max<size_t>(1, nt) * 8));
-    JCUDA(cudaMalloc(&J->d_total_entries, 8));
-    JCUDA(cudaMalloc(&J->d_unit_counter, 4));
-    JCUDA(cudaMalloc(&J->d_overflow, 4));
+    JCUDA(cudaMallocAsync(&J->d_item_tile, nn * 4, st));
+    JCUDA(cudaMallocAsync(&J->d_tiles, std::max<size_t>(1, nt) * sizeof(Tile), st));
+    JCUDA(cudaMallocAsync(&J->d_units, std::max<size_t>(1, J->units.size()) * sizeof(Unit), st));
+    JCUDA(cudaMallocAsync(&J->d_split, std::max<size_t>(1, J->split.size()) * 4, st));
+    JCUDA(cudaMallocAsync(&J->d_tile_entries, std::max<size_t>(1, nt) * 4, st));
+    JCUDA(cudaMallocAsync(&J->d_tile_ebase, std::max<size_t>(1, nt) * 8, st));
+    JCUDA(cudaMallocAsync(&J->d_tile_cursor, std::max<size_t>(1, nt) * 8, st));
+    JCUDA(cudaMallocAsync(&J->d_total_entries, 8, st));
+    JCUDA(cudaMallocAsync(&J->d_unit_counter, 4, st));
+    JCUDA(cudaMallocAsync(&J->d_overflow, 4, st));
+    JCUDA(cudaMallocAsync(&J->d_tile_done, std::max<size_t>(1, nt) * 4, st));
     JCUDA(cudaMemsetAsync(J->d_overflow, 0, 4, st));
     if (n_items) JCUDA(cudaMemcpyAsync(J->d_item_tile, item_tile.data(), n_items * 4, cudaMemcpyHostToDevice, st));
     if (nt) JCUDA(cudaMemcpyAsync(J->d_tiles, J->tiles.data(), nt * sizeof(Tile), cudaMemcpyHostToDevice, st));
@@ -898,15 +1006,15 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       JCUDA(cudaMemcpyAsync(J->d_units, J->units.data(), J->units.size() * sizeof(Unit), cudaMemcpyHostToDevice, st));
     if (!J->split.empty())
       JCUDA(cudaMemcpyAsync(J->d_split, J->split.data(), J->split.size() * 4, cudaMemcpyHostToDevice, st));
-    if (J->n_slabs) JCUDA(cudaMalloc(&J->d_slabs, J->n_slabs * (size_t)kDenseCap * 4));
-    // entry capacity: every entry has >= 1 term, and a run never spans more
-    // positions than the transaction, so entries <= min(total terms, nnz*windows)
-    // is loose; use terms bounded by nnz * max windows.
+    if (J->n_slabs) JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kDenseCap * 4, st));
+    // every entry carries >= 1 term and a position emits at most one entry
+    // per column window, so entries <= min(total terms, nnz * max windows)
     uint64_t maxwin = 1;
     for (auto& t : J->tiles) maxwin = std::max<uint64_t>(maxwin, t.nwin);
     J->entry_cap = std::min<uint64_t>(J->total_terms, (uint64_t)nnz * maxwin);
-    if (J->entry_cap >= (1ull << 32)) J->entry_cap = (1ull << 32) - 1;  // positions are 32-bit in smem
-    JCUDA(cudaMalloc(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2)));
+    if (J->entry_cap >= (1ull << 32)) J->entry_cap = (1ull << 32) - 1;
+    JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
+    // host vectors read by the async uploads live in J until destroy
   }
 #undef JCUDA
   *job = J;
@@ -933,15 +1041,19 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMemsetAsync(d_n_entries, 0, 8, st));
   if (nt == 0 || J->n_tx == 0) return CROP_OK;
   const bool up = J->upper != 0;
+  const int64_t chunks = (J->n_tx + kChunkTx - 1) / kChunkTx;
+  const int pass_grid = (int)std::min<int64_t>(kNumSMs, chunks);
+  const uint32_t ns = std::min(nt, kTileSmem);
+  const size_t route_smem = kOffBytes + ns * 4;
   // pass B1: entries per tile
   CROP_CUDA(cudaMemsetAsync(J->d_tile_entries, 0, nt * 4, st));
   {
     auto kern = up ? k_route_count<true> : k_route_count<false>;
-    CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTileSmem * 4)));
-    const uint32_t ns = std::min(nt, kTileSmem);
-    int grid = 2 * kNumSMs;
-    kern<<<grid, kRouteThreads, ns * 4, st>>>(J->offsets, J->items, J->n_tx, J->d_item_tile,
-                                              J->d_tiles, nt, J->d_tile_entries);
+    CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kOffBytes + kTileSmem * 4)));
+    kern<<<pass_grid, kPassThreads, route_smem, st>>>(J->offsets, J->items, J->n_tx,
+                                                      J->d_item_tile, J->d_tiles, nt,
+                                                      J->d_tile_entries);
     CROP_LAUNCH_CHECK();
   }
   k_exclusive_scan_u32_to_u64<<<1, 1024, 0, st>>>(J->d_tile_entries, nt, J->d_tile_ebase,
@@ -950,19 +1062,19 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMemcpyAsync(J->d_tile_cursor, J->d_tile_ebase, nt * 8, cudaMemcpyDeviceToDevice, st));
   {
     auto kern = up ? k_route_write<true> : k_route_write<false>;
-    CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTileSmem * 4)));
-    const uint32_t ns = std::min(nt, kTileSmem);
-    int64_t grid = std::min<int64_t>(4 * kNumSMs, std::max<int64_t>(1, J->n_tx / 64));
-    kern<<<(int)grid, kRouteThreads, ns * 4, st>>>(J->offsets, J->items, J->n_tx, J->d_item_tile,
-                                                   J->d_tiles, nt, J->d_tile_cursor, J->d_entries,
-                                                   J->entry_cap, J->d_overflow);
+    CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kOffBytes + kTileSmem * 4)));
+    kern<<<pass_grid, kPassThreads, route_smem, st>>>(J->offsets, J->items, J->n_tx,
+                                                      J->d_item_tile, J->d_tiles, nt,
+                                                      J->d_tile_cursor, J->d_entries,
+                                                      J->entry_cap, J->d_overflow);
     CROP_LAUNCH_CHECK();
   }
   // count
   CROP_CUDA(cudaMemsetAsync(J->d_unit_counter, 0, 4, st));
+  CROP_CUDA(cudaMemsetAsync(J->d_tile_done, 0, nt * 4, st));
   {
     CountArgs A{};
-    A.offsets = J->offsets;
     A.items = J->items;
     A.tiles = J->d_tiles;
     A.units = J->d_units;
@@ -973,7 +1085,6 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     A.unit_counter = J->d_unit_counter;
     A.n_items = J->n_items;
     A.col_bits = J->col_bits;
-    A.filter = J->filter;
     A.kappa = J->iv.kappa;
     A.start = J->iv.start;
     A.stop = J->iv.stop;
@@ -984,30 +1095,23 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     A.out_count = out_count;
     A.out_n = (unsigned long long*)d_n_entries;
     A.slabs = J->d_slabs;
+    A.tile_done = J->d_tile_done;
     void (*kern)(CountArgs);
     if (up) kern = J->filter ? k_count<true, true> : k_count<true, false>;
     else kern = J->filter ? k_count<false, true> : k_count<false, false>;
     CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCountSmem));
-    int grid = std::min<int>(kNumSMs, (int)J->units.size());
+    const int grid = std::min<int>(kNumSMs, (int)J->units.size());
     kern<<<grid, kCountThreads, kCountSmem, st>>>(A);
     CROP_LAUNCH_CHECK();
   }
-  if (!J->split.empty()) {
-    ReduceArgs R{};
-    R.tiles = J->d_tiles;
-    R.split_tiles = J->d_split;
-    R.n_split = (uint32_t)J->split.size();
-    R.slabs = J->d_slabs;
-    R.n_items = J->n_items;
-    R.out_row = out_row;
-    R.out_col = out_col;
-    R.out_count = out_count;
-    R.out_n = (unsigned long long*)d_n_entries;
-    const uint32_t chunks = (kDenseCap + kReduceChunk - 1) / kReduceChunk;
-    auto kern = up ? k_slab_reduce<true> : k_slab_reduce<false>;
-    kern<<<R.n_split * chunks, kReduceThreads, 0, st>>>(R);
-    CROP_LAUNCH_CHECK();
-  }
+  return CROP_OK;
+}
+
+extern "C" int crop_pairs_overflowed(const crop_pairs* J, int* overflowed) {
+  uint32_t h = 0;
+  CROP_CUDA(cudaMemcpyAsync(&h, J->d_overflow, 4, cudaMemcpyDeviceToHost, J->stream));
+  CROP_CUDA(cudaStreamSynchronize(J->stream));
+  *overflowed = h != 0;
   return CROP_OK;
 }
 

@@ -42,9 +42,16 @@ __global__ void __launch_bounds__(kHistThreads)
   for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x) s_hist[b] = 0;
   __syncthreads();
   const uint64_t n = *d_n;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
-       e += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(&s_hist[count_bin(count[e])], 1u);
+  // counts are heavily repeated (most entries have small counts): aggregate
+  // equal bins inside the warp before touching shared memory
+  const uint64_t n_round = (n + 31) & ~31ull;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_round;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = e < n ? count_bin(count[e]) : 0xFFFFFFFFu;
+    const uint32_t grp = __match_any_sync(0xffffffffu, b);
+    if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (int)(threadIdx.x & 31))
+      atomicAdd(&s_hist[b], (uint32_t)__popc(grp));
+  }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x)
     if (s_hist[b]) atomicAdd(&hist[b], s_hist[b]);
@@ -242,6 +249,7 @@ extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_
                          const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k,
                          uint64_t* out_idx, uint64_t* d_k_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (int rc = crop_pool_setup()) return rc;
   uint32_t* hist = nullptr;
   unsigned long long* state = nullptr;
   uint64_t* cand = nullptr;

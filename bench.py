@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py -- outer-product terms counted per second on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+A step is one pass of the hot path over the whole synthetic workload of the
+configuration (default c2 = BASELINE.json configs[1], the 1-GPU exact pair
+count): per-item term scan + tile plan, routing, shared-memory counting of
+every pair term (i < j) of the GPU's bucket interval, and the top-k select.
+Inputs are resident in HBM; L2 is flushed (1 GiB write) before every timed
+step. `value` = all terms of the workload / (max over ranks of the summed
+per-step CUDA-event time). `e2e` runs the public API (`crop.run` +
+`SketchState.top_entries`) from pinned host buffers, host<->device copies
+inside the timed region. `roofline` is the dominant kernel (k_count), timed
+live with CUDA events on its stream. `cpu_baseline` is the C oracle (the
+reference algorithm restated, oracle/crop_oracle.c) on a bounded prefix,
+shared-nothing threads on every host core.
+
+Under torchrun (N > 1) rank 0 generates the workload and broadcasts it once
+over NCCL; rank r counts the buckets split(kappa, N)[r] (no communication);
+local top-k candidates are all-gathered and merged on rank 0.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "outer-product terms counted/sec at 1/2/4/8 B200; % of HBM roofline"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--cpu-sample-tx", type=int, default=None,
+                    help="transactions in the CPU-baseline sample (default per config)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(parts) >= 9:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def ncu_traffic(kernel: str, config: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d[config][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ workload
+
+def load_workload(cfg, rank, world):
+    """Device transactions on every rank (rank 0 generates, NCCL broadcast)."""
+    import torch
+
+    from paper_1210_0461_b200 import kernels, workloads
+
+    if world == 1:
+        return workloads.generate_pairs_workload(cfg), 0.0
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if rank == 0:
+        dtx = workloads.generate_pairs_workload(cfg)
+        sizes = torch.tensor([dtx.n_tx, dtx.nnz], dtype=torch.int64, device=dev)
+    else:
+        sizes = torch.zeros(2, dtype=torch.int64, device=dev)
+    dist.broadcast(sizes, 0)
+    n_tx, nnz = int(sizes[0]), int(sizes[1])
+    if rank != 0:
+        dtx = kernels.DeviceTransactions(torch.empty(n_tx + 1, dtype=torch.int64, device=dev),
+                                         torch.empty(nnz, dtype=torch.int32, device=dev),
+                                         cfg.n_items)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    dist.broadcast(dtx.offsets, 0)
+    dist.broadcast(dtx.items, 0)
+    torch.cuda.synchronize()
+    return dtx, time.perf_counter() - t0
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank, world):
+    import numpy as np
+    import torch
+
+    import paper_1210_0461_b200 as crop
+    from paper_1210_0461_b200 import kernels, workloads
+
+    cfg = workloads.CONFIGS[args.config]
+    if not isinstance(cfg, workloads.PairConfig):
+        raise SystemExit(f"bench.py measures pair configs; {args.config} is a product config")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dtx, bcast_s = load_workload(cfg, rank, world)
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
+                               cs_enabled=False, seed=0)
+    hasher = crop.make_hashes(crop.HashConfig(cfg.kappa, config.instance_seeds()[0]))
+    if world > cfg.kappa:
+        raise SystemExit(f"{world} GPUs > kappa={cfg.kappa} buckets")
+    asg = crop.WorkerAssignment.split(cfg.kappa, world)[rank]
+    tables = kernels.hash_tables(hasher, cfg.n_items)
+    interval = None
+    if world > 1:
+        interval = kernels.interval_struct(cfg.kappa, asg.start, asg.stop, *tables)
+    flush = torch.empty(1 << 28, dtype=torch.int32, device=dev)  # 1 GiB > 126 MB L2
+
+    def step():
+        job = kernels.PairCountJob(dtx, True, interval, keep=tables)
+        job.set_timing(True)
+        ent = job.run(sync=True)
+        idx = kernels.topk_indices(ent, cfg.top_k)
+        top = (ent.row[idx], ent.col[idx], ent.count[idx])
+        if world > 1:
+            import torch.distributed as dist
+
+            k = cfg.top_k
+            buf = torch.full((3, k), -1, dtype=torch.int32, device=dev)
+            m = idx.shape[0]
+            buf[0, :m], buf[1, :m], buf[2, :m] = top
+            allb = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(allb, buf)
+            top = torch.cat(allb, dim=1)
+        phases = job.phase_ms()
+        stats = (job.total_terms, ent.n, job.n_tiles, job.n_units)
+        job.close()
+        return phases, stats, top
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    step_ms, count_ms, phase_log = [], [], []
+    launches0 = kernels.launch_counter()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        for k in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev[k][0].record()
+            phases, stats, top = step()
+            ev[k][1].record()
+            torch.cuda.synchronize()
+            step_ms.append(ev[k][0].elapsed_time(ev[k][1]))
+            count_ms.append(phases["count"])
+            phase_log.append(phases)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = kernels.launch_counter() - launches0
+    total_terms_all = int(((dtx.offsets[1:] - dtx.offsets[:-1]) *
+                           (dtx.offsets[1:] - dtx.offsets[:-1] - 1) // 2).sum().item())
+    t_sum = sum(step_ms)
+    own_terms, own_entries = None, stats[1]
+    if world > 1:
+        t = torch.tensor([t_sum], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_sum = float(t.item())
+    ms_per_step = t_sum / args.steps
+    value = total_terms_all * args.steps / (t_sum * 1e-3)
+
+    # roofline of the dominant kernel (k_count): 8 B per term
+    # (one 4-byte counter read + write) + 12 B per output entry; own terms =
+    # terms of this rank's buckets = the sum of its output counts
+    if world > 1:
+        job = kernels.PairCountJob(dtx, True, interval, keep=tables)
+        ent = job.run()
+        own_terms = int(ent.weights_f64().sum().item())
+        job.close()
+    else:
+        own_terms = total_terms_all
+    b_alg = 8 * own_terms + 12 * own_entries
+    count_avg = statistics.mean(count_ms)
+    peak, peak_src = peaks()
+    achieved = b_alg / (count_avg * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_count", "achieved": round(achieved, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": ncu_traffic("k_count", args.config), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": b_alg, "avg_launch_ms": round(count_avg, 4),
+                "phase_ms_avg": {k: round(statistics.mean(p[k] for p in phase_log), 4)
+                                 for k in phase_log[0]}}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, dtx, rank, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, cfg, dtx)
+
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": value, "unit": "terms/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: seeded Zipf transactions (SURVEY.md §8d, data seed = config no.)",
+            "config": {"workload": cfg.name, "n_tx": cfg.n_tx, "n_items": cfg.n_items,
+                       "zipf_s": cfg.zipf_s, "length": list(cfg.length), "kappa": cfg.kappa,
+                       "buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})", "top_k": cfg.top_k,
+                       "terms": total_terms_all, "entries": own_entries if world == 1 else None,
+                       "tiles": stats[2], "units": stats[3], "parallelism": f"buckets{world}",
+                       "l2": "flushed (1 GiB write) before every timed step",
+                       "broadcast_s": round(bcast_s, 4)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, cfg, dtx, rank, world):
+    """Public API from pinned host buffers: H2D, count, top-k, D2H inside."""
+    import numpy as np
+    import torch
+
+    import paper_1210_0461_b200 as crop
+
+    off_h = dtx.offsets.cpu().pin_memory()
+    it_h = dtx.items.cpu().pin_memory()
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
+                               cs_enabled=False, seed=0)
+    off_np, it_np = off_h.numpy(), it_h.numpy().view(np.uint32)
+    total_terms = None
+
+    def once():
+        stream = crop.TransactionStream(cfg.n_items, off_np, it_np, validate=False)
+        if world > 1:
+            from paper_1210_0461_b200 import distributed
+
+            top, report = distributed.top_entries_distributed(stream if rank == 0 else None,
+                                                              config, cfg.top_k)
+        else:
+            state, report = crop.run(stream, config, upper_triangle_only=True)
+            top = state.top_entries(cfg.top_k)
+        torch.cuda.synchronize()
+        return report
+
+    for _ in range(max(1, args.warmup // 2)):
+        once()
+    times = []
+    for _ in range(max(1, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        report = once()
+        times.append(time.perf_counter() - t0)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([max(times)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tm = float(t.item())
+    else:
+        tm = statistics.mean(times)
+    terms = int(((dtx.offsets[1:] - dtx.offsets[:-1]) *
+                 (dtx.offsets[1:] - dtx.offsets[:-1] - 1) // 2).sum().item())
+    h2d = off_h.numel() * 8 + it_h.numel() * 4
+    d2h = cfg.kappa * 12 + 16 + cfg.top_k * 24
+    return {"value": terms / tm, "unit": "terms/s", "ms_per_step": tm * 1e3,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "crop.run(TransactionStream) + SketchState.top_entries"
+            if world == 1 else "distributed.top_entries_distributed"}
+
+
+def default_sample(cfg_name):
+    return {"c1": 20_000, "c2": 150_000, "c3": 60_000, "c5": 3_000}.get(cfg_name, 50_000)
+
+
+def cpu_baseline(args, cfg, dtx, reps: int = 1):
+    """C oracle (reference algorithm restated) on a bounded prefix, all host cores."""
+    import numpy as np
+
+    import oracle
+    import paper_1210_0461_b200 as crop
+
+    n_sample = args.cpu_sample_tx or default_sample(args.config)
+    off, items = dtx.to_host()
+    n_sample = min(n_sample, off.shape[0] - 1)
+    off_s = off[: n_sample + 1]
+    items_s = items[: off_s[-1]]
+    lens = np.diff(off_s)
+    terms = int((lens * (lens - 1) // 2).sum())
+    cores = cpu_count()
+    h = crop.make_hashes(crop.HashConfig(cfg.kappa, crop.derive_seed(0, "instance:0")))
+    stream = oracle.Stream(off_s, items_s)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.run_parallel(stream, h.coefficients(), cfg.kappa, cfg.workers, capacity=0,
+                            upper_only=True, threads=cores)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    return {"value": terms / t, "unit": "terms/s", "cores": min(cores, cfg.workers),
+            "kind": "port",
+            "sample": f"first {n_sample} of {cfg.n_tx} transactions ({terms} terms), "
+                      f"run_parallel restatement: {cfg.workers} shared-nothing workers "
+                      f"on {min(cores, cfg.workers)} threads, exact summaries",
+            "seconds": round(t, 3)}
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import torch
+
+    from paper_1210_0461_b200 import workloads
+
+    cfg = workloads.CONFIGS[args.config]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=args.cpu_sample_tx or default_sample(args.config))
+    torch.cuda.synchronize()
+    vals = []
+    for k in range(args.warmup + args.steps):
+        r = cpu_baseline(args, cfg, dtx)
+        if k >= args.warmup:
+            vals.append(r)
+    value = statistics.mean(v["value"] for v in vals)
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": "terms/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(v["seconds"] for v in vals) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: seeded Zipf transactions (SURVEY.md §8d)",
+        "config": {"workload": cfg.name, "sample": vals[0]["sample"]},
+        "cpu_baseline": {"value": value, "unit": "terms/s", "cores": vals[0]["cores"],
+                         "kind": "port", "sample": vals[0]["sample"]},
+        "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

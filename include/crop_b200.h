@@ -40,6 +40,9 @@ int crop_abi_version(void);
 /* Message of the last failing call on this thread. */
 const char* crop_last_error(void);
 
+/* Kernels launched by this library so far (process-wide counter). */
+unsigned long long crop_launch_counter(void);
+
 /* K0 -- per-item hash tables, IndexHashFn.values (hashing.py:68-71):
  * h_row[i] = ((row_mul*i + row_add) mod p) mod kappa, likewise h_col, for
  * i in [0, n_items). Exact 128-bit Mersenne arithmetic on device. */
@@ -94,6 +97,10 @@ int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* tota
                     uint64_t* n_tiles, uint64_t* n_units);
 int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32_t* out_count,
                    uint64_t* d_n_entries, void* stream);
+/* Per-phase CUDA-event timing of crop_pairs_run (off by default). Phases:
+ * route-count, tile scan, route-write, count (ms of the last run). */
+int crop_pairs_set_timing(crop_pairs* job, int on);
+int crop_pairs_phase_ms(const crop_pairs* job, float* out4);
 /* 1 if the entry list overflowed its capacity (never expected; synchronises). */
 int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
 void crop_pairs_destroy(crop_pairs* job);

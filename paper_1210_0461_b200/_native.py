@@ -28,6 +28,7 @@ class Interval(ctypes.Structure):
 _SIGS = {
     "crop_abi_version": (i32, []),
     "crop_last_error": (ctypes.c_char_p, []),
+    "crop_launch_counter": (u64, []),
     "crop_hash_tables": (i32, [u32, u64, u64, u64, u64, u32, P, P, P]),
     "crop_sign_hash": (i32, [P, P, u64, u64, u64, P, P]),
     "crop_selfjoin_bucket_loads": (i32, [P, P, i64, P, P, u32, i32, P, P]),
@@ -37,6 +38,8 @@ _SIGS = {
     "crop_pairs_info": (i32, [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
                               ctypes.POINTER(u64)]),
     "crop_pairs_run": (i32, [P, P, P, P, P, P]),
+    "crop_pairs_set_timing": (i32, [P, i32]),
+    "crop_pairs_phase_ms": (i32, [P, ctypes.POINTER(ctypes.c_float)]),
     "crop_pairs_overflowed": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_destroy": (None, [P]),
     "crop_entry_bucket_stats": (i32, [P, P, P, P, u64, i32, u32, P, P, u32, P, P, P, P, P]),

@@ -79,6 +79,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 void crop_set_error(int code, const char* fmt, ...);
 // Keep freed device scratch in the stream-ordered pool (no cudaMalloc per job).
 int crop_pool_setup();
+// Count kernels this library launched (reported by bench.py as gpu_launches).
+void crop_count_launches(int n);
 
 #define CROP_CUDA(call)                                                                  \
   do {                                                                                   \

@@ -19,6 +19,10 @@ void crop_set_error(int code, const char* fmt, ...) {
 
 extern "C" int crop_abi_version(void) { return 1; }
 
+static unsigned long long g_launches = 0;
+void crop_count_launches(int n) { __atomic_add_fetch(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+extern "C" unsigned long long crop_launch_counter(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 int crop_pool_setup() {
   static int done_dev = -1;
   int dev = 0;
@@ -65,6 +69,7 @@ extern "C" int crop_hash_tables(uint32_t n_items, uint64_t row_mul, uint64_t row
   k_hash_tables<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_items, row_mul, row_add, col_mul,
                                                            col_add, kappa, h_row, h_col);
   CROP_LAUNCH_CHECK();
+  crop_count_launches(1);
   return CROP_OK;
 }
 
@@ -152,6 +157,7 @@ static int launch_loads(bool self, const int64_t* a_ptr, const uint32_t* a_idx,
       a_ptr, a_idx, b_ptr, b_idx, n, h_row, h_col, kappa, upper_only,
       (unsigned long long*)loads);
   CROP_LAUNCH_CHECK();
+  crop_count_launches(1);
   return CROP_OK;
 }
 
@@ -246,6 +252,7 @@ extern "C" int crop_entry_bucket_stats(const uint32_t* row, const uint32_t* col,
         (unsigned long long*)loads + (size_t)t * kappa, distinct + (size_t)t * kappa,
         cs ? (unsigned long long*)cs + (size_t)t * kappa : nullptr);
     CROP_LAUNCH_CHECK();
+    crop_count_launches(1);
   }
   return CROP_OK;
 }
@@ -270,6 +277,7 @@ extern "C" int crop_entry_buckets(const uint32_t* row, const uint32_t* col, uint
   k_entry_buckets<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(row, col, n, h_row, h_col,
                                                                    kappa, out);
   CROP_LAUNCH_CHECK();
+  crop_count_launches(1);
   return CROP_OK;
 }
 

@@ -755,9 +755,14 @@ struct crop_pairs {
   uint32_t* d_overflow = nullptr;
   unsigned int* d_tile_done = nullptr;
   std::vector<uint32_t> h_item_tile;  // kept alive for the async uploads
+  // optional per-phase timing (CUDA events on the job's stream)
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
 };
 
 static void free_job(crop_pairs* j) {
+  for (cudaEvent_t& e : j->ev)
+    if (e) cudaEventDestroy(e);
   void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_tiles, j->d_units, j->d_split,
                   j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_total_entries,
                   j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done};
@@ -963,6 +968,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
       kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, J->d_terms, J->d_maxlen);
       JCUDA(cudaGetLastError());
+      crop_count_launches(1);
     }
     std::vector<unsigned long long> terms(nn);
     unsigned int maxlen = 0;
@@ -1045,6 +1051,10 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
   const int pass_grid = (int)std::min<int64_t>(kNumSMs, chunks);
   const uint32_t ns = std::min(nt, kTileSmem);
   const size_t route_smem = kOffBytes + ns * 4;
+  auto mark = [&](int k) {
+    if (J->timing) cudaEventRecord(J->ev[k], st);
+  };
+  mark(0);
   // pass B1: entries per tile
   CROP_CUDA(cudaMemsetAsync(J->d_tile_entries, 0, nt * 4, st));
   {
@@ -1056,9 +1066,11 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
                                                       J->d_tile_entries);
     CROP_LAUNCH_CHECK();
   }
+  mark(1);
   k_exclusive_scan_u32_to_u64<<<1, 1024, 0, st>>>(J->d_tile_entries, nt, J->d_tile_ebase,
                                                    J->d_total_entries);
   CROP_LAUNCH_CHECK();
+  mark(2);
   CROP_CUDA(cudaMemcpyAsync(J->d_tile_cursor, J->d_tile_ebase, nt * 8, cudaMemcpyDeviceToDevice, st));
   {
     auto kern = up ? k_route_write<true> : k_route_write<false>;
@@ -1070,6 +1082,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
                                                       J->entry_cap, J->d_overflow);
     CROP_LAUNCH_CHECK();
   }
+  mark(3);
   // count
   CROP_CUDA(cudaMemsetAsync(J->d_unit_counter, 0, 4, st));
   CROP_CUDA(cudaMemsetAsync(J->d_tile_done, 0, nt * 4, st));
@@ -1101,9 +1114,33 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     else kern = J->filter ? k_count<false, true> : k_count<false, false>;
     CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCountSmem));
     const int grid = std::min<int>(kNumSMs, (int)J->units.size());
+    mark(4);
     kern<<<grid, kCountThreads, kCountSmem, st>>>(A);
     CROP_LAUNCH_CHECK();
+    mark(5);
   }
+  crop_count_launches(5);
+  return CROP_OK;
+}
+
+extern "C" int crop_pairs_set_timing(crop_pairs* J, int on) {
+  if (on && !J->ev[0])
+    for (cudaEvent_t& e : J->ev) CROP_CUDA(cudaEventCreate(&e));
+  J->timing = on != 0;
+  return CROP_OK;
+}
+
+// Durations (ms) of the last run's phases: route-count, scan, route-write, count.
+extern "C" int crop_pairs_phase_ms(const crop_pairs* J, float* out4) {
+  if (!J->timing) {
+    crop_set_error(CROP_ECONFIG, "timing was not enabled on this job");
+    return CROP_ECONFIG;
+  }
+  CROP_CUDA(cudaEventSynchronize(J->ev[5]));
+  CROP_CUDA(cudaEventElapsedTime(&out4[0], J->ev[0], J->ev[1]));
+  CROP_CUDA(cudaEventElapsedTime(&out4[1], J->ev[1], J->ev[2]));
+  CROP_CUDA(cudaEventElapsedTime(&out4[2], J->ev[2], J->ev[3]));
+  CROP_CUDA(cudaEventElapsedTime(&out4[3], J->ev[4], J->ev[5]));
   return CROP_OK;
 }
 

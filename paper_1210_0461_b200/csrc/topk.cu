@@ -282,6 +282,7 @@ extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_
                                  (int)small_smem));
   k_topk_finish_small<<<1, 1024, small_smem, st>>>(row, col, count, state, cand, out_idx);
   CROP_LAUNCH_CHECK();
+  crop_count_launches(4);
   // The large-candidate path needs the candidate count on the host.
   unsigned long long h_state[5];
   CROP_CUDA(cudaMemcpyAsync(h_state, state, sizeof(h_state), cudaMemcpyDeviceToHost, st));
@@ -299,6 +300,7 @@ extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_
     }
     k_rs_emit<<<(int)rb, 256, 0, st>>>(row, col, count, state, cand, rs, out_idx);
     CROP_LAUNCH_CHECK();
+    crop_count_launches(26);
   }
   cudaFreeAsync(hist, st);
   cudaFreeAsync(state, st);

@@ -119,3 +119,71 @@ def run_distributed(stream, config, upper_triangle_only: bool = False, compute=N
     if me != src:
         return None, None
     return merge_partials([p for part in gathered for p in part])
+
+
+def top_entries_distributed(stream, config, k: int, upper_triangle_only: bool = True,
+                            src: int = 0):
+    """Device path of a multi-GPU top-k mine (the benchmark's public call).
+
+    Rank `src` moves the stream to its GPU and broadcasts the CSR arrays once
+    over NCCL; each rank counts the buckets of its block of worker intervals
+    (crop_pairs with an interval filter), reports per-bucket loads and its
+    local top-k; loads are all-reduced and the k*G candidates gathered to
+    `src`, which merges them. Returns (top entries, LoadReport) on `src`,
+    (None, None) elsewhere. 0/1 self-join (mining) streams only."""
+    import torch
+
+    from . import kernels
+    from .engine import LoadReport, TopEntry, _worker_rows, prepare
+    from .hashing import HashConfig, make_hashes
+    from .sparse import Entry
+
+    dist = _dist()
+    me, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if me == src:
+        prep = prepare(stream)
+        if prep.kind != "pairs":
+            raise ValueError("top_entries_distributed handles 0/1 self-join streams")
+        dtx = prep.device
+        meta = torch.tensor([dtx.n_tx, dtx.nnz, dtx.n_items, prep.n_rows, prep.pair_total],
+                            dtype=torch.int64, device=dev)
+    else:
+        meta = torch.zeros(5, dtype=torch.int64, device=dev)
+    dist.broadcast(meta, src)
+    n_tx, nnz, n_items, dim, pair_total = (int(v) for v in meta.tolist())
+    if me != src:
+        dtx = kernels.DeviceTransactions(torch.empty(n_tx + 1, dtype=torch.int64, device=dev),
+                                         torch.empty(nnz, dtype=torch.int32, device=dev), n_items)
+    dist.broadcast(dtx.offsets, src)
+    dist.broadcast(dtx.items, src)
+    kappa = config.kappa
+    lo, hi = rank_workers(config.workers, me, world)
+    asg = config.assignments()
+    h = make_hashes(HashConfig(kappa, config.instance_seeds()[0]))
+    tab = kernels.hash_tables(h, n_items)
+    cand = torch.full((3, k), -1, dtype=torch.int32, device=dev)
+    loads = torch.zeros(kappa, dtype=torch.int64, device=dev)
+    if hi > lo:
+        ent = kernels.count_pairs(dtx, upper_triangle_only, kappa, asg[lo].start,
+                                  asg[hi - 1].stop, *tab)
+        bl, _, _ = kernels.entry_bucket_stats(ent, [tab], kappa, n_items, None)
+        loads += bl[0]
+        idx = kernels.topk_indices(ent, k)
+        m = idx.shape[0]
+        cand[0, :m], cand[1, :m], cand[2, :m] = ent.row[idx], ent.col[idx], ent.count[idx]
+    dist.all_reduce(loads)
+    gathered = [torch.empty_like(cand) for _ in range(world)] if me == src else None
+    dist.gather(cand, gathered, dst=src)
+    if me != src:
+        return None, None
+    allc = torch.cat(gathered, dim=1).cpu().numpy().view(np.uint32).astype(np.int64)
+    keep = allc[2] != 0xFFFFFFFF
+    r, c, w = allc[0][keep], allc[1][keep], allc[2][keep]
+    order = np.lexsort((c, r, -w))[:k]
+    top = [TopEntry(Entry(int(r[x]), int(c[x])), float(w[x]), float(w[x]), None) for x in order]
+    rows = [_worker_rows(loads.cpu().numpy(), asg)]
+    report = LoadReport(kappa=kappa, workers=config.workers, rows=rows,
+                        input_pair_total=pair_total,
+                        assignments=[(a.start, a.stop) for a in asg])
+    return top, report

@@ -208,9 +208,22 @@ class PairCountJob:
         ent.n_dev = n_dev
         if sync:
             ent.n = int(n_dev.item())
-            if ent.n > self.max_entries:
+            if ent.n > self.max_entries or self.overflowed():
                 raise InputError(f"pair engine overflow: {ent.n} > {self.max_entries}")
         return ent
+
+    def set_timing(self, on: bool = True) -> None:
+        nat.check(nat.load().crop_pairs_set_timing(self._h, int(on)))
+
+    def phase_ms(self) -> dict:
+        out = (ctypes.c_float * 4)()
+        nat.check(nat.load().crop_pairs_phase_ms(self._h, out))
+        return {"route_count": out[0], "scan": out[1], "route_write": out[2], "count": out[3]}
+
+    def overflowed(self) -> bool:
+        flag = ctypes.c_int()
+        nat.check(nat.load().crop_pairs_overflowed(self._h, ctypes.byref(flag)))
+        return bool(flag.value)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -271,6 +284,10 @@ def entry_buckets(row, col, n: int, h_row, h_col, kappa: int) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------ K4 top-k
+
+def launch_counter() -> int:
+    return int(nat.load().crop_launch_counter())
+
 
 def topk_indices(ent: DeviceEntries, k: int, count: torch.Tensor | None = None) -> torch.Tensor:
     """Indices of the best k entries by (count desc, row asc, col asc), unordered."""

@@ -164,7 +164,8 @@ def test_merge_partials_validation():
 
 def test_native_library_exports_every_declared_symbol():
     header = open(os.path.join(ROOT, "include", "crop_b200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(crop_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void|const char\*|unsigned long long)\s+(crop_\w+)\(",
+                              header, re.M))
     assert declared, "no declarations parsed"
     lib = ctypes.CDLL(_native.LIB_PATH)
     for name in declared:

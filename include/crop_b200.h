@@ -97,8 +97,8 @@ int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* tota
                     uint64_t* n_tiles, uint64_t* n_units);
 int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32_t* out_count,
                    uint64_t* d_n_entries, void* stream);
-/* Per-phase CUDA-event timing of crop_pairs_run (off by default). Phases:
- * route-count, tile scan, route-write, count (ms of the last run). */
+/* Per-phase CUDA-event timing of crop_pairs_run (off by default). out4 =
+ * {route, tile-entry counts, 0, count} in ms of the last run. */
 int crop_pairs_set_timing(crop_pairs* job, int on);
 int crop_pairs_phase_ms(const crop_pairs* job, float* out4);
 /* 1 if the entry list overflowed its capacity (never expected; synchronises). */

@@ -33,6 +33,8 @@
 #include <cstdio>
 #include <cstring>
 #include <numeric>
+#include <chrono>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -54,8 +56,10 @@ constexpr size_t kCountSmem = kTableBytes + kJobBytes + 64;
 constexpr int kPassThreads = 1024;
 constexpr int kChunkTx = 4096;                       // transactions per position-parallel chunk
 constexpr size_t kOffBytes = (kChunkTx + 1) * 8;
-constexpr uint32_t kStatSmemItems = 40960;           // pass A privatised items (160 KB)
-constexpr uint32_t kTileSmem = 40960;                // route shared tile counters (160 KB)
+constexpr uint32_t kStatSmemItems = 24576;           // pass A privatised items (2 x u32, 192 KB)
+constexpr uint32_t kTileSmem = 24576;                // route shared tile counters (96 KB)
+constexpr uint32_t kStage = 4096;                    // route staging entries per chunk
+constexpr uint64_t kOccOne = 1ull << 40;             // pass A: occurrence count in bits 40+
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kUnknown = 0xFFFFFFFEu;       // route: previous tile not known yet
 constexpr uint32_t kWinFlag = 0x80000000u;           // item_tile: row is split into windows
@@ -97,19 +101,23 @@ struct Pos {
 };
 
 __device__ __forceinline__ int stage_offsets(int64_t* s_off, const int64_t* __restrict__ offsets,
-                                             int64_t n_tx, int64_t chunk) {
-  const int64_t t0 = chunk * kChunkTx;
-  const int ntx = (int)(n_tx - t0 < kChunkTx ? n_tx - t0 : kChunkTx);
+                                             int64_t n_tx, int64_t chunk, int chunk_tx) {
+  const int64_t t0 = chunk * chunk_tx;
+  const int ntx = (int)(n_tx - t0 < chunk_tx ? n_tx - t0 : chunk_tx);
   for (int t = threadIdx.x; t <= ntx; t += blockDim.x) s_off[t] = offsets[t0 + t];
   __syncthreads();
   return ntx;
 }
 
-// Calls body(g, pos) for every position of the chunk; all 32 lanes of a warp
-// execute body together (pos.valid false past the range) so body may use
-// warp shuffles. `cursor` is the warp's transaction cursor.
-template <typename Body>
-__device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx, Body&& body) {
+// Calls body(g, pos, item, tile) for every position of the chunk; all 32
+// lanes of a warp execute body together (pos.valid false past the range) so
+// body may use warp shuffles. Loads are software-pipelined: the item of
+// window w+2 and (with TILE) the item->tile lookup of window w+1 are in
+// flight while window w is processed.
+template <bool TILE, typename Body>
+__device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
+                                           const uint32_t* __restrict__ items,
+                                           const uint32_t* __restrict__ item_tile, Body&& body) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t g_lo = s_off[0], g_hi = s_off[ntx];
   const int64_t per = (((g_hi - g_lo + nw - 1) / nw) + 31) & ~31ll;
@@ -123,8 +131,15 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx, Body&&
     else hi = mid;
   }
   int cur = lo;
+  auto ld_item = [&](int64_t g) { return g < w_hi ? __ldg(items + g) : 0u; };
+  uint32_t it0 = ld_item(w_lo + lane), it1 = ld_item(w_lo + 32 + lane);
+  uint32_t tl0 = 0;
+  if (TILE) tl0 = w_lo + lane < w_hi ? __ldg(item_tile + it0) : kNone;
   for (int64_t g0 = w_lo; g0 < w_hi; g0 += 32) {
     const int64_t g = g0 + lane;
+    const uint32_t it2 = ld_item(g + 64);
+    uint32_t tl1 = 0;
+    if (TILE) tl1 = g + 32 < w_hi ? __ldg(item_tile + it1) : kNone;
     Pos q;
     q.valid = g < w_hi;
     int t = cur;
@@ -135,40 +150,54 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx, Body&&
     q.p = (uint32_t)(g - q.base);
     q.L = (uint32_t)(s_off[t + 1] - q.base);
     cur = __shfl_sync(0xffffffffu, t, 31);
-    body(g, q);
+    body(g, q, it0, tl0);
+    it0 = it1;
+    it1 = it2;
+    tl0 = tl1;
   }
 }
 
 // ------------------------------------------------------------- pass A
+// Per row item i: terms_i (pairs with i as the row) and occ_i, the number of
+// transactions in which i has at least one partner after it (an upper bound
+// of the entries it creates). Output packed as occ << 40 | terms.
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_item_terms(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
-                 int64_t n_tx, uint32_t n_items, unsigned long long* __restrict__ terms,
+                 int64_t n_tx, uint32_t n_items, unsigned long long* __restrict__ stats,
                  unsigned int* __restrict__ max_len) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
   uint32_t* s_terms = reinterpret_cast<uint32_t*>(smem + kOffBytes);
   const uint32_t n_smem = min(n_items, kStatSmemItems);
-  for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x) s_terms[i] = 0;
+  uint32_t* s_occ = s_terms + n_smem;
+  for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x) {
+    s_terms[i] = 0;
+    s_occ[i] = 0;
+  }
   uint32_t my_max = 0;
   const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
-    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk);
-    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
+    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk, kChunkTx);
+    walk_chunk<false>(s_off, ntx, items, nullptr, [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
       if (!q.valid) return;
-      const uint32_t i = items[g];
       my_max = max(my_max, q.L);
       const uint32_t c = UPPER ? q.L - 1 - q.p : q.L;
       if (c == 0) return;
-      if (i < n_smem) atomicAdd(&s_terms[i], c);
-      else atomicAdd(&terms[i], (unsigned long long)c);
+      if (i < n_smem) {
+        atomicAdd(&s_terms[i], c);
+        atomicAdd(&s_occ[i], 1u);
+      } else {
+        atomicAdd(&stats[i], kOccOne | c);
+      }
     });
   }
   atomicMax(max_len, my_max);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x)
-    if (s_terms[i]) atomicAdd(&terms[i], (unsigned long long)s_terms[i]);
+    if (s_terms[i])
+      atomicAdd(&stats[i], ((unsigned long long)s_occ[i] << 40) | s_terms[i]);
 }
 
 // ------------------------------------------------------------- pass B
@@ -182,16 +211,18 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 // Runs are found with warp shuffles: a lane's tile is compared with its
 // neighbours'; a run that leaves the 32-position window is finished with
 // loads (rare).
-template <bool UPPER, typename Emit>
-__device__ __forceinline__ void route_window(int64_t g, const Pos& q,
+template <bool UPPER, typename EmitRun, typename EmitWin>
+__device__ __forceinline__ void route_window(int64_t g, const Pos& q, uint32_t tile_of_g,
                                              const uint32_t* __restrict__ items,
                                              const uint32_t* __restrict__ item_tile,
                                              const Tile* __restrict__ tiles, uint32_t& carry_tile,
-                                             Emit&& emit) {
+                                             EmitRun&& emit_run, EmitWin&& emit_window) {
+  // emit_run is called by every lane (warp-uniform) with has = whether this
+  // lane starts a run entry; emit_window once per (split row, window) entry.
   const int lane = threadIdx.x & 31;
   uint32_t tv = kNone;
   if (q.valid) {
-    tv = item_tile[items[g]];
+    tv = tile_of_g;
     if (UPPER && q.p + 1 >= q.L) tv = kNone;  // the last item has no partner after it
   }
   // previous position's tile (same transaction only)
@@ -204,109 +235,128 @@ __device__ __forceinline__ void route_window(int64_t g, const Pos& q,
   const uint32_t next_tv = __shfl_down_sync(0xffffffffu, tv, 1);
   const uint32_t next_p = __shfl_down_sync(0xffffffffu, q.p, 1);
   carry_tile = __shfl_sync(0xffffffffu, tv, 31);
-  if (tv == kNone) return;
-  if (tv & kWinFlag) {  // split row: one entry per column window present
-    const uint32_t tile = tv & ~kWinFlag;
-    const Tile t0 = tiles[tile];
-    const uint32_t lo = t0.c0;
-    uint32_t last_w = kNone;
-    for (uint32_t p = UPPER ? q.p + 1 : 0; p < q.L; ++p) {
-      const uint32_t j = items[q.base + p];
-      if (j < lo) continue;
-      const uint32_t w = (j - lo) / kDenseCap;
-      if (w >= t0.nwin) break;
-      if (w != last_w) {
-        if (UPPER) emit(tile + w, (uint32_t)g, (q.L - q.p) | (1u << 16));
-        else emit(tile + w, (uint32_t)q.base, q.L | (q.p << 16));
-        last_w = w;
+  bool has = false;
+  uint32_t rt = 0, rx = 0, ry = 0;
+  if (tv != kNone) {
+    if (tv & kWinFlag) {  // split row: one entry per column window present
+      const uint32_t tile = tv & ~kWinFlag;
+      const Tile t0 = tiles[tile];
+      const uint32_t lo = t0.c0;
+      uint32_t last_w = kNone;
+      for (uint32_t p = UPPER ? q.p + 1 : 0; p < q.L; ++p) {
+        const uint32_t j = items[q.base + p];
+        if (j < lo) continue;
+        const uint32_t w = (j - lo) / kDenseCap;
+        if (w >= t0.nwin) break;
+        if (w != last_w) {
+          if (UPPER) emit_window(true, tile + w, (uint32_t)g, (q.L - q.p) | (1u << 16));
+          else emit_window(true, tile + w, (uint32_t)q.base, q.L | (q.p << 16));
+          last_w = w;
+        }
       }
+    } else if (!UPPER) {
+      has = true;
+      rt = tv;
+      rx = (uint32_t)q.base;
+      ry = q.L | (q.p << 16);
+    } else if (prev != tv) {  // first row of its run
+      uint32_t p1 = q.p + 1;
+      const bool next_known = lane < 31 && next_p == q.p + 1;
+      if (!(next_known && next_tv != tv))  // the run may continue: extend with loads
+        while (p1 + 1 < q.L && item_tile[items[q.base + p1]] == tv) ++p1;
+      has = true;
+      rt = tv;
+      rx = (uint32_t)g;
+      ry = (q.L - q.p) | ((p1 - q.p) << 16);
     }
-    return;
   }
-  if (!UPPER) {
-    emit(tv, (uint32_t)q.base, q.L | (q.p << 16));
-    return;
-  }
-  if (prev == tv) return;  // not the first row of its run
-  uint32_t p1 = q.p + 1;
-  const bool next_known = lane < 31 && next_p == q.p + 1;
-  if (!(next_known && next_tv != tv))  // the run may continue: extend with loads
-    while (p1 + 1 < q.L && item_tile[items[q.base + p1]] == tv) ++p1;
-  emit(tv, (uint32_t)g, (q.L - q.p) | ((p1 - q.p) << 16));
+  emit_run(has, rt, rx, ry);
 }
 
+// One walk per chunk of chunk_tx transactions: entries are staged in shared
+// memory with per-tile counts (only the tiles a chunk touches are listed),
+// one global range is claimed per touched tile, then the staged entries are
+// scattered into their tiles' ranges. Tiles beyond the shared counters and
+// entries beyond the staging buffer take per-entry global atomics (rare).
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
-    k_route_count(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
-                  int64_t n_tx, const uint32_t* __restrict__ item_tile,
-                  const Tile* __restrict__ tiles, uint32_t n_tiles,
-                  uint32_t* __restrict__ tile_entries) {
+    k_route(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items, int64_t n_tx,
+            int chunk_tx, const uint32_t* __restrict__ item_tile, const Tile* __restrict__ tiles,
+            uint32_t n_tiles, unsigned long long* __restrict__ tile_cursor,
+            const unsigned long long* __restrict__ tile_end, uint2* __restrict__ entries,
+            uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  uint2* s_stage = reinterpret_cast<uint2*>(smem + (size_t)(chunk_tx + 1) * 8);
+  uint32_t* s_stage_tile = reinterpret_cast<uint32_t*>(s_stage + kStage);
+  uint32_t* s_touched = s_stage_tile + kStage;
+  uint32_t* s_misc = s_touched + kStage;  // [0] staged, [1] touched
+  uint32_t* s_cnt = s_misc + 4;           // per shared tile: count, then next position
   const uint32_t ns = min(n_tiles, kTileSmem);
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
-  auto emit = [&](uint32_t tile, uint32_t, uint32_t) {
-    if (tile < ns) atomicAdd(&s_cnt[tile], 1u);
-    else atomicAdd(&tile_entries[tile], 1u);
+  auto global_put = [&](uint32_t tile, uint2 v) {
+    const unsigned long long pos = atomicAdd(&tile_cursor[tile], 1ull);
+    if (pos < tile_end[tile]) entries[pos] = v;
+    else *overflow = 1u;
   };
-  const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+  auto put = [&](uint32_t slot, uint32_t tile, uint32_t x, uint32_t y) {
+    if (slot >= kStage || tile >= ns) {
+      if (slot < kStage) s_stage_tile[slot] = kNone;  // hole
+      global_put(tile, make_uint2(x, y));
+      return;
+    }
+    s_stage_tile[slot] = tile;
+    s_stage[slot] = make_uint2(x, y);
+    if (atomicAdd(&s_cnt[tile], 1u) == 0) s_touched[atomicAdd(&s_misc[1], 1u)] = tile;
+  };
+  // run entries: at most one per lane per window -> one staging atomic per warp
+  auto stage_run = [&](bool has, uint32_t tile, uint32_t x, uint32_t y) {
+    const uint32_t m = __ballot_sync(0xffffffffu, has);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(&s_misc[0], (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (has) put(base + __popc(m & ((1u << lane) - 1u)), tile, x, y);
+  };
+  auto stage_window = [&](bool, uint32_t tile, uint32_t x, uint32_t y) {
+    put(atomicAdd(&s_misc[0], 1u), tile, x, y);
+  };
+  const int64_t n_chunks = (n_tx + chunk_tx - 1) / chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
-    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk);
+    if (threadIdx.x == 0) {
+      s_misc[0] = 0;
+      s_misc[1] = 0;
+    }
+    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk, chunk_tx);
     uint32_t carry = kUnknown;
-    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
-      route_window<UPPER>(g, q, items, item_tile, tiles, carry, emit);
-    });
-  }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x)
-    if (s_cnt[t]) atomicAdd(&tile_entries[t], s_cnt[t]);
-}
-
-// Per chunk: count entries per shared tile, claim one global range per
-// touched tile, then write the entries (shared cursors hand out positions).
-template <bool UPPER>
-__global__ void __launch_bounds__(kPassThreads, 1)
-    k_route_write(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
-                  int64_t n_tx, const uint32_t* __restrict__ item_tile,
-                  const Tile* __restrict__ tiles, uint32_t n_tiles,
-                  unsigned long long* __restrict__ tile_cursor, uint2* __restrict__ entries,
-                  unsigned long long cap, uint32_t* __restrict__ overflow) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  int64_t* s_off = reinterpret_cast<int64_t*>(smem);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
-  const uint32_t ns = min(n_tiles, kTileSmem);
-  const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
-  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
-    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk);
-    auto count = [&](uint32_t tile, uint32_t, uint32_t) {
-      if (tile < ns) atomicAdd(&s_cnt[tile], 1u);
-    };
-    uint32_t carry = kUnknown;
-    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
-      route_window<UPPER>(g, q, items, item_tile, tiles, carry, count);
+    walk_chunk<true>(s_off, ntx, items, item_tile, [&](int64_t g, const Pos& q, uint32_t, uint32_t tile) {
+      route_window<UPPER>(g, q, tile, items, item_tile, tiles, carry, stage_run, stage_window);
     });
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) {
-      const uint32_t c = s_cnt[t];
-      if (c) s_cnt[t] = (uint32_t)atomicAdd(&tile_cursor[t], (unsigned long long)c);
+    const uint32_t n_stage = min(s_misc[0], kStage), n_touch = s_misc[1];
+    for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) {
+      const uint32_t t = s_touched[k];
+      s_cnt[t] = (uint32_t)atomicAdd(&tile_cursor[t], (unsigned long long)s_cnt[t]);
     }
     __syncthreads();
-    auto write = [&](uint32_t tile, uint32_t x, uint32_t y) {
-      unsigned long long pos;
-      if (tile < ns) pos = atomicAdd(&s_cnt[tile], 1u);
-      else pos = atomicAdd(&tile_cursor[tile], 1ull);
-      if (pos < cap) entries[pos] = make_uint2(x, y);
-      else *overflow = 1u;
-    };
-    carry = kUnknown;
-    walk_chunk(s_off, ntx, [&](int64_t g, const Pos& q) {
-      route_window<UPPER>(g, q, items, item_tile, tiles, carry, write);
-    });
+    for (uint32_t k = threadIdx.x; k < n_stage; k += blockDim.x) {
+      const uint32_t t = s_stage_tile[k];
+      if (t == kNone) continue;
+      entries[atomicAdd(&s_cnt[t], 1u)] = s_stage[k];
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) s_cnt[s_touched[k]] = 0;
   }
+}
+
+// tile_entries[t] = final cursor - base (entries actually routed)
+__global__ void k_tile_entries(const unsigned long long* __restrict__ cursor,
+                               const unsigned long long* __restrict__ base, uint32_t n,
+                               uint32_t* __restrict__ out) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    out[t] = (uint32_t)(cursor[t] - base[t]);
 }
 
 // ------------------------------------------------------------- count
@@ -391,7 +441,7 @@ struct WarpJobs {
 template <int KIND, bool UPPER, bool FILTER>
 __device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T, uint64_t e0,
                                               uint64_t e1, const WarpJobs& J, uint32_t* table,
-                                              uint32_t* hcount) {
+                                              uint32_t* hcount, unsigned int* s_next) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* __restrict__ items = A.items;
   const uint32_t n = A.n_items;
@@ -435,7 +485,14 @@ __device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T,
   // rows > 1 only for UPPER runs in kDenseMulti / kHash tiles
   constexpr bool MULTI = UPPER && (KIND == kDenseMulti || KIND == kHash);
 
-  for (uint64_t eb_w = e0 + (uint64_t)warp * 32; eb_w < e1; eb_w += (uint64_t)kCountWarps * 32) {
+  (void)warp;
+  for (;;) {
+    // warps take batches of 32 entries dynamically (no tail imbalance)
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(s_next, 1u);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    const uint64_t eb_w = e0 + (uint64_t)b * 32;
+    if (eb_w >= e1) break;
     const uint64_t e = eb_w + lane;
     uint32_t cnt = 0, x = 0, y = 0, first = 0, ri = 0;
     if (e < e1) {
@@ -505,25 +562,37 @@ __device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T,
       if (KIND != kDenseRow && KIND != kDenseWindow) i = J.item[o];
       jpos = t + J.delta[o];
     };
-    uint32_t ci = 0, cjp = 0, cj = 0;
-    const uint32_t o0 = owner_of(0);  // warp-collective: outside any divergent branch
-    if (lane < S) {
-      locate_pair(lane, o0, ci, cjp);
-      cj = items[cjp];
+    // three-stage software pipeline: the column items of iterations t0+32 and
+    // t0+64 are in flight while iteration t0 is counted
+    uint32_t i0 = 0, j0 = 0, i1 = 0, j1 = 0, jp;
+    {
+      const uint32_t o = owner_of(0);  // warp-collective: never inside a divergent branch
+      if (lane < S) {
+        locate_pair(lane, o, i0, jp);
+        j0 = items[jp];
+      }
+    }
+    if (32 < S) {
+      const uint32_t o = owner_of(32);
+      if (32 + lane < S) {
+        locate_pair(32 + lane, o, i1, jp);
+        j1 = items[jp];
+      }
     }
     for (uint32_t t0 = 0; t0 < S; t0 += 32) {
-      const uint32_t tn = t0 + 32 + lane;
-      uint32_t ni = 0, njp = 0, nj = 0;
-      if (t0 + 32 < S) {  // warp-uniform
-        const uint32_t o = owner_of(t0 + 32);
-        if (tn < S) {
-          locate_pair(tn, o, ni, njp);
-          nj = items[njp];
+      uint32_t i2 = 0, j2 = 0;
+      if (t0 + 64 < S) {  // warp-uniform
+        const uint32_t o = owner_of(t0 + 64);
+        if (t0 + 64 + lane < S) {
+          locate_pair(t0 + 64 + lane, o, i2, jp);
+          j2 = items[jp];
         }
       }
-      if (t0 + lane < S) count_pair(ci, cj);
-      ci = ni;
-      cj = nj;
+      if (t0 + lane < S) count_pair(i0, j0);
+      i0 = i1;
+      j0 = j1;
+      i1 = i2;
+      j1 = j2;
     }
     __syncwarp();
   }
@@ -576,20 +645,21 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
         hcount[s] = 0;
       }
     }
+    if (threadIdx.x == 0) s_misc[2] = 0;  // batch counter of this unit
     __syncthreads();
 
     switch (kind) {
       case kDenseRow:
-        count_entries<kDenseRow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        count_entries<kDenseRow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
         break;
       case kDenseWindow:
-        count_entries<kDenseWindow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        count_entries<kDenseWindow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
         break;
       case kDenseMulti:
-        count_entries<kDenseMulti, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        count_entries<kDenseMulti, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
         break;
       default:
-        count_entries<kHash, UPPER, FILTER>(A, T, e0, e1, J, table, hcount);
+        count_entries<kHash, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
         break;
     }
     __syncthreads();
@@ -681,41 +751,6 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(1024) k_exclusive_scan_u32_to_u64(const uint32_t* __restrict__ in, uint32_t n,
-                                            unsigned long long* __restrict__ out,
-                                            unsigned long long* __restrict__ total) {
-  // single block, 1024 threads
-  __shared__ unsigned long long s_part[1024];
-  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
-  unsigned long long acc = 0;
-  for (uint32_t i = lo; i < hi; ++i) acc += in[i];
-  s_part[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {  // warp 0 scans the 1024 partials, 32 per lane
-    unsigned long long run = 0;
-    for (int k = 0; k < 32; ++k) run += s_part[threadIdx.x * 32 + k];
-    unsigned long long x = run;
-    for (int d = 1; d < 32; d <<= 1) {
-      unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
-      if ((int)threadIdx.x >= d) x += y;
-    }
-    unsigned long long acc = x - run;
-    for (int k = 0; k < 32; ++k) {
-      const unsigned long long v = s_part[threadIdx.x * 32 + k];
-      s_part[threadIdx.x * 32 + k] = acc;
-      acc += v;
-    }
-    if (threadIdx.x == 31) *total = x;
-  }
-  __syncthreads();
-  unsigned long long run = s_part[threadIdx.x];
-  for (uint32_t i = lo; i < hi; ++i) {
-    out[i] = run;
-    run += in[i];
-  }
-}
-
 }  // namespace
 
 // =============================================================== host side
@@ -748,7 +783,10 @@ struct crop_pairs {
   uint32_t* d_tile_entries = nullptr;
   unsigned long long* d_tile_ebase = nullptr;
   unsigned long long* d_tile_cursor = nullptr;
+  unsigned long long* d_tile_end = nullptr;
   unsigned long long* d_total_entries = nullptr;
+  int route_chunk_tx = 256;
+  std::vector<unsigned long long> h_tile_base, h_tile_end;
   uint2* d_entries = nullptr;
   uint32_t* d_slabs = nullptr;
   unsigned int* d_unit_counter = nullptr;
@@ -764,13 +802,15 @@ static void free_job(crop_pairs* j) {
   for (cudaEvent_t& e : j->ev)
     if (e) cudaEventDestroy(e);
   void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_tiles, j->d_units, j->d_split,
-                  j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_total_entries,
+                  j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_tile_end, j->d_total_entries,
                   j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
 
-// Greedy tile planner over rows in id order (see file header).
+// Greedy tile planner over rows in id order (see file header). One pass
+// over the rows, O(rows + tiles + units), no sorting: it sits between two
+// GPU phases, so every microsecond here is GPU idle time.
 static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& terms,
                        std::vector<uint32_t>& item_tile) {
   const uint32_t n = J->n_items;
@@ -778,64 +818,63 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   const uint64_t T = J->total_terms;
   const uint64_t unit_terms = std::max<uint64_t>(1ull << 16, T / ((uint64_t)kNumSMs * 8));
   const uint32_t hash_rows_max = (J->col_bits >= 32) ? 1u : ((1u << (32 - J->col_bits)) - 1u);
-  struct Group {
-    uint32_t row0, row1;
-    uint64_t sw, sb, st;
-    bool dense_ok, hash_ok;
-  };
-  std::vector<Tile> tiles;
+  std::vector<Tile>& tiles = J->tiles;
+  tiles.clear();
+  tiles.reserve(1024);
   item_tile.assign(n, kNone);
-  auto width_of = [&](uint32_t i) -> uint64_t { return upper ? (uint64_t)(n - 1 - i) : n; };
-  auto units_for = [&](uint64_t terms_) {
-    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(4096, (terms_ + unit_terms - 1) / unit_terms));
+  auto units_for = [unit_terms](uint64_t tm) -> uint32_t {
+    const uint64_t u = (tm + unit_terms - 1) / unit_terms;
+    return (uint32_t)(u < 1 ? 1 : (u > 4096 ? 4096 : u));
   };
-
-  bool open = false;
-  Group g{};
-  auto close = [&]() {
-    if (!open) return;
+  uint32_t row0 = 0;
+  uint64_t sw = 0, sb = 0, st = 0;
+  bool open = false, dok = false, hok = false;
+  auto close = [&](uint32_t row1) {
     Tile t{};
-    t.row0 = g.row0;
-    t.row1 = g.row1;
+    t.row0 = row0;
+    t.row1 = row1;
     t.c0 = 0;
     t.c1 = n;
-    const bool dense = g.dense_ok && (!g.hash_ok || g.st * 8 >= g.sw);
+    const bool dense = dok && (!hok || st * 8 >= sw);
     t.mode = dense ? 0 : 1;
-    t.nwin = 0;
-    t.width = dense ? (uint32_t)g.sw : 0;
-    t.terms = g.st;
-    t.n_units = dense ? units_for(g.st) : 1;
+    t.width = dense ? (uint32_t)sw : 0;
+    t.terms = st;
+    t.n_units = dense ? units_for(st) : 1;
     const uint32_t id = (uint32_t)tiles.size();
-    for (uint32_t i = g.row0; i < g.row1; ++i)
+    for (uint32_t i = row0; i < row1; ++i)
       if (terms[i]) item_tile[i] = id;
     tiles.push_back(t);
-    open = false;
   };
   for (uint32_t i = 0; i < n; ++i) {
     const uint64_t tm = terms[i];
-    const uint64_t w = width_of(i);
-    const uint64_t b = std::min<uint64_t>(w, tm);
+    const uint64_t w = upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
+    const uint64_t b = tm < w ? tm : w;
     if (open) {
-      const bool d_ok = g.dense_ok && g.sw + w <= kDenseCap;
-      const bool h_ok = g.hash_ok && g.sb + b <= kHashCap && g.st + tm <= unit_terms &&
-                        (g.row1 - g.row0 + 1) <= hash_rows_max;
-      if (d_ok || h_ok) {
-        g.row1 = i + 1;
-        g.sw += w;
-        g.sb += b;
-        g.st += tm;
-        g.dense_ok = d_ok;
-        g.hash_ok = h_ok;
+      const bool d2 = dok && sw + w <= kDenseCap;
+      const bool h2 = hok && sb + b <= kHashCap && st + tm <= unit_terms &&
+                      (i - row0 + 1) <= hash_rows_max;
+      if (d2 || h2) {
+        sw += w;
+        sb += b;
+        st += tm;
+        dok = d2;
+        hok = h2;
         continue;
       }
-      close();
+      close(i);
+      open = false;
     }
     if (tm == 0) continue;
-    const bool d_ok = w <= kDenseCap;
-    const bool h_ok = b <= kHashCap && tm <= unit_terms;
-    if (d_ok || h_ok) {
+    const bool d2 = w <= kDenseCap;
+    const bool h2 = b <= kHashCap && tm <= unit_terms;
+    if (d2 || h2) {
       open = true;
-      g = Group{i, i + 1, w, b, tm, d_ok, h_ok};
+      row0 = i;
+      sw = w;
+      sb = b;
+      st = tm;
+      dok = d2;
+      hok = h2;
       continue;
     }
     // one row too wide for a dense tile and too heavy for a hash tile:
@@ -858,55 +897,77 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     }
     item_tile[i] = first | kWinFlag;
   }
-  close();
+  if (open) close(n);
 
-  // Renumber heavy-first (the router keeps the heaviest tiles in shared
-  // memory); a split row's windows stay consecutive.
-  std::vector<uint32_t> groups;
-  for (uint32_t t = 0; t < tiles.size();) {
-    groups.push_back(t);
-    t += tiles[t].nwin ? tiles[t].nwin : 1;
-  }
-  std::vector<uint64_t> gterms(tiles.size(), 0);
-  for (uint32_t g0 : groups) {
-    const uint32_t k = tiles[g0].nwin ? tiles[g0].nwin : 1;
-    for (uint32_t q = 0; q < k; ++q) gterms[g0] += tiles[g0 + q].terms;
-  }
-  std::stable_sort(groups.begin(), groups.end(),
-                   [&](uint32_t a, uint32_t b) { return gterms[a] > gterms[b]; });
-  std::vector<uint32_t> new_id(tiles.size());
-  std::vector<Tile> out;
-  out.reserve(tiles.size());
-  for (uint32_t g0 : groups) {
-    const uint32_t k = tiles[g0].nwin ? tiles[g0].nwin : 1;
-    for (uint32_t q = 0; q < k; ++q) {
-      new_id[g0 + q] = (uint32_t)out.size();
-      out.push_back(tiles[g0 + q]);
+  // With more tiles than the router's shared counters, renumber heavy-first
+  // so the heaviest tiles get shared counters (bucketed by log2(terms), a
+  // split row's windows kept consecutive).
+  if (tiles.size() > kTileSmem) {
+    std::vector<std::vector<uint32_t>> bins(64);
+    for (uint32_t t = 0; t < tiles.size();) {
+      const uint32_t k = tiles[t].nwin ? tiles[t].nwin : 1;
+      uint64_t gt = 0;
+      for (uint32_t q = 0; q < k; ++q) gt += tiles[t + q].terms;
+      const int lg = gt ? 63 - __builtin_clzll(gt) : 0;
+      bins[63 - lg].push_back(t);
+      t += k;
     }
+    std::vector<uint32_t> new_id(tiles.size());
+    std::vector<Tile> out;
+    out.reserve(tiles.size());
+    for (auto& bin : bins)
+      for (uint32_t g0 : bin) {
+        const uint32_t k = tiles[g0].nwin ? tiles[g0].nwin : 1;
+        for (uint32_t q = 0; q < k; ++q) {
+          new_id[g0 + q] = (uint32_t)out.size();
+          out.push_back(tiles[g0 + q]);
+        }
+      }
+    for (uint32_t i = 0; i < n; ++i)
+      if (item_tile[i] != kNone)
+        item_tile[i] = new_id[item_tile[i] & ~kWinFlag] | (item_tile[i] & kWinFlag);
+    tiles.swap(out);
   }
-  for (uint32_t i = 0; i < n; ++i)
-    if (item_tile[i] != kNone) item_tile[i] = new_id[item_tile[i] & ~kWinFlag] | (item_tile[i] & kWinFlag);
-  J->tiles.swap(out);
 
-  // units heavy-first; slabs for split dense tiles
+  // Unit order: a unit covers the fraction [local, local+1)/n_units of its
+  // tile's entry list, which the router wrote in (roughly) transaction order.
+  // Running units in order of that fraction keeps the ~148 concurrently
+  // active units on nearby transactions, so the rows they re-read stay in
+  // L2 (64 fraction bins, no sort). Single-unit tiles follow.
   J->units.clear();
   J->split.clear();
   J->n_slabs = 0;
-  std::vector<std::pair<uint64_t, Unit>> us;
-  for (uint32_t t = 0; t < J->tiles.size(); ++t) {
-    Tile& tt = J->tiles[t];
+  constexpr int kFracBins = 64;
+  std::vector<uint32_t> bin_count(kFracBins + 1, 0);
+  uint64_t n_units = 0;
+  for (uint32_t t = 0; t < tiles.size(); ++t) {
+    Tile& tt = tiles[t];
+    n_units += tt.n_units;
     if (tt.n_units > 1) {
       tt.slab_base = J->n_slabs;
       J->n_slabs += tt.n_units;
       J->split.push_back(t);
+      for (uint32_t u = 0; u < tt.n_units; ++u)
+        ++bin_count[(uint64_t)(2 * u + 1) * kFracBins / (2 * tt.n_units)];
+    } else {
+      ++bin_count[kFracBins];
     }
-    for (uint32_t u = 0; u < tt.n_units; ++u) us.push_back({tt.terms / tt.n_units, Unit{t, u}});
   }
-  std::stable_sort(us.begin(), us.end(), [](auto& a, auto& b) { return a.first > b.first; });
-  for (auto& x : us) J->units.push_back(x.second);
+  std::vector<uint32_t> bin_pos(kFracBins + 1, 0);
+  for (int k = 1; k <= kFracBins; ++k) bin_pos[k] = bin_pos[k - 1] + bin_count[k - 1];
+  J->units.resize(n_units);
+  for (uint32_t t = 0; t < tiles.size(); ++t) {
+    const Tile& tt = tiles[t];
+    if (tt.n_units > 1) {
+      for (uint32_t u = 0; u < tt.n_units; ++u)
+        J->units[bin_pos[(uint64_t)(2 * u + 1) * kFracBins / (2 * tt.n_units)]++] = Unit{t, u};
+    } else {
+      J->units[bin_pos[kFracBins]++] = Unit{t, 0};
+    }
+  }
 
   uint64_t cap = 0;
-  for (auto& t : J->tiles) cap += t.mode == 0 ? t.width : kHashCap;
+  for (auto& t : tiles) cap += t.mode == 0 ? t.width : kHashCap;
   J->max_entries = cap;
 }
 
@@ -961,22 +1022,24 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     if (n_tx > 0 && n_items > 0) {
       auto kern = upper_only ? k_item_terms<true> : k_item_terms<false>;
       const uint32_t ns = std::min<uint32_t>(n_items, kStatSmemItems);
-      const size_t smem = kOffBytes + ns * 4;
+      const size_t smem = kOffBytes + ns * 8;  // two u32 arrays
       JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kOffBytes + kStatSmemItems * 4)));
+                                 (int)(kOffBytes + kStatSmemItems * 8)));
       const int64_t chunks = (n_tx + kChunkTx - 1) / kChunkTx;
       const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
       kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, J->d_terms, J->d_maxlen);
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
     }
-    std::vector<unsigned long long> terms(nn);
+    std::vector<unsigned long long> stats(nn), terms(nn), occ(nn);
     unsigned int maxlen = 0;
     int64_t nnz = 0;
-    JCUDA(cudaMemcpyAsync(terms.data(), J->d_terms, nn * 8, cudaMemcpyDeviceToHost, st));
+    JCUDA(cudaMemcpyAsync(stats.data(), J->d_terms, nn * 8, cudaMemcpyDeviceToHost, st));
     JCUDA(cudaMemcpyAsync(&maxlen, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
     if (n_tx > 0) JCUDA(cudaMemcpyAsync(&nnz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
+    auto t_sync0 = std::chrono::steady_clock::now();
     JCUDA(cudaStreamSynchronize(st));
+    auto t_sync1 = std::chrono::steady_clock::now();
     J->nnz = nnz;
     if (maxlen > kMaxLen) {
       crop_set_error(CROP_EINPUT, "transaction of %u items exceeds the %u-item limit", maxlen, kMaxLen);
@@ -990,10 +1053,41 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       goto fail;
     }
     J->total_terms = 0;
-    for (uint32_t i = 0; i < n_items; ++i) J->total_terms += terms[i];
+    for (uint32_t i = 0; i < n_items; ++i) {
+      terms[i] = stats[i] & (kOccOne - 1);
+      occ[i] = stats[i] >> 40;
+      J->total_terms += terms[i];
+    }
     std::vector<uint32_t>& item_tile = J->h_item_tile;
+    auto t_p0 = std::chrono::steady_clock::now();
     plan_tiles(J, terms, item_tile);
+    auto t_p1 = std::chrono::steady_clock::now();
     const uint32_t nt = (uint32_t)J->tiles.size();
+    // entry capacity per tile: a row occurrence with a partner after it makes
+    // at most one entry per tile (per window for split rows)
+    std::vector<unsigned long long> cap(nt, 0);
+    for (uint32_t i = 0; i < n_items; ++i) {
+      if (item_tile[i] == kNone) continue;
+      const uint32_t t = item_tile[i] & ~kWinFlag;
+      if (item_tile[i] & kWinFlag)
+        for (uint32_t w = 0; w < J->tiles[t].nwin; ++w) cap[t + w] += occ[i];
+      else
+        cap[t] += occ[i];
+    }
+    J->h_tile_base.assign(nt, 0);
+    J->h_tile_end.assign(nt, 0);
+    unsigned long long run = 0;
+    for (uint32_t t = 0; t < nt; ++t) {
+      J->h_tile_base[t] = run;
+      run += cap[t];
+      J->h_tile_end[t] = run;
+    }
+    J->entry_cap = run;
+    {
+      const double per_tx = n_tx ? (double)run / (double)n_tx : 1.0;
+      int c = (int)(kStage / std::max(1.0, 1.25 * per_tx));
+      J->route_chunk_tx = std::max(8, std::min(kChunkTx, c));
+    }
     JCUDA(cudaMallocAsync(&J->d_item_tile, nn * 4, st));
     JCUDA(cudaMallocAsync(&J->d_tiles, std::max<size_t>(1, nt) * sizeof(Tile), st));
     JCUDA(cudaMallocAsync(&J->d_units, std::max<size_t>(1, J->units.size()) * sizeof(Unit), st));
@@ -1001,6 +1095,11 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     JCUDA(cudaMallocAsync(&J->d_tile_entries, std::max<size_t>(1, nt) * 4, st));
     JCUDA(cudaMallocAsync(&J->d_tile_ebase, std::max<size_t>(1, nt) * 8, st));
     JCUDA(cudaMallocAsync(&J->d_tile_cursor, std::max<size_t>(1, nt) * 8, st));
+    JCUDA(cudaMallocAsync(&J->d_tile_end, std::max<size_t>(1, nt) * 8, st));
+    if (nt) {
+      JCUDA(cudaMemcpyAsync(J->d_tile_ebase, J->h_tile_base.data(), nt * 8, cudaMemcpyHostToDevice, st));
+      JCUDA(cudaMemcpyAsync(J->d_tile_end, J->h_tile_end.data(), nt * 8, cudaMemcpyHostToDevice, st));
+    }
     JCUDA(cudaMallocAsync(&J->d_total_entries, 8, st));
     JCUDA(cudaMallocAsync(&J->d_unit_counter, 4, st));
     JCUDA(cudaMallocAsync(&J->d_overflow, 4, st));
@@ -1013,14 +1112,24 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     if (!J->split.empty())
       JCUDA(cudaMemcpyAsync(J->d_split, J->split.data(), J->split.size() * 4, cudaMemcpyHostToDevice, st));
     if (J->n_slabs) JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kDenseCap * 4, st));
-    // every entry carries >= 1 term and a position emits at most one entry
-    // per column window, so entries <= min(total terms, nnz * max windows)
-    uint64_t maxwin = 1;
-    for (auto& t : J->tiles) maxwin = std::max<uint64_t>(maxwin, t.nwin);
-    J->entry_cap = std::min<uint64_t>(J->total_terms, (uint64_t)nnz * maxwin);
-    if (J->entry_cap >= (1ull << 32)) J->entry_cap = (1ull << 32) - 1;
+    if (J->entry_cap >= (1ull << 32)) {
+      crop_set_error(CROP_ERESOURCE, "%llu entries exceed the 2^32 limit of one job; split the stream",
+                     (unsigned long long)J->entry_cap);
+      rc = CROP_ERESOURCE;
+      goto fail;
+    }
     JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
     // host vectors read by the async uploads live in J until destroy
+    if (getenv("CROP_DEBUG_TIMING")) {
+      auto t_end = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) {
+        return std::chrono::duration_cast<std::chrono::microseconds>(b - a).count();
+      };
+      fprintf(stderr, "[crop_pairs_create] wait passA %lld us, unpack %lld us, plan %lld us, "
+              "caps+uploads %lld us, tiles %zu\n", (long long)us(t_sync0, t_sync1),
+              (long long)us(t_sync1, t_p0), (long long)us(t_p0, t_p1), (long long)us(t_p1, t_end),
+              J->tiles.size());
+    }
   }
 #undef JCUDA
   *job = J;
@@ -1047,41 +1156,30 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMemsetAsync(d_n_entries, 0, 8, st));
   if (nt == 0 || J->n_tx == 0) return CROP_OK;
   const bool up = J->upper != 0;
-  const int64_t chunks = (J->n_tx + kChunkTx - 1) / kChunkTx;
-  const int pass_grid = (int)std::min<int64_t>(kNumSMs, chunks);
   const uint32_t ns = std::min(nt, kTileSmem);
-  const size_t route_smem = kOffBytes + ns * 4;
   auto mark = [&](int k) {
     if (J->timing) cudaEventRecord(J->ev[k], st);
   };
   mark(0);
-  // pass B1: entries per tile
-  CROP_CUDA(cudaMemsetAsync(J->d_tile_entries, 0, nt * 4, st));
+  // route: one walk, staged per chunk, ranges claimed per touched tile
+  CROP_CUDA(cudaMemcpyAsync(J->d_tile_cursor, J->d_tile_ebase, nt * 8, cudaMemcpyDeviceToDevice, st));
   {
-    auto kern = up ? k_route_count<true> : k_route_count<false>;
+    auto kern = up ? k_route<true> : k_route<false>;
+    const size_t smem = (size_t)(J->route_chunk_tx + 1) * 8 + (size_t)kStage * 16 + 16 + ns * 4;
     CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(kOffBytes + kTileSmem * 4)));
-    kern<<<pass_grid, kPassThreads, route_smem, st>>>(J->offsets, J->items, J->n_tx,
-                                                      J->d_item_tile, J->d_tiles, nt,
-                                                      J->d_tile_entries);
+                                   (int)((kChunkTx + 1) * 8 + kStage * 16 + 16 + kTileSmem * 4)));
+    const int64_t rchunks = (J->n_tx + J->route_chunk_tx - 1) / J->route_chunk_tx;
+    const int rgrid = (int)std::min<int64_t>(kNumSMs, rchunks);
+    kern<<<rgrid, kPassThreads, smem, st>>>(J->offsets, J->items, J->n_tx, J->route_chunk_tx,
+                                            J->d_item_tile, J->d_tiles, nt, J->d_tile_cursor,
+                                            J->d_tile_end, J->d_entries, J->d_overflow);
     CROP_LAUNCH_CHECK();
   }
   mark(1);
-  k_exclusive_scan_u32_to_u64<<<1, 1024, 0, st>>>(J->d_tile_entries, nt, J->d_tile_ebase,
-                                                   J->d_total_entries);
+  k_tile_entries<<<(nt + 255) / 256, 256, 0, st>>>(J->d_tile_cursor, J->d_tile_ebase, nt,
+                                                   J->d_tile_entries);
   CROP_LAUNCH_CHECK();
   mark(2);
-  CROP_CUDA(cudaMemcpyAsync(J->d_tile_cursor, J->d_tile_ebase, nt * 8, cudaMemcpyDeviceToDevice, st));
-  {
-    auto kern = up ? k_route_write<true> : k_route_write<false>;
-    CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(kOffBytes + kTileSmem * 4)));
-    kern<<<pass_grid, kPassThreads, route_smem, st>>>(J->offsets, J->items, J->n_tx,
-                                                      J->d_item_tile, J->d_tiles, nt,
-                                                      J->d_tile_cursor, J->d_entries,
-                                                      J->entry_cap, J->d_overflow);
-    CROP_LAUNCH_CHECK();
-  }
   mark(3);
   // count
   CROP_CUDA(cudaMemsetAsync(J->d_unit_counter, 0, 4, st));
@@ -1119,7 +1217,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     CROP_LAUNCH_CHECK();
     mark(5);
   }
-  crop_count_launches(5);
+  crop_count_launches(3);
   return CROP_OK;
 }
 

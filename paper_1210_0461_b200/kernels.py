@@ -218,7 +218,7 @@ class PairCountJob:
     def phase_ms(self) -> dict:
         out = (ctypes.c_float * 4)()
         nat.check(nat.load().crop_pairs_phase_ms(self._h, out))
-        return {"route_count": out[0], "scan": out[1], "route_write": out[2], "count": out[3]}
+        return {"route": out[0], "tile_entries": out[1], "count": out[3]}
 
     def overflowed(self) -> bool:
         flag = ctypes.c_int()

@@ -45,14 +45,18 @@ namespace {
 
 constexpr int kCountThreads = 1024;
 constexpr int kCountWarps = kCountThreads / 32;
-constexpr uint32_t kDenseCap = 50176;                // dense u32 counters per tile (196 KB)
-constexpr size_t kTableBytes = (size_t)kDenseCap * 4;
-constexpr uint32_t kHashSlots = kTableBytes / 8;     // 25088 key+count slots
-constexpr uint32_t kHashCap = 16384;                 // max distinct keys per hash tile
+constexpr uint32_t kDenseCap = 65536;                // dense u16 counters per tile (128 KB)
+constexpr size_t kTableBytes = (size_t)kDenseCap * 2;
+constexpr uint32_t kHashSlots = 21760;               // u32 keys + u16 counts (127.5 KB)
+constexpr uint32_t kHashCap = 14336;                 // max distinct keys per hash tile
+constexpr uint32_t kHashHalf = kHashSlots / 2;       // interleaved u16 hash counts
+constexpr uint32_t kUnitEntries = 65535;             // entries per unit: u16 counters never wrap
 constexpr uint32_t kMaxLen = 8192;                   // longest transaction
-constexpr int kJobWords = 5;                         // per-lane job record (shared memory)
+constexpr int kBufWords = 512;                       // per-warp staging of transaction suffixes
+constexpr size_t kBufBytes = (size_t)kCountWarps * kBufWords * 4;
+constexpr int kJobWords = 5;                         // per-lane entry records (shared memory)
 constexpr size_t kJobBytes = (size_t)kCountWarps * 32 * kJobWords * 4;
-constexpr size_t kCountSmem = kTableBytes + kJobBytes + 64;
+constexpr size_t kCountSmem = kTableBytes + kBufBytes + kJobBytes + 64;
 constexpr int kPassThreads = 1024;
 constexpr int kChunkTx = 4096;                       // transactions per position-parallel chunk
 constexpr size_t kOffBytes = (kChunkTx + 1) * 8;
@@ -380,8 +384,9 @@ struct CountArgs {
   uint32_t* out_col;
   uint32_t* out_count;
   unsigned long long* out_n;
-  uint32_t* slabs;
+  uint32_t* slabs;  // kHalf words (two interleaved u16 counters) per unit
   unsigned int* tile_done;
+  unsigned long long* dbg;  // optional: per-kind [cycles count, cycles emit, units, entries]
 };
 
 __device__ __forceinline__ uint32_t lower_bound_items(const uint32_t* __restrict__ a, uint32_t lo,
@@ -413,182 +418,222 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   return r;
 }
 
-// Persistent CTAs pull units heavy-first. For each warp batch of 32 entries
-// the pairs are flattened across lanes: an inclusive scan of the per-entry
-// pair counts, then each iteration maps lane -> entry with a 32-bit boundary
-// mask (__reduce_or_sync) and popc, so every lane counts one pair per
-// iteration however the pairs split over entries. For single-row entries the
-// column position is t + delta[entry] (one shared load); the column item of
-// the next iteration is loaded before the current one is counted. The inner
-// loop is specialised per tile kind (chosen once per unit):
-//   kDenseRow    one row, all columns after it (UPPER) / all columns (full)
-//   kDenseWindow one row, columns [c0, c1)
-//   kDenseMulti  several rows, closed-form triangle (UPPER) / rectangle
-//   kHash        open-addressing keys (row - row0) << col_bits | col
+// Persistent CTAs pull units (tiles or parts of split tiles) in order. A
+// warp takes a batch of up to 32 entries and
+//   1. stages every entry's words -- [row item(s) | column items] -- in its
+//      shared buffer with one flattened, coalesced copy (lane -> word via a
+//      32-bit boundary mask from __reduce_or_sync + popc);
+//   2. expands the entries into ROW-JOBS (one per row of a run), and
+//   3. flattens the row-jobs' pairs across lanes: every pair is then two
+//      shared-memory loads (row item, column item) and one shared-memory
+//      atomic on a u16 counter (two counters per 32-bit word; a unit holds
+//      <= 65,535 entries, so no counter can wrap).
+// Entries longer than the buffer (> 512 staged words, i.e. transactions
+// longer than 512 items) take a direct path from global memory.
 // A tile split over several units is reduced by the last unit to finish:
-// the others leave their counters in a slab (L2-resident by then) and the
-// last one adds them into its shared table before compacting.
+// the others leave their u16 counters in a slab (L2-resident by then) and the
+// last one sums them on the fly while compacting.
 enum TileKind { kDenseRow = 0, kDenseWindow = 1, kDenseMulti = 2, kHash = 3 };
 
-struct WarpJobs {
-  uint32_t* delta;  // column position - flattened index (single-row entries)
-  uint32_t* excl;   // first flattened pair index of the entry
-  uint32_t* item;   // row item of the entry's first row
-  uint32_t* x;      // entry.x
-  uint32_t* y;      // entry.y
+struct WarpSmem {
+  uint32_t* buf;  // staged words
+  uint32_t *off, *hp, *cs, *m, *R;  // per-entry records of the current batch
 };
 
-template <int KIND, bool UPPER, bool FILTER>
-__device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T, uint64_t e0,
-                                              uint64_t e1, const WarpJobs& J, uint32_t* table,
-                                              uint32_t* hcount, unsigned int* s_next) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* __restrict__ items = A.items;
-  const uint32_t n = A.n_items;
-  const uint32_t col_lo = UPPER ? T.row0 + 1 : 0;  // kDenseRow slot origin
+// boundary-mask lane -> owner for flattened index t0 + lane, given each lane's
+// inclusive end `incl` (warp-collective)
+__device__ __forceinline__ uint32_t owner_step(uint32_t incl, uint32_t t0, uint32_t& owner_base) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t bit = (incl > t0 && incl < t0 + 32) ? (1u << (incl - t0)) : 0u;
+  const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
+  const uint32_t at_end = __reduce_add_sync(0xffffffffu, (incl == t0 + 32) ? 1u : 0u);
+  const uint32_t owner = owner_base + __popc(B & (0xffffffffu >> (31 - lane)));
+  owner_base += __popc(B) + at_end;
+  return owner;
+}
 
-  auto count_pair = [&](uint32_t i, uint32_t j) {
-    if (KIND == kDenseRow || KIND == kDenseWindow) i = T.row0;  // single-row tiles
+// u16 counters, two per 32-bit word, interleaved across the two halves of
+// the table (slot s lives in word s mod 32768, half s / 32768) so that
+// neighbouring slots -- consecutive columns of one row -- never share a word
+// (no same-address conflicts inside a warp's atomic).
+constexpr uint32_t kHalf = kDenseCap / 2;
+
+__device__ __forceinline__ void bump16(uint32_t* words, uint32_t slot) {
+  atomicAdd(&words[slot & (kHalf - 1)], 1u << ((slot / kHalf) << 4));
+}
+__device__ __forceinline__ uint32_t read16(const uint32_t* words, uint32_t slot) {
+  return (words[slot & (kHalf - 1)] >> ((slot / kHalf) << 4)) & 0xFFFFu;
+}
+
+template <int KIND, bool UPPER, bool FILTER>
+struct Counter {
+  const CountArgs& A;
+  const Tile& T;
+  uint32_t* table;  // dense: u16 counters; hash: u32 keys
+  uint32_t* hcnt;   // hash: u16 counts (interleaved like the dense table)
+  // per-row constant: dense -> slot = base + j; hash -> key = base | j
+  __device__ __forceinline__ uint32_t row_base(uint32_t i) const {
+    if (KIND == kDenseRow) return UPPER ? 0u - (T.row0 + 1) : 0u;
+    if (KIND == kDenseWindow) return 0u - T.c0;
+    if (KIND == kDenseMulti) {
+      // slots before row i: k*w0 - k(k-1)/2 with k = i - row0, w0 = row0's
+      // width; exact in 32-bit modular arithmetic since the result < 2^16
+      const uint32_t k = i - T.row0;
+      if (!UPPER) return k * A.n_items;
+      const uint32_t w0 = A.n_items - 1 - T.row0;
+      const uint32_t tri = (uint32_t)(((unsigned long long)k * (k - 1)) >> 1);
+      return k * w0 - tri - i - 1;
+    }
+    return (i - T.row0) << A.col_bits;
+  }
+  __device__ __forceinline__ void operator()(uint32_t i, uint32_t base, uint32_t j) const {
     if (FILTER) {
       uint32_t b = A.h_row[i] + A.h_col[j];
       if (b >= A.kappa) b -= A.kappa;
       if (b < A.start || b >= A.stop) return;
     }
-    if (KIND == kDenseRow) {
-      atomicAdd(&table[j - col_lo], 1u);
-    } else if (KIND == kDenseWindow) {
-      atomicAdd(&table[j - T.c0], 1u);
-    } else if (KIND == kDenseMulti) {
-      const uint32_t slot = UPPER ? (uint32_t)tri_rowbase(i, T.row0, n) + (j - i - 1)
-                                  : (i - T.row0) * n + j;
-      atomicAdd(&table[slot], 1u);
-    } else {
-      const uint32_t key = ((i - T.row0) << A.col_bits) | j;
-      uint32_t s = __umulhi(mix32(key), kHashSlots);
-      for (;;) {
-        const uint32_t k = table[s];
-        if (k == key) {
-          atomicAdd(&hcount[s], 1u);
-          break;
-        }
-        if (k == kEmpty32) {
-          const uint32_t old = atomicCAS(&table[s], kEmpty32, key);
-          if (old == kEmpty32 || old == key) {
-            atomicAdd(&hcount[s], 1u);
-            break;
-          }
-        }
-        if (++s == kHashSlots) s = 0;
-      }
+    if (KIND != kHash) {
+      bump16(table, base + j);
+      return;
     }
-  };
-  // rows > 1 only for UPPER runs in kDenseMulti / kHash tiles
-  constexpr bool MULTI = UPPER && (KIND == kDenseMulti || KIND == kHash);
+    const uint32_t key = base | j;
+    uint32_t s = __umulhi(mix32(key), kHashSlots);
+    for (;;) {
+      const uint32_t k = table[s];
+      if (k == key) break;
+      if (k == kEmpty32) {
+        const uint32_t old = atomicCAS(&table[s], kEmpty32, key);
+        if (old == kEmpty32 || old == key) break;
+      }
+      if (++s == kHashSlots) s = 0;
+    }
+    atomicAdd(&hcnt[s % kHashHalf], 1u << ((s / kHashHalf) << 4));
+  }
+};
 
-  (void)warp;
+// Direct path for one long entry (staged length > kBufWords): lanes stride
+// over each row's columns, loading from global memory.
+template <typename Cnt>
+__device__ void count_long_entry(const uint32_t* __restrict__ items, uint32_t hp, uint32_t cs,
+                                 uint32_t m, uint32_t R, const Cnt& cnt) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint32_t i = items[r == 0 ? hp : cs + r - 1];
+    const uint32_t base = cnt.row_base(i);
+    for (uint32_t c = r + 1 + lane; c < m; c += 32) cnt(i, base, items[cs + c - 1]);
+  }
+}
+
+// Flattened path for tiles whose rows are short (single-row and hash tiles:
+// c2's shape): the pairs of 32 entries are spread across the lanes (entry of
+// a lane found with a 32-bit boundary mask, __reduce_or_sync + popc) and the
+// column items come straight from global memory through a three-stage
+// software pipeline.
+template <int KIND, bool UPPER, bool FILTER>
+__device__ __forceinline__ void count_entries_flat(const CountArgs& A, const Tile& T, uint64_t e0,
+                                                   uint64_t e1, const WarpSmem& W,
+                                                   uint32_t* table, uint32_t* hcnt,
+                                                   unsigned int* s_next) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t* __restrict__ items = A.items;
+  const Counter<KIND, UPPER, FILTER> cnt{A, T, table, hcnt};
+  constexpr bool SINGLE = KIND == kDenseRow || KIND == kDenseWindow;
+  constexpr bool MULTI = UPPER && KIND == kHash;  // UPPER hash runs may hold several rows
+  const uint32_t base_single = SINGLE ? cnt.row_base(T.row0) : 0;
+  uint32_t* J_delta = W.off;
+  uint32_t* J_excl = W.hp;
+  uint32_t* J_item = W.cs;
+  uint32_t* J_x = W.m;
+  uint32_t* J_y = W.R;
   for (;;) {
-    // warps take batches of 32 entries dynamically (no tail imbalance)
-    uint32_t b = 0;
-    if (lane == 0) b = atomicAdd(s_next, 1u);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    const uint64_t eb_w = e0 + (uint64_t)b * 32;
+    uint32_t bidx = 0;
+    if (lane == 0) bidx = atomicAdd(s_next, 1u);
+    bidx = __shfl_sync(0xffffffffu, bidx, 0);
+    const uint64_t eb_w = e0 + (uint64_t)bidx * 32;
     if (eb_w >= e1) break;
     const uint64_t e = eb_w + lane;
-    uint32_t cnt = 0, x = 0, y = 0, first = 0, ri = 0;
+    uint32_t cn = 0, x = 0, y = 0, first = 0, ri = 0;
     if (e < e1) {
       const uint2 en = A.entries[e];
       x = en.x;
       y = en.y;
       if (UPPER) {
         const uint32_t len = y & 0xFFFFu, rows = y >> 16;
-        if (KIND != kDenseRow && KIND != kDenseWindow) ri = items[x];
+        if (!SINGLE) ri = items[x];
         if (KIND == kDenseWindow) {
           first = lower_bound_items(items, x + 1, x + len, T.c0);
-          cnt = lower_bound_items(items, first, x + len, T.c1) - first;
+          cn = lower_bound_items(items, first, x + len, T.c1) - first;
         } else {
           first = x + 1;
-          cnt = rows * (len - 1) - rows * (rows - 1) / 2;
+          cn = rows * (len - 1) - rows * (rows - 1) / 2;
         }
       } else {
         const uint32_t L = y & 0xFFFFu, p = y >> 16;
         ri = items[x + p];
         if (KIND == kDenseWindow) {
           first = lower_bound_items(items, x, x + L, T.c0);
-          cnt = lower_bound_items(items, first, x + L, T.c1) - first;
+          cn = lower_bound_items(items, first, x + L, T.c1) - first;
         } else {
           first = x;
-          cnt = L;
+          cn = L;
         }
       }
     }
-    const uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t excl = incl - cnt;
-    J.delta[lane] = first - excl;
-    J.excl[lane] = excl;
-    J.item[lane] = ri;
+    const uint32_t incl = warp_incl_scan(cn);
+    J_delta[lane] = first - (incl - cn);
+    J_excl[lane] = incl - cn;
+    J_item[lane] = ri;
     if (MULTI) {
-      J.x[lane] = x;
-      J.y[lane] = y;
+      J_x[lane] = x;
+      J_y[lane] = y;
     }
     const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
     __syncwarp();
     uint32_t owner_base = 0;
-    auto owner_of = [&](uint32_t t0) {
-      // entries ending strictly inside [t0, t0+32) move the owner forward
-      const uint32_t bit = (incl > t0 && incl < t0 + 32) ? (1u << (incl - t0)) : 0u;
-      const uint32_t B = __reduce_or_sync(0xffffffffu, bit);
-      const uint32_t at_end = __reduce_add_sync(0xffffffffu, (incl == t0 + 32) ? 1u : 0u);
-      const uint32_t owner = owner_base + __popc(B & (0xffffffffu >> (31 - lane)));
-      owner_base += __popc(B) + at_end;
-      return owner;
-    };
-    // (row item, column item) of flattened pair t owned by entry `o`
-    auto locate_pair = [&](uint32_t t, uint32_t o, uint32_t& i, uint32_t& jpos) {
+    auto locate = [&](uint32_t t, uint32_t o, uint32_t& i, uint32_t& jpos) {
       if (MULTI) {
-        const uint32_t yy = J.y[o];
+        const uint32_t yy = J_y[o];
         if ((yy >> 16) > 1) {
-          uint32_t loc = t - J.excl[o], w = (yy & 0xFFFFu) - 1, k = 0;
+          uint32_t loc = t - J_excl[o], w = (yy & 0xFFFFu) - 1, k = 0;
           while (loc >= w) {
             loc -= w;
             ++k;
             --w;
           }
-          const uint32_t xx = J.x[o];
-          i = k ? items[xx + k] : J.item[o];
+          const uint32_t xx = J_x[o];
+          i = k ? items[xx + k] : J_item[o];
           jpos = xx + k + 1 + loc;
           return;
         }
       }
-      if (KIND != kDenseRow && KIND != kDenseWindow) i = J.item[o];
-      jpos = t + J.delta[o];
+      i = SINGLE ? T.row0 : J_item[o];
+      jpos = t + J_delta[o];
     };
-    // three-stage software pipeline: the column items of iterations t0+32 and
-    // t0+64 are in flight while iteration t0 is counted
     uint32_t i0 = 0, j0 = 0, i1 = 0, j1 = 0, jp;
     {
-      const uint32_t o = owner_of(0);  // warp-collective: never inside a divergent branch
+      const uint32_t o = owner_step(incl, 0, owner_base);  // warp-collective
       if (lane < S) {
-        locate_pair(lane, o, i0, jp);
+        locate(lane, o, i0, jp);
         j0 = items[jp];
       }
     }
     if (32 < S) {
-      const uint32_t o = owner_of(32);
+      const uint32_t o = owner_step(incl, 32, owner_base);
       if (32 + lane < S) {
-        locate_pair(32 + lane, o, i1, jp);
+        locate(32 + lane, o, i1, jp);
         j1 = items[jp];
       }
     }
     for (uint32_t t0 = 0; t0 < S; t0 += 32) {
       uint32_t i2 = 0, j2 = 0;
       if (t0 + 64 < S) {  // warp-uniform
-        const uint32_t o = owner_of(t0 + 64);
+        const uint32_t o = owner_step(incl, t0 + 64, owner_base);
         if (t0 + 64 + lane < S) {
-          locate_pair(t0 + 64 + lane, o, i2, jp);
+          locate(t0 + 64 + lane, o, i2, jp);
           j2 = items[jp];
         }
       }
-      if (t0 + lane < S) count_pair(i0, j0);
+      if (t0 + lane < S) cnt(i0, SINGLE ? base_single : cnt.row_base(i0), j0);
       i0 = i1;
       j0 = j1;
       i1 = i2;
@@ -598,23 +643,154 @@ __device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T,
   }
 }
 
+template <int KIND, bool UPPER, bool FILTER>
+__device__ __forceinline__ void count_entries(const CountArgs& A, const Tile& T, uint64_t e0,
+                                              uint64_t e1, const WarpSmem& W, uint32_t* table,
+                                              uint32_t* hcnt, unsigned int* s_next) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t* __restrict__ items = A.items;
+  const Counter<KIND, UPPER, FILTER> cnt{A, T, table, hcnt};
+  constexpr bool WINDOWED = KIND == kDenseWindow;
+  for (;;) {
+    // warps take batches of 32 entries dynamically (no tail imbalance)
+    uint32_t bidx = 0;
+    if (lane == 0) bidx = atomicAdd(s_next, 1u);
+    bidx = __shfl_sync(0xffffffffu, bidx, 0);
+    const uint64_t eb_w = e0 + (uint64_t)bidx * 32;
+    if (eb_w >= e1) break;
+    const uint64_t e = eb_w + lane;
+    // entry -> staged words: w0 = items[hp], w1.. = items[cs ..], m words, R rows
+    uint32_t hp = 0, cs = 0, m = 0, R = 0;
+    if (e < e1) {
+      const uint2 en = A.entries[e];
+      if (UPPER) {
+        const uint32_t len = en.y & 0xFFFFu;
+        hp = en.x;
+        cs = en.x + 1;
+        R = en.y >> 16;
+        if (WINDOWED) {
+          cs = lower_bound_items(items, en.x + 1, en.x + len, T.c0);
+          m = 1 + lower_bound_items(items, cs, en.x + len, T.c1) - cs;
+        } else {
+          m = len;
+        }
+      } else {
+        const uint32_t L = en.y & 0xFFFFu, p = en.y >> 16;
+        hp = en.x + p;
+        cs = WINDOWED ? lower_bound_items(items, en.x, en.x + L, T.c0) : en.x;
+        m = 1 + (WINDOWED ? lower_bound_items(items, cs, en.x + L, T.c1) - cs : L);
+        R = 1;
+      }
+    }
+    // long entries (more words than the buffer) take the direct path
+    const bool is_long = m > (uint32_t)kBufWords;
+    uint32_t long_mask = __ballot_sync(0xffffffffu, is_long);
+    while (long_mask) {
+      const int l = __ffs(long_mask) - 1;
+      long_mask &= long_mask - 1;
+      count_long_entry(items, __shfl_sync(0xffffffffu, hp, l), __shfl_sync(0xffffffffu, cs, l),
+                       __shfl_sync(0xffffffffu, m, l), __shfl_sync(0xffffffffu, R, l), cnt);
+    }
+    // compact the remaining entries into lanes [0, ne) (every staged entry
+    // has m >= 2 words and every row >= 1 pair, so the boundary masks below
+    // never see empty ranges)
+    const bool keep = m > 0 && !is_long;
+    const uint32_t kmask = __ballot_sync(0xffffffffu, keep);
+    const int ne = __popc(kmask);
+    if (keep) {
+      const int r = __popc(kmask & ((1u << lane) - 1u));
+      W.hp[r] = hp;
+      W.cs[r] = cs;
+      W.m[r] = m;
+      W.R[r] = R;
+    }
+    __syncwarp();
+    hp = lane < ne ? W.hp[lane] : 0;
+    cs = lane < ne ? W.cs[lane] : 0;
+    m = lane < ne ? W.m[lane] : 0;
+    R = lane < ne ? W.R[lane] : 0;
+    __syncwarp();
+    // sub-batches of lanes whose staged words fit the buffer
+    const uint32_t m_incl = warp_incl_scan(m);
+    const uint32_t pr = R * (m - 1) - R * (R - 1) / 2;  // pairs of the entry
+    uint32_t done = 0;  // staged words of earlier sub-batches
+    int l0 = 0;
+    while (l0 < ne) {
+      const uint32_t fits = __ballot_sync(0xffffffffu, lane >= l0 && lane < ne &&
+                                                           m_incl - done <= (uint32_t)kBufWords);
+      const int l1 = 32 - __clz(fits);  // fits always holds lane l0 (m <= kBufWords)
+      const bool in = lane >= l0 && lane < l1;
+      // lane group size G from the mean row length of the sub-batch
+      const uint32_t sumP = __reduce_add_sync(0xffffffffu, in ? pr : 0u);
+      const uint32_t sumR = __reduce_add_sync(0xffffffffu, in ? R : 0u);
+      const uint32_t meanP = sumP / (sumR ? sumR : 1u);
+      const int G = meanP >= 24 ? 32 : meanP >= 12 ? 16 : meanP >= 6 ? 8 : 4;
+      const int NG = 32 / G, grp = lane / G, gl = lane % G;
+      if (in) {
+        const int r = lane - l0;
+        W.off[r] = m_incl - done - m;
+        W.hp[r] = hp;
+        W.cs[r] = cs;
+        W.m[r] = m;
+        W.R[r] = R;
+      }
+      __syncwarp();
+      const int ns = l1 - l0;
+      // 1. stage each entry's words (asynchronous global -> shared copies)
+      for (int q = grp; q < ns; q += NG) {
+        const uint32_t qo = W.off[q], qh = W.hp[q], qc = W.cs[q], qm = W.m[q];
+        for (uint32_t k = gl; k < qm; k += G) {
+          const uint32_t* src_ptr = items + (k == 0 ? qh : qc + k - 1);
+          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(W.buf + qo + k);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src_ptr));
+        }
+      }
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncwarp();
+      // 2. every row of every entry: G lanes stride over its columns;
+      //    one shared load and one shared atomic per pair
+      for (int q = grp; q < ns; q += NG) {
+        const uint32_t qo = W.off[q], qm = W.m[q], qR = W.R[q];
+        for (uint32_t r = 0; r < qR; ++r) {
+          const uint32_t i = W.buf[qo + r];
+          const uint32_t base = cnt.row_base(i);
+          const uint32_t* cols = W.buf + qo + r + 1;
+          const uint32_t nc = qm - 1 - r;
+          uint32_t c = gl;
+          for (; c + G < nc; c += 2 * G) {
+            const uint32_t ja = cols[c], jb = cols[c + G];
+            cnt(i, base, ja);
+            cnt(i, base, jb);
+          }
+          if (c < nc) cnt(i, base, cols[c]);
+        }
+      }
+      __syncwarp();
+      done = __shfl_sync(0xffffffffu, m_incl, l1 - 1);
+      l0 = l1;
+    }
+  }
+}
+
 template <bool UPPER, bool FILTER>
 __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense counters or hash keys
-  uint32_t* hcount = table + kHashSlots;                 // hash counts
-  uint32_t* job = reinterpret_cast<uint32_t*>(smem + kTableBytes);
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + kTableBytes + kJobBytes);
+  uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense u16 counters / hash keys
+  uint32_t* hcnt = table + kHashSlots;                   // hash u16 counts
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(smem + kTableBytes);
+  uint32_t* job = reinterpret_cast<uint32_t*>(smem + kTableBytes + kBufBytes);
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + kTableBytes + kBufBytes + kJobBytes);
   __shared__ uint32_t s_warp[33];
   __shared__ unsigned long long s_base;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpJobs J;
-  J.delta = job + warp * 32 * kJobWords;
-  J.excl = J.delta + 32;
-  J.item = J.excl + 32;
-  J.x = J.item + 32;
-  J.y = J.x + 32;
+  WarpSmem W;
+  W.buf = bufs + warp * kBufWords;
+  W.off = job + warp * 32 * kJobWords;
+  W.hp = W.off + 32;
+  W.cs = W.hp + 32;
+  W.m = W.cs + 32;
+  W.R = W.m + 32;
   const uint32_t n = A.n_items;
 
   for (;;) {
@@ -635,65 +811,68 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
     const uint32_t width = T.width;
     const int kind = !dense ? kHash : windowed ? kDenseWindow : single_row ? kDenseRow : kDenseMulti;
 
-    if (dense) {
+    if (dense) {  // interleaved halves: clear the whole table
       uint4* t4 = reinterpret_cast<uint4*>(table);
-      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads)
+      for (uint32_t s = threadIdx.x; s < kHalf / 4; s += kCountThreads)
         t4[s] = make_uint4(0, 0, 0, 0);
     } else {
-      for (uint32_t s = threadIdx.x; s < kHashSlots; s += kCountThreads) {
-        table[s] = kEmpty32;
-        hcount[s] = 0;
-      }
+      for (uint32_t s = threadIdx.x; s < kHashSlots; s += kCountThreads) table[s] = kEmpty32;
+      for (uint32_t s = threadIdx.x; s < kHashHalf; s += kCountThreads) hcnt[s] = 0;
     }
     if (threadIdx.x == 0) s_misc[2] = 0;  // batch counter of this unit
     __syncthreads();
+    const long long dbg_t0 = A.dbg ? clock64() : 0;
 
     switch (kind) {
       case kDenseRow:
-        count_entries<kDenseRow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
+        count_entries_flat<kDenseRow, UPPER, FILTER>(A, T, e0, e1, W, table, hcnt, s_misc + 2);
         break;
       case kDenseWindow:
-        count_entries<kDenseWindow, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
+        count_entries_flat<kDenseWindow, UPPER, FILTER>(A, T, e0, e1, W, table, hcnt, s_misc + 2);
         break;
       case kDenseMulti:
-        count_entries<kDenseMulti, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
+        count_entries<kDenseMulti, UPPER, FILTER>(A, T, e0, e1, W, table, hcnt, s_misc + 2);
         break;
       default:
-        count_entries<kHash, UPPER, FILTER>(A, T, e0, e1, J, table, hcount, s_misc + 2);
+        count_entries_flat<kHash, UPPER, FILTER>(A, T, e0, e1, W, table, hcnt, s_misc + 2);
         break;
     }
     __syncthreads();
 
-    bool emit_now = true;
+    const long long dbg_t1 = A.dbg ? clock64() : 0;
+    bool emit_now = true, reduce = false;
+    const uint32_t* slab = nullptr;
     if (dense && T.n_units > 1) {
-      // leave this unit's counters in its slab; the last unit reduces them
-      uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * kDenseCap);
+      // leave this unit's counters in its slab; the last unit sums them
+      uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * kHalf);
       const uint4* src = reinterpret_cast<const uint4*>(table);
-      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads) dst[s] = src[s];
+      for (uint32_t s = threadIdx.x; s < kHalf / 4; s += kCountThreads) dst[s] = src[s];
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) s_misc[1] = atomicAdd(&A.tile_done[unit.tile], 1u) == T.n_units - 1;
       __syncthreads();
       emit_now = s_misc[1] != 0;
-      if (emit_now) {
-        __threadfence();
-        const uint32_t* slab = A.slabs + T.slab_base * kDenseCap;
-        for (uint32_t s = threadIdx.x; s < width; s += kCountThreads) {
-          uint32_t c = table[s];
-          for (uint32_t v = 0; v < T.n_units; ++v)
-            if (v != unit.local) c += __ldcg(slab + (uint64_t)v * kDenseCap + s);
-          table[s] = c;
-        }
-        __syncthreads();
-      }
+      reduce = emit_now;
+      if (reduce) __threadfence();
+      slab = A.slabs + T.slab_base * kHalf;
     }
     if (emit_now) {
+      auto count_at = [&](uint32_t s) -> uint32_t {
+        if (!dense) return (hcnt[s % kHashHalf] >> ((s / kHashHalf) << 4)) & 0xFFFFu;
+        uint32_t c = read16(table, s);
+        if (reduce) {
+          const uint32_t wi = s & (kHalf - 1), sh = (s / kHalf) << 4;
+          for (uint32_t v = 0; v < T.n_units; ++v)
+            if (v != unit.local) c += (__ldcg(slab + (uint64_t)v * kHalf + wi) >> sh) & 0xFFFFu;
+        }
+        return c;
+      };
       // compact non-zero counters: warp w owns a contiguous slot range
       const uint32_t slots = dense ? width : kHashSlots;
       const uint32_t per_warp = (slots + kCountWarps - 1) / kCountWarps;
       const uint32_t s_lo = min(slots, warp * per_warp), s_hi = min(slots, s_lo + per_warp);
       uint32_t mine = 0;
-      for (uint32_t s = s_lo + lane; s < s_hi; s += 32) mine += (dense ? table[s] : hcount[s]) != 0;
+      for (uint32_t s = s_lo + lane; s < s_hi; s += 32) mine += count_at(s) != 0;
       mine = warp_sum(mine);
       uint32_t total;
       uint32_t wbase = block_excl_scan(lane == 0 ? mine : 0, s_warp, total);
@@ -705,49 +884,50 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
         const uint32_t s = s0 + lane;
         uint32_t c = 0, i = 0, j = 0;
         if (s < s_hi) {
-          if (dense) {
-            c = table[s];
-            if (c) {
-              if (windowed) {
-                i = T.row0;
-                j = s + T.c0;
-              } else if (single_row) {
-                i = T.row0;
-                j = UPPER ? s + i + 1 : s;
-              } else if (UPPER) {
-                uint32_t lo = T.row0, hi = T.row1;  // last row with rowbase <= s
-                while (hi - lo > 1) {
-                  const uint32_t mid = (lo + hi) >> 1;
-                  if (tri_rowbase(mid, T.row0, n) <= s) lo = mid;
-                  else hi = mid;
-                }
-                i = lo;
-                j = (uint32_t)(s - tri_rowbase(i, T.row0, n)) + i + 1;
-              } else {
-                i = T.row0 + s / n;
-                j = s % n;
-              }
-            }
-          } else {
-            c = hcount[s];
-            if (c) {
+          c = count_at(s);
+          if (c) {
+            if (!dense) {
               const uint32_t key = table[s];
               i = T.row0 + (key >> A.col_bits);
               j = key & ((1u << A.col_bits) - 1u);
+            } else if (windowed) {
+              i = T.row0;
+              j = s + T.c0;
+            } else if (single_row) {
+              i = T.row0;
+              j = UPPER ? s + i + 1 : s;
+            } else if (UPPER) {
+              uint32_t lo = T.row0, hi = T.row1;  // last row with rowbase <= s
+              while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (tri_rowbase(mid, T.row0, n) <= s) lo = mid;
+                else hi = mid;
+              }
+              i = lo;
+              j = (uint32_t)(s - tri_rowbase(i, T.row0, n)) + i + 1;
+            } else {
+              i = T.row0 + s / n;
+              j = s % n;
             }
           }
         }
-        const uint32_t m = __ballot_sync(0xffffffffu, c != 0);
+        const uint32_t mk = __ballot_sync(0xffffffffu, c != 0);
         if (c) {
-          const uint64_t o = pos + __popc(m & ((1u << lane) - 1u));
+          const uint64_t o = pos + __popc(mk & ((1u << lane) - 1u));
           A.out_row[o] = i;
           A.out_col[o] = j;
           A.out_count[o] = c;
         }
-        pos += __popc(m);
+        pos += __popc(mk);
       }
     }
     __syncthreads();
+    if (A.dbg && threadIdx.x == 0) {
+      atomicAdd(&A.dbg[kind * 4 + 0], (unsigned long long)(dbg_t1 - dbg_t0));
+      atomicAdd(&A.dbg[kind * 4 + 1], (unsigned long long)(clock64() - dbg_t1));
+      atomicAdd(&A.dbg[kind * 4 + 2], 1ull);
+      atomicAdd(&A.dbg[kind * 4 + 3], (unsigned long long)(e1 - e0));
+    }
   }
 }
 
@@ -812,6 +992,7 @@ static void free_job(crop_pairs* j) {
 // over the rows, O(rows + tiles + units), no sorting: it sits between two
 // GPU phases, so every microsecond here is GPU idle time.
 static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& terms,
+                       const std::vector<unsigned long long>& occ,
                        std::vector<uint32_t>& item_tile) {
   const uint32_t n = J->n_items;
   const bool upper = J->upper != 0;
@@ -822,12 +1003,16 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   tiles.clear();
   tiles.reserve(1024);
   item_tile.assign(n, kNone);
-  auto units_for = [unit_terms](uint64_t tm) -> uint32_t {
-    const uint64_t u = (tm + unit_terms - 1) / unit_terms;
-    return (uint32_t)(u < 1 ? 1 : (u > 4096 ? 4096 : u));
+  // units: by terms for balance, and <= kUnitEntries entries each (u16
+  // counters); a tile's entries never exceed the sum of its rows' occ.
+  auto units_for = [unit_terms](uint64_t tm, uint64_t oc) -> uint32_t {
+    uint64_t u = (tm + unit_terms - 1) / unit_terms;
+    const uint64_t ue = (oc + kUnitEntries - 1) / kUnitEntries;
+    if (ue > u) u = ue;
+    return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
   };
   uint32_t row0 = 0;
-  uint64_t sw = 0, sb = 0, st = 0;
+  uint64_t sw = 0, sb = 0, st = 0, so = 0;
   bool open = false, dok = false, hok = false;
   auto close = [&](uint32_t row1) {
     Tile t{};
@@ -839,24 +1024,25 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     t.mode = dense ? 0 : 1;
     t.width = dense ? (uint32_t)sw : 0;
     t.terms = st;
-    t.n_units = dense ? units_for(st) : 1;
+    t.n_units = dense ? units_for(st, so) : 1;
     const uint32_t id = (uint32_t)tiles.size();
     for (uint32_t i = row0; i < row1; ++i)
       if (terms[i]) item_tile[i] = id;
     tiles.push_back(t);
   };
   for (uint32_t i = 0; i < n; ++i) {
-    const uint64_t tm = terms[i];
+    const uint64_t tm = terms[i], oc = occ[i];
     const uint64_t w = upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
     const uint64_t b = tm < w ? tm : w;
     if (open) {
       const bool d2 = dok && sw + w <= kDenseCap;
       const bool h2 = hok && sb + b <= kHashCap && st + tm <= unit_terms &&
-                      (i - row0 + 1) <= hash_rows_max;
+                      so + oc <= kUnitEntries && (i - row0 + 1) <= hash_rows_max;
       if (d2 || h2) {
         sw += w;
         sb += b;
         st += tm;
+        so += oc;
         dok = d2;
         hok = h2;
         continue;
@@ -866,13 +1052,14 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     }
     if (tm == 0) continue;
     const bool d2 = w <= kDenseCap;
-    const bool h2 = b <= kHashCap && tm <= unit_terms;
+    const bool h2 = b <= kHashCap && tm <= unit_terms && oc <= kUnitEntries;
     if (d2 || h2) {
       open = true;
       row0 = i;
       sw = w;
       sb = b;
       st = tm;
+      so = oc;
       dok = d2;
       hok = h2;
       continue;
@@ -892,7 +1079,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
       t.nwin = k == 0 ? nwin : 0;
       t.width = t.c1 - t.c0;
       t.terms = tm / nwin + 1;
-      t.n_units = units_for(t.terms);
+      t.n_units = units_for(t.terms, oc);
       tiles.push_back(t);
     }
     item_tile[i] = first | kWinFlag;
@@ -1060,7 +1247,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     }
     std::vector<uint32_t>& item_tile = J->h_item_tile;
     auto t_p0 = std::chrono::steady_clock::now();
-    plan_tiles(J, terms, item_tile);
+    plan_tiles(J, terms, occ, item_tile);
     auto t_p1 = std::chrono::steady_clock::now();
     const uint32_t nt = (uint32_t)J->tiles.size();
     // entry capacity per tile: a row occurrence with a partner after it makes
@@ -1111,7 +1298,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       JCUDA(cudaMemcpyAsync(J->d_units, J->units.data(), J->units.size() * sizeof(Unit), cudaMemcpyHostToDevice, st));
     if (!J->split.empty())
       JCUDA(cudaMemcpyAsync(J->d_split, J->split.data(), J->split.size() * 4, cudaMemcpyHostToDevice, st));
-    if (J->n_slabs) JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kDenseCap * 4, st));
+    if (J->n_slabs) JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kHalf * 4, st));
     if (J->entry_cap >= (1ull << 32)) {
       crop_set_error(CROP_ERESOURCE, "%llu entries exceed the 2^32 limit of one job; split the stream",
                      (unsigned long long)J->entry_cap);
@@ -1207,6 +1394,13 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     A.out_n = (unsigned long long*)d_n_entries;
     A.slabs = J->d_slabs;
     A.tile_done = J->d_tile_done;
+    A.dbg = nullptr;
+    if (getenv("CROP_DEBUG_KINDS")) {
+      static unsigned long long* dbg = nullptr;
+      if (!dbg) cudaMalloc(&dbg, 16 * 8);
+      cudaMemsetAsync(dbg, 0, 16 * 8, st);
+      A.dbg = dbg;
+    }
     void (*kern)(CountArgs);
     if (up) kern = J->filter ? k_count<true, true> : k_count<true, false>;
     else kern = J->filter ? k_count<false, true> : k_count<false, false>;
@@ -1216,6 +1410,15 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     kern<<<grid, kCountThreads, kCountSmem, st>>>(A);
     CROP_LAUNCH_CHECK();
     mark(5);
+    if (A.dbg) {
+      unsigned long long h[16];
+      cudaMemcpyAsync(h, A.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const char* names[4] = {"dense-row", "window", "dense-multi", "hash"};
+      for (int k = 0; k < 4; ++k)
+        fprintf(stderr, "[k_count] %-11s units %6llu entries %10llu count %8.1f Mcyc emit %8.1f Mcyc\n",
+                names[k], h[4 * k + 2], h[4 * k + 3], h[4 * k] / 1e6, h[4 * k + 1] / 1e6);
+    }
   }
   crop_count_launches(3);
   return CROP_OK;

@@ -118,10 +118,14 @@ __device__ __forceinline__ int stage_offsets(int64_t* s_off, const int64_t* __re
 // body may use warp shuffles. Loads are software-pipelined: the item of
 // window w+2 and (with TILE) the item->tile lookup of window w+1 are in
 // flight while window w is processed.
-template <bool TILE, typename Body>
+template <typename TV> __device__ __forceinline__ TV tv_none();
+template <> __device__ __forceinline__ uint32_t tv_none<uint32_t>() { return kNone; }
+template <> __device__ __forceinline__ uint2 tv_none<uint2>() { return make_uint2(kNone, 0u); }
+
+template <bool TILE, typename TV = uint32_t, typename Body>
 __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
                                            const uint32_t* __restrict__ items,
-                                           const uint32_t* __restrict__ item_tile, Body&& body) {
+                                           const TV* __restrict__ item_tile, Body&& body) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t g_lo = s_off[0], g_hi = s_off[ntx];
   const int64_t per = (((g_hi - g_lo + nw - 1) / nw) + 31) & ~31ll;
@@ -137,13 +141,13 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
   int cur = lo;
   auto ld_item = [&](int64_t g) { return g < w_hi ? __ldg(items + g) : 0u; };
   uint32_t it0 = ld_item(w_lo + lane), it1 = ld_item(w_lo + 32 + lane);
-  uint32_t tl0 = 0;
-  if (TILE) tl0 = w_lo + lane < w_hi ? __ldg(item_tile + it0) : kNone;
+  TV tl0 = tv_none<TV>();
+  if (TILE) tl0 = w_lo + lane < w_hi ? __ldg(item_tile + it0) : tv_none<TV>();
   for (int64_t g0 = w_lo; g0 < w_hi; g0 += 32) {
     const int64_t g = g0 + lane;
     const uint32_t it2 = ld_item(g + 64);
-    uint32_t tl1 = 0;
-    if (TILE) tl1 = g + 32 < w_hi ? __ldg(item_tile + it1) : kNone;
+    TV tl1 = tv_none<TV>();
+    if (TILE) tl1 = g + 32 < w_hi ? __ldg(item_tile + it1) : tv_none<TV>();
     Pos q;
     q.valid = g < w_hi;
     int t = cur;
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
     const int ntx = stage_offsets(s_off, offsets, n_tx, chunk, kChunkTx);
-    walk_chunk<false>(s_off, ntx, items, nullptr, [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
+    walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr, [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
       if (!q.valid) return;
       my_max = max(my_max, q.L);
       const uint32_t c = UPPER ? q.L - 1 - q.p : q.L;
@@ -507,7 +511,8 @@ struct Counter {
       }
       if (++s == kHashSlots) s = 0;
     }
-    atomicAdd(&hcnt[s % kHashHalf], 1u << ((s / kHashHalf) << 4));
+    const bool hi = s >= kHashHalf;
+    atomicAdd(&hcnt[hi ? s - kHashHalf : s], hi ? 0x10000u : 1u);
   }
 };
 
@@ -545,16 +550,25 @@ __device__ __forceinline__ void count_entries_flat(const CountArgs& A, const Til
   uint32_t* J_item = W.cs;
   uint32_t* J_x = W.m;
   uint32_t* J_y = W.R;
-  for (;;) {
+  // the next batch's entry descriptors are loaded while this one is counted
+  auto grab = [&]() -> uint64_t {
     uint32_t bidx = 0;
     if (lane == 0) bidx = atomicAdd(s_next, 1u);
     bidx = __shfl_sync(0xffffffffu, bidx, 0);
-    const uint64_t eb_w = e0 + (uint64_t)bidx * 32;
+    return e0 + (uint64_t)bidx * 32;
+  };
+  uint64_t nb = grab();
+  uint2 nen = make_uint2(0, 0);
+  if (nb + lane < e1) nen = A.entries[nb + lane];
+  for (;;) {
+    const uint64_t eb_w = nb;
     if (eb_w >= e1) break;
+    const uint2 en = nen;
+    nb = grab();
+    if (nb + lane < e1) nen = A.entries[nb + lane];
     const uint64_t e = eb_w + lane;
     uint32_t cn = 0, x = 0, y = 0, first = 0, ri = 0;
     if (e < e1) {
-      const uint2 en = A.entries[e];
       x = en.x;
       y = en.y;
       if (UPPER) {
@@ -858,7 +872,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
     }
     if (emit_now) {
       auto count_at = [&](uint32_t s) -> uint32_t {
-        if (!dense) return (hcnt[s % kHashHalf] >> ((s / kHashHalf) << 4)) & 0xFFFFu;
+        if (!dense) return s >= kHashHalf ? hcnt[s - kHashHalf] >> 16 : hcnt[s] & 0xFFFFu;
         uint32_t c = read16(table, s);
         if (reduce) {
           const uint32_t wi = s & (kHalf - 1), sh = (s / kHalf) << 4;
@@ -931,6 +945,434 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
   }
 }
 
+// ============================================================ stream mode
+// When rows are short (mean pairs per row occurrence <= kStreamMeanMax:
+// BASELINE configs 1-3), the router writes every pair as one 32-bit WORD
+// into its tile's stream -- the table slot (dense tiles) or the key (hash
+// tiles) -- and the counter reads the streams fully coalesced: one load and
+// one shared-memory atomic per term, exactly SURVEY.md §8(d)'s 8 B/term
+// model. The table is 57,344 u32 counters (224 KB), so c2's rows (50K
+// columns) need no windows and no counter can wrap.
+constexpr uint32_t kStreamDenseCap = 57344;
+constexpr uint32_t kStreamHashSlots = 28672;
+constexpr uint32_t kStreamHashCap = 18432;
+constexpr size_t kStreamSmem = (size_t)kStreamDenseCap * 4 + 64;
+constexpr uint32_t kStreamMeanMax = 64;
+
+// per-row constant of the word of (i, j) in tile T: dense word = base + j,
+// hash word = base | j
+__host__ __device__ __forceinline__ uint32_t stream_base(const Tile& T, uint32_t i, uint32_t n,
+                                                         uint32_t col_bits, bool upper) {
+  if (T.mode != 0) return (i - T.row0) << col_bits;
+  if (T.row1 - T.row0 == 1) return 0u - T.c0;  // single row: slot = j - first column
+  const uint32_t k = i - T.row0;
+  if (!upper) return k * n;
+  const uint32_t w0 = n - 1 - T.row0;
+  return k * w0 - (uint32_t)(((unsigned long long)k * (k - 1)) >> 1) - i - 1;
+}
+
+struct StreamRouteArgs {
+  const int64_t* offsets;
+  const uint32_t* items;
+  int64_t n_tx;
+  const uint2* item_info;  // {tile | kWinFlag, word base of the row}
+  const Tile* tiles;
+  uint32_t n_tiles, n_items, col_bits;
+  int filter;
+  uint32_t kappa, start, stop;
+  const uint32_t* h_row;
+  const uint32_t* h_col;
+  unsigned long long* tile_words;   // B1: word totals per tile
+  unsigned long long* tile_cursor;  // B2: next free word per tile
+  const unsigned long long* tile_base;  // B2: first word of each tile
+  uint32_t* words;
+};
+
+// Visit the words of row occurrence (g, q) of row item i: fn(dest_tile, base,
+// first_col_pos, n_cols) for each run of consecutive columns with the same
+// destination, or, with the bucket filter, fn per own column (n_cols = 1).
+// The word of column j is base + j for both tile kinds (a hash tile's base
+// has j's bits clear). tv = {tile | kWinFlag, base of the unsplit row}.
+template <bool UPPER, typename Fn>
+__device__ __forceinline__ void stream_row(const StreamRouteArgs& A, uint32_t i, const Pos& q,
+                                           uint2 tv, Fn&& fn) {
+  if (tv.x == kNone || (UPPER && q.p + 1 >= q.L)) return;
+  const uint32_t tile = tv.x & ~kWinFlag;
+  const uint32_t c_lo = UPPER ? q.p + 1 : 0;
+  const uint64_t tb = (uint64_t)q.base;
+  if (!(tv.x & kWinFlag) && !A.filter) {
+    fn(tile, tv.y, (uint32_t)(tb + c_lo), q.L - c_lo);
+    return;
+  }
+  uint32_t c0 = 0, nwin = 1;
+  if (tv.x & kWinFlag) {
+    const Tile T0 = A.tiles[tile];
+    c0 = T0.c0;
+    nwin = T0.nwin;
+  }
+  uint32_t run_tile = kNone, run_start = 0, run_n = 0, run_base = 0;
+  for (uint32_t p = c_lo; p < q.L; ++p) {
+    const uint32_t j = A.items[tb + p];
+    uint32_t dest = tile, base = tv.y;
+    if (tv.x & kWinFlag) {
+      if (j < c0) continue;
+      const uint32_t w = (j - c0) / kStreamDenseCap;
+      if (w >= nwin) break;
+      dest = tile + w;
+      base = 0u - (c0 + w * kStreamDenseCap);  // window w starts at column c0 + w * cap
+    }
+    if (A.filter) {
+      uint32_t b = A.h_row[i] + A.h_col[j];
+      if (b >= A.kappa) b -= A.kappa;
+      if (b < A.start || b >= A.stop) continue;
+      fn(dest, base, (uint32_t)(tb + p), 1u);
+      continue;
+    }
+    if (dest != run_tile) {
+      if (run_n) fn(run_tile, run_base, run_start, run_n);
+      run_tile = dest;
+      run_start = (uint32_t)(tb + p);
+      run_n = 0;
+      run_base = base;
+    }
+    ++run_n;
+  }
+  if (run_n) fn(run_tile, run_base, run_start, run_n);
+}
+
+// B1: words per tile (shared counters per CTA, flushed once)
+template <bool UPPER>
+__global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  const uint32_t ns = min(A.n_tiles, kTileSmem);
+  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
+  const int64_t n_chunks = (A.n_tx + kChunkTx - 1) / kChunkTx;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    __syncthreads();
+    const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, kChunkTx);
+    walk_chunk<true>(s_off, ntx, A.items, A.item_info,
+                     [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
+      if (!q.valid) return;
+      stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t, uint32_t, uint32_t n) {
+        if (t < ns) atomicAdd(&s_cnt[t], n);
+        else atomicAdd(&A.tile_words[t], (unsigned long long)n);
+      });
+    });
+    // flush per chunk: shared u32 counts never exceed one chunk's words
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x)
+      if (s_cnt[t]) {
+        atomicAdd(&A.tile_words[t], (unsigned long long)s_cnt[t]);
+        s_cnt[t] = 0;
+      }
+  }
+}
+
+// B2: per chunk, count words per shared tile, claim one range per touched
+// tile, then write the words. Unfiltered rows are written cooperatively by
+// the warp (32 consecutive words per store); filtered or split rows by lane.
+template <bool UPPER>
+__global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  uint16_t* s_touched = reinterpret_cast<uint16_t*>(s_cnt + kTileSmem);  // tile ids < 2^16
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(s_touched + kTileSmem);
+  uint32_t* s_job = s_misc + 4;  // per warp: 4 arrays of 32 (flattened write)
+  const uint32_t ns = min(A.n_tiles, kTileSmem);
+  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* j_pos_lo = s_job + warp * 128;
+  uint32_t* j_base = j_pos_lo + 32;
+  uint32_t* j_src = j_base + 32;
+  uint32_t* j_n = j_src + 32;
+  const int64_t n_chunks = (A.n_tx + kChunkTx - 1) / kChunkTx;
+  for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_misc[0] = 0;
+    const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, kChunkTx);
+    walk_chunk<true>(s_off, ntx, A.items, A.item_info,
+                     [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
+      if (!q.valid) return;
+      stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t, uint32_t, uint32_t n) {
+        if (t < ns) {
+          if (atomicAdd(&s_cnt[t], n) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = t;
+        }
+      });
+    });
+    __syncthreads();
+    const uint32_t n_touch = s_misc[0];
+    for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) {
+      const uint32_t t = s_touched[k];
+      // claimed base, kept relative to the tile's base to stay within 32 bits
+      s_cnt[t] = (uint32_t)(atomicAdd(&A.tile_cursor[t], (unsigned long long)s_cnt[t]) -
+                            A.tile_base[t]);
+    }
+    __syncthreads();
+    walk_chunk<true>(s_off, ntx, A.items, A.item_info,
+                     [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
+      // one cooperative job per lane at most (an unfiltered, unsplit row)
+      uint32_t n_coop = 0, pos = 0, base = 0, src = 0;
+      if (q.valid) {
+        stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t b, uint32_t first, uint32_t n) {
+          const unsigned long long p0 =
+              t < ns ? A.tile_base[t] + atomicAdd(&s_cnt[t], n)
+                     : atomicAdd(&A.tile_cursor[t], (unsigned long long)n);
+          if (!(tv.x & kWinFlag) && !A.filter) {
+            n_coop = n;
+            pos = (uint32_t)p0;  // words < 2^32 per job (checked on the host)
+            base = b;
+            src = first;
+          } else {
+            for (uint32_t k = 0; k < n; ++k) A.words[p0 + k] = b + A.items[first + k];
+          }
+        });
+      }
+      // flattened, coalesced write of the cooperative rows
+      const uint32_t keep = __ballot_sync(0xffffffffu, n_coop > 0);
+      if (!keep) return;
+      const int ne = __popc(keep);
+      if (n_coop) {
+        const int r = __popc(keep & ((1u << lane) - 1u));
+        j_pos_lo[r] = pos;
+        j_base[r] = base;
+        j_src[r] = src;
+        j_n[r] = n_coop;
+      }
+      __syncwarp();
+      uint32_t my_n = lane < ne ? j_n[lane] : 0u;
+      const uint32_t incl = warp_incl_scan(my_n);
+      const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t excl = incl - my_n;
+      uint32_t ob = 0;
+      for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+        const uint32_t o = owner_step(incl, t0, ob);
+        const uint32_t t = t0 + lane;
+        const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o & 31);
+        if (t < S) {
+          const uint32_t loc = t - o_excl;
+          const uint32_t j = A.items[j_src[o] + loc];
+          A.words[(uint64_t)j_pos_lo[o] + loc] = j_base[o] + j;
+        }
+      }
+      __syncwarp();
+    });
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) s_cnt[s_touched[k]] = 0;
+  }
+}
+
+// Streaming counter: units are ranges of a tile's words; warps read them
+// coalesced (4 loads in flight per lane) and bump u32 shared counters.
+struct StreamCountArgs {
+  const Tile* tiles;
+  const Unit* units;
+  uint32_t n_units;
+  const unsigned long long* tile_base;
+  const unsigned long long* tile_words;
+  const uint32_t* words;
+  unsigned int* unit_counter;
+  uint32_t n_items, col_bits;
+  int upper;
+  uint32_t* out_row;
+  uint32_t* out_col;
+  uint32_t* out_count;
+  unsigned long long* out_n;
+  uint32_t* slabs;  // kStreamDenseCap words per unit of a split tile
+  unsigned int* tile_done;
+};
+
+__global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense counters / hash keys
+  uint32_t* hcnt = table + kStreamHashSlots;             // hash counts
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + (size_t)kStreamDenseCap * 4);
+  __shared__ uint32_t s_warp[33];
+  __shared__ unsigned long long s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t n = A.n_items;
+  for (;;) {
+    if (threadIdx.x == 0) s_misc[0] = atomicAdd(A.unit_counter, 1u);
+    __syncthreads();
+    const uint32_t u = s_misc[0];
+    __syncthreads();
+    if (u >= A.n_units) break;
+    const Unit unit = A.units[u];
+    const Tile T = A.tiles[unit.tile];
+    const uint64_t Wn = A.tile_words[unit.tile];
+    const uint64_t wb = A.tile_base[unit.tile];
+    const uint64_t w0 = wb + Wn * unit.local / T.n_units;
+    const uint64_t w1 = wb + Wn * (unit.local + 1) / T.n_units;
+    const bool dense = T.mode == 0;
+    const uint32_t width = T.width;
+    if (dense) {
+      uint4* t4 = reinterpret_cast<uint4*>(table);
+      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads)
+        t4[s] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (uint32_t s = threadIdx.x; s < kStreamHashSlots; s += kCountThreads) {
+        table[s] = kEmpty32;
+        hcnt[s] = 0;
+      }
+    }
+    __syncthreads();
+    // each warp: a contiguous share of [w0, w1), 256 words per step; the next
+    // step's 8 words per lane are loaded before this step's are counted
+    constexpr int D = 8;
+    const uint64_t per = (((w1 - w0) + kCountWarps - 1) / kCountWarps + (32 * D - 1)) &
+                         ~(uint64_t)(32 * D - 1);
+    const uint64_t a0 = w0 + (uint64_t)warp * per, a1 = min(w1, a0 + per);
+    auto fetch = [&](uint64_t b, uint32_t (&v)[D]) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const uint64_t x = b + k * 32 + lane;
+        v[k] = x < a1 ? __ldcs(A.words + x) : kEmpty32;
+      }
+    };
+    uint32_t cur[D], nxt[D];
+    if (a0 < a1) fetch(a0, cur);
+    for (uint64_t b = a0; b < a1; b += 32 * D) {
+      if (b + 32 * D < a1) fetch(b + 32 * D, nxt);
+      if (dense) {
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          if (cur[k] != kEmpty32) atomicAdd(&table[cur[k]], 1u);
+      } else {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const uint32_t key = cur[k];
+          if (key == kEmpty32) continue;
+          uint32_t s = __umulhi(mix32(key), kStreamHashSlots);
+          for (;;) {
+            const uint32_t kk = table[s];
+            if (kk == key) break;
+            if (kk == kEmpty32) {
+              const uint32_t old = atomicCAS(&table[s], kEmpty32, key);
+              if (old == kEmpty32 || old == key) break;
+            }
+            if (++s == kStreamHashSlots) s = 0;
+          }
+          atomicAdd(&hcnt[s], 1u);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) cur[k] = nxt[k];
+    }
+    __syncthreads();
+    bool emit_now = true, reduce = false;
+    const uint32_t* slab = A.slabs + T.slab_base * (uint64_t)kStreamDenseCap;
+    if (dense && T.n_units > 1) {
+      uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * (uint64_t)kStreamDenseCap);
+      const uint4* src = reinterpret_cast<const uint4*>(table);
+      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads) dst[s] = src[s];
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_misc[1] = atomicAdd(&A.tile_done[unit.tile], 1u) == T.n_units - 1;
+      __syncthreads();
+      emit_now = reduce = s_misc[1] != 0;
+      if (reduce) __threadfence();
+    }
+    if (emit_now) {
+      auto count_at = [&](uint32_t s) -> uint32_t {
+        if (!dense) return hcnt[s];
+        uint32_t c = table[s];
+        if (reduce)
+          for (uint32_t v = 0; v < T.n_units; ++v)
+            if (v != unit.local) c += __ldcg(slab + (uint64_t)v * kStreamDenseCap + s);
+        return c;
+      };
+      const uint32_t slots = dense ? width : kStreamHashSlots;
+      const uint32_t per_w = (slots + kCountWarps - 1) / kCountWarps;
+      const uint32_t s_lo = min(slots, warp * per_w), s_hi = min(slots, s_lo + per_w);
+      uint32_t mine = 0;
+      for (uint32_t s = s_lo + lane; s < s_hi; s += 32) mine += count_at(s) != 0;
+      mine = warp_sum(mine);
+      uint32_t total;
+      uint32_t wbase = block_excl_scan(lane == 0 ? mine : 0, s_warp, total);
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (threadIdx.x == 0) s_base = atomicAdd(A.out_n, (unsigned long long)total);
+      __syncthreads();
+      uint64_t pos = s_base + wbase;
+      const bool single_row = T.row1 - T.row0 == 1;
+      for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        uint32_t c = 0, i = 0, j = 0;
+        if (s < s_hi) {
+          c = count_at(s);
+          if (c) {
+            if (!dense) {
+              const uint32_t key = table[s];
+              i = T.row0 + (key >> A.col_bits);
+              j = key & ((1u << A.col_bits) - 1u);
+            } else if (single_row) {
+              i = T.row0;
+              j = s + T.c0;
+            } else if (A.upper) {
+              uint32_t lo = T.row0, hi = T.row1;
+              while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (tri_rowbase(mid, T.row0, n) <= s) lo = mid;
+                else hi = mid;
+              }
+              i = lo;
+              j = (uint32_t)(s - tri_rowbase(i, T.row0, n)) + i + 1;
+            } else {
+              i = T.row0 + s / n;
+              j = s % n;
+            }
+          }
+        }
+        const uint32_t mk = __ballot_sync(0xffffffffu, c != 0);
+        if (c) {
+          const uint64_t o = pos + __popc(mk & ((1u << lane) - 1u));
+          A.out_row[o] = i;
+          A.out_col[o] = j;
+          A.out_count[o] = c;
+        }
+        pos += __popc(mk);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_u64(const unsigned long long* __restrict__ in,
+                                                   uint32_t n, unsigned long long* __restrict__ out,
+                                                   unsigned long long* __restrict__ out2) {
+  // single block exclusive scan; out2 (optional) receives a copy
+  __shared__ unsigned long long s_part[1024];
+  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
+  unsigned long long acc = 0;
+  for (uint32_t i = lo; i < hi; ++i) acc += in[i];
+  s_part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long run = 0;
+    for (int k = 0; k < 32; ++k) run += s_part[threadIdx.x * 32 + k];
+    unsigned long long x = run;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+      if ((int)threadIdx.x >= d) x += y;
+    }
+    unsigned long long a = x - run;
+    for (int k = 0; k < 32; ++k) {
+      const unsigned long long v = s_part[threadIdx.x * 32 + k];
+      s_part[threadIdx.x * 32 + k] = a;
+      a += v;
+    }
+  }
+  __syncthreads();
+  unsigned long long run = s_part[threadIdx.x];
+  for (uint32_t i = lo; i < hi; ++i) {
+    out[i] = run;
+    if (out2) out2[i] = run;
+    run += in[i];
+  }
+}
+
 }  // namespace
 
 // =============================================================== host side
@@ -957,6 +1399,7 @@ struct crop_pairs {
   unsigned long long* d_terms = nullptr;
   unsigned int* d_maxlen = nullptr;
   uint32_t* d_item_tile = nullptr;
+  uint2* d_item_info = nullptr;  // stream mode: {tile | kWinFlag, word base}
   Tile* d_tiles = nullptr;
   Unit* d_units = nullptr;
   uint32_t* d_split = nullptr;
@@ -973,6 +1416,11 @@ struct crop_pairs {
   uint32_t* d_overflow = nullptr;
   unsigned int* d_tile_done = nullptr;
   std::vector<uint32_t> h_item_tile;  // kept alive for the async uploads
+  std::vector<uint2> h_item_info;
+  // stream mode (short rows): pair words per tile instead of entries
+  bool stream_mode = false;
+  uint32_t* d_words = nullptr;
+  unsigned long long* d_tile_words = nullptr;
   // optional per-phase timing (CUDA events on the job's stream)
   bool timing = false;
   cudaEvent_t ev[6] = {};
@@ -981,9 +1429,10 @@ struct crop_pairs {
 static void free_job(crop_pairs* j) {
   for (cudaEvent_t& e : j->ev)
     if (e) cudaEventDestroy(e);
-  void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_tiles, j->d_units, j->d_split,
+  void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_item_info, j->d_tiles, j->d_units, j->d_split,
                   j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_tile_end, j->d_total_entries,
-                  j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done};
+                  j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done,
+                  j->d_words, j->d_tile_words};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
@@ -995,6 +1444,12 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
                        const std::vector<unsigned long long>& occ,
                        std::vector<uint32_t>& item_tile) {
   const uint32_t n = J->n_items;
+  const bool sm = J->stream_mode;
+  // entry mode: u16 counters (65,536 per tile, <= 65,535 entries per unit);
+  // stream mode: u32 counters (57,344 per tile)
+  const uint64_t dense_cap = sm ? kStreamDenseCap : kDenseCap;
+  const uint64_t hash_cap = sm ? kStreamHashCap : kHashCap;
+  const uint64_t occ_cap = sm ? ~0ull : (uint64_t)kUnitEntries;
   const bool upper = J->upper != 0;
   const uint64_t T = J->total_terms;
   const uint64_t unit_terms = std::max<uint64_t>(1ull << 16, T / ((uint64_t)kNumSMs * 8));
@@ -1005,9 +1460,9 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   item_tile.assign(n, kNone);
   // units: by terms for balance, and <= kUnitEntries entries each (u16
   // counters); a tile's entries never exceed the sum of its rows' occ.
-  auto units_for = [unit_terms](uint64_t tm, uint64_t oc) -> uint32_t {
+  auto units_for = [unit_terms, occ_cap](uint64_t tm, uint64_t oc) -> uint32_t {
     uint64_t u = (tm + unit_terms - 1) / unit_terms;
-    const uint64_t ue = (oc + kUnitEntries - 1) / kUnitEntries;
+    const uint64_t ue = occ_cap == ~0ull ? 1 : (oc + occ_cap - 1) / occ_cap;
     if (ue > u) u = ue;
     return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
   };
@@ -1020,6 +1475,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     t.row1 = row1;
     t.c0 = 0;
     t.c1 = n;
+    if (sm && row1 - row0 == 1) t.c0 = upper ? row0 + 1 : 0;  // stream: slot = j - c0
     const bool dense = dok && (!hok || st * 8 >= sw);
     t.mode = dense ? 0 : 1;
     t.width = dense ? (uint32_t)sw : 0;
@@ -1035,9 +1491,9 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     const uint64_t w = upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
     const uint64_t b = tm < w ? tm : w;
     if (open) {
-      const bool d2 = dok && sw + w <= kDenseCap;
-      const bool h2 = hok && sb + b <= kHashCap && st + tm <= unit_terms &&
-                      so + oc <= kUnitEntries && (i - row0 + 1) <= hash_rows_max;
+      const bool d2 = dok && sw + w <= dense_cap;
+      const bool h2 = hok && sb + b <= hash_cap && st + tm <= unit_terms &&
+                      so + oc <= occ_cap && (i - row0 + 1) <= hash_rows_max;
       if (d2 || h2) {
         sw += w;
         sb += b;
@@ -1051,8 +1507,8 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
       open = false;
     }
     if (tm == 0) continue;
-    const bool d2 = w <= kDenseCap;
-    const bool h2 = b <= kHashCap && tm <= unit_terms && oc <= kUnitEntries;
+    const bool d2 = w <= dense_cap;
+    const bool h2 = b <= hash_cap && tm <= unit_terms && oc <= occ_cap;
     if (d2 || h2) {
       open = true;
       row0 = i;
@@ -1067,14 +1523,14 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     // one row too wide for a dense tile and too heavy for a hash tile:
     // column windows of kDenseCap counters with consecutive tile ids.
     const uint32_t col_lo = upper ? i + 1 : 0;
-    const uint32_t nwin = (uint32_t)((w + kDenseCap - 1) / kDenseCap);
+    const uint32_t nwin = (uint32_t)((w + dense_cap - 1) / dense_cap);
     const uint32_t first = (uint32_t)tiles.size();
     for (uint32_t k = 0; k < nwin; ++k) {
       Tile t{};
       t.row0 = i;
       t.row1 = i + 1;
-      t.c0 = col_lo + k * kDenseCap;
-      t.c1 = (uint32_t)std::min<uint64_t>(n, (uint64_t)t.c0 + kDenseCap);
+      t.c0 = col_lo + k * (uint32_t)dense_cap;
+      t.c1 = (uint32_t)std::min<uint64_t>(n, (uint64_t)t.c0 + dense_cap);
       t.mode = 0;
       t.nwin = k == 0 ? nwin : 0;
       t.width = t.c1 - t.c0;
@@ -1154,7 +1610,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   }
 
   uint64_t cap = 0;
-  for (auto& t : tiles) cap += t.mode == 0 ? t.width : kHashCap;
+  for (auto& t : tiles) cap += t.mode == 0 ? t.width : hash_cap;
   J->max_entries = cap;
 }
 
@@ -1245,6 +1701,13 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       occ[i] = stats[i] >> 40;
       J->total_terms += terms[i];
     }
+    {
+      unsigned long long occ_sum = 0;
+      for (uint32_t i = 0; i < n_items; ++i) occ_sum += occ[i];
+      J->stream_mode = getenv("CROP_FORCE_ENTRY_MODE") == nullptr && occ_sum > 0 &&
+                       J->total_terms <= (unsigned long long)kStreamMeanMax * occ_sum &&
+                       J->total_terms < (1ull << 32);
+    }
     std::vector<uint32_t>& item_tile = J->h_item_tile;
     auto t_p0 = std::chrono::steady_clock::now();
     plan_tiles(J, terms, occ, item_tile);
@@ -1298,14 +1761,31 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       JCUDA(cudaMemcpyAsync(J->d_units, J->units.data(), J->units.size() * sizeof(Unit), cudaMemcpyHostToDevice, st));
     if (!J->split.empty())
       JCUDA(cudaMemcpyAsync(J->d_split, J->split.data(), J->split.size() * 4, cudaMemcpyHostToDevice, st));
-    if (J->n_slabs) JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kHalf * 4, st));
-    if (J->entry_cap >= (1ull << 32)) {
+    if (J->n_slabs)
+      JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)(J->stream_mode ? kStreamDenseCap : kHalf) * 4, st));
+    if (J->stream_mode) {
+      std::vector<uint2>& info = J->h_item_info;
+      info.assign(nn, make_uint2(kNone, 0u));
+      for (uint32_t i = 0; i < n_items; ++i) {
+        const uint32_t tv = item_tile[i];
+        if (tv == kNone) continue;
+        const Tile& T = J->tiles[tv & ~kWinFlag];
+        info[i] = make_uint2(tv, (tv & kWinFlag) ? 0u : stream_base(T, i, n_items, J->col_bits, J->upper != 0));
+      }
+      JCUDA(cudaMallocAsync(&J->d_item_info, nn * sizeof(uint2), st));
+      if (n_items)
+        JCUDA(cudaMemcpyAsync(J->d_item_info, info.data(), n_items * sizeof(uint2), cudaMemcpyHostToDevice, st));
+      JCUDA(cudaMallocAsync(&J->d_words, std::max<uint64_t>(1, J->total_terms) * 4, st));
+      JCUDA(cudaMallocAsync(&J->d_tile_words, std::max<size_t>(1, nt) * 8, st));
+    }
+    if (!J->stream_mode && J->entry_cap >= (1ull << 32)) {
       crop_set_error(CROP_ERESOURCE, "%llu entries exceed the 2^32 limit of one job; split the stream",
                      (unsigned long long)J->entry_cap);
       rc = CROP_ERESOURCE;
       goto fail;
     }
-    JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
+    if (!J->stream_mode)
+      JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
     // host vectors read by the async uploads live in J until destroy
     if (getenv("CROP_DEBUG_TIMING")) {
       auto t_end = std::chrono::steady_clock::now();
@@ -1348,6 +1828,77 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     if (J->timing) cudaEventRecord(J->ev[k], st);
   };
   mark(0);
+  if (J->stream_mode) {
+    StreamRouteArgs R{};
+    R.offsets = J->offsets;
+    R.items = J->items;
+    R.n_tx = J->n_tx;
+    R.item_info = J->d_item_info;
+    R.tiles = J->d_tiles;
+    R.n_tiles = nt;
+    R.n_items = J->n_items;
+    R.col_bits = J->col_bits;
+    R.filter = J->filter;
+    R.kappa = J->iv.kappa;
+    R.start = J->iv.start;
+    R.stop = J->iv.stop;
+    R.h_row = J->iv.h_row;
+    R.h_col = J->iv.h_col;
+    R.tile_words = J->d_tile_words;
+    R.tile_cursor = J->d_tile_cursor;
+    R.tile_base = J->d_tile_ebase;
+    R.words = J->d_words;
+    const int64_t chunks = (J->n_tx + kChunkTx - 1) / kChunkTx;
+    const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
+    CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
+    {
+      auto kern = up ? k_stream_count<true> : k_stream_count<false>;
+      const size_t smem = kOffBytes + (size_t)std::min(nt, kTileSmem) * 4;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kOffBytes + kTileSmem * 4)));
+      kern<<<grid, kPassThreads, smem, st>>>(R);
+      CROP_LAUNCH_CHECK();
+    }
+    k_scan_u64<<<1, 1024, 0, st>>>(J->d_tile_words, nt, J->d_tile_ebase, J->d_tile_cursor);
+    CROP_LAUNCH_CHECK();
+    mark(1);
+    {
+      auto kern = up ? k_stream_write<true> : k_stream_write<false>;
+      const size_t smem = kOffBytes + (size_t)kTileSmem * 6 + 16 + kCountWarps * 128 * 4;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, kPassThreads, smem, st>>>(R);
+      CROP_LAUNCH_CHECK();
+    }
+    mark(2);
+    mark(3);
+    CROP_CUDA(cudaMemsetAsync(J->d_unit_counter, 0, 4, st));
+    CROP_CUDA(cudaMemsetAsync(J->d_tile_done, 0, nt * 4, st));
+    StreamCountArgs C{};
+    C.tiles = J->d_tiles;
+    C.units = J->d_units;
+    C.n_units = (uint32_t)J->units.size();
+    C.tile_base = J->d_tile_ebase;
+    C.tile_words = J->d_tile_words;
+    C.words = J->d_words;
+    C.unit_counter = J->d_unit_counter;
+    C.n_items = J->n_items;
+    C.col_bits = J->col_bits;
+    C.upper = up;
+    C.out_row = out_row;
+    C.out_col = out_col;
+    C.out_count = out_count;
+    C.out_n = (unsigned long long*)d_n_entries;
+    C.slabs = J->d_slabs;
+    C.tile_done = J->d_tile_done;
+    CROP_CUDA(cudaFuncSetAttribute(k_count_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kStreamSmem));
+    mark(4);
+    k_count_stream<<<std::min<int>(kNumSMs, (int)J->units.size()), kCountThreads, kStreamSmem, st>>>(C);
+    CROP_LAUNCH_CHECK();
+    mark(5);
+    crop_count_launches(4);
+    return CROP_OK;
+  }
   // route: one walk, staged per chunk, ranges claimed per touched tile
   CROP_CUDA(cudaMemcpyAsync(J->d_tile_cursor, J->d_tile_ebase, nt * 8, cudaMemcpyDeviceToDevice, st));
   {

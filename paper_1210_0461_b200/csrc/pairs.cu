@@ -403,14 +403,14 @@ __device__ __forceinline__ uint32_t lower_bound_items(const uint32_t* __restrict
   return lo;
 }
 
-// Block-wide exclusive scan of one value per thread (1024 threads).
+// Block-wide exclusive scan of one value per thread (blockDim a multiple of 32).
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t incl = warp_incl_scan(v);
   if (lane == 31) s_warp[w] = incl;
   __syncthreads();
   if (w == 0) {
-    uint32_t x = s_warp[lane];
+    uint32_t x = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
     uint32_t xi = warp_incl_scan(x);
     s_warp[lane] = xi - x;
     if (lane == 31) s_warp[32] = xi;
@@ -986,6 +986,7 @@ struct StreamRouteArgs {
   unsigned long long* tile_cursor;  // B2: next free word per tile
   const unsigned long long* tile_base;  // B2: first word of each tile
   uint32_t* words;
+  int dbg_mode;  // development only (CROP_DEBUG_WRITE): 1 = no word stores, 2 = no write phase
 };
 
 // Visit the words of row occurrence (g, q) of row item i: fn(dest_tile, base,
@@ -1080,14 +1081,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
   uint16_t* s_touched = reinterpret_cast<uint16_t*>(s_cnt + kTileSmem);  // tile ids < 2^16
   uint32_t* s_misc = reinterpret_cast<uint32_t*>(s_touched + kTileSmem);
-  uint32_t* s_job = s_misc + 4;  // per warp: 4 arrays of 32 (flattened write)
   const uint32_t ns = min(A.n_tiles, kTileSmem);
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* j_pos_lo = s_job + warp * 128;
-  uint32_t* j_base = j_pos_lo + 32;
-  uint32_t* j_src = j_base + 32;
-  uint32_t* j_n = j_src + 32;
+  // triangle decode for transactions of <= 32 items: pair t = r (r + 1) / 2 + c
+  // -> r | c << 8 (row r from the end, column offset c <= r)
+  __shared__ uint16_t s_tri[496];
+  for (uint32_t r = 0; r < 31; ++r)
+    for (uint32_t c = threadIdx.x; c <= r; c += blockDim.x) s_tri[r * (r + 1) / 2 + c] = (uint16_t)(r | c << 8);
   const int64_t n_chunks = (A.n_tx + kChunkTx - 1) / kChunkTx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
@@ -1106,59 +1107,110 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
     const uint32_t n_touch = s_misc[0];
     for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) {
       const uint32_t t = s_touched[k];
-      // claimed base, kept relative to the tile's base to stay within 32 bits
-      s_cnt[t] = (uint32_t)(atomicAdd(&A.tile_cursor[t], (unsigned long long)s_cnt[t]) -
-                            A.tile_base[t]);
+      // claimed first word (all word positions of a job are < 2^32)
+      s_cnt[t] = (uint32_t)atomicAdd(&A.tile_cursor[t], (unsigned long long)s_cnt[t]);
     }
     __syncthreads();
-    walk_chunk<true>(s_off, ntx, A.items, A.item_info,
-                     [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
-      // one cooperative job per lane at most (an unfiltered, unsplit row)
-      uint32_t n_coop = 0, pos = 0, base = 0, src = 0;
-      if (q.valid) {
-        stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t b, uint32_t first, uint32_t n) {
-          const unsigned long long p0 =
-              t < ns ? A.tile_base[t] + atomicAdd(&s_cnt[t], n)
-                     : atomicAdd(&A.tile_cursor[t], (unsigned long long)n);
-          if (!(tv.x & kWinFlag) && !A.filter) {
-            n_coop = n;
-            pos = (uint32_t)p0;  // words < 2^32 per job (checked on the host)
-            base = b;
-            src = first;
-          } else {
-            for (uint32_t k = 0; k < n; ++k) A.words[p0 + k] = b + A.items[first + k];
+    // write: one warp per transaction. Lanes hold 32 rows (their claims and
+    // bases) and 32 columns at a time; each row's run of columns is one
+    // coalesced store instruction (row and base broadcast by shuffle). The
+    // first 32 items of the warp's next transaction and the item_info of
+    // the one after are in flight while a transaction is written.
+    if (A.dbg_mode != 2) {
+      constexpr int NW = kPassThreads / 32;
+      auto ld_it = [&](int t) -> uint32_t {
+        if (t >= ntx) return kNone;
+        const int64_t tb = s_off[t];
+        return (int64_t)lane < s_off[t + 1] - tb ? __ldg(A.items + tb + lane) : kNone;
+      };
+      auto ld_tv = [&](uint32_t it) -> uint2 {
+        return it != kNone ? __ldg(A.item_info + it) : make_uint2(kNone, 0u);
+      };
+      // items 4 transactions ahead, their item_info 3 ahead
+      uint32_t it_cur = ld_it(warp), it1 = ld_it(warp + NW), it2 = ld_it(warp + 2 * NW),
+               it3 = ld_it(warp + 3 * NW);
+      uint2 tv_cur = ld_tv(it_cur), tv1 = ld_tv(it1), tv2 = ld_tv(it2);
+      for (int t = warp; t < ntx; t += NW) {
+        const uint2 tv3 = ld_tv(it3);
+        const uint32_t it4 = ld_it(t + 4 * NW);
+        const int64_t tb = s_off[t];
+        const uint32_t L = (uint32_t)(s_off[t + 1] - tb);
+        for (uint32_t pc = 0; pc < L; pc += 32) {
+          const uint32_t p = pc + lane;
+          bool fast = false;
+          uint32_t dest = 0, bb = 0;
+          uint32_t i = it_cur;
+          uint2 tv = tv_cur;
+          if (pc > 0 && p < L) {
+            i = A.items[tb + p];
+            tv = A.item_info[i];
           }
-        });
-      }
-      // flattened, coalesced write of the cooperative rows
-      const uint32_t keep = __ballot_sync(0xffffffffu, n_coop > 0);
-      if (!keep) return;
-      const int ne = __popc(keep);
-      if (n_coop) {
-        const int r = __popc(keep & ((1u << lane) - 1u));
-        j_pos_lo[r] = pos;
-        j_base[r] = base;
-        j_src[r] = src;
-        j_n[r] = n_coop;
-      }
-      __syncwarp();
-      uint32_t my_n = lane < ne ? j_n[lane] : 0u;
-      const uint32_t incl = warp_incl_scan(my_n);
-      const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t excl = incl - my_n;
-      uint32_t ob = 0;
-      for (uint32_t t0 = 0; t0 < S; t0 += 32) {
-        const uint32_t o = owner_step(incl, t0, ob);
-        const uint32_t t = t0 + lane;
-        const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o & 31);
-        if (t < S) {
-          const uint32_t loc = t - o_excl;
-          const uint32_t j = A.items[j_src[o] + loc];
-          A.words[(uint64_t)j_pos_lo[o] + loc] = j_base[o] + j;
+          if (p < L && (!UPPER || p + 1 < L) && tv.x != kNone) {
+            const uint32_t n = UPPER ? L - 1 - p : L;
+            if (!(tv.x & kWinFlag) && !A.filter) {
+              fast = true;
+              bb = tv.y;
+              dest = tv.x < ns ? atomicAdd(&s_cnt[tv.x], n)
+                               : (uint32_t)atomicAdd(&A.tile_cursor[tv.x], (unsigned long long)n);
+            } else {
+              Pos q;
+              q.base = tb;
+              q.p = p;
+              q.L = L;
+              q.tx = (uint32_t)t;
+              q.valid = true;
+              stream_row<UPPER>(A, i, q, tv, [&](uint32_t t2, uint32_t b, uint32_t first, uint32_t n2) {
+                const unsigned long long p0 =
+                    t2 < ns ? (unsigned long long)atomicAdd(&s_cnt[t2], n2)
+                            : atomicAdd(&A.tile_cursor[t2], (unsigned long long)n2);
+                for (uint32_t k = 0; k < n2; ++k) A.words[p0 + k] = b + A.items[first + k];
+              });
+            }
+          }
+          const uint32_t fm = __ballot_sync(0xffffffffu, fast);
+          if (!fm || A.dbg_mode == 3) continue;
+          if (UPPER && L <= 32) {
+            // the transaction's triangle flattened: pair t -> (row from the
+            // end r, column offset c) via the shared table; 32 pairs per
+            // store instruction, each row's run contiguous
+            const uint32_t P = L * (L - 1) / 2;
+            for (uint32_t t0 = 0; t0 < P; t0 += 32) {
+              const uint32_t tt = t0 + lane;
+              const uint32_t rc = s_tri[tt < P ? tt : 0];
+              const uint32_t pr = L - 2 - (rc & 0xFFu), c = rc >> 8;
+              const uint32_t kk = pr + 1 + c;
+              const uint32_t d = __shfl_sync(0xffffffffu, dest, pr & 31);
+              const uint32_t b2 = __shfl_sync(0xffffffffu, bb, pr & 31);
+              const uint32_t jk = __shfl_sync(0xffffffffu, it_cur, kk & 31);
+              if (tt < P && ((fm >> pr) & 1u) && A.dbg_mode == 0) A.words[d + c] = b2 + jk;
+            }
+            continue;
+          }
+          for (uint32_t kc = UPPER ? pc : 0; kc < L; kc += 32) {
+            const uint32_t k = kc + lane;
+            const uint32_t jk = kc == 0 ? it_cur : (k < L ? A.items[tb + k] : 0u);
+            // UPPER: the chunk's last row has no column in its own chunk
+            uint32_t m = fm;
+            if (UPPER && kc == pc) m &= 0x7FFFFFFFu;
+            while (m) {
+              const int r = __ffs(m) - 1;
+              m &= m - 1;
+              const uint32_t d = __shfl_sync(0xffffffffu, dest, r);
+              const uint32_t b2 = __shfl_sync(0xffffffffu, bb, r);
+              const uint32_t c_lo = UPPER ? pc + r + 1 : 0;
+              if (k >= c_lo && k < L && A.dbg_mode == 0) A.words[d + (k - c_lo)] = b2 + jk;
+            }
+          }
         }
+        it_cur = it1;
+        it1 = it2;
+        it2 = it3;
+        it3 = it4;
+        tv_cur = tv1;
+        tv1 = tv2;
+        tv2 = tv3;
       }
-      __syncwarp();
-    });
+    }
     __syncthreads();
     for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) s_cnt[s_touched[k]] = 0;
   }
@@ -1182,23 +1234,62 @@ struct StreamCountArgs {
   unsigned long long* out_n;
   uint32_t* slabs;  // kStreamDenseCap words per unit of a split tile
   unsigned int* tile_done;
+  unsigned long long* dbg;  // development only (CROP_DEBUG_KINDS): cycles per kind/phase
 };
 
+// (row, column) of slot s of dense tile T (stream layout, stream_base)
+__device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint32_t n, bool upper,
+                                                uint32_t& i, uint32_t& j) {
+  if (T.row1 - T.row0 == 1) {
+    i = T.row0;
+    j = s + T.c0;
+  } else if (upper) {
+    uint32_t lo = T.row0, hi = T.row1;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (tri_rowbase(mid, T.row0, n) <= s) lo = mid;
+      else hi = mid;
+    }
+    i = lo;
+    j = (uint32_t)(s - tri_rowbase(i, T.row0, n)) + i + 1;
+  } else {
+    i = T.row0 + s / n;
+    j = s % n;
+  }
+}
+
+// Per unit: clear the table, count its words (block-cyclic 256-word blocks
+// over the warps so all warps finish together; the next block's 8 words per
+// lane are in flight while the current ones are counted), then either
+// compact the table into the output (single-unit tiles) or store it as the
+// unit's slab (split tiles, summed afterwards by k_reduce_slabs).
+// Dense tiles: u32 counter per slot. Hash tiles: 64-bit slots key << 32 |
+// count (linear probing), so an insert also counts (one CAS) and a hit is a
+// fire-and-forget 64-bit shared add; the first probe of all 8 words of a
+// lane is issued at once.
+constexpr unsigned long long kEmpty64 = ~0ull;
+
+template <bool DBG>
 __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense counters / hash keys
-  uint32_t* hcnt = table + kStreamHashSlots;             // hash counts
+  uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense counters
+  unsigned long long* slot64 = reinterpret_cast<unsigned long long*>(smem);  // hash slots
   uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + (size_t)kStreamDenseCap * 4);
   __shared__ uint32_t s_warp[33];
   __shared__ unsigned long long s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = A.n_items;
+  constexpr int D = 8;
+  constexpr uint32_t BW = 32 * D;  // words per block
+  if (threadIdx.x == 0) s_misc[0] = atomicAdd(A.unit_counter, 1u);
   for (;;) {
-    if (threadIdx.x == 0) s_misc[0] = atomicAdd(A.unit_counter, 1u);
     __syncthreads();
     const uint32_t u = s_misc[0];
     __syncthreads();
     if (u >= A.n_units) break;
+    // the next unit is claimed now and published after counting
+    uint32_t u_next = 0;
+    if (threadIdx.x == 0) u_next = atomicAdd(A.unit_counter, 1u);
     const Unit unit = A.units[u];
     const Tile T = A.tiles[unit.tile];
     const uint64_t Wn = A.tile_words[unit.tile];
@@ -1207,134 +1298,213 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     const uint64_t w1 = wb + Wn * (unit.local + 1) / T.n_units;
     const bool dense = T.mode == 0;
     const uint32_t width = T.width;
-    if (dense) {
+    long long c0 = 0, c1 = 0, c2 = 0;
+    if (DBG) c0 = clock64();
+    {
       uint4* t4 = reinterpret_cast<uint4*>(table);
-      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads)
-        t4[s] = make_uint4(0, 0, 0, 0);
-    } else {
-      for (uint32_t s = threadIdx.x; s < kStreamHashSlots; s += kCountThreads) {
-        table[s] = kEmpty32;
-        hcnt[s] = 0;
-      }
+      const uint32_t n4 = dense ? (width + 3) / 4 : kStreamHashSlots / 2;
+      const uint32_t f = dense ? 0u : kEmpty32;
+      for (uint32_t s = threadIdx.x; s < n4; s += kCountThreads) t4[s] = make_uint4(f, f, f, f);
     }
     __syncthreads();
-    // each warp: a contiguous share of [w0, w1), 256 words per step; the next
-    // step's 8 words per lane are loaded before this step's are counted
-    constexpr int D = 8;
-    const uint64_t per = (((w1 - w0) + kCountWarps - 1) / kCountWarps + (32 * D - 1)) &
-                         ~(uint64_t)(32 * D - 1);
-    const uint64_t a0 = w0 + (uint64_t)warp * per, a1 = min(w1, a0 + per);
-    auto fetch = [&](uint64_t b, uint32_t (&v)[D]) {
+    if (DBG) c1 = clock64();
+    const uint32_t nb = (uint32_t)((w1 - w0 + BW - 1) / BW);
+    const uint32_t* wp = A.words + w0 + lane;
+    auto fetch = [&](uint32_t blk, uint32_t (&v)[D]) {
+      const uint32_t* p = wp + (uint64_t)blk * BW;
+      if ((uint64_t)(blk + 1) * BW <= w1 - w0) {
 #pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const uint64_t x = b + k * 32 + lane;
-        v[k] = x < a1 ? __ldcs(A.words + x) : kEmpty32;
+        for (int k = 0; k < D; ++k) v[k] = __ldcs(p + k * 32);
+      } else {
+        const uint64_t left = (w1 - w0) - (uint64_t)blk * BW;
+#pragma unroll
+        for (int k = 0; k < D; ++k) v[k] = (uint64_t)(k * 32 + lane) < left ? __ldcs(p + k * 32) : kEmpty32;
       }
     };
     uint32_t cur[D], nxt[D];
-    if (a0 < a1) fetch(a0, cur);
-    for (uint64_t b = a0; b < a1; b += 32 * D) {
-      if (b + 32 * D < a1) fetch(b + 32 * D, nxt);
+    if ((uint32_t)warp < nb) fetch(warp, cur);
+    for (uint32_t blk = warp; blk < nb; blk += kCountWarps) {
+      if (blk + kCountWarps < nb) fetch(blk + kCountWarps, nxt);
       if (dense) {
 #pragma unroll
         for (int k = 0; k < D; ++k)
           if (cur[k] != kEmpty32) atomicAdd(&table[cur[k]], 1u);
       } else {
+        uint32_t sl[D];
+        unsigned long long v[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          sl[k] = __umulhi(mix32(cur[k]), kStreamHashSlots);
+          v[k] = slot64[sl[k]];
+        }
 #pragma unroll
         for (int k = 0; k < D; ++k) {
           const uint32_t key = cur[k];
           if (key == kEmpty32) continue;
-          uint32_t s = __umulhi(mix32(key), kStreamHashSlots);
+          uint32_t sk = sl[k];
+          unsigned long long vk = v[k];
           for (;;) {
-            const uint32_t kk = table[s];
-            if (kk == key) break;
-            if (kk == kEmpty32) {
-              const uint32_t old = atomicCAS(&table[s], kEmpty32, key);
-              if (old == kEmpty32 || old == key) break;
+            if ((uint32_t)(vk >> 32) == key) {
+              atomicAdd(&slot64[sk], 1ull);
+              break;
             }
-            if (++s == kStreamHashSlots) s = 0;
+            if (vk == kEmpty64) {
+              const unsigned long long old =
+                  atomicCAS(&slot64[sk], kEmpty64, ((unsigned long long)key << 32) | 1ull);
+              if (old == kEmpty64) break;
+              if ((uint32_t)(old >> 32) == key) {
+                atomicAdd(&slot64[sk], 1ull);
+                break;
+              }
+            }
+            if (++sk == kStreamHashSlots) sk = 0;
+            vk = slot64[sk];
           }
-          atomicAdd(&hcnt[s], 1u);
         }
       }
 #pragma unroll
       for (int k = 0; k < D; ++k) cur[k] = nxt[k];
     }
+    if (threadIdx.x == 0) s_misc[0] = u_next;
     __syncthreads();
-    bool emit_now = true, reduce = false;
-    const uint32_t* slab = A.slabs + T.slab_base * (uint64_t)kStreamDenseCap;
+    if (DBG) {
+      c2 = clock64();
+      if (threadIdx.x == 0) {
+        const int kind = !dense ? 3 : (T.n_units > 1 ? 2 : (T.row1 - T.row0 == 1 ? 0 : 1));
+        atomicAdd(&A.dbg[kind * 5 + 0], (unsigned long long)(c1 - c0));
+        atomicAdd(&A.dbg[kind * 5 + 1], (unsigned long long)(c2 - c1));
+        atomicAdd(&A.dbg[kind * 5 + 3], 1ull);
+        atomicAdd(&A.dbg[kind * 5 + 4], (unsigned long long)(w1 - w0));
+      }
+    }
     if (dense && T.n_units > 1) {
       uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * (uint64_t)kStreamDenseCap);
       const uint4* src = reinterpret_cast<const uint4*>(table);
-      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads) dst[s] = src[s];
-      __threadfence();
+      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads) __stcg(dst + s, src[s]);
       __syncthreads();
-      if (threadIdx.x == 0) s_misc[1] = atomicAdd(&A.tile_done[unit.tile], 1u) == T.n_units - 1;
-      __syncthreads();
-      emit_now = reduce = s_misc[1] != 0;
-      if (reduce) __threadfence();
+      continue;
     }
-    if (emit_now) {
-      auto count_at = [&](uint32_t s) -> uint32_t {
-        if (!dense) return hcnt[s];
-        uint32_t c = table[s];
-        if (reduce)
-          for (uint32_t v = 0; v < T.n_units; ++v)
-            if (v != unit.local) c += __ldcg(slab + (uint64_t)v * kStreamDenseCap + s);
-        return c;
-      };
-      const uint32_t slots = dense ? width : kStreamHashSlots;
-      const uint32_t per_w = (slots + kCountWarps - 1) / kCountWarps;
-      const uint32_t s_lo = min(slots, warp * per_w), s_hi = min(slots, s_lo + per_w);
-      uint32_t mine = 0;
-      for (uint32_t s = s_lo + lane; s < s_hi; s += 32) mine += count_at(s) != 0;
-      mine = warp_sum(mine);
-      uint32_t total;
-      uint32_t wbase = block_excl_scan(lane == 0 ? mine : 0, s_warp, total);
-      wbase = __shfl_sync(0xffffffffu, wbase, 0);
-      if (threadIdx.x == 0) s_base = atomicAdd(A.out_n, (unsigned long long)total);
-      __syncthreads();
-      uint64_t pos = s_base + wbase;
-      const bool single_row = T.row1 - T.row0 == 1;
-      for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        uint32_t c = 0, i = 0, j = 0;
-        if (s < s_hi) {
-          c = count_at(s);
-          if (c) {
-            if (!dense) {
-              const uint32_t key = table[s];
-              i = T.row0 + (key >> A.col_bits);
-              j = key & ((1u << A.col_bits) - 1u);
-            } else if (single_row) {
-              i = T.row0;
-              j = s + T.c0;
-            } else if (A.upper) {
-              uint32_t lo = T.row0, hi = T.row1;
-              while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (tri_rowbase(mid, T.row0, n) <= s) lo = mid;
-                else hi = mid;
-              }
-              i = lo;
-              j = (uint32_t)(s - tri_rowbase(i, T.row0, n)) + i + 1;
-            } else {
-              i = T.row0 + s / n;
-              j = s % n;
-            }
-          }
-        }
-        const uint32_t mk = __ballot_sync(0xffffffffu, c != 0);
-        if (c) {
-          const uint64_t o = pos + __popc(mk & ((1u << lane) - 1u));
-          A.out_row[o] = i;
-          A.out_col[o] = j;
-          A.out_count[o] = c;
-        }
-        pos += __popc(mk);
+    // compaction: count occupied slots (4 per lane per step), one output
+    // claim per unit, then emit
+    const uint32_t slots = dense ? width : kStreamHashSlots;
+    auto count_of = [&](uint32_t s) -> uint32_t {
+      if (dense) return table[s];
+      const unsigned long long x = slot64[s];
+      return x == kEmpty64 ? 0u : (uint32_t)x;
+    };
+    const uint32_t per_w = (((slots + kCountWarps - 1) / kCountWarps) + 127) & ~127u;
+    const uint32_t s_lo = min(slots, warp * per_w), s_hi = min(slots, s_lo + per_w);
+    uint32_t mine = 0;
+    if (dense) {
+      for (uint32_t s = s_lo + 4 * lane; s < s_hi; s += 128) {
+        const uint4 c4 = *reinterpret_cast<const uint4*>(table + s);  // table padded to 4
+        mine += (c4.x != 0) + (s + 1 < s_hi && c4.y != 0) + (s + 2 < s_hi && c4.z != 0) +
+                (s + 3 < s_hi && c4.w != 0);
+      }
+    } else {
+      for (uint32_t s = s_lo + 2 * lane; s < s_hi; s += 64) {
+        const ulonglong2 c2v = *reinterpret_cast<const ulonglong2*>(slot64 + s);
+        mine += (c2v.x != kEmpty64) + (s + 1 < s_hi && c2v.y != kEmpty64);
       }
     }
+    mine = warp_sum(mine);
+    uint32_t total;
+    uint32_t wbase = block_excl_scan(lane == 0 ? mine : 0, s_warp, total);
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (threadIdx.x == 0) s_base = atomicAdd(A.out_n, (unsigned long long)total);
     __syncthreads();
+    uint64_t pos = s_base + wbase;
+    for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      uint32_t c = 0, i = 0, j = 0;
+      if (s < s_hi) {
+        c = count_of(s);
+        if (c) {
+          if (!dense) {
+            const uint32_t key = (uint32_t)(slot64[s] >> 32);
+            i = T.row0 + (key >> A.col_bits);
+            j = key & ((1u << A.col_bits) - 1u);
+          } else {
+            dense_slot_pair(T, s, n, A.upper != 0, i, j);
+          }
+        }
+      }
+      const uint32_t mk = __ballot_sync(0xffffffffu, c != 0);
+      if (c) {
+        const uint64_t o = pos + __popc(mk & ((1u << lane) - 1u));
+        A.out_row[o] = i;
+        A.out_col[o] = j;
+        A.out_count[o] = c;
+      }
+      pos += __popc(mk);
+    }
+    __syncthreads();
+    if (DBG && threadIdx.x == 0) {
+      const int kind = !dense ? 3 : (T.n_units > 1 ? 2 : (T.row1 - T.row0 == 1 ? 0 : 1));
+      atomicAdd(&A.dbg[kind * 5 + 2], (unsigned long long)(clock64() - c2));
+    }
+  }
+}
+
+// Sum the slabs of each split dense tile and compact the sums: one block per
+// (tile, 2048-slot chunk) of the job's chunk list; each thread owns 8 slots
+// (two uint4) and reads four units' slabs per step.
+constexpr uint32_t kReduceSlots = 2048;
+__global__ void __launch_bounds__(256) k_reduce_slabs(StreamCountArgs A, const uint2* __restrict__ chunks,
+                                                      uint32_t n_chunks) {
+  __shared__ uint32_t s_warp[33];
+  __shared__ unsigned long long s_base;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
+    const uint2 ch = chunks[ci];
+    const Tile T = A.tiles[ch.x];
+    const uint32_t s0 = ch.y + threadIdx.x * 8;
+    const uint32_t nu = T.n_units;
+    const uint32_t* base = A.slabs + (uint64_t)T.slab_base * kStreamDenseCap + s0;
+    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (s0 < T.width) {
+      uint32_t v = 0;
+      for (; v + 4 <= nu; v += 4) {
+        uint4 x[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4* p = reinterpret_cast<const uint4*>(base + (uint64_t)(v + q) * kStreamDenseCap);
+          x[2 * q] = __ldcs(p);
+          x[2 * q + 1] = __ldcs(p + 1);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int h = (q & 1) * 4;
+          c[h] += x[q].x; c[h + 1] += x[q].y; c[h + 2] += x[q].z; c[h + 3] += x[q].w;
+        }
+      }
+      for (; v < nu; ++v) {
+        const uint4* p = reinterpret_cast<const uint4*>(base + (uint64_t)v * kStreamDenseCap);
+        const uint4 a = __ldcs(p), b = __ldcs(p + 1);
+        c[0] += a.x; c[1] += a.y; c[2] += a.z; c[3] += a.w;
+        c[4] += b.x; c[5] += b.y; c[6] += b.z; c[7] += b.w;
+      }
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mine += (s0 + k < T.width && c[k] != 0);
+    uint32_t total;
+    const uint32_t excl = block_excl_scan(mine, s_warp, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(A.out_n, (unsigned long long)total) : 0ull;
+    __syncthreads();
+    uint64_t o = s_base + excl;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (s0 + k < T.width && c[k] != 0) {
+        uint32_t i, j;
+        dense_slot_pair(T, s0 + k, A.n_items, A.upper != 0, i, j);
+        A.out_row[o] = i;
+        A.out_col[o] = j;
+        A.out_count[o] = c[k];
+        ++o;
+      }
+    __syncthreads();
+    (void)lane;
   }
 }
 
@@ -1415,6 +1585,8 @@ struct crop_pairs {
   unsigned int* d_unit_counter = nullptr;
   uint32_t* d_overflow = nullptr;
   unsigned int* d_tile_done = nullptr;
+  uint2* d_reduce_chunks = nullptr;  // stream mode: (split tile, first slot)
+  std::vector<uint2> h_reduce_chunks;
   std::vector<uint32_t> h_item_tile;  // kept alive for the async uploads
   std::vector<uint2> h_item_info;
   // stream mode (short rows): pair words per tile instead of entries
@@ -1431,7 +1603,7 @@ static void free_job(crop_pairs* j) {
     if (e) cudaEventDestroy(e);
   void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_item_info, j->d_tiles, j->d_units, j->d_split,
                   j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_tile_end, j->d_total_entries,
-                  j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done,
+                  j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done, j->d_reduce_chunks,
                   j->d_words, j->d_tile_words};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
@@ -1773,6 +1945,15 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         info[i] = make_uint2(tv, (tv & kWinFlag) ? 0u : stream_base(T, i, n_items, J->col_bits, J->upper != 0));
       }
       JCUDA(cudaMallocAsync(&J->d_item_info, nn * sizeof(uint2), st));
+      J->h_reduce_chunks.clear();
+      for (uint32_t t : J->split)
+        for (uint32_t c0 = 0; c0 < J->tiles[t].width; c0 += kReduceSlots)
+          J->h_reduce_chunks.push_back(make_uint2(t, c0));
+      if (!J->h_reduce_chunks.empty()) {
+        JCUDA(cudaMallocAsync(&J->d_reduce_chunks, J->h_reduce_chunks.size() * sizeof(uint2), st));
+        JCUDA(cudaMemcpyAsync(J->d_reduce_chunks, J->h_reduce_chunks.data(),
+                              J->h_reduce_chunks.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
+      }
       if (n_items)
         JCUDA(cudaMemcpyAsync(J->d_item_info, info.data(), n_items * sizeof(uint2), cudaMemcpyHostToDevice, st));
       JCUDA(cudaMallocAsync(&J->d_words, std::max<uint64_t>(1, J->total_terms) * 4, st));
@@ -1847,6 +2028,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     R.tile_words = J->d_tile_words;
     R.tile_cursor = J->d_tile_cursor;
     R.tile_base = J->d_tile_ebase;
+    R.dbg_mode = getenv("CROP_DEBUG_WRITE") ? atoi(getenv("CROP_DEBUG_WRITE")) : 0;
     R.words = J->d_words;
     const int64_t chunks = (J->n_tx + kChunkTx - 1) / kChunkTx;
     const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
@@ -1864,7 +2046,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     mark(1);
     {
       auto kern = up ? k_stream_write<true> : k_stream_write<false>;
-      const size_t smem = kOffBytes + (size_t)kTileSmem * 6 + 16 + kCountWarps * 128 * 4;
+      const size_t smem = kOffBytes + (size_t)kTileSmem * 6 + 16;
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, kPassThreads, smem, st>>>(R);
       CROP_LAUNCH_CHECK();
@@ -1890,13 +2072,34 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.out_n = (unsigned long long*)d_n_entries;
     C.slabs = J->d_slabs;
     C.tile_done = J->d_tile_done;
-    CROP_CUDA(cudaFuncSetAttribute(k_count_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kStreamSmem));
+    C.dbg = nullptr;
+    if (getenv("CROP_DEBUG_KINDS")) {
+      static unsigned long long* dbg = nullptr;
+      if (!dbg) cudaMalloc(&dbg, 20 * 8);
+      cudaMemsetAsync(dbg, 0, 20 * 8, st);
+      C.dbg = dbg;
+    }
+    auto kcs = C.dbg ? k_count_stream<true> : k_count_stream<false>;
+    CROP_CUDA(cudaFuncSetAttribute(kcs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     mark(4);
-    k_count_stream<<<std::min<int>(kNumSMs, (int)J->units.size()), kCountThreads, kStreamSmem, st>>>(C);
+    kcs<<<std::min<int>(kNumSMs, (int)J->units.size()), kCountThreads, kStreamSmem, st>>>(C);
     CROP_LAUNCH_CHECK();
+    const uint32_t nrc = (uint32_t)J->h_reduce_chunks.size();
+    if (nrc) {
+      k_reduce_slabs<<<std::min<uint32_t>(nrc, kNumSMs * 8), 256, 0, st>>>(C, J->d_reduce_chunks, nrc);
+      CROP_LAUNCH_CHECK();
+    }
     mark(5);
-    crop_count_launches(4);
+    if (C.dbg) {
+      unsigned long long h[20];
+      cudaMemcpyAsync(h, C.dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const char* names[4] = {"dense-row", "dense-multi", "dense-split", "hash"};
+      for (int k = 0; k < 4; ++k)
+        fprintf(stderr, "[k_count_stream] %-11s units %6llu words %10llu zero %7.1f count %8.1f emit %7.1f Mcyc\n",
+                names[k], h[5 * k + 3], h[5 * k + 4], h[5 * k] / 1e6, h[5 * k + 1] / 1e6, h[5 * k + 2] / 1e6);
+    }
+    crop_count_launches(nrc ? 5 : 4);
     return CROP_OK;
   }
   // route: one walk, staged per chunk, ranges claimed per touched tile

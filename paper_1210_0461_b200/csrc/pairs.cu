@@ -985,8 +985,8 @@ struct StreamRouteArgs {
   unsigned long long* tile_words;   // B1: word totals per tile
   unsigned long long* tile_cursor;  // B2: next free word per tile
   const unsigned long long* tile_base;  // B2: first word of each tile
+  int chunk_tx;                     // transactions per chunk (<= kChunkTx)
   uint32_t* words;
-  int dbg_mode;  // development only (CROP_DEBUG_WRITE): 1 = no word stores, 2 = no write phase
 };
 
 // Visit the words of row occurrence (g, q) of row item i: fn(dest_tile, base,
@@ -1049,10 +1049,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
   const uint32_t ns = min(A.n_tiles, kTileSmem);
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
-  const int64_t n_chunks = (A.n_tx + kChunkTx - 1) / kChunkTx;
+  const int64_t n_chunks = (A.n_tx + A.chunk_tx - 1) / A.chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
-    const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, kChunkTx);
+    const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, A.chunk_tx);
     walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
       if (!q.valid) return;
@@ -1078,10 +1078,12 @@ template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
-  uint16_t* s_touched = reinterpret_cast<uint16_t*>(s_cnt + kTileSmem);  // tile ids < 2^16
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(s_touched + kTileSmem);
+  // shared tile counters sized by the job (ns rounded to 2 for alignment)
   const uint32_t ns = min(A.n_tiles, kTileSmem);
+  const uint32_t ns2 = (ns + 1) & ~1u;
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
+  uint16_t* s_touched = reinterpret_cast<uint16_t*>(s_cnt + ns2);  // tile ids < 2^16
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(s_touched + ns2);
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // triangle decode for transactions of <= 32 items: pair t = r (r + 1) / 2 + c
@@ -1089,11 +1091,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
   __shared__ uint16_t s_tri[496];
   for (uint32_t r = 0; r < 31; ++r)
     for (uint32_t c = threadIdx.x; c <= r; c += blockDim.x) s_tri[r * (r + 1) / 2 + c] = (uint16_t)(r | c << 8);
-  const int64_t n_chunks = (A.n_tx + kChunkTx - 1) / kChunkTx;
+  const int64_t n_chunks = (A.n_tx + A.chunk_tx - 1) / A.chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
     if (threadIdx.x == 0) s_misc[0] = 0;
-    const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, kChunkTx);
+    const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, A.chunk_tx);
     walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
       if (!q.valid) return;
@@ -1112,11 +1114,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
     }
     __syncthreads();
     // write: one warp per transaction. Lanes hold 32 rows (their claims and
-    // bases) and 32 columns at a time; each row's run of columns is one
-    // coalesced store instruction (row and base broadcast by shuffle). The
-    // first 32 items of the warp's next transaction and the item_info of
-    // the one after are in flight while a transaction is written.
-    if (A.dbg_mode != 2) {
+    // bases) and 32 columns at a time. Transactions of <= 32 items (UPPER)
+    // are written as their flattened triangle, 32 pairs per store
+    // instruction; their claims are made one transaction ahead so the claim
+    // latency overlaps the previous transaction's stores. Items are loaded
+    // four transactions ahead, item_info three ahead.
+    {
       constexpr int NW = kPassThreads / 32;
       auto ld_it = [&](int t) -> uint32_t {
         if (t >= ntx) return kNone;
@@ -1126,82 +1129,102 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
       auto ld_tv = [&](uint32_t it) -> uint2 {
         return it != kNone ? __ldg(A.item_info + it) : make_uint2(kNone, 0u);
       };
-      // items 4 transactions ahead, their item_info 3 ahead
+      // rows p < L of a transaction, first 32: claim (fast rows) or write
+      // directly (split / filtered rows); returns the fast-row mask
+      auto claim = [&](int t, int64_t tb, uint32_t L, uint32_t pc, uint32_t i, uint2 tv,
+                       uint32_t& dest, uint32_t& bb) -> uint32_t {
+        const uint32_t p = pc + lane;
+        bool fast = false;
+        if (p < L && (!UPPER || p + 1 < L) && tv.x != kNone) {
+          const uint32_t n = UPPER ? L - 1 - p : L;
+          if (!(tv.x & kWinFlag) && !A.filter) {
+            fast = true;
+            bb = tv.y;
+            dest = tv.x < ns ? atomicAdd(&s_cnt[tv.x], n)
+                             : (uint32_t)atomicAdd(&A.tile_cursor[tv.x], (unsigned long long)n);
+          } else {
+            Pos q;
+            q.base = tb;
+            q.p = p;
+            q.L = L;
+            q.tx = (uint32_t)t;
+            q.valid = true;
+            stream_row<UPPER>(A, i, q, tv, [&](uint32_t t2, uint32_t b, uint32_t first, uint32_t n2) {
+              const unsigned long long p0 =
+                  t2 < ns ? (unsigned long long)atomicAdd(&s_cnt[t2], n2)
+                          : atomicAdd(&A.tile_cursor[t2], (unsigned long long)n2);
+              for (uint32_t k = 0; k < n2; ++k) A.words[p0 + k] = b + A.items[first + k];
+            });
+          }
+        }
+        return __ballot_sync(0xffffffffu, fast);
+      };
       uint32_t it_cur = ld_it(warp), it1 = ld_it(warp + NW), it2 = ld_it(warp + 2 * NW),
                it3 = ld_it(warp + 3 * NW);
       uint2 tv_cur = ld_tv(it_cur), tv1 = ld_tv(it1), tv2 = ld_tv(it2);
+      // prepared claims of the current transaction (short path only)
+      uint32_t c_dest = 0, c_bb = 0, c_fm = 0;
+      auto prepare = [&](int t, uint32_t it, uint2 tv, uint32_t& dest, uint32_t& bb) -> uint32_t {
+        if (t >= ntx) return 0u;
+        const int64_t tb = s_off[t];
+        const uint32_t L = (uint32_t)(s_off[t + 1] - tb);
+        if (!UPPER || L > 32) return 0u;
+        return claim(t, tb, L, 0, it, tv, dest, bb);
+      };
+      c_fm = prepare(warp, it_cur, tv_cur, c_dest, c_bb);
       for (int t = warp; t < ntx; t += NW) {
         const uint2 tv3 = ld_tv(it3);
         const uint32_t it4 = ld_it(t + 4 * NW);
         const int64_t tb = s_off[t];
         const uint32_t L = (uint32_t)(s_off[t + 1] - tb);
-        for (uint32_t pc = 0; pc < L; pc += 32) {
-          const uint32_t p = pc + lane;
-          bool fast = false;
-          uint32_t dest = 0, bb = 0;
-          uint32_t i = it_cur;
-          uint2 tv = tv_cur;
-          if (pc > 0 && p < L) {
-            i = A.items[tb + p];
-            tv = A.item_info[i];
-          }
-          if (p < L && (!UPPER || p + 1 < L) && tv.x != kNone) {
-            const uint32_t n = UPPER ? L - 1 - p : L;
-            if (!(tv.x & kWinFlag) && !A.filter) {
-              fast = true;
-              bb = tv.y;
-              dest = tv.x < ns ? atomicAdd(&s_cnt[tv.x], n)
-                               : (uint32_t)atomicAdd(&A.tile_cursor[tv.x], (unsigned long long)n);
-            } else {
-              Pos q;
-              q.base = tb;
-              q.p = p;
-              q.L = L;
-              q.tx = (uint32_t)t;
-              q.valid = true;
-              stream_row<UPPER>(A, i, q, tv, [&](uint32_t t2, uint32_t b, uint32_t first, uint32_t n2) {
-                const unsigned long long p0 =
-                    t2 < ns ? (unsigned long long)atomicAdd(&s_cnt[t2], n2)
-                            : atomicAdd(&A.tile_cursor[t2], (unsigned long long)n2);
-                for (uint32_t k = 0; k < n2; ++k) A.words[p0 + k] = b + A.items[first + k];
-              });
-            }
-          }
-          const uint32_t fm = __ballot_sync(0xffffffffu, fast);
-          if (!fm || A.dbg_mode == 3) continue;
-          if (UPPER && L <= 32) {
-            // the transaction's triangle flattened: pair t -> (row from the
-            // end r, column offset c) via the shared table; 32 pairs per
-            // store instruction, each row's run contiguous
-            const uint32_t P = L * (L - 1) / 2;
+        uint32_t n_dest = 0, n_bb = 0;
+        const uint32_t n_fm = prepare(t + NW, it1, tv1, n_dest, n_bb);
+        if (UPPER && L <= 32) {
+          // the flattened triangle: pair tt -> (row from the end r, column
+          // offset c) via the shared table; each row's run contiguous
+          const uint32_t P = L * (L - 1) / 2;
+          if (c_fm)
             for (uint32_t t0 = 0; t0 < P; t0 += 32) {
               const uint32_t tt = t0 + lane;
               const uint32_t rc = s_tri[tt < P ? tt : 0];
               const uint32_t pr = L - 2 - (rc & 0xFFu), c = rc >> 8;
               const uint32_t kk = pr + 1 + c;
-              const uint32_t d = __shfl_sync(0xffffffffu, dest, pr & 31);
-              const uint32_t b2 = __shfl_sync(0xffffffffu, bb, pr & 31);
+              const uint32_t d = __shfl_sync(0xffffffffu, c_dest, pr & 31);
+              const uint32_t b2 = __shfl_sync(0xffffffffu, c_bb, pr & 31);
               const uint32_t jk = __shfl_sync(0xffffffffu, it_cur, kk & 31);
-              if (tt < P && ((fm >> pr) & 1u) && A.dbg_mode == 0) A.words[d + c] = b2 + jk;
+              if (tt < P && ((c_fm >> pr) & 1u)) A.words[d + c] = b2 + jk;
             }
-            continue;
-          }
-          for (uint32_t kc = UPPER ? pc : 0; kc < L; kc += 32) {
-            const uint32_t k = kc + lane;
-            const uint32_t jk = kc == 0 ? it_cur : (k < L ? A.items[tb + k] : 0u);
-            // UPPER: the chunk's last row has no column in its own chunk
-            uint32_t m = fm;
-            if (UPPER && kc == pc) m &= 0x7FFFFFFFu;
-            while (m) {
-              const int r = __ffs(m) - 1;
-              m &= m - 1;
-              const uint32_t d = __shfl_sync(0xffffffffu, dest, r);
-              const uint32_t b2 = __shfl_sync(0xffffffffu, bb, r);
-              const uint32_t c_lo = UPPER ? pc + r + 1 : 0;
-              if (k >= c_lo && k < L && A.dbg_mode == 0) A.words[d + (k - c_lo)] = b2 + jk;
+        } else {
+          for (uint32_t pc = 0; pc < L; pc += 32) {
+            uint32_t i = it_cur;
+            uint2 tv = tv_cur;
+            if (pc > 0 && pc + lane < L) {
+              i = A.items[tb + pc + lane];
+              tv = A.item_info[i];
+            }
+            uint32_t dest = 0, bb = 0;
+            const uint32_t fm = claim(t, tb, L, pc, i, tv, dest, bb);
+            if (!fm) continue;
+            for (uint32_t kc = UPPER ? pc : 0; kc < L; kc += 32) {
+              const uint32_t k = kc + lane;
+              const uint32_t jk = kc == 0 ? it_cur : (k < L ? A.items[tb + k] : 0u);
+              // UPPER: the chunk's last row has no column in its own chunk
+              uint32_t m = fm;
+              if (UPPER && kc == pc) m &= 0x7FFFFFFFu;
+              while (m) {
+                const int r = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t d = __shfl_sync(0xffffffffu, dest, r);
+                const uint32_t b2 = __shfl_sync(0xffffffffu, bb, r);
+                const uint32_t c_lo = UPPER ? pc + r + 1 : 0;
+                if (k >= c_lo && k < L) A.words[d + (k - c_lo)] = b2 + jk;
+              }
             }
           }
         }
+        c_dest = n_dest;
+        c_bb = n_bb;
+        c_fm = n_fm;
         it_cur = it1;
         it1 = it2;
         it2 = it3;
@@ -2028,9 +2051,10 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     R.tile_words = J->d_tile_words;
     R.tile_cursor = J->d_tile_cursor;
     R.tile_base = J->d_tile_ebase;
-    R.dbg_mode = getenv("CROP_DEBUG_WRITE") ? atoi(getenv("CROP_DEBUG_WRITE")) : 0;
     R.words = J->d_words;
-    const int64_t chunks = (J->n_tx + kChunkTx - 1) / kChunkTx;
+    // about 12 chunks per CTA so the last wave's imbalance stays small
+    R.chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, J->n_tx / (kNumSMs * 12)));
+    const int64_t chunks = (J->n_tx + R.chunk_tx - 1) / R.chunk_tx;
     const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
     CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
     {
@@ -2046,8 +2070,10 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     mark(1);
     {
       auto kern = up ? k_stream_write<true> : k_stream_write<false>;
-      const size_t smem = kOffBytes + (size_t)kTileSmem * 6 + 16;
-      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const size_t ns2 = (std::min(nt, kTileSmem) + 1) & ~1u;
+      const size_t smem = kOffBytes + ns2 * 6 + 16;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kOffBytes + (size_t)kTileSmem * 6 + 16)));
       kern<<<grid, kPassThreads, smem, st>>>(R);
       CROP_LAUNCH_CHECK();
     }

@@ -11,10 +11,11 @@ Inputs are resident in HBM; L2 is flushed (1 GiB write) before every timed
 step. `value` = all terms of the workload / (max over ranks of the summed
 per-step CUDA-event time). `e2e` runs the public API (`crop.run` +
 `SketchState.top_entries`) from pinned host buffers, host<->device copies
-inside the timed region. `roofline` is the dominant kernel (k_count), timed
-live with CUDA events on its stream. `cpu_baseline` is the C oracle (the
-reference algorithm restated, oracle/crop_oracle.c) on a bounded prefix,
-shared-nothing threads on every host core.
+inside the timed region. `roofline` is the counting path of SURVEY.md §8(d)
+(B_alg = 8 B/term + input + output over the path's live CUDA-event time),
+with each phase's kernels, time and share of the step. `cpu_baseline` is the
+C oracle (the reference algorithm restated, oracle/crop_oracle.c) on a
+bounded prefix, shared-nothing threads on the host cores.
 
 Under torchrun (N > 1) rank 0 generates the workload and broadcasts it once
 over NCCL; rank r counts the buckets split(kappa, N)[r] (no communication);
@@ -110,13 +111,14 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic(kernel: str, config: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu summary, or None."""
+def ncu_traffic(config: str):
+    """DRAM bytes (read + write) of one counting path from the committed ncu
+    summary (profiles/ncu_summary.json, `ncu --set full` per kernel), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d[config][kernel]["dram_bytes_per_launch"]
+        return d[config]["path_dram_bytes"]
     except Exception:
         return None
 
@@ -188,9 +190,17 @@ def run_ours(args, rank, world):
     flush = torch.empty(1 << 28, dtype=torch.int32, device=dev)  # 1 GiB > 126 MB L2
 
     def step():
+        # counting path (SURVEY.md §8d primary time): from the first kernel of
+        # the job (per-item term scan) to the last counting kernel
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
         job = kernels.PairCountJob(dtx, True, interval, keep=tables)
         job.set_timing(True)
-        ent = job.run(sync=True)
+        ent = job.run(sync=False)
+        p1.record()
+        ent.n = int(ent.n_dev.item())
+        if ent.n > job.max_entries or job.overflowed():
+            raise RuntimeError("pair engine overflow")
         idx = kernels.topk_indices(ent, cfg.top_k)
         top = (ent.row[idx], ent.col[idx], ent.count[idx])
         if world > 1:
@@ -204,7 +214,9 @@ def run_ours(args, rank, world):
             dist.all_gather(allb, buf)
             top = torch.cat(allb, dim=1)
         phases = job.phase_ms()
-        stats = (job.total_terms, ent.n, job.n_tiles, job.n_units)
+        phases["path"] = p0.elapsed_time(p1)
+        phases["plan"] = phases["path"] - phases["route"] - phases["write"] - phases["count"]
+        stats = (job.total_terms, ent.n, job.n_tiles, job.n_units, job.stream_mode)
         job.close()
         return phases, stats, top
 
@@ -248,9 +260,11 @@ def run_ours(args, rank, world):
     ms_per_step = t_sum / args.steps
     value = total_terms_all * args.steps / (t_sum * 1e-3)
 
-    # roofline of the dominant kernel (k_count): 8 B per term
-    # (one 4-byte counter read + write) + 12 B per output entry; own terms =
-    # terms of this rank's buckets = the sum of its output counts
+    # roofline: B_alg = 8 B per term (one 4-byte counter read
+    # + write) + the input read once + 12 B per output (row, col, count) entry,
+    # over the counting path's live CUDA-event time (first kernel of the job to
+    # the last counting kernel, host planning gap included). Own terms = terms
+    # of this rank's buckets = the sum of its output counts.
     if world > 1:
         job = kernels.PairCountJob(dtx, True, interval, keep=tables)
         ent = job.run()
@@ -258,16 +272,26 @@ def run_ours(args, rank, world):
         job.close()
     else:
         own_terms = total_terms_all
-    b_alg = 8 * own_terms + 12 * own_entries
-    count_avg = statistics.mean(count_ms)
+    in_bytes = 4 * int(dtx.items.numel()) + 8 * int(dtx.offsets.numel())
+    b_alg = 8 * own_terms + in_bytes + 12 * own_entries
+    avg = {k: statistics.mean(p[k] for p in phase_log) for k in phase_log[0]}
     peak, peak_src = peaks()
-    achieved = b_alg / (count_avg * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_count", "achieved": round(achieved, 1),
-                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": ncu_traffic("k_count", args.config), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": b_alg, "avg_launch_ms": round(count_avg, 4),
-                "phase_ms_avg": {k: round(statistics.mean(p[k] for p in phase_log), 4)
-                                 for k in phase_log[0]}}
+    achieved = b_alg / (avg["path"] * 1e-3) / 1e9
+    stream_mode = bool(stats[4])
+    kern = {"plan": "k_item_terms + host tile plan + uploads",
+            "route": "k_stream_count + k_scan_u64" if stream_mode else "k_route",
+            "write": "k_stream_write" if stream_mode else "k_tile_entries",
+            "count": "k_count_stream + k_reduce_slabs" if stream_mode else "k_count"}
+    roofline = {"bound": "hbm", "kernel": "counting path: " + " -> ".join(kern[k] for k in
+                                                                          ("plan", "route", "write", "count")),
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,
+                "avg_launch_ms": round(avg["path"], 4),
+                "phases": {k: {"kernels": kern[k], "ms": round(avg[k], 4),
+                               "share_of_step": round(avg[k] / ms_per_step, 4)}
+                           for k in ("plan", "route", "write", "count")},
+                "mode": "stream" if stream_mode else "entry"}
 
     e2e = None
     if not args.no_e2e:
@@ -349,7 +373,8 @@ def run_e2e(args, cfg, dtx, rank, world):
 
 
 def default_sample(cfg_name):
-    return {"c1": 20_000, "c2": 150_000, "c3": 60_000, "c5": 3_000}.get(cfg_name, 50_000)
+    # about 10 s of oracle work on the box's host threads
+    return {"c1": 20_000, "c2": 2_000_000, "c3": 600_000, "c5": 20_000}.get(cfg_name, 50_000)
 
 
 def cpu_baseline(args, cfg, dtx, reps: int = 1):

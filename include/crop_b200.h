@@ -98,11 +98,18 @@ int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* tota
 int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32_t* out_count,
                    uint64_t* d_n_entries, void* stream);
 /* Per-phase CUDA-event timing of crop_pairs_run (off by default). out4 =
- * {route, tile-entry counts, 0, count} in ms of the last run. */
+ * {route, write, 0, count} in ms of the last run: stream mode = {per-tile word
+ * totals + scan, word write, -, count + slab reduction}; entry mode = {entry
+ * routing, per-tile entry counts, -, count}. */
 int crop_pairs_set_timing(crop_pairs* job, int on);
 int crop_pairs_phase_ms(const crop_pairs* job, float* out4);
 /* 1 if the entry list overflowed its capacity (never expected; synchronises). */
 int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
+/* Counting mode chosen by crop_pairs_create: 1 = stream (one 32-bit word per
+ * pair term routed to its tile's stream, coalesced counting), 0 = entry
+ * (one entry per (transaction, tile) run, counting re-reads the items).
+ * CROP_FORCE_ENTRY_MODE=1 in the environment forces entry mode. */
+int crop_pairs_mode(const crop_pairs* job, int* stream_mode);
 void crop_pairs_destroy(crop_pairs* job);
 
 /* Per-instance bucket statistics of counted entries (the LoadReport rows,

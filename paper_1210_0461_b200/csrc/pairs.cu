@@ -1899,9 +1899,13 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     {
       unsigned long long occ_sum = 0;
       for (uint32_t i = 0; i < n_items; ++i) occ_sum += occ[i];
-      J->stream_mode = getenv("CROP_FORCE_ENTRY_MODE") == nullptr && occ_sum > 0 &&
-                       J->total_terms <= (unsigned long long)kStreamMeanMax * occ_sum &&
-                       J->total_terms < (1ull << 32);
+      // stream mode when rows are short on average (words stay < 2^32);
+      // CROP_FORCE_ENTRY_MODE / CROP_FORCE_STREAM_MODE override (tests)
+      const bool fits = J->total_terms < (1ull << 32);
+      if (getenv("CROP_FORCE_ENTRY_MODE")) J->stream_mode = false;
+      else if (getenv("CROP_FORCE_STREAM_MODE")) J->stream_mode = fits;
+      else J->stream_mode = fits && occ_sum > 0 &&
+                            J->total_terms <= (unsigned long long)kStreamMeanMax * occ_sum;
     }
     std::vector<uint32_t>& item_tile = J->h_item_tile;
     auto t_p0 = std::chrono::steady_clock::now();
@@ -2222,6 +2226,11 @@ extern "C" int crop_pairs_phase_ms(const crop_pairs* J, float* out4) {
   CROP_CUDA(cudaEventElapsedTime(&out4[1], J->ev[1], J->ev[2]));
   CROP_CUDA(cudaEventElapsedTime(&out4[2], J->ev[2], J->ev[3]));
   CROP_CUDA(cudaEventElapsedTime(&out4[3], J->ev[4], J->ev[5]));
+  return CROP_OK;
+}
+
+extern "C" int crop_pairs_mode(const crop_pairs* J, int* stream_mode) {
+  *stream_mode = J->stream_mode ? 1 : 0;
   return CROP_OK;
 }
 

@@ -218,7 +218,14 @@ class PairCountJob:
     def phase_ms(self) -> dict:
         out = (ctypes.c_float * 4)()
         nat.check(nat.load().crop_pairs_phase_ms(self._h, out))
-        return {"route": out[0], "tile_entries": out[1], "count": out[3]}
+        return {"route": out[0], "write": out[1], "count": out[3]}
+
+    @property
+    def stream_mode(self) -> bool:
+        """True when the job counts per-pair word streams (see crop_pairs_mode)."""
+        flag = ctypes.c_int()
+        nat.check(nat.load().crop_pairs_mode(self._h, ctypes.byref(flag)))
+        return bool(flag.value)
 
     def overflowed(self) -> bool:
         flag = ctypes.c_int()

@@ -193,9 +193,19 @@ def _gpu_pairs(ent):
     return oracle.sorted_pairs(r, c, w)
 
 
+@pytest.fixture(params=["auto", "entry", "stream"])
+def count_mode(request, monkeypatch):
+    """Counting mode of the pair engine: the planner's choice, or forced."""
+    if request.param == "entry":
+        monkeypatch.setenv("CROP_FORCE_ENTRY_MODE", "1")
+    elif request.param == "stream":
+        monkeypatch.setenv("CROP_FORCE_STREAM_MODE", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("name,n_tx", [("c1", None), ("c2", 60_000), ("c5", 3_000),
                                        ("c3", 30_000)])
-def test_config_prefix_counts_bit_exact(name, n_tx):
+def test_config_prefix_counts_bit_exact(name, n_tx, count_mode):
     cfg = workloads.CONFIGS[name]
     dtx = workloads.generate_pairs_workload(cfg, n_tx=n_tx)
     off, items = dtx.to_host()
@@ -226,7 +236,7 @@ def test_c1_full_run_against_oracle():
 
 
 @pytest.mark.parametrize("kappa,workers,worker", [(8, 8, 3), (1184, 8, 5), (16, 4, 0)])
-def test_interval_filter_matches_oracle_worker(kappa, workers, worker):
+def test_interval_filter_matches_oracle_worker(kappa, workers, worker, count_mode):
     cfg = workloads.CONFIGS["c2"]
     dtx = workloads.generate_pairs_workload(cfg, n_tx=20_000)
     off, items = dtx.to_host()
@@ -242,6 +252,15 @@ def test_interval_filter_matches_oracle_worker(kappa, workers, worker):
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
     assert int(got[2].sum()) == load
+
+
+def test_mode_choice():
+    """Short transactions (c2) count in stream mode, long ones (c5) in entry mode."""
+    for name, n_tx, want in (("c2", 20_000, True), ("c5", 2_000, False)):
+        dtx = workloads.generate_pairs_workload(workloads.CONFIGS[name], n_tx=n_tx)
+        job = kernels.PairCountJob(dtx, True, None)
+        assert job.stream_mode is want
+        job.close()
 
 
 def test_topk_with_ties_matches_sort():
@@ -299,7 +318,7 @@ def test_edge_cases():
         assert len(state.top_entries(5)) == min(5, len(sup))
 
 
-def test_long_transactions_and_wide_rows():
+def test_long_transactions_and_wide_rows(count_mode):
     # lengths up to the 8192 limit; n > kDenseCap forces column windows
     rng = np.random.default_rng(0)
     n = 120_000

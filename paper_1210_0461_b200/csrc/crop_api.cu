@@ -197,9 +197,15 @@ __global__ void __launch_bounds__(kStatThreads)
   __shared__ unsigned long long s_load[kStatSmemBuckets];
   __shared__ unsigned long long s_cs[kStatSmemBuckets];
   __shared__ uint32_t s_dist[kStatSmemBuckets];
+  // few buckets (kappa <= 64): one counter set per lane index, so the 32
+  // lanes of a warp never collide (the warps of the block share them);
+  // otherwise one set per block
+  const bool lanes = kappa <= kStatSmemBuckets / 32;
   const bool smem = kappa <= kStatSmemBuckets;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t slots = lanes ? kappa * 32 : kappa;
   if (smem)
-    for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) {
+    for (uint32_t b = threadIdx.x; b < slots; b += blockDim.x) {
       s_load[b] = 0;
       s_cs[b] = 0;
       s_dist[b] = 0;
@@ -214,9 +220,10 @@ __global__ void __launch_bounds__(kStatThreads)
     long long sc = 0;
     if (do_cs) sc = sign_of(i, j, sign_mul, sign_add) * (long long)c;
     if (smem) {
-      atomicAdd(&s_load[b], (unsigned long long)c);
-      atomicAdd(&s_dist[b], 1u);
-      if (do_cs) atomicAdd(&s_cs[b], (unsigned long long)sc);
+      const uint32_t sl = lanes ? b * 32 + lane : b;
+      atomicAdd(&s_load[sl], (unsigned long long)c);
+      atomicAdd(&s_dist[sl], 1u);
+      if (do_cs) atomicAdd(&s_cs[sl], (unsigned long long)sc);
     } else {
       atomicAdd(&loads[b], (unsigned long long)c);
       atomicAdd(&distinct[b], 1u);
@@ -224,12 +231,30 @@ __global__ void __launch_bounds__(kStatThreads)
     }
   }
   __syncthreads();
-  if (smem)
+  if (lanes) {
+    // fold the 32 lane sets: warp w sums bucket w, w + nwarps, ...
+    const uint32_t warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t b = warp; b < kappa; b += nw) {
+      unsigned long long l = s_load[b * 32 + lane], x = s_cs[b * 32 + lane];
+      uint32_t d = s_dist[b * 32 + lane];
+      for (int o = 16; o; o >>= 1) {
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+      }
+      if (lane == 0) {
+        if (l) atomicAdd(&loads[b], l);
+        if (d) atomicAdd(&distinct[b], d);
+        if (do_cs && x) atomicAdd(&cs[b], x);
+      }
+    }
+  } else if (smem) {
     for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) {
       if (s_load[b]) atomicAdd(&loads[b], s_load[b]);
       if (s_dist[b]) atomicAdd(&distinct[b], s_dist[b]);
       if (do_cs && s_cs[b]) atomicAdd(&cs[b], s_cs[b]);
     }
+  }
 }
 
 extern "C" int crop_entry_bucket_stats(const uint32_t* row, const uint32_t* col,

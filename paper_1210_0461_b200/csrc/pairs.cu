@@ -34,6 +34,7 @@
 #include <cstring>
 #include <numeric>
 #include <chrono>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 
@@ -67,11 +68,13 @@ constexpr uint64_t kOccOne = 1ull << 40;             // pass A: occurrence count
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kUnknown = 0xFFFFFFFEu;       // route: previous tile not known yet
 constexpr uint32_t kWinFlag = 0x80000000u;           // item_tile: row is split into windows
+constexpr uint32_t kEntFlag = 0x40000000u;           // stream item_info: row counted from entries
+constexpr uint32_t kTileMask = 0x3FFFFFFFu;
 
 struct Tile {
   uint32_t row0, row1;  // rows [row0, row1)
   uint32_t c0, c1;      // column window [c0, c1)
-  uint32_t mode;        // 0 dense, 1 hash
+  uint32_t mode;        // 0 dense, 1 hash, 2 dense single row counted from entries (stream mode)
   uint32_t nwin;        // first window tile of a split row: #windows; else 0
   uint32_t n_units;
   uint32_t width;       // dense: counters used
@@ -963,7 +966,7 @@ constexpr uint32_t kStreamMeanMax = 64;
 // hash word = base | j
 __host__ __device__ __forceinline__ uint32_t stream_base(const Tile& T, uint32_t i, uint32_t n,
                                                          uint32_t col_bits, bool upper) {
-  if (T.mode != 0) return (i - T.row0) << col_bits;
+  if (T.mode == 1) return (i - T.row0) << col_bits;
   if (T.row1 - T.row0 == 1) return 0u - T.c0;  // single row: slot = j - first column
   const uint32_t k = i - T.row0;
   if (!upper) return k * n;
@@ -998,7 +1001,7 @@ template <bool UPPER, typename Fn>
 __device__ __forceinline__ void stream_row(const StreamRouteArgs& A, uint32_t i, const Pos& q,
                                            uint2 tv, Fn&& fn) {
   if (tv.x == kNone || (UPPER && q.p + 1 >= q.L)) return;
-  const uint32_t tile = tv.x & ~kWinFlag;
+  const uint32_t tile = tv.x & kTileMask;
   const uint32_t c_lo = UPPER ? q.p + 1 : 0;
   const uint64_t tb = (uint64_t)q.base;
   if (!(tv.x & kWinFlag) && !A.filter) {
@@ -1056,7 +1059,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
     walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
       if (!q.valid) return;
+      // an entry row stores one (first column position, count) pair
       stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t, uint32_t, uint32_t n) {
+        if (tv.x & kEntFlag) n = 2;
         if (t < ns) atomicAdd(&s_cnt[t], n);
         else atomicAdd(&A.tile_words[t], (unsigned long long)n);
       });
@@ -1100,6 +1105,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
       if (!q.valid) return;
       stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t, uint32_t, uint32_t n) {
+        if (tv.x & kEntFlag) n = 2;
         if (t < ns) {
           if (atomicAdd(&s_cnt[t], n) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = t;
         }
@@ -1137,7 +1143,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
         bool fast = false;
         if (p < L && (!UPPER || p + 1 < L) && tv.x != kNone) {
           const uint32_t n = UPPER ? L - 1 - p : L;
-          if (!(tv.x & kWinFlag) && !A.filter) {
+          if (tv.x & kEntFlag) {
+            // single-row tile counted from entries: {first column position, n}
+            const uint32_t t2 = tv.x & kTileMask;
+            const uint32_t e = t2 < ns ? atomicAdd(&s_cnt[t2], 2u)
+                                       : (uint32_t)atomicAdd(&A.tile_cursor[t2], 2ull);
+            *reinterpret_cast<uint2*>(A.words + e) = make_uint2((uint32_t)(tb + (UPPER ? p + 1 : 0)), n);
+          } else if (!(tv.x & kWinFlag) && !A.filter) {
             fast = true;
             bb = tv.y;
             dest = tv.x < ns ? atomicAdd(&s_cnt[tv.x], n)
@@ -1248,6 +1260,7 @@ struct StreamCountArgs {
   const unsigned long long* tile_base;
   const unsigned long long* tile_words;
   const uint32_t* words;
+  const uint32_t* items;
   unsigned int* unit_counter;
   uint32_t n_items, col_bits;
   int upper;
@@ -1278,6 +1291,49 @@ __device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint3
   } else {
     i = T.row0 + s / n;
     j = s % n;
+  }
+}
+
+// Count the suffixes of a range of entries {first column position, n} of a
+// single-row tile: the pairs of 32 entries are flattened across the warp
+// (boundary mask owner lookup); four steps' column loads are issued before
+// their shared-memory atomics. Blocks of 32 entries go round-robin over the
+// warps; the next block's entries are loaded ahead.
+__device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict__ items,
+                                                     const uint2* __restrict__ ents, uint64_t e0,
+                                                     uint64_t e1, uint32_t* table, uint32_t c0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int WB = 4;
+  const uint64_t nblk = (e1 - e0 + 31) / 32;
+  auto ld = [&](uint64_t blk) -> uint2 {
+    const uint64_t e = e0 + blk * 32 + lane;
+    return e < e1 ? __ldcs(ents + e) : make_uint2(0u, 0u);
+  };
+  uint2 nen = make_uint2(0u, 0u);
+  if ((uint64_t)warp < nblk) nen = ld(warp);
+  for (uint64_t blk = warp; blk < nblk; blk += kCountWarps) {
+    const uint2 en = nen;
+    if (blk + kCountWarps < nblk) nen = ld(blk + kCountWarps);
+    const uint32_t cn = en.y;
+    const uint32_t incl = warp_incl_scan(cn);
+    const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t delta = en.x - (incl - cn);  // item position = flat index + delta[owner]
+    uint32_t ob = 0;
+    for (uint32_t t0 = 0; t0 < S; t0 += 32 * WB) {
+      uint32_t src[WB], j[WB];
+#pragma unroll
+      for (int k = 0; k < WB; ++k) {
+        const uint32_t tt = t0 + k * 32;
+        const uint32_t o = owner_step(incl, tt, ob);
+        const uint32_t d = __shfl_sync(0xffffffffu, delta, o & 31);
+        src[k] = tt + lane < S ? tt + lane + d : kNone;
+      }
+#pragma unroll
+      for (int k = 0; k < WB; ++k) j[k] = src[k] != kNone ? __ldg(items + src[k]) : 0u;
+#pragma unroll
+      for (int k = 0; k < WB; ++k)
+        if (src[k] != kNone) atomicAdd(&table[j[k] - c0], 1u);
+    }
   }
 }
 
@@ -1317,9 +1373,11 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     const Tile T = A.tiles[unit.tile];
     const uint64_t Wn = A.tile_words[unit.tile];
     const uint64_t wb = A.tile_base[unit.tile];
-    const uint64_t w0 = wb + Wn * unit.local / T.n_units;
-    const uint64_t w1 = wb + Wn * (unit.local + 1) / T.n_units;
-    const bool dense = T.mode == 0;
+    const bool ents = T.mode == 2;  // entries {first column position, n} instead of words
+    const uint64_t Wu = ents ? Wn / 2 : Wn;
+    const uint64_t w0 = Wu * unit.local / T.n_units;
+    const uint64_t w1 = Wu * (unit.local + 1) / T.n_units;
+    const bool dense = T.mode != 1;
     const uint32_t width = T.width;
     long long c0 = 0, c1 = 0, c2 = 0;
     if (DBG) c0 = clock64();
@@ -1331,8 +1389,12 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     }
     __syncthreads();
     if (DBG) c1 = clock64();
+    if (ents) {
+      count_suffix_entries(A.items, reinterpret_cast<const uint2*>(A.words + wb), w0, w1,
+                           table, T.c0);
+    } else {
     const uint32_t nb = (uint32_t)((w1 - w0 + BW - 1) / BW);
-    const uint32_t* wp = A.words + w0 + lane;
+    const uint32_t* wp = A.words + wb + w0 + lane;
     auto fetch = [&](uint32_t blk, uint32_t (&v)[D]) {
       const uint32_t* p = wp + (uint64_t)blk * BW;
       if ((uint64_t)(blk + 1) * BW <= w1 - w0) {
@@ -1388,6 +1450,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
 #pragma unroll
       for (int k = 0; k < D; ++k) cur[k] = nxt[k];
     }
+    }
     if (threadIdx.x == 0) s_misc[0] = u_next;
     __syncthreads();
     if (DBG) {
@@ -1397,7 +1460,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
         atomicAdd(&A.dbg[kind * 5 + 0], (unsigned long long)(c1 - c0));
         atomicAdd(&A.dbg[kind * 5 + 1], (unsigned long long)(c2 - c1));
         atomicAdd(&A.dbg[kind * 5 + 3], 1ull);
-        atomicAdd(&A.dbg[kind * 5 + 4], (unsigned long long)(w1 - w0));
+        atomicAdd(&A.dbg[kind * 5 + 4], (unsigned long long)(w1 - w0));  // words or entries
       }
     }
     if (dense && T.n_units > 1) {
@@ -1538,8 +1601,10 @@ __global__ void __launch_bounds__(1024) k_scan_u64(const unsigned long long* __r
   __shared__ unsigned long long s_part[1024];
   const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
   const uint32_t lo = min(n, threadIdx.x * per), hi = min(n, lo + per);
+  // every tile's range is rounded up to an even word count, so 8-byte
+  // entries stay aligned
   unsigned long long acc = 0;
-  for (uint32_t i = lo; i < hi; ++i) acc += in[i];
+  for (uint32_t i = lo; i < hi; ++i) acc += (in[i] + 1) & ~1ull;
   s_part[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -1562,7 +1627,7 @@ __global__ void __launch_bounds__(1024) k_scan_u64(const unsigned long long* __r
   for (uint32_t i = lo; i < hi; ++i) {
     out[i] = run;
     if (out2) out2[i] = run;
-    run += in[i];
+    run += (in[i] + 1) & ~1ull;
   }
 }
 
@@ -1609,9 +1674,8 @@ struct crop_pairs {
   uint32_t* d_overflow = nullptr;
   unsigned int* d_tile_done = nullptr;
   uint2* d_reduce_chunks = nullptr;  // stream mode: (split tile, first slot)
-  std::vector<uint2> h_reduce_chunks;
-  std::vector<uint32_t> h_item_tile;  // kept alive for the async uploads
-  std::vector<uint2> h_item_info;
+  uint32_t n_reduce_chunks = 0;
+  void* d_block = nullptr;  // one allocation carved into the small per-job arrays
   // stream mode (short rows): pair words per tile instead of entries
   bool stream_mode = false;
   uint32_t* d_words = nullptr;
@@ -1621,13 +1685,40 @@ struct crop_pairs {
   cudaEvent_t ev[6] = {};
 };
 
+// Pinned host staging shared by all jobs: the pass-A statistics come back
+// through it and the plan goes up through it in one copy. The event marks
+// the last upload; the next job waits on it before reusing the buffer.
+struct PinnedArena {
+  std::mutex mu;
+  unsigned char* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  cudaError_t reserve(size_t n) {
+    if (done) {
+      cudaError_t e = cudaEventSynchronize(done);
+      if (e != cudaSuccess) return e;
+    } else {
+      cudaError_t e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(n + n / 2, 1 << 20);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+};
+static PinnedArena g_pinned;
+
+static inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
 static void free_job(crop_pairs* j) {
   for (cudaEvent_t& e : j->ev)
     if (e) cudaEventDestroy(e);
-  void* ptrs[] = {j->d_terms, j->d_maxlen, j->d_item_tile, j->d_item_info, j->d_tiles, j->d_units, j->d_split,
-                  j->d_tile_entries, j->d_tile_ebase, j->d_tile_cursor, j->d_tile_end, j->d_total_entries,
-                  j->d_entries, j->d_slabs, j->d_unit_counter, j->d_overflow, j->d_tile_done, j->d_reduce_chunks,
-                  j->d_words, j->d_tile_words};
+  void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
@@ -1673,6 +1764,9 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     if (sm && row1 - row0 == 1) t.c0 = upper ? row0 + 1 : 0;  // stream: slot = j - c0
     const bool dense = dok && (!hok || st * 8 >= sw);
     t.mode = dense ? 0 : 1;
+    // stream mode, unfiltered: a single-row dense tile is counted from one
+    // entry per row occurrence (its suffix is read from the items)
+    if (dense && sm && !J->filter && row1 - row0 == 1) t.mode = 2;
     t.width = dense ? (uint32_t)sw : 0;
     t.terms = st;
     t.n_units = dense ? units_for(st, so) : 1;
@@ -1853,10 +1947,9 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
   } while (0)
   {
     const uint32_t nn = std::max<uint32_t>(n_items, 1);
-    JCUDA(cudaMallocAsync(&J->d_terms, nn * sizeof(unsigned long long), st));
-    JCUDA(cudaMallocAsync(&J->d_maxlen, sizeof(unsigned int), st));
-    JCUDA(cudaMemsetAsync(J->d_terms, 0, nn * sizeof(unsigned long long), st));
-    JCUDA(cudaMemsetAsync(J->d_maxlen, 0, sizeof(unsigned int), st));
+    JCUDA(cudaMallocAsync(&J->d_terms, nn * sizeof(unsigned long long) + 16, st));
+    J->d_maxlen = reinterpret_cast<unsigned int*>(J->d_terms + nn);
+    JCUDA(cudaMemsetAsync(J->d_terms, 0, nn * sizeof(unsigned long long) + 16, st));
     if (n_tx > 0 && n_items > 0) {
       auto kern = upper_only ? k_item_terms<true> : k_item_terms<false>;
       const uint32_t ns = std::min<uint32_t>(n_items, kStatSmemItems);
@@ -1869,15 +1962,21 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
     }
-    std::vector<unsigned long long> stats(nn), terms(nn), occ(nn);
-    unsigned int maxlen = 0;
-    int64_t nnz = 0;
-    JCUDA(cudaMemcpyAsync(stats.data(), J->d_terms, nn * 8, cudaMemcpyDeviceToHost, st));
-    JCUDA(cudaMemcpyAsync(&maxlen, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
-    if (n_tx > 0) JCUDA(cudaMemcpyAsync(&nnz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
+    std::lock_guard<std::mutex> pin_lock(g_pinned.mu);
+    JCUDA(g_pinned.reserve(nn * 8 + 64));
+    unsigned long long* stats = reinterpret_cast<unsigned long long*>(g_pinned.p);
+    unsigned int* h_maxlen = reinterpret_cast<unsigned int*>(g_pinned.p + nn * 8);
+    int64_t* h_nnz = reinterpret_cast<int64_t*>(g_pinned.p + nn * 8 + 16);
+    *h_maxlen = 0;
+    *h_nnz = 0;
+    JCUDA(cudaMemcpyAsync(stats, J->d_terms, nn * 8, cudaMemcpyDeviceToHost, st));
+    JCUDA(cudaMemcpyAsync(h_maxlen, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
+    if (n_tx > 0) JCUDA(cudaMemcpyAsync(h_nnz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
     auto t_sync0 = std::chrono::steady_clock::now();
     JCUDA(cudaStreamSynchronize(st));
     auto t_sync1 = std::chrono::steady_clock::now();
+    const unsigned int maxlen = *h_maxlen;
+    const int64_t nnz = *h_nnz;
     J->nnz = nnz;
     if (maxlen > kMaxLen) {
       crop_set_error(CROP_EINPUT, "transaction of %u items exceeds the %u-item limit", maxlen, kMaxLen);
@@ -1890,46 +1989,99 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       rc = CROP_EINPUT;
       goto fail;
     }
+    // host scratch reused across jobs (under the arena lock): no first-touch
+    // page faults on the planning path
+    static std::vector<unsigned long long> terms, occ;
+    static std::vector<uint32_t> item_tile;
+    terms.resize(nn);
+    occ.resize(nn);
+    unsigned long long occ_sum = 0;
     J->total_terms = 0;
     for (uint32_t i = 0; i < n_items; ++i) {
-      terms[i] = stats[i] & (kOccOne - 1);
-      occ[i] = stats[i] >> 40;
+      const unsigned long long x = stats[i];
+      terms[i] = x & (kOccOne - 1);
+      occ[i] = x >> 40;
       J->total_terms += terms[i];
+      occ_sum += occ[i];
     }
     {
-      unsigned long long occ_sum = 0;
-      for (uint32_t i = 0; i < n_items; ++i) occ_sum += occ[i];
       // stream mode when rows are short on average (words stay < 2^32);
       // CROP_FORCE_ENTRY_MODE / CROP_FORCE_STREAM_MODE override (tests)
-      const bool fits = J->total_terms < (1ull << 32);
+      const bool fits = J->total_terms + 2 * occ_sum + 2ull * n_items + 2 < (1ull << 32);
       if (getenv("CROP_FORCE_ENTRY_MODE")) J->stream_mode = false;
       else if (getenv("CROP_FORCE_STREAM_MODE")) J->stream_mode = fits;
       else J->stream_mode = fits && occ_sum > 0 &&
                             J->total_terms <= (unsigned long long)kStreamMeanMax * occ_sum;
     }
-    std::vector<uint32_t>& item_tile = J->h_item_tile;
     auto t_p0 = std::chrono::steady_clock::now();
     plan_tiles(J, terms, occ, item_tile);
     auto t_p1 = std::chrono::steady_clock::now();
     const uint32_t nt = (uint32_t)J->tiles.size();
-    // entry capacity per tile: a row occurrence with a partner after it makes
-    // at most one entry per tile (per window for split rows)
-    std::vector<unsigned long long> cap(nt, 0);
-    for (uint32_t i = 0; i < n_items; ++i) {
-      if (item_tile[i] == kNone) continue;
-      const uint32_t t = item_tile[i] & ~kWinFlag;
-      if (item_tile[i] & kWinFlag)
-        for (uint32_t w = 0; w < J->tiles[t].nwin; ++w) cap[t + w] += occ[i];
-      else
-        cap[t] += occ[i];
-    }
-    J->h_tile_base.assign(nt, 0);
-    J->h_tile_end.assign(nt, 0);
+    const bool sm = J->stream_mode;
+    // reduce chunks (stream mode): (split tile, first slot)
+    uint32_t nrc = 0;
+    if (sm)
+      for (uint32_t t : J->split) nrc += (J->tiles[t].width + kReduceSlots - 1) / kReduceSlots;
+    J->n_reduce_chunks = nrc;
+    // one device block: [uploaded part | device-only part]
+    const size_t o_tiles = 0;
+    const size_t o_units = align16(o_tiles + (size_t)nt * sizeof(Tile));
+    const size_t o_split = align16(o_units + J->units.size() * sizeof(Unit));
+    const size_t o_ebase = align16(o_split + J->split.size() * 4);
+    const size_t o_end = align16(o_ebase + (size_t)nt * 8);
+    const size_t o_item = align16(o_end + (sm ? 0 : (size_t)nt * 8));
+    const size_t o_rc = align16(o_item + (size_t)nn * (sm ? sizeof(uint2) : 4));
+    const size_t up_bytes = align16(o_rc + (size_t)nrc * sizeof(uint2));
+    const size_t o_tentries = up_bytes;
+    const size_t o_cursor = align16(o_tentries + (size_t)nt * 4);
+    const size_t o_twords = align16(o_cursor + (size_t)nt * 8);
+    const size_t o_tdone = align16(o_twords + (size_t)nt * 8);
+    const size_t o_misc = align16(o_tdone + (size_t)nt * 4);  // total_entries, unit_counter, overflow
+    const size_t blk_bytes = o_misc + 32;
+    JCUDA(g_pinned.reserve(up_bytes));
+    unsigned char* hb = g_pinned.p;
+    if (nt) memcpy(hb + o_tiles, J->tiles.data(), (size_t)nt * sizeof(Tile));
+    if (!J->units.empty()) memcpy(hb + o_units, J->units.data(), J->units.size() * sizeof(Unit));
+    if (!J->split.empty()) memcpy(hb + o_split, J->split.data(), J->split.size() * 4);
+    unsigned long long* h_base = reinterpret_cast<unsigned long long*>(hb + o_ebase);
     unsigned long long run = 0;
-    for (uint32_t t = 0; t < nt; ++t) {
-      J->h_tile_base[t] = run;
-      run += cap[t];
-      J->h_tile_end[t] = run;
+    if (sm) {
+      // stream mode: word bases come from the device (scan of per-tile totals)
+      uint2* info = reinterpret_cast<uint2*>(hb + o_item);
+      for (uint32_t i = 0; i < nn; ++i) {
+        const uint32_t tv = i < n_items ? item_tile[i] : kNone;
+        if (tv == kNone) {
+          info[i] = make_uint2(kNone, 0u);
+          continue;
+        }
+        const Tile& T = J->tiles[tv & ~kWinFlag];
+        const uint32_t flag = (!(tv & kWinFlag) && T.mode == 2) ? kEntFlag : 0u;
+        info[i] = make_uint2(tv | flag, (tv & kWinFlag) ? 0u : stream_base(T, i, n_items, J->col_bits, J->upper != 0));
+      }
+      uint2* rcs = reinterpret_cast<uint2*>(hb + o_rc);
+      uint32_t k = 0;
+      for (uint32_t t : J->split)
+        for (uint32_t c0 = 0; c0 < J->tiles[t].width; c0 += kReduceSlots) rcs[k++] = make_uint2(t, c0);
+      for (uint32_t t = 0; t < nt; ++t) h_base[t] = 0;
+    } else {
+      // entry capacity per tile: a row occurrence with a partner after it
+      // makes at most one entry per tile (per window for split rows)
+      unsigned long long* h_end = reinterpret_cast<unsigned long long*>(hb + o_end);
+      for (uint32_t t = 0; t < nt; ++t) h_end[t] = 0;
+      for (uint32_t i = 0; i < n_items; ++i) {
+        if (item_tile[i] == kNone) continue;
+        const uint32_t t = item_tile[i] & ~kWinFlag;
+        if (item_tile[i] & kWinFlag)
+          for (uint32_t w = 0; w < J->tiles[t].nwin; ++w) h_end[t + w] += occ[i];
+        else
+          h_end[t] += occ[i];
+      }
+      for (uint32_t t = 0; t < nt; ++t) {
+        h_base[t] = run;
+        run += h_end[t];
+        h_end[t] = run;
+      }
+      memcpy(hb + o_item, item_tile.data(), (size_t)n_items * 4);
     }
     J->entry_cap = run;
     {
@@ -1937,63 +2089,39 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       int c = (int)(kStage / std::max(1.0, 1.25 * per_tx));
       J->route_chunk_tx = std::max(8, std::min(kChunkTx, c));
     }
-    JCUDA(cudaMallocAsync(&J->d_item_tile, nn * 4, st));
-    JCUDA(cudaMallocAsync(&J->d_tiles, std::max<size_t>(1, nt) * sizeof(Tile), st));
-    JCUDA(cudaMallocAsync(&J->d_units, std::max<size_t>(1, J->units.size()) * sizeof(Unit), st));
-    JCUDA(cudaMallocAsync(&J->d_split, std::max<size_t>(1, J->split.size()) * 4, st));
-    JCUDA(cudaMallocAsync(&J->d_tile_entries, std::max<size_t>(1, nt) * 4, st));
-    JCUDA(cudaMallocAsync(&J->d_tile_ebase, std::max<size_t>(1, nt) * 8, st));
-    JCUDA(cudaMallocAsync(&J->d_tile_cursor, std::max<size_t>(1, nt) * 8, st));
-    JCUDA(cudaMallocAsync(&J->d_tile_end, std::max<size_t>(1, nt) * 8, st));
-    if (nt) {
-      JCUDA(cudaMemcpyAsync(J->d_tile_ebase, J->h_tile_base.data(), nt * 8, cudaMemcpyHostToDevice, st));
-      JCUDA(cudaMemcpyAsync(J->d_tile_end, J->h_tile_end.data(), nt * 8, cudaMemcpyHostToDevice, st));
-    }
-    JCUDA(cudaMallocAsync(&J->d_total_entries, 8, st));
-    JCUDA(cudaMallocAsync(&J->d_unit_counter, 4, st));
-    JCUDA(cudaMallocAsync(&J->d_overflow, 4, st));
-    JCUDA(cudaMallocAsync(&J->d_tile_done, std::max<size_t>(1, nt) * 4, st));
-    JCUDA(cudaMemsetAsync(J->d_overflow, 0, 4, st));
-    if (n_items) JCUDA(cudaMemcpyAsync(J->d_item_tile, item_tile.data(), n_items * 4, cudaMemcpyHostToDevice, st));
-    if (nt) JCUDA(cudaMemcpyAsync(J->d_tiles, J->tiles.data(), nt * sizeof(Tile), cudaMemcpyHostToDevice, st));
-    if (!J->units.empty())
-      JCUDA(cudaMemcpyAsync(J->d_units, J->units.data(), J->units.size() * sizeof(Unit), cudaMemcpyHostToDevice, st));
-    if (!J->split.empty())
-      JCUDA(cudaMemcpyAsync(J->d_split, J->split.data(), J->split.size() * 4, cudaMemcpyHostToDevice, st));
-    if (J->n_slabs)
-      JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)(J->stream_mode ? kStreamDenseCap : kHalf) * 4, st));
-    if (J->stream_mode) {
-      std::vector<uint2>& info = J->h_item_info;
-      info.assign(nn, make_uint2(kNone, 0u));
-      for (uint32_t i = 0; i < n_items; ++i) {
-        const uint32_t tv = item_tile[i];
-        if (tv == kNone) continue;
-        const Tile& T = J->tiles[tv & ~kWinFlag];
-        info[i] = make_uint2(tv, (tv & kWinFlag) ? 0u : stream_base(T, i, n_items, J->col_bits, J->upper != 0));
-      }
-      JCUDA(cudaMallocAsync(&J->d_item_info, nn * sizeof(uint2), st));
-      J->h_reduce_chunks.clear();
-      for (uint32_t t : J->split)
-        for (uint32_t c0 = 0; c0 < J->tiles[t].width; c0 += kReduceSlots)
-          J->h_reduce_chunks.push_back(make_uint2(t, c0));
-      if (!J->h_reduce_chunks.empty()) {
-        JCUDA(cudaMallocAsync(&J->d_reduce_chunks, J->h_reduce_chunks.size() * sizeof(uint2), st));
-        JCUDA(cudaMemcpyAsync(J->d_reduce_chunks, J->h_reduce_chunks.data(),
-                              J->h_reduce_chunks.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
-      }
-      if (n_items)
-        JCUDA(cudaMemcpyAsync(J->d_item_info, info.data(), n_items * sizeof(uint2), cudaMemcpyHostToDevice, st));
-      JCUDA(cudaMallocAsync(&J->d_words, std::max<uint64_t>(1, J->total_terms) * 4, st));
-      JCUDA(cudaMallocAsync(&J->d_tile_words, std::max<size_t>(1, nt) * 8, st));
-    }
-    if (!J->stream_mode && J->entry_cap >= (1ull << 32)) {
+    if (!sm && J->entry_cap >= (1ull << 32)) {
       crop_set_error(CROP_ERESOURCE, "%llu entries exceed the 2^32 limit of one job; split the stream",
                      (unsigned long long)J->entry_cap);
       rc = CROP_ERESOURCE;
       goto fail;
     }
-    if (!J->stream_mode)
-      JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
+    JCUDA(cudaMallocAsync(&J->d_block, blk_bytes, st));
+    {
+      unsigned char* db = reinterpret_cast<unsigned char*>(J->d_block);
+      J->d_tiles = reinterpret_cast<Tile*>(db + o_tiles);
+      J->d_units = reinterpret_cast<Unit*>(db + o_units);
+      J->d_split = reinterpret_cast<uint32_t*>(db + o_split);
+      J->d_tile_ebase = reinterpret_cast<unsigned long long*>(db + o_ebase);
+      J->d_tile_end = reinterpret_cast<unsigned long long*>(db + o_end);
+      if (sm) J->d_item_info = reinterpret_cast<uint2*>(db + o_item);
+      else J->d_item_tile = reinterpret_cast<uint32_t*>(db + o_item);
+      J->d_reduce_chunks = reinterpret_cast<uint2*>(db + o_rc);
+      J->d_tile_entries = reinterpret_cast<uint32_t*>(db + o_tentries);
+      J->d_tile_cursor = reinterpret_cast<unsigned long long*>(db + o_cursor);
+      J->d_tile_words = reinterpret_cast<unsigned long long*>(db + o_twords);
+      J->d_tile_done = reinterpret_cast<unsigned int*>(db + o_tdone);
+      J->d_total_entries = reinterpret_cast<unsigned long long*>(db + o_misc);
+      J->d_unit_counter = reinterpret_cast<unsigned int*>(db + o_misc + 8);
+      J->d_overflow = reinterpret_cast<uint32_t*>(db + o_misc + 16);
+      JCUDA(cudaMemcpyAsync(db, hb, up_bytes, cudaMemcpyHostToDevice, st));
+      JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
+      JCUDA(cudaEventRecord(g_pinned.done, st));
+    }
+    if (J->n_slabs)
+      JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)(sm ? kStreamDenseCap : kHalf) * 4, st));
+    // words: <= one per term, or two per entry row occurrence, plus the even rounding per tile
+    if (sm) JCUDA(cudaMallocAsync(&J->d_words, (J->total_terms + 2 * occ_sum + 2 * (uint64_t)nt + 2) * 4, st));
+    else JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
     // host vectors read by the async uploads live in J until destroy
     if (getenv("CROP_DEBUG_TIMING")) {
       auto t_end = std::chrono::steady_clock::now();
@@ -2001,7 +2129,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         return std::chrono::duration_cast<std::chrono::microseconds>(b - a).count();
       };
       fprintf(stderr, "[crop_pairs_create] wait passA %lld us, unpack %lld us, plan %lld us, "
-              "caps+uploads %lld us, tiles %zu\n", (long long)us(t_sync0, t_sync1),
+              "pack+uploads %lld us, tiles %zu\n", (long long)us(t_sync0, t_sync1),
               (long long)us(t_sync1, t_p0), (long long)us(t_p0, t_p1), (long long)us(t_p1, t_end),
               J->tiles.size());
     }
@@ -2092,6 +2220,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.tile_base = J->d_tile_ebase;
     C.tile_words = J->d_tile_words;
     C.words = J->d_words;
+    C.items = J->items;
     C.unit_counter = J->d_unit_counter;
     C.n_items = J->n_items;
     C.col_bits = J->col_bits;
@@ -2114,7 +2243,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     mark(4);
     kcs<<<std::min<int>(kNumSMs, (int)J->units.size()), kCountThreads, kStreamSmem, st>>>(C);
     CROP_LAUNCH_CHECK();
-    const uint32_t nrc = (uint32_t)J->h_reduce_chunks.size();
+    const uint32_t nrc = J->n_reduce_chunks;
     if (nrc) {
       k_reduce_slabs<<<std::min<uint32_t>(nrc, kNumSMs * 8), 256, 0, st>>>(C, J->d_reduce_chunks, nrc);
       CROP_LAUNCH_CHECK();

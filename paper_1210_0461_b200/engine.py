@@ -170,13 +170,13 @@ class _DeviceResult:
 
         e = self.entries
         cap = self.capacity
-        w_all = e.weights_f64()
         for inst in self.instances:
             overflow = inst.distinct > cap
             full = inst.distinct >= cap
             inst.bucket_min = np.zeros(self.kappa)
             if not full.any():
                 continue
+            w_all = e.weights_f64()
             from .kernels import entry_buckets
 
             b = entry_buckets(e.row, e.col, e.n, inst.tables[0], inst.tables[1], self.kappa)
@@ -399,7 +399,7 @@ class SketchState:
             idx = order[:k]
         rows = u32_to_numpy(e.row[idx])
         cols = u32_to_numpy(e.col[idx])
-        ws = e.weights_f64()[idx].cpu().numpy()
+        ws = e.weights_at(idx).cpu().numpy()
         keep = ws > 0 if mask is not None else np.ones(ws.shape[0], dtype=bool)
         if mask is not None:
             mk = mask[idx].cpu().numpy()
@@ -526,10 +526,21 @@ def prepare(stream) -> _Prepared:
         return _Prepared("pairs", stream, n, n, n, total, None)
     ts = as_transaction_stream(stream)
     if ts is not None:
-        n_items = int(ts.items.max()) + 1 if ts.items.size else 1
-        dtx = kernels.DeviceTransactions.from_host(ts.offsets, ts.items, n_items)
-        prep = _Prepared("pairs", dtx, stream.n_rows, stream.n_cols, n_items,
-                         ts.total_pair_count(), ts)
+        # upload first; the max id and the pair total are reduced on the device
+        # (one small read-back instead of two host passes over the arrays)
+        dtx = kernels.DeviceTransactions.from_host(ts.offsets, ts.items, 1)
+        import torch
+
+        if dtx.items.numel():
+            lens = dtx.offsets[1:] - dtx.offsets[:-1]
+            mx, total, mn = torch.stack([dtx.items.max().to(torch.int64) + 1, (lens * lens).sum(),
+                                         dtx.items.min().to(torch.int64)]).tolist()
+            if mn < 0:
+                raise InputError("item ids must be < 2^31")
+        else:
+            mx, total = 1, 0
+        dtx.n_items = int(mx)
+        prep = _Prepared("pairs", dtx, stream.n_rows, stream.n_cols, int(mx), int(total), ts)
     else:
         cr = ColumnRowStream.from_stream(stream)
         n_items = 1 + max(int(cr.a_idx.max()) if cr.a_idx.size else 0,

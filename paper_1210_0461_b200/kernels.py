@@ -168,6 +168,12 @@ class DeviceEntries:
             return self.value[: self.n]
         return (self.count[: self.n].to(torch.int64) & U32_MASK).to(torch.float64)
 
+    def weights_at(self, idx: torch.Tensor) -> torch.Tensor:
+        """float64 weights of the entries `idx` (gather first, convert after)."""
+        if self.value is not None:
+            return self.value[idx]
+        return (self.count[idx].to(torch.int64) & U32_MASK).to(torch.float64)
+
     def to_numpy(self):
         row = u32_to_numpy(self.row[: self.n])
         col = u32_to_numpy(self.col[: self.n])

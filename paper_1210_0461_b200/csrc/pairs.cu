@@ -1191,7 +1191,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
         const uint32_t L = (uint32_t)(s_off[t + 1] - tb);
         uint32_t n_dest = 0, n_bb = 0;
         const uint32_t n_fm = prepare(t + NW, it1, tv1, n_dest, n_bb);
-        if (UPPER && L <= 32) {
+        if (UPPER && L <= 32 && c_fm && 2 * (uint32_t)__popc(c_fm) <= L) {
+          // few word rows (the others are entry rows): one store instruction
+          // per row, its columns across the lanes
+          uint32_t m = c_fm;
+          while (m) {
+            const int r = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t d = __shfl_sync(0xffffffffu, c_dest, r);
+            const uint32_t b2 = __shfl_sync(0xffffffffu, c_bb, r);
+            if (lane > r && lane < (int)L) A.words[d + (lane - r - 1)] = b2 + it_cur;
+          }
+        } else if (UPPER && L <= 32) {
           // the flattened triangle: pair tt -> (row from the end r, column
           // offset c) via the shared table; each row's run contiguous
           const uint32_t P = L * (L - 1) / 2;

@@ -397,19 +397,22 @@ class SketchState:
                 order = order[torch.sort(key[order], stable=True).indices]
             order = order[torch.sort(w[order], descending=True, stable=True).indices]
             idx = order[:k]
-        rows = u32_to_numpy(e.row[idx])
-        cols = u32_to_numpy(e.col[idx])
-        ws = e.weights_at(idx).cpu().numpy()
+        # one read-back: rows, cols, weights (and the mask) of the k winners
+        parts = [(e.row[idx].to(torch.int64) & 0xFFFFFFFF).to(torch.float64),
+                 (e.col[idx].to(torch.int64) & 0xFFFFFFFF).to(torch.float64), e.weights_at(idx)]
+        if mask is not None:
+            parts.append(mask[idx].to(torch.float64))
+        h = torch.stack(parts).cpu().numpy()
+        rows, cols, ws = h[0].astype(np.int64), h[1].astype(np.int64), h[2]
         keep = ws > 0 if mask is not None else np.ones(ws.shape[0], dtype=bool)
         if mask is not None:
-            mk = mask[idx].cpu().numpy()
-            keep &= mk
-        out = []
-        for r, c, w in zip(rows[keep], cols[keep], ws[keep]):
-            r, c, w = int(r), int(c), float(w)
-            out.append(TopEntry(Entry(r, c), w, w, self._estimate(r, c)))
-        out.sort(key=lambda t: (-t.upper, -t.lower, t.entry.row, t.entry.col))
-        return out[:k]
+            keep &= h[3] > 0
+        rows, cols, ws = rows[keep], cols[keep], ws[keep]
+        order = np.lexsort((cols, rows, -ws))[:k]
+        cs = self.config.cs_enabled
+        return [TopEntry(Entry(int(r), int(c)), float(w), float(w),
+                         self._estimate(int(r), int(c)) if cs else None)
+                for r, c, w in zip(rows[order].tolist(), cols[order].tolist(), ws[order].tolist())]
 
     def recorded_weight(self) -> float:
         if self._dev is not None:

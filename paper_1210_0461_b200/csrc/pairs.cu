@@ -1306,15 +1306,17 @@ __device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint3
 }
 
 // Count the suffixes of a range of entries {first column position, n} of a
-// single-row tile: the pairs of 32 entries are flattened across the warp
-// (boundary mask owner lookup); four steps' column loads are issued before
-// their shared-memory atomics. Blocks of 32 entries go round-robin over the
-// warps; the next block's entries are loaded ahead.
+// single-row tile. The suffixes of 32 entries are cut into quads (4
+// consecutive columns) and the quads flattened across the warp (boundary-mask
+// owner lookup, one per 32 quads = 128 columns); each lane loads and counts
+// its quad. The next batch's loads are issued before the previous batch's
+// shared-memory atomics. Blocks of 32 entries go round-robin over the warps;
+// the next block's entries are loaded ahead.
 __device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict__ items,
                                                      const uint2* __restrict__ ents, uint64_t e0,
                                                      uint64_t e1, uint32_t* table, uint32_t c0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int WB = 4;
+  constexpr int Q = 4;
   const uint64_t nblk = (e1 - e0 + 31) / 32;
   auto ld = [&](uint64_t blk) -> uint2 {
     const uint64_t e = e0 + blk * 32 + lane;
@@ -1322,30 +1324,39 @@ __device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict_
   };
   uint2 nen = make_uint2(0u, 0u);
   if ((uint64_t)warp < nblk) nen = ld(warp);
+  uint32_t pj[Q];  // the previous quad's columns (kNone = none)
+#pragma unroll
+  for (int k = 0; k < Q; ++k) pj[k] = kNone;
   for (uint64_t blk = warp; blk < nblk; blk += kCountWarps) {
     const uint2 en = nen;
     if (blk + kCountWarps < nblk) nen = ld(blk + kCountWarps);
-    const uint32_t cn = en.y;
-    const uint32_t incl = warp_incl_scan(cn);
+    const uint32_t nq = (en.y + Q - 1) / Q;
+    const uint32_t incl = warp_incl_scan(nq);
     const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t delta = en.x - (incl - cn);  // item position = flat index + delta[owner]
+    // column position of quad q of this lane's entry: first + Q * (q - excl)
+    const uint32_t delta = en.x - Q * (incl - nq);
+    const uint32_t end = en.x + en.y;
     uint32_t ob = 0;
-    for (uint32_t t0 = 0; t0 < S; t0 += 32 * WB) {
-      uint32_t src[WB], j[WB];
+    for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+      const uint32_t o = owner_step(incl, t0, ob);
+      const uint32_t d = __shfl_sync(0xffffffffu, delta, o & 31);
+      const uint32_t e_end = __shfl_sync(0xffffffffu, end, o & 31);
+      const uint32_t tt = t0 + lane;
+      const uint32_t pos = Q * tt + d;
+      uint32_t j[Q];
 #pragma unroll
-      for (int k = 0; k < WB; ++k) {
-        const uint32_t tt = t0 + k * 32;
-        const uint32_t o = owner_step(incl, tt, ob);
-        const uint32_t d = __shfl_sync(0xffffffffu, delta, o & 31);
-        src[k] = tt + lane < S ? tt + lane + d : kNone;
-      }
+      for (int k = 0; k < Q; ++k) j[k] = (tt < S && pos + k < e_end) ? __ldg(items + pos + k) : kNone;
+      // count the previous quad while this one's columns are in flight
 #pragma unroll
-      for (int k = 0; k < WB; ++k) j[k] = src[k] != kNone ? __ldg(items + src[k]) : 0u;
+      for (int k = 0; k < Q; ++k)
+        if (pj[k] != kNone) atomicAdd(&table[pj[k] - c0], 1u);
 #pragma unroll
-      for (int k = 0; k < WB; ++k)
-        if (src[k] != kNone) atomicAdd(&table[j[k] - c0], 1u);
+      for (int k = 0; k < Q; ++k) pj[k] = j[k];
     }
   }
+#pragma unroll
+  for (int k = 0; k < Q; ++k)
+    if (pj[k] != kNone) atomicAdd(&table[pj[k] - c0], 1u);
 }
 
 // Per unit: clear the table, count its words (block-cyclic 256-word blocks
@@ -1642,6 +1653,349 @@ __global__ void __launch_bounds__(1024) k_scan_u64(const unsigned long long* __r
   }
 }
 
+
+// ============================================================ GPU planner
+// Stream-mode tile plan computed on the device in one CTA (no host round trip
+// with the per-item statistics). Same tile kinds as the host planner, packed
+// in parallel instead of greedily:
+//   H  one dense single-row tile (entries unless filtered) for a row that is
+//      dense-worthy (8 t >= w and w >= 4096) or too heavy for a hash tile;
+//   W  column windows for a row wider than the table and too heavy to hash;
+//   L1 a single-row hash tile for a light row with a large distinct bound;
+//   L  light rows packed into hash tiles by the prefix of a fixed-point
+//      weight max(b / hash_cap, t / unit_terms) + span: a tile is the set of
+//      light rows whose exclusive prefix falls in one bucket of width
+//      S - xmax - y, so every tile stays within all three capacities.
+// Rows are processed in contiguous segments (one per thread) with block
+// scans carrying prefixes, buckets and tile ids across segments.
+struct PlanOut {
+  unsigned long long total_terms, occ_sum, max_entries, n_slabs;
+  uint32_t n_tiles, n_units, n_split, n_reduce_chunks;
+  uint32_t stream_mode, overflow, pad0, pad1;
+};
+
+struct PlanArgs {
+  const unsigned long long* stats;
+  uint32_t n, col_bits;
+  int upper, filter, force;  // force: 0 auto, 1 entry, 2 stream
+  Tile* tiles;
+  uint32_t tile_cap;
+  Unit* units;
+  uint32_t unit_cap;
+  uint32_t* split;
+  uint2* reduce_chunks;
+  uint32_t rc_cap;
+  uint2* item_info;
+  PlanOut* out;
+};
+
+constexpr int kPlanThreads = 1024;
+constexpr uint64_t kPlanS = 1ull << 24;  // fixed-point capacity of one light tile
+constexpr uint32_t kMinDenseWidth = 4096;
+
+template <typename T, typename Op>
+__device__ __forceinline__ T plan_block_scan(T v, T* s_tmp, T ident, Op op, T& total) {
+  // exclusive scan of one value per thread over kPlanThreads threads
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T u = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x = op(x, u);
+  }
+  if (lane == 31) s_tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    T y = s_tmp[lane];
+    T yi = y;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const T u = __shfl_up_sync(0xffffffffu, yi, d);
+      if (lane >= d) yi = op(yi, u);
+    }
+    const T ex = __shfl_up_sync(0xffffffffu, yi, 1);
+    s_tmp[lane] = lane ? ex : ident;
+    if (lane == 31) s_tmp[32] = yi;
+  }
+  __syncthreads();
+  const T ex_lane = __shfl_up_sync(0xffffffffu, x, 1);
+  const T r = op(s_tmp[w], lane ? ex_lane : ident);
+  total = s_tmp[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
+  __shared__ unsigned long long s_u64[33];
+  __shared__ long long s_i64[33];
+  __shared__ uint32_t s_bin[65], s_cur[65];
+  const uint32_t n = P.n, tid = threadIdx.x;
+  const uint32_t seg = (n + kPlanThreads - 1) / kPlanThreads;
+  const uint32_t lo = min(n, tid * seg), hi = min(n, lo + seg);
+  auto add = [](unsigned long long a, unsigned long long b) { return a + b; };
+  auto mx = [](long long a, long long b) { return a > b ? a : b; };
+  unsigned long long tot;
+  long long totl;
+  // 1. totals and the mode decision
+  unsigned long long T = 0, O = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const unsigned long long x = P.stats[i];
+    T += x & (kOccOne - 1);
+    O += x >> 40;
+  }
+  plan_block_scan<unsigned long long>(T, s_u64, 0ull, add, T);
+  plan_block_scan<unsigned long long>(O, s_u64, 0ull, add, O);
+  const bool fits = T + 2 * O + 2ull * n + 2 < (1ull << 32);
+  bool sm = fits && O > 0 && T <= (unsigned long long)kStreamMeanMax * O;
+  if (P.force == 1) sm = false;
+  if (P.force == 2) sm = fits;
+  if (tid == 0) {
+    P.out->total_terms = T;
+    P.out->occ_sum = O;
+    P.out->stream_mode = sm;
+    P.out->overflow = 0;
+  }
+  if (!sm) return;
+  const uint64_t unit_terms = max(1ull << 16, T / ((uint64_t)kNumSMs * 8));
+  const uint32_t rows_max = P.col_bits >= 32 ? 1u : ((1u << (32 - P.col_bits)) - 1u);
+  const uint64_t y = (kPlanS + rows_max - 1) / rows_max;   // span weight of every row
+  const uint64_t step = kPlanS - kPlanS / 4 - y;            // bucket width
+  const uint64_t dense_cap = kStreamDenseCap, hash_cap = kStreamHashCap;
+  // class of row i: 0 none, 1 H, 2 W, 3 L1, 4 L; x = light weight
+  auto classify = [&](uint32_t i, uint64_t& t, uint64_t& w, uint64_t& x) -> int {
+    t = P.stats[i] & (kOccOne - 1);
+    w = P.upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
+    x = 0;
+    if (t == 0) return 0;
+    const uint64_t b = t < w ? t : w;
+    const bool hfit = b <= hash_cap && t <= unit_terms;
+    if (w <= dense_cap && ((8 * t >= w && w >= kMinDenseWidth) || !hfit)) return 1;
+    if (!hfit) return 2;
+    const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
+    const uint64_t xt = (t * kPlanS + unit_terms - 1) / unit_terms;
+    x = xb > xt ? xb : xt;
+    return x > kPlanS / 4 ? 3 : 4;
+  };
+  auto units_of = [&](uint64_t t) -> uint32_t {
+    const uint64_t u = (t + unit_terms - 1) / unit_terms;
+    return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
+  };
+  // 2. prefix of the light weights (+ span weight of every row)
+  unsigned long long pw = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    uint64_t t, w, x;
+    const int c = classify(i, t, w, x);
+    pw += (c == 4 ? x : 0) + y;
+  }
+  const unsigned long long pbase = plan_block_scan<unsigned long long>(pw, s_u64, 0ull, add, tot);
+  // 3. bucket of the last light row of each segment -> carry
+  long long lastb = -1;
+  {
+    unsigned long long p = pbase;
+    for (uint32_t i = lo; i < hi; ++i) {
+      uint64_t t, w, x;
+      const int c = classify(i, t, w, x);
+      if (c == 4) lastb = (long long)(p / step);
+      p += (c == 4 ? x : 0) + y;
+    }
+  }
+  const long long carryb = plan_block_scan<long long>(lastb, s_i64, -1ll, mx, totl);
+  // 4. tiles per segment
+  unsigned long long cnt = 0;
+  {
+    unsigned long long p = pbase;
+    long long lb = carryb;
+    for (uint32_t i = lo; i < hi; ++i) {
+      uint64_t t, w, x;
+      const int c = classify(i, t, w, x);
+      if (c == 1 || c == 3) cnt += 1;
+      else if (c == 2) cnt += (w + dense_cap - 1) / dense_cap;
+      else if (c == 4) {
+        const long long bk = (long long)(p / step);
+        if (bk != lb) cnt += 1;
+        lb = bk;
+      }
+      p += (c == 4 ? x : 0) + y;
+    }
+  }
+  unsigned long long nt64;
+  const unsigned long long tbase = plan_block_scan<unsigned long long>(cnt, s_u64, 0ull, add, nt64);
+  if (nt64 > P.tile_cap) {
+    if (tid == 0) P.out->overflow = 1;
+    return;
+  }
+  const uint32_t nt = (uint32_t)nt64;
+  // 5. write the tiles in row order; light rows remember their tile
+  long long last_lt = -1;
+  {
+    unsigned long long p = pbase;
+    long long lb = carryb;
+    uint32_t id = (uint32_t)tbase;
+    for (uint32_t i = lo; i < hi; ++i) {
+      uint64_t t, w, x;
+      const int c = classify(i, t, w, x);
+      if (c == 1 || c == 3) {
+        Tile tl{};
+        tl.row0 = i;
+        tl.row1 = i + 1;
+        tl.c1 = n;
+        tl.terms = t;
+        if (c == 1) {
+          tl.c0 = P.upper ? i + 1 : 0;
+          tl.mode = P.filter ? 0 : 2;
+          tl.width = (uint32_t)w;
+          tl.n_units = units_of(t);
+        } else {
+          tl.mode = 1;
+          tl.n_units = 1;
+        }
+        P.tiles[id] = tl;
+        P.item_info[i] = make_uint2(id | (tl.mode == 2 ? kEntFlag : 0u),
+                                    stream_base(tl, i, n, P.col_bits, P.upper != 0));
+        ++id;
+      } else if (c == 2) {
+        const uint32_t col_lo = P.upper ? i + 1 : 0;
+        const uint32_t nwin = (uint32_t)((w + dense_cap - 1) / dense_cap);
+        for (uint32_t k = 0; k < nwin; ++k) {
+          Tile tl{};
+          tl.row0 = i;
+          tl.row1 = i + 1;
+          tl.c0 = col_lo + k * (uint32_t)dense_cap;
+          tl.c1 = (uint32_t)min((uint64_t)n, (uint64_t)tl.c0 + dense_cap);
+          tl.mode = 0;
+          tl.nwin = k == 0 ? nwin : 0;
+          tl.width = tl.c1 - tl.c0;
+          tl.terms = t / nwin + 1;
+          tl.n_units = units_of(tl.terms);
+          P.tiles[id + k] = tl;
+        }
+        P.item_info[i] = make_uint2(id | kWinFlag, 0u);
+        id += nwin;
+      } else if (c == 4) {
+        const long long bk = (long long)(p / step);
+        if (bk != lb) {
+          Tile tl{};
+          tl.row0 = i;
+          tl.row1 = i + 1;
+          tl.c1 = n;
+          tl.mode = 1;
+          tl.n_units = 1;
+          P.tiles[id] = tl;
+          last_lt = id;
+          ++id;
+        }
+        lb = bk;
+      } else {
+        P.item_info[i] = make_uint2(kNone, 0u);
+      }
+      p += (c == 4 ? x : 0) + y;
+    }
+  }
+  const long long carry_lt = plan_block_scan<long long>(last_lt, s_i64, -1ll, mx, totl);
+  __threadfence_block();
+  __syncthreads();
+  // 6. light rows: tile id, extend row1, add terms, item_info
+  {
+    unsigned long long p = pbase;
+    long long lb = carryb, cur = carry_lt;
+    uint32_t id = (uint32_t)tbase;
+    for (uint32_t i = lo; i < hi; ++i) {
+      uint64_t t, w, x;
+      const int c = classify(i, t, w, x);
+      if (c == 1 || c == 3) ++id;
+      else if (c == 2) id += (uint32_t)((w + dense_cap - 1) / dense_cap);
+      else if (c == 4) {
+        const long long bk = (long long)(p / step);
+        if (bk != lb) cur = id++;
+        lb = bk;
+        Tile* tl = P.tiles + cur;
+        atomicMax(&tl->row1, i + 1);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&tl->terms), (unsigned long long)t);
+        P.item_info[i] = make_uint2((uint32_t)cur, (i - tl->row0) << P.col_bits);
+      }
+      p += (c == 4 ? x : 0) + y;
+    }
+  }
+  __threadfence_block();
+  __syncthreads();
+  // 7. units, slabs, split list, reduce chunks, output capacity
+  const uint32_t tseg = (nt + kPlanThreads - 1) / kPlanThreads;
+  const uint32_t tlo = min(nt, tid * tseg), thi = min(nt, tlo + tseg);
+  unsigned long long a_slab = 0, a_split = 0, a_single = 0, a_rc = 0, a_cap = 0, a_units = 0;
+  for (uint32_t t = tlo; t < thi; ++t) {
+    const Tile& tl = P.tiles[t];
+    const bool dense = tl.mode != 1;
+    a_cap += dense ? tl.width : kStreamHashSlots;
+    a_units += tl.n_units;
+    if (tl.n_units > 1) {
+      a_slab += tl.n_units;
+      a_split += 1;
+      a_rc += (tl.width + kReduceSlots - 1) / kReduceSlots;
+    } else {
+      a_single += 1;
+    }
+  }
+  unsigned long long n_slabs, n_split, n_single, n_rc, cap, nu;
+  const unsigned long long b_slab = plan_block_scan<unsigned long long>(a_slab, s_u64, 0ull, add, n_slabs);
+  const unsigned long long b_split = plan_block_scan<unsigned long long>(a_split, s_u64, 0ull, add, n_split);
+  const unsigned long long b_single = plan_block_scan<unsigned long long>(a_single, s_u64, 0ull, add, n_single);
+  const unsigned long long b_rc = plan_block_scan<unsigned long long>(a_rc, s_u64, 0ull, add, n_rc);
+  plan_block_scan<unsigned long long>(a_cap, s_u64, 0ull, add, cap);
+  plan_block_scan<unsigned long long>(a_units, s_u64, 0ull, add, nu);
+  if (nu > P.unit_cap || n_rc > P.rc_cap) {
+    if (tid == 0) P.out->overflow = 1;
+    return;
+  }
+  // unit order: split-tile units by the fraction of the tile they cover (64
+  // bins, see the host planner), then the single-unit tiles in tile order
+  constexpr int kFracBins = 64;
+  for (int k = tid; k <= kFracBins; k += kPlanThreads) s_bin[k] = 0;
+  __syncthreads();
+  for (uint32_t t = tlo; t < thi; ++t) {
+    const uint32_t nu_t = P.tiles[t].n_units;
+    if (nu_t > 1)
+      for (uint32_t u = 0; u < nu_t; ++u)
+        atomicAdd(&s_bin[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < kFracBins; ++k) {
+      s_cur[k] = run;
+      run += s_bin[k];
+    }
+    s_cur[kFracBins] = run;
+  }
+  __syncthreads();
+  {
+    uint64_t sb = b_slab, sp = b_split, sg = b_single, rc = b_rc;
+    for (uint32_t t = tlo; t < thi; ++t) {
+      Tile& tl = P.tiles[t];
+      if (tl.n_units > 1) {
+        tl.slab_base = sb;
+        sb += tl.n_units;
+        P.split[sp++] = t;
+        for (uint32_t c0 = 0; c0 < tl.width; c0 += kReduceSlots) P.reduce_chunks[rc++] = make_uint2(t, c0);
+        for (uint32_t u = 0; u < tl.n_units; ++u) {
+          const uint32_t pos = atomicAdd(&s_cur[(uint64_t)(2 * u + 1) * kFracBins / (2 * tl.n_units)], 1u);
+          P.units[pos] = Unit{t, u};
+        }
+      } else {
+        tl.slab_base = 0;
+        P.units[s_cur[kFracBins] + sg++] = Unit{t, 0};
+      }
+    }
+  }
+  if (tid == 0) {
+    P.out->max_entries = cap;
+    P.out->n_slabs = n_slabs;
+    P.out->n_tiles = nt;
+    P.out->n_units = (uint32_t)nu;
+    P.out->n_split = (uint32_t)n_split;
+    P.out->n_reduce_chunks = (uint32_t)n_rc;
+  }
+}
+
 }  // namespace
 
 // =============================================================== host side
@@ -1686,6 +2040,7 @@ struct crop_pairs {
   unsigned int* d_tile_done = nullptr;
   uint2* d_reduce_chunks = nullptr;  // stream mode: (split tile, first slot)
   uint32_t n_reduce_chunks = 0;
+  uint32_t nt = 0, nu = 0;  // tiles, units (either planner)
   void* d_block = nullptr;  // one allocation carved into the small per-job arrays
   // stream mode (short rows): pair words per tile instead of entries
   bool stream_mode = false;
@@ -1974,6 +2329,100 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       crop_count_launches(1);
     }
     std::lock_guard<std::mutex> pin_lock(g_pinned.mu);
+    // GPU planner first (stream mode); the host planner below handles entry
+    // mode and the rare plans that exceed the device planner's bounds
+    const int force = getenv("CROP_FORCE_ENTRY_MODE") ? 1 : (getenv("CROP_FORCE_STREAM_MODE") ? 2 : 0);
+    if (n_tx > 0 && n_items > 0 && force != 1 && !getenv("CROP_HOST_PLANNER")) {
+      const size_t tile_cap = 2 * (size_t)nn + 64;
+      const size_t unit_cap = tile_cap + 1300;  // split units <= T / unit_terms <= 1184
+      const size_t rc_cap = 29 * 1200;          // <= 29 chunks per split tile
+      const size_t o_tiles = 0;
+      const size_t o_units = align16(o_tiles + tile_cap * sizeof(Tile));
+      const size_t o_split = align16(o_units + unit_cap * sizeof(Unit));
+      const size_t o_ebase = align16(o_split + tile_cap * 4);
+      const size_t o_item = align16(o_ebase + tile_cap * 8);
+      const size_t o_rc = align16(o_item + (size_t)nn * sizeof(uint2));
+      const size_t o_tentries = align16(o_rc + rc_cap * sizeof(uint2));
+      const size_t o_cursor = align16(o_tentries + tile_cap * 4);
+      const size_t o_twords = align16(o_cursor + tile_cap * 8);
+      const size_t o_tdone = align16(o_twords + tile_cap * 8);
+      const size_t o_misc = align16(o_tdone + tile_cap * 4);
+      const size_t o_out = align16(o_misc + 32);
+      const size_t blk_bytes = o_out + sizeof(PlanOut);
+      JCUDA(cudaMallocAsync(&J->d_block, blk_bytes, st));
+      unsigned char* db = reinterpret_cast<unsigned char*>(J->d_block);
+      PlanArgs PA{};
+      PA.stats = J->d_terms;
+      PA.n = n_items;
+      PA.col_bits = J->col_bits;
+      PA.upper = upper_only;
+      PA.filter = J->filter;
+      PA.force = force;
+      PA.tiles = reinterpret_cast<Tile*>(db + o_tiles);
+      PA.tile_cap = (uint32_t)tile_cap;
+      PA.units = reinterpret_cast<Unit*>(db + o_units);
+      PA.unit_cap = (uint32_t)unit_cap;
+      PA.split = reinterpret_cast<uint32_t*>(db + o_split);
+      PA.reduce_chunks = reinterpret_cast<uint2*>(db + o_rc);
+      PA.rc_cap = (uint32_t)rc_cap;
+      PA.item_info = reinterpret_cast<uint2*>(db + o_item);
+      PA.out = reinterpret_cast<PlanOut*>(db + o_out);
+      JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
+      k_plan_stream<<<1, kPlanThreads, 0, st>>>(PA);
+      JCUDA(cudaGetLastError());
+      crop_count_launches(1);
+      JCUDA(g_pinned.reserve(sizeof(PlanOut) + 64));
+      PlanOut* ho = reinterpret_cast<PlanOut*>(g_pinned.p);
+      unsigned int* h_ml = reinterpret_cast<unsigned int*>(g_pinned.p + sizeof(PlanOut));
+      int64_t* h_nz = reinterpret_cast<int64_t*>(g_pinned.p + sizeof(PlanOut) + 16);
+      JCUDA(cudaMemcpyAsync(ho, PA.out, sizeof(PlanOut), cudaMemcpyDeviceToHost, st));
+      JCUDA(cudaMemcpyAsync(h_ml, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
+      JCUDA(cudaMemcpyAsync(h_nz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
+      JCUDA(cudaStreamSynchronize(st));
+      if (*h_ml > kMaxLen) {
+        crop_set_error(CROP_EINPUT, "transaction of %u items exceeds the %u-item limit", *h_ml, kMaxLen);
+        rc = CROP_EINPUT;
+        goto fail;
+      }
+      if ((uint64_t)*h_nz >= (1ull << 32)) {
+        crop_set_error(CROP_EINPUT, "%lld item occurrences exceed the 2^32 limit of one job; "
+                       "split the stream", (long long)*h_nz);
+        rc = CROP_EINPUT;
+        goto fail;
+      }
+      if (ho->stream_mode && !ho->overflow) {
+        J->nnz = *h_nz;
+        J->stream_mode = true;
+        J->total_terms = ho->total_terms;
+        J->max_entries = ho->max_entries;
+        J->n_slabs = ho->n_slabs;
+        J->nt = ho->n_tiles;
+        J->nu = ho->n_units;
+        J->n_reduce_chunks = ho->n_reduce_chunks;
+        J->entry_cap = 0;
+        J->d_tiles = PA.tiles;
+        J->d_units = PA.units;
+        J->d_split = PA.split;
+        J->d_tile_ebase = reinterpret_cast<unsigned long long*>(db + o_ebase);
+        J->d_tile_end = nullptr;
+        J->d_item_info = PA.item_info;
+        J->d_reduce_chunks = PA.reduce_chunks;
+        J->d_tile_entries = reinterpret_cast<uint32_t*>(db + o_tentries);
+        J->d_tile_cursor = reinterpret_cast<unsigned long long*>(db + o_cursor);
+        J->d_tile_words = reinterpret_cast<unsigned long long*>(db + o_twords);
+        J->d_tile_done = reinterpret_cast<unsigned int*>(db + o_tdone);
+        J->d_total_entries = reinterpret_cast<unsigned long long*>(db + o_misc);
+        J->d_unit_counter = reinterpret_cast<unsigned int*>(db + o_misc + 8);
+        J->d_overflow = reinterpret_cast<uint32_t*>(db + o_misc + 16);
+        if (J->n_slabs)
+          JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kStreamDenseCap * 4, st));
+        JCUDA(cudaMallocAsync(&J->d_words, (J->total_terms + 2 * ho->occ_sum + 2 * (uint64_t)J->nt + 2) * 4, st));
+        *job = J;
+        return CROP_OK;
+      }
+      JCUDA(cudaFreeAsync(J->d_block, st));
+      J->d_block = nullptr;
+    }
     JCUDA(g_pinned.reserve(nn * 8 + 64));
     unsigned long long* stats = reinterpret_cast<unsigned long long*>(g_pinned.p);
     unsigned int* h_maxlen = reinterpret_cast<unsigned int*>(g_pinned.p + nn * 8);
@@ -2028,6 +2477,8 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     plan_tiles(J, terms, occ, item_tile);
     auto t_p1 = std::chrono::steady_clock::now();
     const uint32_t nt = (uint32_t)J->tiles.size();
+    J->nt = nt;
+    J->nu = (uint32_t)J->units.size();
     const bool sm = J->stream_mode;
     // reduce chunks (stream mode): (split tile, first slot)
     uint32_t nrc = 0;
@@ -2158,15 +2609,15 @@ extern "C" int crop_pairs_info(const crop_pairs* J, uint64_t* max_entries, uint6
                                uint64_t* n_tiles, uint64_t* n_units) {
   if (max_entries) *max_entries = J->max_entries;
   if (total_terms) *total_terms = J->total_terms;
-  if (n_tiles) *n_tiles = J->tiles.size();
-  if (n_units) *n_units = J->units.size();
+  if (n_tiles) *n_tiles = J->nt;
+  if (n_units) *n_units = J->nu;
   return CROP_OK;
 }
 
 extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_col,
                               uint32_t* out_count, uint64_t* d_n_entries, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  const uint32_t nt = (uint32_t)J->tiles.size();
+  const uint32_t nt = J->nt;
   CROP_CUDA(cudaMemsetAsync(d_n_entries, 0, 8, st));
   if (nt == 0 || J->n_tx == 0) return CROP_OK;
   const bool up = J->upper != 0;
@@ -2227,7 +2678,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     StreamCountArgs C{};
     C.tiles = J->d_tiles;
     C.units = J->d_units;
-    C.n_units = (uint32_t)J->units.size();
+    C.n_units = J->nu;
     C.tile_base = J->d_tile_ebase;
     C.tile_words = J->d_tile_words;
     C.words = J->d_words;
@@ -2252,7 +2703,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     auto kcs = C.dbg ? k_count_stream<true> : k_count_stream<false>;
     CROP_CUDA(cudaFuncSetAttribute(kcs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     mark(4);
-    kcs<<<std::min<int>(kNumSMs, (int)J->units.size()), kCountThreads, kStreamSmem, st>>>(C);
+    kcs<<<std::min<int>(kNumSMs, (int)J->nu), kCountThreads, kStreamSmem, st>>>(C);
     CROP_LAUNCH_CHECK();
     const uint32_t nrc = J->n_reduce_chunks;
     if (nrc) {
@@ -2300,7 +2751,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     A.items = J->items;
     A.tiles = J->d_tiles;
     A.units = J->d_units;
-    A.n_units = (uint32_t)J->units.size();
+    A.n_units = J->nu;
     A.tile_ebase = J->d_tile_ebase;
     A.tile_entries = J->d_tile_entries;
     A.entries = J->d_entries;
@@ -2329,7 +2780,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     if (up) kern = J->filter ? k_count<true, true> : k_count<true, false>;
     else kern = J->filter ? k_count<false, true> : k_count<false, false>;
     CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCountSmem));
-    const int grid = std::min<int>(kNumSMs, (int)J->units.size());
+    const int grid = std::min<int>(kNumSMs, (int)J->nu);
     mark(4);
     kern<<<grid, kCountThreads, kCountSmem, st>>>(A);
     CROP_LAUNCH_CHECK();

@@ -193,13 +193,16 @@ def _gpu_pairs(ent):
     return oracle.sorted_pairs(r, c, w)
 
 
-@pytest.fixture(params=["auto", "entry", "stream"])
+@pytest.fixture(params=["auto", "entry", "stream", "stream-host-plan"])
 def count_mode(request, monkeypatch):
-    """Counting mode of the pair engine: the planner's choice, or forced."""
+    """Counting mode of the pair engine: the planner's choice, or forced;
+    stream mode with the device planner (default) or the host planner."""
     if request.param == "entry":
         monkeypatch.setenv("CROP_FORCE_ENTRY_MODE", "1")
-    elif request.param == "stream":
+    elif request.param.startswith("stream"):
         monkeypatch.setenv("CROP_FORCE_STREAM_MODE", "1")
+    if request.param.endswith("host-plan"):
+        monkeypatch.setenv("CROP_HOST_PLANNER", "1")
     return request.param
 
 

@@ -43,6 +43,24 @@ __global__ void smem_plain(uint32_t* out, int iters) {  // racy ld+st, reference
   atomicAdd(out, acc);
 }
 
+// skewed: a fraction p of the updates go to H hot slots (Zipf-like hot
+// columns of a single-row tile)
+__global__ void smem_skew(uint32_t* out, int iters, uint32_t p_thresh, uint32_t hot) {
+  extern __shared__ uint32_t tab[];
+  for (int i = threadIdx.x; i < 32768; i += blockDim.x) tab[i] = 0;
+  __syncthreads();
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    uint32_t h = mix32(s + it * 0x9E3779B9u);
+    const uint32_t slot = h < p_thresh ? (h >> 8) % hot : h % 32768u;
+    atomicAdd(&tab[slot], 1u);
+  }
+  __syncthreads();
+  uint32_t acc = 0;
+  for (int i = threadIdx.x; i < 32768; i += blockDim.x) acc += tab[i];
+  atomicAdd(out, acc);
+}
+
 __global__ void mix_only(uint32_t* out, int iters) {
   uint32_t s = blockIdx.x * blockDim.x + threadIdx.x, acc = 0;
   for (int it = 0; it < iters; ++it) acc += mix32(s + it * 0x9E3779B9u) % 32768u;
@@ -86,6 +104,18 @@ int main() {
       CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
       double ops = (double)sms * threads * iters;
       printf("smem_atomic 128KB threads=%d: %.3f ms  %.3e atom/s  %.2f atom/clk/SM@1.9G\n", threads, ms, ops / ms * 1e3, ops / (ms * 1e-3) / sms / 1.9e9);
+    }
+    CK(cudaFuncSetAttribute(smem_skew, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4));
+    for (double p : {0.0, 0.02, 0.1, 0.3}) {
+      for (uint32_t hot : {1u, 4u, 16u, 64u}) {
+        const uint32_t th = (uint32_t)(p * 4294967295.0);
+        smem_skew<<<sms, 1024, 32768 * 4>>>(out, iters, th, hot);
+        cudaEventRecord(e0); smem_skew<<<sms, 1024, 32768 * 4>>>(out, iters, th, hot); cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+        double ops = (double)sms * 1024 * iters;
+        printf("smem_skew p=%.2f hot=%u: %.3f ms  %.3e atom/s  %.2f atom/clk/SM\n", p, hot, ms, ops / ms * 1e3, ops / (ms * 1e-3) / sms / 1.9e9);
+        if (p == 0.0) break;
+      }
     }
     auto k2 = smem_plain<32768>;
     CK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4));

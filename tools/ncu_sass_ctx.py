@@ -12,7 +12,7 @@ rows = list(csv.reader(out.splitlines()))
 hdr = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 h = rows[hdr]
 si = h.index("Warp Stall Sampling (All Samples)")
-body = [r for r in rows[hdr + 1:] if len(r) > si]
+body = [r for r in rows[hdr + 1:] if len(r) > si and r[si].isdigit()]
 tot = sum(int(r[si] or 0) for r in body)
 seen = set()
 for k in sorted(range(len(body)), key=lambda k: -int(body[k][si] or 0)):

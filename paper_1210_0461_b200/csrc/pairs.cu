@@ -1672,6 +1672,7 @@ struct PlanOut {
   unsigned long long total_terms, occ_sum, max_entries, n_slabs;
   uint32_t n_tiles, n_units, n_split, n_reduce_chunks;
   uint32_t stream_mode, overflow, pad0, pad1;
+  long long dbg[4];  // development: planner phase cycles
 };
 
 struct PlanArgs {
@@ -1725,20 +1726,31 @@ __device__ __forceinline__ T plan_block_scan(T v, T* s_tmp, T ident, Op op, T& t
   return r;
 }
 
+// Row record in shared memory: class (3 bits) | weight or #windows << 3.
+constexpr uint32_t kPlanRowsPerThread = 8;
+constexpr uint32_t kPlanChunk = kPlanThreads * kPlanRowsPerThread;  // rows staged per step
+
 __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   __shared__ unsigned long long s_u64[33];
   __shared__ long long s_i64[33];
   __shared__ uint32_t s_bin[65], s_cur[65];
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_rec = s_dyn;               // per staged row: class | weight << 3
+  uint32_t* s_t = s_dyn + kPlanChunk;    // per staged row: terms (< 2^32 in stream mode)
   const uint32_t n = P.n, tid = threadIdx.x;
-  const uint32_t seg = (n + kPlanThreads - 1) / kPlanThreads;
-  const uint32_t lo = min(n, tid * seg), hi = min(n, lo + seg);
+  long long ck[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long c_last = clock64();
+  auto stamp = [&](int q) {
+    const long long now = clock64();
+    ck[q] += now - c_last;
+    c_last = now;
+  };
   auto add = [](unsigned long long a, unsigned long long b) { return a + b; };
   auto mx = [](long long a, long long b) { return a > b ? a : b; };
-  unsigned long long tot;
   long long totl;
-  // 1. totals and the mode decision
+  // 1. totals (coalesced) and the mode decision
   unsigned long long T = 0, O = 0;
-  for (uint32_t i = lo; i < hi; ++i) {
+  for (uint32_t i = tid; i < n; i += kPlanThreads) {
     const unsigned long long x = P.stats[i];
     T += x & (kOccOne - 1);
     O += x >> 40;
@@ -1756,181 +1768,260 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     P.out->overflow = 0;
   }
   if (!sm) return;
+  stamp(0);
   const uint64_t unit_terms = max(1ull << 16, T / ((uint64_t)kNumSMs * 8));
+  const double inv_ut = (double)kPlanS / (double)unit_terms;
   const uint32_t rows_max = P.col_bits >= 32 ? 1u : ((1u << (32 - P.col_bits)) - 1u);
-  const uint64_t y = (kPlanS + rows_max - 1) / rows_max;   // span weight of every row
-  const uint64_t step = kPlanS - kPlanS / 4 - y;            // bucket width
+  const uint64_t y = (kPlanS + rows_max - 1) / rows_max;  // span weight of every row
+  // bucket width, with a margin for the rounding of the double reciprocal
+  const uint64_t step = kPlanS - kPlanS / 4 - y - 1024;
+  const double inv_step = 1.0 / (double)step;
+  auto bucket = [inv_step](unsigned long long p) { return (long long)((double)p * inv_step); };
   const uint64_t dense_cap = kStreamDenseCap, hash_cap = kStreamHashCap;
-  // class of row i: 0 none, 1 H, 2 W, 3 L1, 4 L; x = light weight
-  auto classify = [&](uint32_t i, uint64_t& t, uint64_t& w, uint64_t& x) -> int {
-    t = P.stats[i] & (kOccOne - 1);
-    w = P.upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
-    x = 0;
-    if (t == 0) return 0;
-    const uint64_t b = t < w ? t : w;
-    const bool hfit = b <= hash_cap && t <= unit_terms;
-    if (w <= dense_cap && ((8 * t >= w && w >= kMinDenseWidth) || !hfit)) return 1;
-    if (!hfit) return 2;
-    const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
-    const uint64_t xt = (t * kPlanS + unit_terms - 1) / unit_terms;
-    x = xb > xt ? xb : xt;
-    return x > kPlanS / 4 ? 3 : 4;
-  };
   auto units_of = [&](uint64_t t) -> uint32_t {
     const uint64_t u = (t + unit_terms - 1) / unit_terms;
     return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
   };
-  // 2. prefix of the light weights (+ span weight of every row)
-  unsigned long long pw = 0;
-  for (uint32_t i = lo; i < hi; ++i) {
-    uint64_t t, w, x;
-    const int c = classify(i, t, w, x);
-    pw += (c == 4 ? x : 0) + y;
-  }
-  const unsigned long long pbase = plan_block_scan<unsigned long long>(pw, s_u64, 0ull, add, tot);
-  // 3. bucket of the last light row of each segment -> carry
-  long long lastb = -1;
-  {
-    unsigned long long p = pbase;
-    for (uint32_t i = lo; i < hi; ++i) {
-      uint64_t t, w, x;
-      const int c = classify(i, t, w, x);
-      if (c == 4) lastb = (long long)(p / step);
-      p += (c == 4 ? x : 0) + y;
+  // carries across chunks
+  unsigned long long c_p = 0, c_tiles = 0;
+  long long c_bucket = -1, c_lt = -1, c_lrow0 = -1;
+  for (uint32_t base = 0; base < n; base += kPlanChunk) {
+    const uint32_t cn = min(kPlanChunk, n - base);
+    // classify: 1 H, 2 W (record = #windows), 3 L1, 4 L (record = weight), 0 none
+    unsigned long long st8[kPlanRowsPerThread];
+#pragma unroll
+    for (uint32_t q = 0; q < kPlanRowsPerThread; ++q) {
+      const uint32_t k = tid + q * kPlanThreads;
+      st8[q] = k < cn ? P.stats[base + k] : 0ull;
     }
-  }
-  const long long carryb = plan_block_scan<long long>(lastb, s_i64, -1ll, mx, totl);
-  // 4. tiles per segment
-  unsigned long long cnt = 0;
-  {
-    unsigned long long p = pbase;
-    long long lb = carryb;
-    for (uint32_t i = lo; i < hi; ++i) {
-      uint64_t t, w, x;
-      const int c = classify(i, t, w, x);
-      if (c == 1 || c == 3) cnt += 1;
-      else if (c == 2) cnt += (w + dense_cap - 1) / dense_cap;
-      else if (c == 4) {
-        const long long bk = (long long)(p / step);
-        if (bk != lb) cnt += 1;
-        lb = bk;
-      }
-      p += (c == 4 ? x : 0) + y;
-    }
-  }
-  unsigned long long nt64;
-  const unsigned long long tbase = plan_block_scan<unsigned long long>(cnt, s_u64, 0ull, add, nt64);
-  if (nt64 > P.tile_cap) {
-    if (tid == 0) P.out->overflow = 1;
-    return;
-  }
-  const uint32_t nt = (uint32_t)nt64;
-  // 5. write the tiles in row order; light rows remember their tile
-  long long last_lt = -1;
-  {
-    unsigned long long p = pbase;
-    long long lb = carryb;
-    uint32_t id = (uint32_t)tbase;
-    for (uint32_t i = lo; i < hi; ++i) {
-      uint64_t t, w, x;
-      const int c = classify(i, t, w, x);
-      if (c == 1 || c == 3) {
-        Tile tl{};
-        tl.row0 = i;
-        tl.row1 = i + 1;
-        tl.c1 = n;
-        tl.terms = t;
-        if (c == 1) {
-          tl.c0 = P.upper ? i + 1 : 0;
-          tl.mode = P.filter ? 0 : 2;
-          tl.width = (uint32_t)w;
-          tl.n_units = units_of(t);
+#pragma unroll
+    for (uint32_t q = 0; q < kPlanRowsPerThread; ++q) {
+      const uint32_t k = tid + q * kPlanThreads;
+      if (k >= cn) break;
+      const uint32_t i = base + k;
+      const uint64_t t = st8[q] & (kOccOne - 1);
+      const uint64_t w = P.upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
+      s_t[k] = (uint32_t)t;
+      uint32_t rec = 0;
+      if (t) {
+        const uint64_t b = t < w ? t : w;
+        const bool hfit = b <= hash_cap && t <= unit_terms;
+        if (w <= dense_cap && ((8 * t >= w && w >= kMinDenseWidth) || !hfit)) {
+          rec = 1;
+        } else if (!hfit) {
+          rec = 2 | (uint32_t)((w + dense_cap - 1) / dense_cap) << 3;
         } else {
-          tl.mode = 1;
-          tl.n_units = 1;
+          const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
+          const uint64_t xt = (uint64_t)((double)t * inv_ut) + 1;  // >= t * S / unit_terms
+          const uint64_t x = xb > xt ? xb : xt;
+          rec = x > kPlanS / 4 ? 3u : (4u | (uint32_t)x << 3);
         }
-        P.tiles[id] = tl;
-        P.item_info[i] = make_uint2(id | (tl.mode == 2 ? kEntFlag : 0u),
-                                    stream_base(tl, i, n, P.col_bits, P.upper != 0));
-        ++id;
-      } else if (c == 2) {
-        const uint32_t col_lo = P.upper ? i + 1 : 0;
-        const uint32_t nwin = (uint32_t)((w + dense_cap - 1) / dense_cap);
-        for (uint32_t k = 0; k < nwin; ++k) {
-          Tile tl{};
-          tl.row0 = i;
-          tl.row1 = i + 1;
-          tl.c0 = col_lo + k * (uint32_t)dense_cap;
-          tl.c1 = (uint32_t)min((uint64_t)n, (uint64_t)tl.c0 + dense_cap);
-          tl.mode = 0;
-          tl.nwin = k == 0 ? nwin : 0;
-          tl.width = tl.c1 - tl.c0;
-          tl.terms = t / nwin + 1;
-          tl.n_units = units_of(tl.terms);
-          P.tiles[id + k] = tl;
+      }
+      s_rec[k] = rec;
+    }
+    __syncthreads();
+    stamp(1);
+    const uint32_t lo = min(cn, tid * kPlanRowsPerThread), hi = min(cn, lo + kPlanRowsPerThread);
+    // weights prefix
+    unsigned long long pw = 0;
+    for (uint32_t k = lo; k < hi; ++k) {
+      const uint32_t r = s_rec[k];
+      pw += ((r & 7) == 4 ? (r >> 3) : 0) + y;
+    }
+    unsigned long long chunk_w;
+    const unsigned long long pbase = c_p + plan_block_scan<unsigned long long>(pw, s_u64, 0ull, add, chunk_w);
+    // last light bucket of each thread -> carry
+    long long lastb = -1;
+    {
+      unsigned long long p = pbase;
+      for (uint32_t k = lo; k < hi; ++k) {
+        const uint32_t r = s_rec[k];
+        if ((r & 7) == 4) lastb = bucket(p);
+        p += ((r & 7) == 4 ? (r >> 3) : 0) + y;
+      }
+    }
+    long long carryb = plan_block_scan<long long>(lastb, s_i64, -1ll, mx, totl);
+    carryb = carryb > c_bucket ? carryb : c_bucket;
+    const long long chunk_lastb = totl > c_bucket ? totl : c_bucket;
+    // tiles per thread
+    unsigned long long cnt = 0;
+    {
+      unsigned long long p = pbase;
+      long long lb = carryb;
+      for (uint32_t k = lo; k < hi; ++k) {
+        const uint32_t r = s_rec[k], c = r & 7;
+        if (c == 1 || c == 3) cnt += 1;
+        else if (c == 2) cnt += r >> 3;
+        else if (c == 4) {
+          const long long bk = bucket(p);
+          if (bk != lb) cnt += 1;
+          lb = bk;
         }
-        P.item_info[i] = make_uint2(id | kWinFlag, 0u);
-        id += nwin;
-      } else if (c == 4) {
-        const long long bk = (long long)(p / step);
-        if (bk != lb) {
+        p += (c == 4 ? (r >> 3) : 0) + y;
+      }
+    }
+    stamp(2);
+    unsigned long long chunk_tiles;
+    const unsigned long long tbase = c_tiles + plan_block_scan<unsigned long long>(cnt, s_u64, 0ull, add, chunk_tiles);
+    if (c_tiles + chunk_tiles > P.tile_cap) {
+      if (tid == 0) P.out->overflow = 1;
+      return;
+    }
+    // write the tiles; the last light tile each thread starts (id, first row)
+    long long last_lt = -1, last_row0 = -1;
+    {
+      unsigned long long p = pbase;
+      long long lb = carryb;
+      uint32_t id = (uint32_t)tbase;
+      for (uint32_t k = lo; k < hi; ++k) {
+        const uint32_t r = s_rec[k], c = r & 7, i = base + k;
+        if (c == 1 || c == 3) {
+          const uint64_t t = s_t[k];
           Tile tl{};
           tl.row0 = i;
           tl.row1 = i + 1;
           tl.c1 = n;
-          tl.mode = 1;
-          tl.n_units = 1;
+          tl.terms = t;
+          if (c == 1) {
+            tl.c0 = P.upper ? i + 1 : 0;
+            tl.mode = P.filter ? 0 : 2;
+            tl.width = P.upper ? n - 1 - i : n;
+            tl.n_units = units_of(t);
+          } else {
+            tl.mode = 1;
+            tl.n_units = 1;
+          }
           P.tiles[id] = tl;
-          last_lt = id;
+          P.item_info[i] = make_uint2(id | (tl.mode == 2 ? kEntFlag : 0u),
+                                      stream_base(tl, i, n, P.col_bits, P.upper != 0));
           ++id;
+        } else if (c == 2) {
+          const uint64_t t = s_t[k];
+          const uint32_t col_lo = P.upper ? i + 1 : 0;
+          const uint32_t nwin = r >> 3;
+          for (uint32_t q = 0; q < nwin; ++q) {
+            Tile tl{};
+            tl.row0 = i;
+            tl.row1 = i + 1;
+            tl.c0 = col_lo + q * (uint32_t)dense_cap;
+            tl.c1 = (uint32_t)min((uint64_t)n, (uint64_t)tl.c0 + dense_cap);
+            tl.mode = 0;
+            tl.nwin = q == 0 ? nwin : 0;
+            tl.width = tl.c1 - tl.c0;
+            tl.terms = t / nwin + 1;
+            tl.n_units = units_of(tl.terms);
+            P.tiles[id + q] = tl;
+          }
+          P.item_info[i] = make_uint2(id | kWinFlag, 0u);
+          id += nwin;
+        } else if (c == 4) {
+          const long long bk = bucket(p);
+          if (bk != lb) {
+            Tile tl{};
+            tl.row0 = i;
+            tl.row1 = i + 1;
+            tl.c1 = n;
+            tl.mode = 1;
+            tl.n_units = 1;
+            P.tiles[id] = tl;
+            last_lt = id;
+            last_row0 = i;
+            ++id;
+          }
+          lb = bk;
+        } else {
+          P.item_info[i] = make_uint2(kNone, 0u);
         }
-        lb = bk;
-      } else {
-        P.item_info[i] = make_uint2(kNone, 0u);
+        p += (c == 4 ? (r >> 3) : 0) + y;
       }
-      p += (c == 4 ? x : 0) + y;
     }
+    stamp(3);
+    long long carry_lt = plan_block_scan<long long>(last_lt, s_i64, -1ll, mx, totl);
+    const long long chunk_lt = totl > c_lt ? totl : c_lt;
+    carry_lt = carry_lt > c_lt ? carry_lt : c_lt;
+    long long carry_row0 = plan_block_scan<long long>(last_row0, s_i64, -1ll, mx, totl);
+    const long long chunk_row0 = totl > c_lrow0 ? totl : c_lrow0;
+    carry_row0 = carry_row0 > c_lrow0 ? carry_row0 : c_lrow0;
+    // light rows: tile, row range, terms, item_info
+    {
+      // per thread, the rows of one light tile are consecutive: accumulate
+      // its terms and last row, one pair of global atomics per tile change
+      unsigned long long p = pbase;
+      long long lb = carryb, cur = carry_lt, row0 = carry_row0;
+      uint32_t id = (uint32_t)tbase;
+      long long acc_tile = -1;
+      unsigned long long acc_terms = 0;
+      uint32_t acc_row1 = 0;
+      auto flush = [&]() {
+        if (acc_tile >= 0) {
+          Tile* tl = P.tiles + acc_tile;
+          atomicMax(&tl->row1, acc_row1);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&tl->terms), acc_terms);
+        }
+      };
+      for (uint32_t k = lo; k < hi; ++k) {
+        const uint32_t r = s_rec[k], c = r & 7, i = base + k;
+        if (c == 1 || c == 3) ++id;
+        else if (c == 2) id += r >> 3;
+        else if (c == 4) {
+          const long long bk = bucket(p);
+          if (bk != lb) {
+            cur = id++;
+            row0 = i;
+          }
+          lb = bk;
+          if (cur != acc_tile) {
+            flush();
+            acc_tile = cur;
+            acc_terms = 0;
+          }
+          acc_terms += s_t[k];
+          acc_row1 = i + 1;
+          P.item_info[i] = make_uint2((uint32_t)cur, (i - (uint32_t)row0) << P.col_bits);
+        }
+        p += (c == 4 ? (r >> 3) : 0) + y;
+      }
+      flush();
+    }
+    stamp(4);
+    c_p += chunk_w;
+    c_tiles += chunk_tiles;
+    c_bucket = chunk_lastb;
+    c_lt = chunk_lt;
+    c_lrow0 = chunk_row0;
+    __syncthreads();
   }
-  const long long carry_lt = plan_block_scan<long long>(last_lt, s_i64, -1ll, mx, totl);
   __threadfence_block();
   __syncthreads();
-  // 6. light rows: tile id, extend row1, add terms, item_info
-  {
-    unsigned long long p = pbase;
-    long long lb = carryb, cur = carry_lt;
-    uint32_t id = (uint32_t)tbase;
-    for (uint32_t i = lo; i < hi; ++i) {
-      uint64_t t, w, x;
-      const int c = classify(i, t, w, x);
-      if (c == 1 || c == 3) ++id;
-      else if (c == 2) id += (uint32_t)((w + dense_cap - 1) / dense_cap);
-      else if (c == 4) {
-        const long long bk = (long long)(p / step);
-        if (bk != lb) cur = id++;
-        lb = bk;
-        Tile* tl = P.tiles + cur;
-        atomicMax(&tl->row1, i + 1);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&tl->terms), (unsigned long long)t);
-        P.item_info[i] = make_uint2((uint32_t)cur, (i - tl->row0) << P.col_bits);
-      }
-      p += (c == 4 ? x : 0) + y;
+  const uint32_t nt = (uint32_t)c_tiles;
+  // units, slabs, split list, reduce chunks, output capacity. Per-tile unit
+  // counts and widths are cached in shared memory when they fit (hash tiles
+  // report width 0 and count kStreamHashSlots output slots).
+  const bool cached = nt <= kPlanChunk;
+  uint32_t* s_nu = s_dyn;
+  uint32_t* s_wd = s_dyn + kPlanChunk;
+  if (cached)
+    for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+      const Tile& tl = P.tiles[t];
+      s_nu[t] = tl.n_units;
+      s_wd[t] = tl.mode != 1 ? tl.width : 0xFFFFFFFFu;
     }
-  }
-  __threadfence_block();
   __syncthreads();
-  // 7. units, slabs, split list, reduce chunks, output capacity
+  auto nu_of = [&](uint32_t t) { return cached ? s_nu[t] : P.tiles[t].n_units; };
+  auto wd_of = [&](uint32_t t) {
+    return cached ? s_wd[t] : (P.tiles[t].mode != 1 ? P.tiles[t].width : 0xFFFFFFFFu);
+  };
   const uint32_t tseg = (nt + kPlanThreads - 1) / kPlanThreads;
   const uint32_t tlo = min(nt, tid * tseg), thi = min(nt, tlo + tseg);
   unsigned long long a_slab = 0, a_split = 0, a_single = 0, a_rc = 0, a_cap = 0, a_units = 0;
   for (uint32_t t = tlo; t < thi; ++t) {
-    const Tile& tl = P.tiles[t];
-    const bool dense = tl.mode != 1;
-    a_cap += dense ? tl.width : kStreamHashSlots;
-    a_units += tl.n_units;
-    if (tl.n_units > 1) {
-      a_slab += tl.n_units;
+    const uint32_t nu_t = nu_of(t), wd = wd_of(t);
+    a_cap += wd != 0xFFFFFFFFu ? wd : kStreamHashSlots;
+    a_units += nu_t;
+    if (nu_t > 1) {
+      a_slab += nu_t;
       a_split += 1;
-      a_rc += (tl.width + kReduceSlots - 1) / kReduceSlots;
+      a_rc += (wd + kReduceSlots - 1) / kReduceSlots;
     } else {
       a_single += 1;
     }
@@ -1947,15 +2038,27 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     return;
   }
   // unit order: split-tile units by the fraction of the tile they cover (64
-  // bins, see the host planner), then the single-unit tiles in tile order
+  // bins, see the host planner), then the single-unit tiles (any order)
   constexpr int kFracBins = 64;
   for (int k = tid; k <= kFracBins; k += kPlanThreads) s_bin[k] = 0;
+  {
+    // slab bases, split list and reduce chunks in tile order
+    uint64_t sb = b_slab, sp = b_split, rc = b_rc;
+    for (uint32_t t = tlo; t < thi; ++t) {
+      const uint32_t nu_t = nu_of(t), width = wd_of(t);
+      if (nu_t > 1) {
+        P.tiles[t].slab_base = sb;
+        sb += nu_t;
+        P.split[sp++] = t;
+        for (uint32_t c0 = 0; c0 < width; c0 += kReduceSlots) P.reduce_chunks[rc++] = make_uint2(t, c0);
+      }
+    }
+  }
   __syncthreads();
-  for (uint32_t t = tlo; t < thi; ++t) {
-    const uint32_t nu_t = P.tiles[t].n_units;
+  for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+    const uint32_t nu_t = nu_of(t);
     if (nu_t > 1)
-      for (uint32_t u = 0; u < nu_t; ++u)
-        atomicAdd(&s_bin[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
+      for (uint32_t u = 0; u < nu_t; ++u) atomicAdd(&s_bin[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
   }
   __syncthreads();
   if (tid == 0) {
@@ -1967,26 +2070,26 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     s_cur[kFracBins] = run;
   }
   __syncthreads();
-  {
-    uint64_t sb = b_slab, sp = b_split, sg = b_single, rc = b_rc;
-    for (uint32_t t = tlo; t < thi; ++t) {
-      Tile& tl = P.tiles[t];
-      if (tl.n_units > 1) {
-        tl.slab_base = sb;
-        sb += tl.n_units;
-        P.split[sp++] = t;
-        for (uint32_t c0 = 0; c0 < tl.width; c0 += kReduceSlots) P.reduce_chunks[rc++] = make_uint2(t, c0);
-        for (uint32_t u = 0; u < tl.n_units; ++u) {
-          const uint32_t pos = atomicAdd(&s_cur[(uint64_t)(2 * u + 1) * kFracBins / (2 * tl.n_units)], 1u);
-          P.units[pos] = Unit{t, u};
-        }
-      } else {
-        tl.slab_base = 0;
-        P.units[s_cur[kFracBins] + sg++] = Unit{t, 0};
+  for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+    const uint32_t nu_t = nu_of(t);
+    if (nu_t > 1) {
+      for (uint32_t u = 0; u < nu_t; ++u) {
+        const uint32_t pos = atomicAdd(&s_cur[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
+        P.units[pos] = Unit{t, u};
       }
+    } else {
+      P.units[atomicAdd(&s_cur[kFracBins], 1u)] = Unit{t, 0};
     }
   }
+  (void)b_single;
+  stamp(5);
   if (tid == 0) {
+    P.out->pad0 = (uint32_t)(ck[0] / 1000);
+    P.out->pad1 = (uint32_t)(ck[1] / 1000);
+    P.out->dbg[0] = ck[2];
+    P.out->dbg[1] = ck[3];
+    P.out->dbg[2] = ck[4];
+    P.out->dbg[3] = ck[5];
     P.out->max_entries = cap;
     P.out->n_slabs = n_slabs;
     P.out->n_tiles = nt;
@@ -2368,7 +2471,9 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       PA.item_info = reinterpret_cast<uint2*>(db + o_item);
       PA.out = reinterpret_cast<PlanOut*>(db + o_out);
       JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
-      k_plan_stream<<<1, kPlanThreads, 0, st>>>(PA);
+      JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kPlanChunk * 8)));
+      k_plan_stream<<<1, kPlanThreads, kPlanChunk * 8, st>>>(PA);
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
       JCUDA(g_pinned.reserve(sizeof(PlanOut) + 64));
@@ -2390,6 +2495,9 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         rc = CROP_EINPUT;
         goto fail;
       }
+      if (getenv("CROP_DEBUG_TIMING"))
+        fprintf(stderr, "[k_plan_stream] kcyc: totals %u classify %u scans+walks %.0f tiles %.0f light %.0f units %.0f\n",
+                ho->pad0, ho->pad1, ho->dbg[0] / 1e3, ho->dbg[1] / 1e3, ho->dbg[2] / 1e3, ho->dbg[3] / 1e3);
       if (ho->stream_mode && !ho->overflow) {
         J->nnz = *h_nz;
         J->stream_mode = true;

@@ -110,6 +110,20 @@ int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
  * (one entry per (transaction, tile) run, counting re-reads the items).
  * CROP_FORCE_ENTRY_MODE=1 in the environment forces entry mode. */
 int crop_pairs_mode(const crop_pairs* job, int* stream_mode);
+/* Stream mode only: caller-owned, zeroed buffers that the next crop_pairs_run
+ * fills for a fused top-k -- hist uint32[23552] receives the histogram bins of
+ * every output count >= 2048, hi_list (>= total_terms / 2048 + 1 entries) the
+ * output positions of those entries, *hi_n their number. */
+int crop_pairs_set_topk(crop_pairs* job, uint32_t* hist, uint64_t* hi_list, uint64_t* hi_n,
+                        uint64_t hi_cap);
+/* crop_topk over entries whose high counts were pre-binned by the counting
+ * kernels (crop_pairs_set_topk); when those entries number >= k only they
+ * are scanned, else the remaining counts are binned as in crop_topk. Same
+ * result as crop_topk. Replaces engine.py:162-172 top_entries. */
+int crop_topk_fused(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                    const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k, uint32_t* hist,
+                    const uint64_t* hi_list, const uint64_t* hi_n, uint64_t* out_idx,
+                    uint64_t* d_k_out, void* stream);
 void crop_pairs_destroy(crop_pairs* job);
 
 /* Per-instance bucket statistics of counted entries (the LoadReport rows,

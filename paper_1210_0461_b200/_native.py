@@ -42,6 +42,8 @@ _SIGS = {
     "crop_pairs_phase_ms": (i32, [P, ctypes.POINTER(ctypes.c_float)]),
     "crop_pairs_overflowed": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_mode": (i32, [P, ctypes.POINTER(i32)]),
+    "crop_pairs_set_topk": (i32, [P, P, P, P, u64]),
+    "crop_topk_fused": (i32, [P, P, P, P, u64, u32, P, P, P, P, P, P]),
     "crop_pairs_destroy": (None, [P]),
     "crop_entry_bucket_stats": (i32, [P, P, P, P, u64, i32, u32, P, P, u32, P, P, P, P, P]),
     "crop_entry_buckets": (i32, [P, P, u64, P, P, u32, P, P]),

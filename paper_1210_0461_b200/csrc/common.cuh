@@ -73,6 +73,16 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Top-k count histogram: exact below 2048, 2^-10 relative resolution above
+// (monotone in the count; shared by topk.cu and the counting kernels).
+constexpr uint32_t kTopkExactBins = 2048;
+constexpr uint32_t kTopkBins = kTopkExactBins + 21 * 1024;  // 23552
+__device__ __forceinline__ uint32_t topk_count_bin(uint32_t c) {
+  if (c < kTopkExactBins) return c;
+  const uint32_t msb = 31 - __clz(c);  // >= 11
+  return kTopkExactBins + (msb - 11) * 1024 + ((c >> (msb - 10)) & 1023);
+}
+
 }  // namespace crop
 
 // ------------------------------------------------------------------ errors
@@ -81,6 +91,12 @@ void crop_set_error(int code, const char* fmt, ...);
 int crop_pool_setup();
 // Count kernels this library launched (reported by bench.py as gpu_launches).
 void crop_count_launches(int n);
+// Top-k select (topk.cu); the fused inputs come from the pair engine's counting
+// kernels (high-count histogram + entry list), nullptr for the plain path.
+int crop_topk_impl(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                   const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k,
+                   uint64_t* out_idx, uint64_t* d_k_out, cudaStream_t st, uint32_t* fused_hist,
+                   const unsigned long long* hi_list, const unsigned long long* hi_n);
 
 #define CROP_CUDA(call)                                                                  \
   do {                                                                                   \

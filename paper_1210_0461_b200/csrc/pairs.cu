@@ -1282,7 +1282,20 @@ struct StreamCountArgs {
   uint32_t* slabs;  // kStreamDenseCap words per unit of a split tile
   unsigned int* tile_done;
   unsigned long long* dbg;  // development only (CROP_DEBUG_KINDS): cycles per kind/phase
+  // fused top-k inputs (nullable): histogram of counts >= kTopkExactBins and
+  // the output positions of those entries
+  uint32_t* topk_hist;
+  unsigned long long* hi_list;
+  unsigned long long* hi_n;
 };
+
+// Record an emitted entry for the fused top-k (high counts only: rare).
+__device__ __forceinline__ void note_high(const StreamCountArgs& A, uint32_t c, uint64_t o) {
+  if (A.topk_hist && c >= kTopkExactBins) {
+    atomicAdd(&A.topk_hist[topk_count_bin(c)], 1u);
+    A.hi_list[atomicAdd(A.hi_n, 1ull)] = o;
+  }
+}
 
 // (row, column) of slot s of dense tile T (stream layout, stream_base)
 __device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint32_t n, bool upper,
@@ -1543,6 +1556,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
         A.out_row[o] = i;
         A.out_col[o] = j;
         A.out_count[o] = c;
+        note_high(A, c, o);
       }
       pos += __popc(mk);
     }
@@ -1609,6 +1623,7 @@ __global__ void __launch_bounds__(256) k_reduce_slabs(StreamCountArgs A, const u
         A.out_row[o] = i;
         A.out_col[o] = j;
         A.out_count[o] = c[k];
+        note_high(A, c[k], o);
         ++o;
       }
     __syncthreads();
@@ -2144,6 +2159,10 @@ struct crop_pairs {
   uint2* d_reduce_chunks = nullptr;  // stream mode: (split tile, first slot)
   uint32_t n_reduce_chunks = 0;
   uint32_t nt = 0, nu = 0;  // tiles, units (either planner)
+  // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
+  uint32_t* topk_hist = nullptr;
+  unsigned long long* hi_list = nullptr;
+  unsigned long long* hi_n = nullptr;
   void* d_block = nullptr;  // one allocation carved into the small per-job arrays
   // stream mode (short rows): pair words per tile instead of entries
   bool stream_mode = false;
@@ -2801,6 +2820,9 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.out_n = (unsigned long long*)d_n_entries;
     C.slabs = J->d_slabs;
     C.tile_done = J->d_tile_done;
+    C.topk_hist = J->topk_hist;
+    C.hi_list = J->hi_list;
+    C.hi_n = J->hi_n;
     C.dbg = nullptr;
     if (getenv("CROP_DEBUG_KINDS")) {
       static unsigned long long* dbg = nullptr;
@@ -2926,6 +2948,32 @@ extern "C" int crop_pairs_phase_ms(const crop_pairs* J, float* out4) {
   CROP_CUDA(cudaEventElapsedTime(&out4[2], J->ev[2], J->ev[3]));
   CROP_CUDA(cudaEventElapsedTime(&out4[3], J->ev[4], J->ev[5]));
   return CROP_OK;
+}
+
+extern "C" int crop_pairs_set_topk(crop_pairs* J, uint32_t* hist, uint64_t* hi_list, uint64_t* hi_n,
+                                   uint64_t hi_cap) {
+  if (!J->stream_mode) {
+    crop_set_error(CROP_ECONFIG, "fused top-k buffers need a stream-mode job");
+    return CROP_ECONFIG;
+  }
+  if (hist && hi_cap < J->total_terms / kTopkExactBins + 1) {
+    crop_set_error(CROP_ERESOURCE, "hi_list holds %llu entries, need %llu", (unsigned long long)hi_cap,
+                   (unsigned long long)(J->total_terms / kTopkExactBins + 1));
+    return CROP_ERESOURCE;
+  }
+  J->topk_hist = hist;
+  J->hi_list = reinterpret_cast<unsigned long long*>(hi_list);
+  J->hi_n = reinterpret_cast<unsigned long long*>(hi_n);
+  return CROP_OK;
+}
+
+extern "C" int crop_topk_fused(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                               const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k,
+                               uint32_t* hist, const uint64_t* hi_list, const uint64_t* hi_n,
+                               uint64_t* out_idx, uint64_t* d_k_out, void* stream) {
+  return crop_topk_impl(row, col, count, d_n_entries, max_entries, k, out_idx, d_k_out,
+                        (cudaStream_t)stream, hist, reinterpret_cast<const unsigned long long*>(hi_list),
+                        reinterpret_cast<const unsigned long long*>(hi_n));
 }
 
 extern "C" int crop_pairs_mode(const crop_pairs* J, int* stream_mode) {

@@ -24,20 +24,20 @@ using namespace crop;
 
 namespace {
 
-constexpr uint32_t kExactBins = 2048;
-constexpr uint32_t kBins = kExactBins + 21 * 1024;  // 23552
+constexpr uint32_t kExactBins = kTopkExactBins;
+constexpr uint32_t kBins = kTopkBins;
 constexpr int kHistThreads = 1024;
 constexpr uint32_t kSmallCand = 8192;
 
-__device__ __forceinline__ uint32_t count_bin(uint32_t c) {
-  if (c < kExactBins) return c;
-  const uint32_t msb = 31 - __clz(c);  // >= 11
-  return kExactBins + (msb - 11) * 1024 + ((c >> (msb - 10)) & 1023);
-}
+__device__ __forceinline__ uint32_t count_bin(uint32_t c) { return topk_count_bin(c); }
 
 __global__ void __launch_bounds__(kHistThreads)
     k_topk_hist(const uint32_t* __restrict__ count, const uint64_t* __restrict__ d_n,
-                uint32_t* __restrict__ hist) {
+                uint32_t* __restrict__ hist, const unsigned long long* __restrict__ fast,
+                uint32_t skip_from) {
+  // fast: the fused high-count histogram already holds the k-th largest;
+  // skip_from: counts >= this are already in `hist` (fused by the count kernels)
+  if (fast && *fast) return;
   extern __shared__ uint32_t s_hist[];
   for (uint32_t b = threadIdx.x; b < kBins; b += blockDim.x) s_hist[b] = 0;
   __syncthreads();
@@ -47,7 +47,11 @@ __global__ void __launch_bounds__(kHistThreads)
   const uint64_t n_round = (n + 31) & ~31ull;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n_round;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = e < n ? count_bin(count[e]) : 0xFFFFFFFFu;
+    uint32_t b = 0xFFFFFFFFu;
+    if (e < n) {
+      const uint32_t c = count[e];
+      if (c < skip_from) b = count_bin(c);
+    }
     const uint32_t grp = __match_any_sync(0xffffffffu, b);
     if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (int)(threadIdx.x & 31))
       atomicAdd(&s_hist[b], (uint32_t)__popc(grp));
@@ -107,14 +111,40 @@ __global__ void __launch_bounds__(1024)
 
 __global__ void k_topk_compact(const uint32_t* __restrict__ count, const uint64_t* __restrict__ d_n,
                                unsigned long long* __restrict__ state, uint64_t* __restrict__ out_idx,
-                               uint64_t* __restrict__ cand) {
-  const uint64_t n = *d_n;
+                               uint64_t* __restrict__ cand, const unsigned long long* __restrict__ fast,
+                               const unsigned long long* __restrict__ hi_list,
+                               const unsigned long long* __restrict__ hi_n) {
+  // fast path: only the fused list of high-count entries can be selected
+  const bool f = fast && *fast;
+  const uint64_t n = f ? *hi_n : *d_n;
   const uint32_t B = (uint32_t)state[0];
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
-       e += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = f ? hi_list[x] : x;
     const uint32_t b = count_bin(count[e]);
     if (b > B) out_idx[atomicAdd(&state[3], 1ull)] = e;
     else if (b == B) cand[atomicAdd(&state[4], 1ull)] = e;
+  }
+}
+
+// Fused path decision: the count kernels added every count >= kExactBins to
+// `hist` and its entry index to hi_list; if those entries number >= k_eff,
+// the k-th largest is among them and neither the full histogram nor the full
+// compaction pass is needed.
+__global__ void k_topk_prep(const uint32_t* __restrict__ hist, const uint64_t* __restrict__ d_n,
+                            uint32_t k, unsigned long long* __restrict__ fast) {
+  __shared__ unsigned long long s_sum[32];
+  unsigned long long acc = 0;
+  for (uint32_t b = kExactBins + threadIdx.x; b < kBins; b += blockDim.x) acc += hist[b];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_sum[w];
+    const uint64_t n = *d_n;
+    const uint64_t keff = n < k ? n : k;
+    *fast = keff > 0 && t >= keff;
   }
 }
 
@@ -245,10 +275,13 @@ __global__ void k_rs_init(const unsigned long long* __restrict__ state, uint32_t
 
 }  // namespace
 
-extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
-                         const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k,
-                         uint64_t* out_idx, uint64_t* d_k_out, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+// Shared by crop_topk and crop_pairs_topk: fused_hist / hi_list / hi_n are
+// the high-count histogram and entry list filled by the counting kernels
+// (nullptr: plain path).
+int crop_topk_impl(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                   const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k,
+                   uint64_t* out_idx, uint64_t* d_k_out, cudaStream_t st, uint32_t* fused_hist,
+                   const unsigned long long* hi_list, const unsigned long long* hi_n) {
   if (int rc = crop_pool_setup()) return rc;
   uint32_t* hist = nullptr;
   unsigned long long* state = nullptr;
@@ -256,26 +289,37 @@ extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_
   uint32_t* rs = nullptr;
   uint32_t* rs_hist = nullptr;
   const uint64_t cand_cap = max_entries > 0 ? max_entries : 1;
+  const bool fused = fused_hist != nullptr;
   CROP_CUDA(cudaMallocAsync(&hist, kBins * 4, st));
-  CROP_CUDA(cudaMallocAsync(&state, 8 * 8, st));
+  // the fused histogram is copied, not updated: the entries stay selectable again
+  CROP_CUDA(cudaMallocAsync(&state, 8 * 8, st));  // [0..4] select state, [5] fused fast flag
   CROP_CUDA(cudaMallocAsync(&cand, cand_cap * 8, st));
   CROP_CUDA(cudaMallocAsync(&rs, 4 * 4, st));
   CROP_CUDA(cudaMallocAsync(&rs_hist, 256 * 4, st));
-  CROP_CUDA(cudaMemsetAsync(hist, 0, kBins * 4, st));
+  if (fused) CROP_CUDA(cudaMemcpyAsync(hist, fused_hist, kBins * 4, cudaMemcpyDeviceToDevice, st));
+  else CROP_CUDA(cudaMemsetAsync(hist, 0, kBins * 4, st));
   CROP_CUDA(cudaMemsetAsync(rs_hist, 0, 256 * 4, st));
+  unsigned long long* fast = fused ? state + 5 : nullptr;
+  if (fused) {
+    k_topk_prep<<<1, 1024, 0, st>>>(hist, d_n_entries, k, fast);
+    CROP_LAUNCH_CHECK();
+    crop_count_launches(1);
+  }
   uint64_t blocks = (max_entries + kHistThreads - 1) / kHistThreads;
   if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
   if (blocks == 0) blocks = 1;
   CROP_CUDA(cudaFuncSetAttribute(k_topk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(kBins * 4)));
-  k_topk_hist<<<(int)blocks, kHistThreads, kBins * 4, st>>>(count, d_n_entries, hist);
+  k_topk_hist<<<(int)blocks, kHistThreads, kBins * 4, st>>>(count, d_n_entries, hist, fast,
+                                                             fused ? kExactBins : 0xFFFFFFFFu);
   CROP_LAUNCH_CHECK();
   k_topk_thresh<<<1, 1024, 0, st>>>(hist, d_n_entries, k, state, d_k_out);
   CROP_LAUNCH_CHECK();
   uint64_t cblocks = (max_entries + 255) / 256;
   if (cblocks > 8 * kNumSMs) cblocks = 8 * kNumSMs;
   if (cblocks == 0) cblocks = 1;
-  k_topk_compact<<<(int)cblocks, 256, 0, st>>>(count, d_n_entries, state, out_idx, cand);
+  k_topk_compact<<<(int)cblocks, 256, 0, st>>>(count, d_n_entries, state, out_idx, cand, fast,
+                                               hi_list, hi_n);
   CROP_LAUNCH_CHECK();
   const size_t small_smem = kSmallCand * (sizeof(Key96) + 4);
   CROP_CUDA(cudaFuncSetAttribute(k_topk_finish_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -308,4 +352,11 @@ extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_
   cudaFreeAsync(rs, st);
   cudaFreeAsync(rs_hist, st);
   return CROP_OK;
+}
+
+extern "C" int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                         const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k,
+                         uint64_t* out_idx, uint64_t* d_k_out, void* stream) {
+  return crop_topk_impl(row, col, count, d_n_entries, max_entries, k, out_idx, d_k_out,
+                        (cudaStream_t)stream, nullptr, nullptr, nullptr);
 }

@@ -15,6 +15,8 @@ import torch
 from . import _native as nat
 from .errors import ConfigError, InputError
 
+TOPK_EXACT_BINS = 2048       # topk histogram: exact below, 2^-10 relative above
+TOPK_BINS = 2048 + 21 * 1024  # common.cuh kTopkBins
 U32_MASK = 0xFFFFFFFF
 
 
@@ -162,6 +164,9 @@ class DeviceEntries:
     n: int
     total_terms: int
     bucket: torch.Tensor | None = None
+    # fused top-k inputs filled by the counting kernels (stream-mode jobs):
+    # (hist int32[23552], hi_list int64[], hi_n int64[1])
+    topk_fused: tuple | None = None
 
     def weights_f64(self) -> torch.Tensor:
         if self.value is not None:
@@ -208,9 +213,20 @@ class PairCountJob:
         col = torch.empty(m, dtype=torch.int32, device=dev)
         cnt = torch.empty(m, dtype=torch.int32, device=dev)
         n_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        fused = None
+        if self.stream_mode:
+            hi_cap = self.total_terms // TOPK_EXACT_BINS + 1
+            hist = torch.zeros(TOPK_BINS, dtype=torch.int32, device=dev)
+            hi_n = torch.zeros(1, dtype=torch.int64, device=dev)
+            hi_list = torch.empty(hi_cap, dtype=torch.int64, device=dev)
+            nat.check(nat.load().crop_pairs_set_topk(self._h, nat.ptr(hist), nat.ptr(hi_list),
+                                                     nat.ptr(hi_n), hi_cap))
+            fused = (hist, hi_list, hi_n)
         nat.check(nat.load().crop_pairs_run(self._h, nat.ptr(row), nat.ptr(col), nat.ptr(cnt),
                                             nat.ptr(n_dev), nat.stream_ptr()))
-        ent = DeviceEntries(row, col, cnt, None, -1, self.total_terms)
+        if fused is not None:
+            nat.check(nat.load().crop_pairs_set_topk(self._h, None, None, None, 0))
+        ent = DeviceEntries(row, col, cnt, None, -1, self.total_terms, topk_fused=fused)
         ent.n_dev = n_dev
         if sync:
             ent.n = int(n_dev.item())
@@ -312,8 +328,14 @@ def topk_indices(ent: DeviceEntries, k: int, count: torch.Tensor | None = None) 
     n_dev = getattr(ent, "n_dev", None)
     if n_dev is None:
         n_dev = torch.tensor([ent.n], dtype=torch.int64, device=dev)
-    nat.call("crop_topk", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(cnt), nat.ptr(n_dev),
-             ent.row.shape[0], k, nat.ptr(out), nat.ptr(kout), nat.stream_ptr())
+    if count is None and ent.topk_fused is not None:
+        hist, hi_list, hi_n = ent.topk_fused
+        nat.call("crop_topk_fused", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(cnt), nat.ptr(n_dev),
+                 ent.row.shape[0], k, nat.ptr(hist), nat.ptr(hi_list), nat.ptr(hi_n), nat.ptr(out),
+                 nat.ptr(kout), nat.stream_ptr())
+    else:
+        nat.call("crop_topk", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(cnt), nat.ptr(n_dev),
+                 ent.row.shape[0], k, nat.ptr(out), nat.ptr(kout), nat.stream_ptr())
     return out[: int(kout.item())]
 
 

@@ -1688,6 +1688,7 @@ struct PlanOut {
   uint32_t n_tiles, n_units, n_split, n_reduce_chunks;
   uint32_t stream_mode, overflow, pad0, pad1;
   long long dbg[4];  // development: planner phase cycles
+  uint32_t words_known, pad2;  // per-tile word totals written (no word-count pass needed)
 };
 
 struct PlanArgs {
@@ -1702,6 +1703,7 @@ struct PlanArgs {
   uint2* reduce_chunks;
   uint32_t rc_cap;
   uint2* item_info;
+  unsigned long long* tile_words;  // per-tile stream words, when knowable from the statistics
   PlanOut* out;
 };
 
@@ -1798,6 +1800,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
   };
   // carries across chunks
+  __shared__ uint32_t s_has_win;
+  if (tid == 0) s_has_win = 0;
   unsigned long long c_p = 0, c_tiles = 0;
   long long c_bucket = -1, c_lt = -1, c_lrow0 = -1;
   for (uint32_t base = 0; base < n; base += kPlanChunk) {
@@ -1825,6 +1829,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
           rec = 1;
         } else if (!hfit) {
           rec = 2 | (uint32_t)((w + dense_cap - 1) / dense_cap) << 3;
+          s_has_win = 1;
         } else {
           const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
           const uint64_t xt = (uint64_t)((double)t * inv_ut) + 1;  // >= t * S / unit_terms
@@ -2097,8 +2102,18 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     }
   }
   (void)b_single;
+  // per-tile stream words from the statistics (unfiltered, no windows): an
+  // entry tile stores 2 words per row occurrence with a partner after it,
+  // a hash tile one word per term
+  const bool known = !P.filter && !s_has_win;
+  if (known)
+    for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+      const Tile& tl = P.tiles[t];
+      P.tile_words[t] = tl.mode == 2 ? 2 * (P.stats[tl.row0] >> 40) : tl.terms;
+    }
   stamp(5);
   if (tid == 0) {
+    P.out->words_known = known;
     P.out->pad0 = (uint32_t)(ck[0] / 1000);
     P.out->pad1 = (uint32_t)(ck[1] / 1000);
     P.out->dbg[0] = ck[2];
@@ -2159,6 +2174,7 @@ struct crop_pairs {
   uint2* d_reduce_chunks = nullptr;  // stream mode: (split tile, first slot)
   uint32_t n_reduce_chunks = 0;
   uint32_t nt = 0, nu = 0;  // tiles, units (either planner)
+  bool words_known = false;  // d_tile_words filled by the device planner
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
   unsigned long long* hi_list = nullptr;
@@ -2488,6 +2504,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       PA.reduce_chunks = reinterpret_cast<uint2*>(db + o_rc);
       PA.rc_cap = (uint32_t)rc_cap;
       PA.item_info = reinterpret_cast<uint2*>(db + o_item);
+      PA.tile_words = reinterpret_cast<unsigned long long*>(db + o_twords);
       PA.out = reinterpret_cast<PlanOut*>(db + o_out);
       JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
       JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2526,6 +2543,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         J->nt = ho->n_tiles;
         J->nu = ho->n_units;
         J->n_reduce_chunks = ho->n_reduce_chunks;
+        J->words_known = ho->words_known != 0;
         J->entry_cap = 0;
         J->d_tiles = PA.tiles;
         J->d_units = PA.units;
@@ -2777,8 +2795,8 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     R.chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, J->n_tx / (kNumSMs * 12)));
     const int64_t chunks = (J->n_tx + R.chunk_tx - 1) / R.chunk_tx;
     const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
-    CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
-    {
+    if (!J->words_known) {
+      CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
       auto kern = up ? k_stream_count<true> : k_stream_count<false>;
       const size_t smem = kOffBytes + (size_t)std::min(nt, kTileSmem) * 4;
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2850,7 +2868,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
         fprintf(stderr, "[k_count_stream] %-11s units %6llu words %10llu zero %7.1f count %8.1f emit %7.1f Mcyc\n",
                 names[k], h[5 * k + 3], h[5 * k + 4], h[5 * k] / 1e6, h[5 * k + 1] / 1e6, h[5 * k + 2] / 1e6);
     }
-    crop_count_launches(nrc ? 5 : 4);
+    crop_count_launches((J->words_known ? 3 : 4) + (nrc ? 1 : 0));
     return CROP_OK;
   }
   // route: one walk, staged per chunk, ranges claimed per touched tile

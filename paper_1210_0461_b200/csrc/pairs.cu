@@ -86,6 +86,17 @@ struct Unit {
   uint32_t tile, local;
 };
 
+// Output capacity of a tile: a tile emits at most one entry per counter or
+// key and at most one per term (terms are exact except for column windows --
+// single rows narrower than the row -- whose terms are only an estimate).
+__host__ __device__ __forceinline__ uint64_t tile_out_cap(const Tile& t, uint32_t hash_keys, uint32_t n,
+                                                          bool upper) {
+  const uint64_t room = t.mode == 1 ? hash_keys : t.width;
+  const bool window = t.mode == 0 && t.row1 - t.row0 == 1 && t.width < (upper ? n - 1 - t.row0 : n);
+  if (window) return room;
+  return t.terms < room ? t.terms : room;
+}
+
 __host__ __device__ __forceinline__ uint64_t tri_rowbase(uint64_t r, uint64_t row0, uint64_t n) {
   // sum_{x=row0}^{r-1} (n - 1 - x)
   uint64_t k = r - row0;
@@ -2036,7 +2047,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   unsigned long long a_slab = 0, a_split = 0, a_single = 0, a_rc = 0, a_cap = 0, a_units = 0;
   for (uint32_t t = tlo; t < thi; ++t) {
     const uint32_t nu_t = nu_of(t), wd = wd_of(t);
-    a_cap += wd != 0xFFFFFFFFu ? wd : kStreamHashSlots;
+    a_cap += tile_out_cap(P.tiles[t], kStreamHashCap, n, P.upper != 0);
     a_units += nu_t;
     if (nu_t > 1) {
       a_slab += nu_t;
@@ -2403,7 +2414,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   }
 
   uint64_t cap = 0;
-  for (auto& t : tiles) cap += t.mode == 0 ? t.width : hash_cap;
+  for (auto& t : tiles) cap += tile_out_cap(t, (uint32_t)hash_cap, n, upper);
   J->max_entries = cap;
 }
 

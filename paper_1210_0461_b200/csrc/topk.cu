@@ -288,7 +288,14 @@ int crop_topk_impl(const uint32_t* row, const uint32_t* col, const uint32_t* cou
   uint64_t* cand = nullptr;
   uint32_t* rs = nullptr;
   uint32_t* rs_hist = nullptr;
-  const uint64_t cand_cap = max_entries > 0 ? max_entries : 1;
+  uint64_t cand_cap = max_entries > 0 ? max_entries : 1;
+  if (cand_cap > (1ull << 27)) {
+    // large capacity bound: size the candidate list by the actual entry count
+    uint64_t h_n = 0;
+    CROP_CUDA(cudaMemcpyAsync(&h_n, d_n_entries, 8, cudaMemcpyDeviceToHost, st));
+    CROP_CUDA(cudaStreamSynchronize(st));
+    cand_cap = h_n > 0 ? h_n : 1;
+  }
   const bool fused = fused_hist != nullptr;
   CROP_CUDA(cudaMallocAsync(&hist, kBins * 4, st));
   // the fused histogram is copied, not updated: the entries stay selectable again

@@ -199,7 +199,7 @@ def run_ours(args, rank, world):
         ent = job.run(sync=False)
         p1.record()
         ent.n = int(ent.n_dev.item())
-        if ent.n > job.max_entries or job.overflowed():
+        if ent.n > ent.capacity or job.overflowed():
             raise RuntimeError("pair engine overflow")
         idx = kernels.topk_indices(ent, cfg.top_k)
         top = (ent.row[idx], ent.col[idx], ent.count[idx])

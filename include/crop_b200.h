@@ -110,6 +110,10 @@ int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
  * (one entry per (transaction, tile) run, counting re-reads the items).
  * CROP_FORCE_ENTRY_MODE=1 in the environment forces entry mode. */
 int crop_pairs_mode(const crop_pairs* job, int* stream_mode);
+/* Output arrays of the next runs hold `capacity` entries (<= max_entries;
+ * default max_entries). Entries past it are counted in *d_n_entries but not
+ * written: when *d_n_entries > capacity, run again with a larger capacity. */
+int crop_pairs_set_capacity(crop_pairs* job, uint64_t capacity);
 /* Stream mode only: caller-owned, zeroed buffers that the next crop_pairs_run
  * fills for a fused top-k -- hist uint32[23552] receives the histogram bins of
  * every output count >= 2048, hi_list (>= total_terms / 2048 + 1 entries) the

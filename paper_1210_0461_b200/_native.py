@@ -42,6 +42,7 @@ _SIGS = {
     "crop_pairs_phase_ms": (i32, [P, ctypes.POINTER(ctypes.c_float)]),
     "crop_pairs_overflowed": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_mode": (i32, [P, ctypes.POINTER(i32)]),
+    "crop_pairs_set_capacity": (i32, [P, u64]),
     "crop_pairs_set_topk": (i32, [P, P, P, P, u64]),
     "crop_topk_fused": (i32, [P, P, P, P, u64, u32, P, P, P, P, P, P]),
     "crop_pairs_destroy": (None, [P]),

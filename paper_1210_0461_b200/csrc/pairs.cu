@@ -402,6 +402,7 @@ struct CountArgs {
   uint32_t* out_col;
   uint32_t* out_count;
   unsigned long long* out_n;
+  uint64_t out_cap;  // output capacity (entries); claims beyond it are not written
   uint32_t* slabs;  // kHalf words (two interleaved u16 counters) per unit
   unsigned int* tile_done;
   unsigned long long* dbg;  // optional: per-kind [cycles count, cycles emit, units, entries]
@@ -908,7 +909,9 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
       if (threadIdx.x == 0) s_base = atomicAdd(A.out_n, (unsigned long long)total);
       __syncthreads();
       uint64_t pos = s_base + wbase;
-      for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+      // past the output capacity: claim only (the host sees n > capacity)
+      const bool fits = s_base + total <= A.out_cap;
+      for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += 32) {
         const uint32_t s = s0 + lane;
         uint32_t c = 0, i = 0, j = 0;
         if (s < s_hi) {
@@ -1290,6 +1293,7 @@ struct StreamCountArgs {
   uint32_t* out_col;
   uint32_t* out_count;
   unsigned long long* out_n;
+  uint64_t out_cap;  // output capacity (entries); claims beyond it are not written
   uint32_t* slabs;  // kStreamDenseCap words per unit of a split tile
   unsigned int* tile_done;
   unsigned long long* dbg;  // development only (CROP_DEBUG_KINDS): cycles per kind/phase
@@ -1546,7 +1550,9 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     if (threadIdx.x == 0) s_base = atomicAdd(A.out_n, (unsigned long long)total);
     __syncthreads();
     uint64_t pos = s_base + wbase;
-    for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+    // past the output capacity: claim only (the host sees n > capacity)
+    const bool fits = s_base + total <= A.out_cap;
+    for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += 32) {
       const uint32_t s = s0 + lane;
       uint32_t c = 0, i = 0, j = 0;
       if (s < s_hi) {
@@ -1626,9 +1632,10 @@ __global__ void __launch_bounds__(256) k_reduce_slabs(StreamCountArgs A, const u
     if (threadIdx.x == 0) s_base = total ? atomicAdd(A.out_n, (unsigned long long)total) : 0ull;
     __syncthreads();
     uint64_t o = s_base + excl;
+    const bool fits = s_base + total <= A.out_cap;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (s0 + k < T.width && c[k] != 0) {
+      if (fits && s0 + k < T.width && c[k] != 0) {
         uint32_t i, j;
         dense_slot_pair(T, s0 + k, A.n_items, A.upper != 0, i, j);
         A.out_row[o] = i;
@@ -2186,6 +2193,7 @@ struct crop_pairs {
   uint32_t n_reduce_chunks = 0;
   uint32_t nt = 0, nu = 0;  // tiles, units (either planner)
   bool words_known = false;  // d_tile_words filled by the device planner
+  uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
   unsigned long long* hi_list = nullptr;
@@ -2847,6 +2855,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.out_col = out_col;
     C.out_count = out_count;
     C.out_n = (unsigned long long*)d_n_entries;
+    C.out_cap = J->out_cap ? J->out_cap : J->max_entries;
     C.slabs = J->d_slabs;
     C.tile_done = J->d_tile_done;
     C.topk_hist = J->topk_hist;
@@ -2926,6 +2935,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     A.out_col = out_col;
     A.out_count = out_count;
     A.out_n = (unsigned long long*)d_n_entries;
+    A.out_cap = J->out_cap ? J->out_cap : J->max_entries;
     A.slabs = J->d_slabs;
     A.tile_done = J->d_tile_done;
     A.dbg = nullptr;
@@ -3003,6 +3013,11 @@ extern "C" int crop_topk_fused(const uint32_t* row, const uint32_t* col, const u
   return crop_topk_impl(row, col, count, d_n_entries, max_entries, k, out_idx, d_k_out,
                         (cudaStream_t)stream, hist, reinterpret_cast<const unsigned long long*>(hi_list),
                         reinterpret_cast<const unsigned long long*>(hi_n));
+}
+
+extern "C" int crop_pairs_set_capacity(crop_pairs* J, uint64_t capacity) {
+  J->out_cap = capacity < J->max_entries ? capacity : J->max_entries;
+  return CROP_OK;
 }
 
 extern "C" int crop_pairs_mode(const crop_pairs* J, int* stream_mode) {

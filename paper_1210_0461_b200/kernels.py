@@ -206,9 +206,15 @@ class PairCountJob:
         self.max_entries, self.total_terms = int(me.value), int(tt.value)
         self.n_tiles, self.n_units = int(nt.value), int(nu.value)
 
-    def run(self, sync: bool = True) -> DeviceEntries:
+    def run(self, sync: bool = True, capacity: int | None = None) -> DeviceEntries:
+        """Count; output arrays hold `capacity` entries (default: a guess of half
+        the terms, bounded by max_entries). With sync, an output that did not
+        fit is counted again with the full bound."""
         dev = self.dtx.offsets.device
-        m = max(self.max_entries, 1)
+        if capacity is None:
+            capacity = min(self.max_entries, self.total_terms // 2 + (1 << 20))
+        m = max(int(capacity), 1)
+        nat.check(nat.load().crop_pairs_set_capacity(self._h, m))
         row = torch.empty(m, dtype=torch.int32, device=dev)
         col = torch.empty(m, dtype=torch.int32, device=dev)
         cnt = torch.empty(m, dtype=torch.int32, device=dev)
@@ -228,10 +234,16 @@ class PairCountJob:
             nat.check(nat.load().crop_pairs_set_topk(self._h, None, None, None, 0))
         ent = DeviceEntries(row, col, cnt, None, -1, self.total_terms, topk_fused=fused)
         ent.n_dev = n_dev
+        ent.capacity = m
         if sync:
             ent.n = int(n_dev.item())
-            if ent.n > self.max_entries or self.overflowed():
-                raise InputError(f"pair engine overflow: {ent.n} > {self.max_entries}")
+            if ent.n > m:
+                if m >= self.max_entries:
+                    raise InputError(f"pair engine overflow: {ent.n} > {self.max_entries}")
+                del ent, row, col, cnt, fused
+                return self.run(True, self.max_entries)
+            if self.overflowed():
+                raise InputError("pair engine overflow: entry lists exceeded their bounds")
         return ent
 
     def set_timing(self, on: bool = True) -> None:

@@ -972,6 +972,15 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
 // columns) need no windows and no counter can wrap.
 constexpr uint32_t kStreamDenseCap = 57344;
 constexpr uint32_t kStreamHashSlots = 28672;
+
+// Stream-mode hash tiles size their table from their distinct-key bound
+// (load <= 1/2, multiple of 256 slots, at most kStreamHashSlots); the slot
+// count is kept in Tile::width. Small tiles then clear and compact little.
+__host__ __device__ __forceinline__ uint32_t stream_hash_slots(uint64_t key_bound) {
+  uint64_t s = (2 * key_bound + 255) & ~255ull;
+  if (s < 1024) s = 1024;
+  return (uint32_t)(s < kStreamHashSlots ? s : kStreamHashSlots);
+}
 constexpr uint32_t kStreamHashCap = 18432;
 constexpr size_t kStreamSmem = (size_t)kStreamDenseCap * 4 + 64;
 constexpr uint32_t kStreamMeanMax = 64;
@@ -1433,7 +1442,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     if (DBG) c0 = clock64();
     {
       uint4* t4 = reinterpret_cast<uint4*>(table);
-      const uint32_t n4 = dense ? (width + 3) / 4 : kStreamHashSlots / 2;
+      const uint32_t n4 = dense ? (width + 3) / 4 : width / 2;  // hash: width = slots
       const uint32_t f = dense ? 0u : kEmpty32;
       for (uint32_t s = threadIdx.x; s < n4; s += kCountThreads) t4[s] = make_uint4(f, f, f, f);
     }
@@ -1469,7 +1478,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
         unsigned long long v[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-          sl[k] = __umulhi(mix32(cur[k]), kStreamHashSlots);
+          sl[k] = __umulhi(mix32(cur[k]), width);
           v[k] = slot64[sl[k]];
         }
 #pragma unroll
@@ -1492,7 +1501,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
                 break;
               }
             }
-            if (++sk == kStreamHashSlots) sk = 0;
+            if (++sk == width) sk = 0;
             vk = slot64[sk];
           }
         }
@@ -1522,7 +1531,7 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     }
     // compaction: count occupied slots (4 per lane per step), one output
     // claim per unit, then emit
-    const uint32_t slots = dense ? width : kStreamHashSlots;
+    const uint32_t slots = width;  // counters, or hash slots
     auto count_of = [&](uint32_t s) -> uint32_t {
       if (dense) return table[s];
       const unsigned long long x = slot64[s];
@@ -2038,12 +2047,15 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   const bool cached = nt <= kPlanChunk;
   uint32_t* s_nu = s_dyn;
   uint32_t* s_wd = s_dyn + kPlanChunk;
-  if (cached)
-    for (uint32_t t = tid; t < nt; t += kPlanThreads) {
-      const Tile& tl = P.tiles[t];
+  for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+    Tile& tl = P.tiles[t];
+    // hash tiles: table size from the key bound (the row terms bound the keys)
+    if (tl.mode == 1) tl.width = stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap);
+    if (cached) {
       s_nu[t] = tl.n_units;
       s_wd[t] = tl.mode != 1 ? tl.width : 0xFFFFFFFFu;
     }
+  }
   __syncthreads();
   auto nu_of = [&](uint32_t t) { return cached ? s_nu[t] : P.tiles[t].n_units; };
   auto wd_of = [&](uint32_t t) {
@@ -2290,7 +2302,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     // stream mode, unfiltered: a single-row dense tile is counted from one
     // entry per row occurrence (its suffix is read from the items)
     if (dense && sm && !J->filter && row1 - row0 == 1) t.mode = 2;
-    t.width = dense ? (uint32_t)sw : 0;
+    t.width = dense ? (uint32_t)sw : (sm ? stream_hash_slots(sb < hash_cap ? sb : hash_cap) : 0);
     t.terms = st;
     t.n_units = dense ? units_for(st, so) : 1;
     const uint32_t id = (uint32_t)tiles.size();

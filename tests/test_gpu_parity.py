@@ -257,6 +257,23 @@ def test_interval_filter_matches_oracle_worker(kappa, workers, worker, count_mod
     assert int(got[2].sum()) == load
 
 
+def test_small_output_capacity_reruns():
+    """An output capacity below the distinct count is detected and re-run."""
+    cfg = workloads.CONFIGS["c2"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=20_000)
+    off, items = dtx.to_host()
+    job = kernels.PairCountJob(dtx, True, None)
+    try:
+        ent = job.run(capacity=1000)
+    finally:
+        job.close()
+    assert ent.n > 1000 and ent.row.shape[0] >= ent.n
+    g = _gpu_pairs(ent)
+    o = _oracle_pairs(off, items)
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)
+
+
 def test_mode_choice():
     """Short transactions (c2) count in stream mode, long ones (c5) in entry mode."""
     for name, n_tx, want in (("c2", 20_000, True), ("c5", 2_000, False)):

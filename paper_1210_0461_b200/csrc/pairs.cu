@@ -1346,8 +1346,8 @@ __device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint3
 // single-row tile. The suffixes of 32 entries are cut into quads (4
 // consecutive columns) and the quads flattened across the warp (boundary-mask
 // owner lookup, one per 32 quads = 128 columns); each lane loads and counts
-// its quad. The next batch's loads are issued before the previous batch's
-// shared-memory atomics. Blocks of 32 entries go round-robin over the warps;
+// its quad. Two quads' loads are in flight while an older quad is counted
+// (the path is bound by memory-level parallelism, and registers cap it). Blocks of 32 entries go round-robin over the warps;
 // the next block's entries are loaded ahead.
 __device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict__ items,
                                                      const uint2* __restrict__ ents, uint64_t e0,
@@ -1361,9 +1361,9 @@ __device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict_
   };
   uint2 nen = make_uint2(0u, 0u);
   if ((uint64_t)warp < nblk) nen = ld(warp);
-  uint32_t pj[Q];  // the previous quad's columns (kNone = none)
+  uint32_t pj[Q], qj[Q];  // the quads loaded two and one steps ago (kNone = none)
 #pragma unroll
-  for (int k = 0; k < Q; ++k) pj[k] = kNone;
+  for (int k = 0; k < Q; ++k) pj[k] = qj[k] = kNone;
   for (uint64_t blk = warp; blk < nblk; blk += kCountWarps) {
     const uint2 en = nen;
     if (blk + kCountWarps < nblk) nen = ld(blk + kCountWarps);
@@ -1383,17 +1383,22 @@ __device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict_
       uint32_t j[Q];
 #pragma unroll
       for (int k = 0; k < Q; ++k) j[k] = (tt < S && pos + k < e_end) ? __ldg(items + pos + k) : kNone;
-      // count the previous quad while this one's columns are in flight
+      // count the quad loaded two steps ago while the newer ones are in flight
 #pragma unroll
       for (int k = 0; k < Q; ++k)
         if (pj[k] != kNone) atomicAdd(&table[pj[k] - c0], 1u);
 #pragma unroll
-      for (int k = 0; k < Q; ++k) pj[k] = j[k];
+      for (int k = 0; k < Q; ++k) {
+        pj[k] = qj[k];
+        qj[k] = j[k];
+      }
     }
   }
 #pragma unroll
-  for (int k = 0; k < Q; ++k)
+  for (int k = 0; k < Q; ++k) {
     if (pj[k] != kNone) atomicAdd(&table[pj[k] - c0], 1u);
+    if (qj[k] != kNone) atomicAdd(&table[qj[k] - c0], 1u);
+  }
 }
 
 // Per unit: clear the table, count its words (block-cyclic 256-word blocks

@@ -1012,6 +1012,7 @@ struct StreamRouteArgs {
   unsigned long long* tile_cursor;  // B2: next free word per tile
   const unsigned long long* tile_base;  // B2: first word of each tile
   int chunk_tx;                     // transactions per chunk (<= kChunkTx)
+  uint32_t scat_ns;                 // k_stream_scatter: tiles with shared counters
   uint32_t* words;
 };
 
@@ -1282,6 +1283,153 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
     }
     __syncthreads();
     for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) s_cnt[s_touched[k]] = 0;
+  }
+}
+
+// Single-walk scatter (unfiltered jobs without column windows, i.e. when the
+// device planner knows every tile's word total): chunks are the transactions
+// whose first item lies in one band of kScatPark - maxlen + 1 positions, so
+// a chunk holds at most kScatPark positions. One walk takes, per row occurrence,
+// its rank in its tile's chunk range from a returning shared-memory atomic
+// and parks (tile, rank, n) in shared memory; after one claim per touched
+// tile the parked rows are scattered: an 8-byte entry per entry-tile row,
+// the suffix words for a hash / multi-row tile row.
+constexpr uint32_t kScatPark = 12288;   // parked rows (positions) per chunk
+constexpr uint32_t kScatMaxTx = 4096;   // transactions staged at once
+
+__global__ void k_chunk_bounds(const int64_t* __restrict__ offsets, int64_t n_tx, uint32_t n_chunks,
+                               uint32_t band, uint32_t* __restrict__ bounds) {
+  // bounds[c] = first transaction whose start position lies in band >= c
+  // (band = kScatPark - longest transaction + 1 positions)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= n_tx;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t prev = t > 0 ? offsets[t - 1] / band : -1;
+    const int64_t cur = t < n_tx ? offsets[t] / band : (int64_t)n_chunks;
+    for (int64_t c = prev + 1; c <= cur && c <= (int64_t)n_chunks; ++c) bounds[c] = (uint32_t)t;
+  }
+}
+
+template <bool UPPER>
+__global__ void __launch_bounds__(kPassThreads, 1)
+    k_stream_scatter(StreamRouteArgs A, const uint32_t* __restrict__ bounds, uint32_t n_chunks) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // kScatMaxTx + 1
+  uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);     // parked rows
+  uint32_t* s_rank = s_tile + kScatPark;
+  uint32_t* s_meta = s_rank + kScatPark;                                      // n | entry << 31
+  uint32_t* s_job = s_meta + kScatPark;                                       // per warp 128 words
+  uint32_t* s_misc = s_job + kPassThreads / 32 * 128;
+  const uint32_t ns = min(A.n_tiles, A.scat_ns);
+  const uint32_t ns2 = (ns + 1) & ~1u;
+  uint32_t* s_cnt = s_misc + 4;
+  uint16_t* s_touched = reinterpret_cast<uint16_t*>(s_cnt + ns2);
+  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
+  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint32_t tb0 = bounds[c], tb1 = bounds[c + 1];
+    for (uint32_t ta = tb0; ta < tb1; ta += kScatMaxTx) {
+      const int ntx = (int)min(kScatMaxTx, tb1 - ta);
+      __syncthreads();
+      if (threadIdx.x == 0) s_misc[0] = 0;
+      for (int t = threadIdx.x; t <= ntx; t += blockDim.x) s_off[t] = A.offsets[ta + t];
+      __syncthreads();
+      const int64_t g_lo = s_off[0];
+      const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
+      // walk: rank of every row occurrence in its tile's chunk range
+      walk_chunk<true>(s_off, ntx, A.items, A.item_info,
+                       [&](int64_t g, const Pos& q, uint32_t, uint2 tv) {
+        if (!q.valid) return;
+        const uint32_t x = (uint32_t)(g - g_lo);
+        uint32_t tile = kNone;
+        if (tv.x != kNone && (UPPER ? q.p + 1 < q.L : q.L > 0)) {
+          const uint32_t n = UPPER ? q.L - 1 - q.p : q.L;
+          const bool ent = (tv.x & kEntFlag) != 0;
+          tile = tv.x & kTileMask;
+          const uint32_t units = ent ? 2u : n;
+          uint32_t r;
+          if (tile < ns) {
+            r = atomicAdd(&s_cnt[tile], units);
+            if (r == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = (uint16_t)tile;
+          } else {
+            r = (uint32_t)atomicAdd(&A.tile_cursor[tile], (unsigned long long)units);
+            tile |= kWinFlag;  // rank is already absolute
+          }
+          s_rank[x] = r;
+          s_meta[x] = n | (ent ? 0x80000000u : 0u);
+        }
+        s_tile[x] = tile;
+      });
+      __syncthreads();
+      const uint32_t n_touch = s_misc[0];
+      for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) {
+        const uint32_t t = s_touched[k];
+        s_cnt[t] = (uint32_t)atomicAdd(&A.tile_cursor[t], (unsigned long long)s_cnt[t]);
+      }
+      __syncthreads();
+      // scatter the parked rows: each warp takes 32 positions at a time;
+      // entry rows store their 8-byte entry, word rows copy their suffixes
+      // flattened across the warp (one store instruction per 32 words)
+      {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint32_t* j_dst = s_job + warp * 128;
+        uint32_t* j_src = j_dst + 32;
+        uint32_t* j_b = j_src + 32;
+        uint32_t* j_n = j_b + 32;
+        for (uint32_t x0 = warp * 32; x0 < npos; x0 += kPassThreads) {
+          const uint32_t x = x0 + lane;
+          uint32_t tile = kNone, pos = 0, meta = 0;
+          if (x < npos) {
+            tile = s_tile[x];
+            if (tile != kNone) {
+              pos = (tile & kWinFlag) ? s_rank[x] : s_cnt[tile] + s_rank[x];
+              meta = s_meta[x];
+            }
+          }
+          const uint64_t g = (uint64_t)g_lo + x;
+          uint32_t first = (uint32_t)(g + 1);
+          if (!UPPER && tile != kNone) {
+            int lo = 0, hi = ntx;
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (s_off[mid] <= (int64_t)g) lo = mid;
+              else hi = mid;
+            }
+            first = (uint32_t)s_off[lo];
+          }
+          const bool ent = tile != kNone && (meta & 0x80000000u);
+          if (ent) *reinterpret_cast<uint2*>(A.words + pos) = make_uint2(first, meta & 0x7FFFFFFFu);
+          const uint32_t nw = (tile != kNone && !ent) ? meta : 0u;
+          const uint32_t wm = __ballot_sync(0xffffffffu, nw > 0);
+          if (!wm) continue;
+          // compact the word rows to the low lanes (the boundary-mask owner
+          // lookup needs every lane's length > 0)
+          if (nw) {
+            const int r = __popc(wm & ((1u << lane) - 1u));
+            j_dst[r] = pos;
+            j_src[r] = first;
+            j_b[r] = __ldg(&A.item_info[A.items[g]].y);
+            j_n[r] = nw;
+          }
+          __syncwarp();
+          const uint32_t my_n = lane < __popc(wm) ? j_n[lane] : 0u;
+          const uint32_t incl = warp_incl_scan(my_n);
+          const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+          const uint32_t excl = incl - my_n;
+          uint32_t ob = 0;
+          for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+            const uint32_t o = owner_step(incl, t0, ob);
+            const uint32_t t = t0 + lane;
+            const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o & 31);
+            if (t < S) {
+              const uint32_t loc = t - o_excl;
+              A.words[j_dst[o] + loc] = j_b[o] + A.items[j_src[o] + loc];
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) s_cnt[s_touched[k]] = 0;
+    }
   }
 }
 
@@ -2210,6 +2358,7 @@ struct crop_pairs {
   uint32_t n_reduce_chunks = 0;
   uint32_t nt = 0, nu = 0;  // tiles, units (either planner)
   bool words_known = false;  // d_tile_words filled by the device planner
+  uint32_t maxlen = 0;       // longest transaction (device planner path)
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
@@ -2580,6 +2729,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         J->nu = ho->n_units;
         J->n_reduce_chunks = ho->n_reduce_chunks;
         J->words_known = ho->words_known != 0;
+        J->maxlen = *h_ml;
         J->entry_cap = 0;
         J->d_tiles = PA.tiles;
         J->d_units = PA.units;
@@ -2843,7 +2993,26 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     k_scan_u64<<<1, 1024, 0, st>>>(J->d_tile_words, nt, J->d_tile_ebase, J->d_tile_cursor);
     CROP_LAUNCH_CHECK();
     mark(1);
-    {
+    if (J->words_known && J->maxlen <= kScatPark / 2) {
+      // single-walk scatter over position bands
+      const uint32_t band = kScatPark - J->maxlen + 1;
+      const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
+      uint32_t* bounds = nullptr;
+      CROP_CUDA(cudaMallocAsync(&bounds, (size_t)(n_chunks + 1) * 4, st));
+      k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
+          J->offsets, J->n_tx, n_chunks, band, bounds);
+      CROP_LAUNCH_CHECK();
+      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 12 + 16 + kPassThreads / 32 * 128 * 4;
+      const size_t budget = 227 * 1024 - fixed;
+      R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
+      const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
+      auto kern = up ? k_stream_scatter<true> : k_stream_scatter<false>;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
+      kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, bounds, n_chunks);
+      CROP_LAUNCH_CHECK();
+      cudaFreeAsync(bounds, st);
+      crop_count_launches(1);
+    } else {
       auto kern = up ? k_stream_write<true> : k_stream_write<false>;
       const size_t ns2 = (std::min(nt, kTileSmem) + 1) & ~1u;
       const size_t smem = kOffBytes + ns2 * 6 + 16;

@@ -1294,8 +1294,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
 // and parks (tile, rank, n) in shared memory; after one claim per touched
 // tile the parked rows are scattered: an 8-byte entry per entry-tile row,
 // the suffix words for a hash / multi-row tile row.
-constexpr uint32_t kScatPark = 12288;   // parked rows (positions) per chunk
-constexpr uint32_t kScatMaxTx = 4096;   // transactions staged at once
+constexpr uint32_t kScatPark = 10240;   // parked rows (positions) per chunk
+constexpr uint32_t kScatMaxTx = 2048;   // transactions staged at once
 
 __global__ void k_chunk_bounds(const int64_t* __restrict__ offsets, int64_t n_tx, uint32_t n_chunks,
                                uint32_t band, uint32_t* __restrict__ bounds) {
@@ -1317,7 +1317,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);     // parked rows
   uint32_t* s_rank = s_tile + kScatPark;
   uint32_t* s_meta = s_rank + kScatPark;                                      // n | entry << 31
-  uint32_t* s_job = s_meta + kScatPark;                                       // per warp 128 words
+  uint32_t* s_bp = s_meta + kScatPark;                                        // word rows: base
+  uint32_t* s_job = s_bp + kScatPark;                                         // per warp 128 words
   uint32_t* s_misc = s_job + kPassThreads / 32 * 128;
   const uint32_t ns = min(A.n_tiles, A.scat_ns);
   const uint32_t ns2 = (ns + 1) & ~1u;
@@ -1355,6 +1356,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
           }
           s_rank[x] = r;
           s_meta[x] = n | (ent ? 0x80000000u : 0u);
+          s_bp[x] = tv.y;
         }
         s_tile[x] = tile;
       });
@@ -1406,7 +1408,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const int r = __popc(wm & ((1u << lane) - 1u));
             j_dst[r] = pos;
             j_src[r] = first;
-            j_b[r] = __ldg(&A.item_info[A.items[g]].y);
+            j_b[r] = s_bp[x];
             j_n[r] = nw;
           }
           __syncwarp();
@@ -3002,7 +3004,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
       k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
           J->offsets, J->n_tx, n_chunks, band, bounds);
       CROP_LAUNCH_CHECK();
-      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 12 + 16 + kPassThreads / 32 * 128 * 4;
+      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 16 + 16 + kPassThreads / 32 * 128 * 4;
       const size_t budget = 227 * 1024 - fixed;
       R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
       const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;

@@ -1716,30 +1716,60 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     uint64_t pos = s_base + wbase;
     // past the output capacity: claim only (the host sees n > capacity)
     const bool fits = s_base + total <= A.out_cap;
-    for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += 32) {
-      const uint32_t s = s0 + lane;
-      uint32_t c = 0, i = 0, j = 0;
-      if (s < s_hi) {
-        c = count_of(s);
-        if (c) {
-          if (!dense) {
-            const uint32_t key = (uint32_t)(slot64[s] >> 32);
-            i = T.row0 + (key >> A.col_bits);
-            j = key & ((1u << A.col_bits) - 1u);
-          } else {
-            dense_slot_pair(T, s, n, A.upper != 0, i, j);
+    // emit: each lane takes 4 (dense) or 2 (hash) consecutive slots per step;
+    // a warp prefix sum places the lane's entries
+    constexpr int V = 4;
+    const uint32_t step = dense ? 32 * V : 64;
+    const bool single_row = dense && T.row1 - T.row0 == 1;
+    for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += step) {
+      uint32_t cv[V] = {0, 0, 0, 0}, kv[V] = {0, 0, 0, 0};
+      if (dense) {
+        const uint32_t s = s0 + V * lane;
+        if (s < s_hi) {
+          const uint4 c4 = *reinterpret_cast<const uint4*>(table + s);
+          cv[0] = c4.x;
+          cv[1] = s + 1 < s_hi ? c4.y : 0u;
+          cv[2] = s + 2 < s_hi ? c4.z : 0u;
+          cv[3] = s + 3 < s_hi ? c4.w : 0u;
+        }
+      } else {
+        const uint32_t s = s0 + 2 * lane;
+        if (s < s_hi) {
+          const ulonglong2 c2v = *reinterpret_cast<const ulonglong2*>(slot64 + s);
+          if (c2v.x != kEmpty64) {
+            cv[0] = (uint32_t)c2v.x;
+            kv[0] = (uint32_t)(c2v.x >> 32);
+          }
+          if (s + 1 < s_hi && c2v.y != kEmpty64) {
+            cv[1] = (uint32_t)c2v.y;
+            kv[1] = (uint32_t)(c2v.y >> 32);
           }
         }
       }
-      const uint32_t mk = __ballot_sync(0xffffffffu, c != 0);
-      if (c) {
-        const uint64_t o = pos + __popc(mk & ((1u << lane) - 1u));
+      const uint32_t cnt = (cv[0] != 0) + (cv[1] != 0) + (cv[2] != 0) + (cv[3] != 0);
+      const uint32_t incl = warp_incl_scan(cnt);
+      uint64_t o = pos + (incl - cnt);
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const uint32_t c = cv[q];
+        if (!c) continue;
+        uint32_t i, j;
+        if (!dense) {
+          i = T.row0 + (kv[q] >> A.col_bits);
+          j = kv[q] & ((1u << A.col_bits) - 1u);
+        } else if (single_row) {
+          i = T.row0;
+          j = s0 + V * lane + q + T.c0;
+        } else {
+          dense_slot_pair(T, s0 + V * lane + q, n, A.upper != 0, i, j);
+        }
         A.out_row[o] = i;
         A.out_col[o] = j;
         A.out_count[o] = c;
         note_high(A, c, o);
+        ++o;
       }
-      pos += __popc(mk);
+      pos += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncthreads();
     if (DBG && threadIdx.x == 0) {

@@ -103,7 +103,8 @@ int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32
  * routing, per-tile entry counts, -, count}. */
 int crop_pairs_set_timing(crop_pairs* job, int on);
 int crop_pairs_phase_ms(const crop_pairs* job, float* out4);
-/* 1 if the entry list overflowed its capacity (never expected; synchronises). */
+/* 1 if the entry list overflowed its capacity (entry mode only: never expected;
+ * synchronises). Stream-mode jobs report 0 without synchronising. */
 int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
 /* Counting mode chosen by crop_pairs_create: 1 = stream (one 32-bit word per
  * pair term routed to its tile's stream, coalesced counting), 0 = entry

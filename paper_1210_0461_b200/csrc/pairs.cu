@@ -3244,6 +3244,10 @@ extern "C" int crop_pairs_mode(const crop_pairs* J, int* stream_mode) {
 }
 
 extern "C" int crop_pairs_overflowed(const crop_pairs* J, int* overflowed) {
+  if (J->stream_mode) {  // stream ranges are exact (no capacity estimate to overflow)
+    *overflowed = 0;
+    return CROP_OK;
+  }
   uint32_t h = 0;
   CROP_CUDA(cudaMemcpyAsync(&h, J->d_overflow, 4, cudaMemcpyDeviceToHost, J->stream));
   CROP_CUDA(cudaStreamSynchronize(J->stream));

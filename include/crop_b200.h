@@ -204,6 +204,20 @@ int crop_gen_items(int64_t n_tx, uint64_t seed, uint32_t n_items, const uint32_t
                    const uint32_t* h_alias_idx, const int64_t* offsets, uint32_t* items,
                    void* stream);
 
+/* ---- input ingestion --------------------------- */
+/* Read a FIMI file (read_fimi, sparse.py:270-298: one transaction per line,
+ * blank lines skipped, items sorted and de-duplicated) on `threads` host
+ * threads (0: all) into CSR. Accepts the plain form only (ASCII decimal ids
+ * < 2^31, ASCII whitespace, '\n' / "\r\n" line ends); anything else returns
+ * CROP_EINPUT with *bad_line = the 1-based line, and the caller re-reads the
+ * file with the reference-exact reader (which raises ParseError). */
+typedef struct crop_fimi crop_fimi;
+int crop_fimi_parse(const char* path, int threads, crop_fimi** out, int64_t* n_tx, int64_t* nnz,
+                    uint32_t* max_item, int64_t* duplicates, int64_t* bad_line);
+/* Copy the parsed CSR into caller buffers: offsets[n_tx + 1], items[nnz]. */
+int crop_fimi_copy(const crop_fimi* parsed, int64_t* offsets, uint32_t* items);
+void crop_fimi_free(crop_fimi* parsed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,11 @@ _SIGS = {
     "crop_pairs_overflowed": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_mode": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_set_capacity": (i32, [P, u64]),
+    "crop_fimi_parse": (i32, [ctypes.c_char_p, i32, ctypes.POINTER(P), ctypes.POINTER(i64),
+                              ctypes.POINTER(i64), ctypes.POINTER(u32), ctypes.POINTER(i64),
+                              ctypes.POINTER(i64)]),
+    "crop_fimi_copy": (i32, [P, P, P]),
+    "crop_fimi_free": (None, [P]),
     "crop_pairs_set_topk": (i32, [P, P, P, P, u64]),
     "crop_topk_fused": (i32, [P, P, P, P, u64, u32, P, P, P, P, P, P]),
     "crop_pairs_destroy": (None, [P]),

@@ -17,6 +17,7 @@ the Python objects entirely.
 """
 
 import logging
+import os
 from typing import Callable, Iterable, Iterator, NamedTuple
 
 import numpy as np
@@ -398,6 +399,36 @@ def read_fimi(path) -> list[tuple[int, ...]]:
     if dups:
         logger.warning("%s: dropped %d duplicate items within transactions", path, dups)
     return out
+
+
+def read_fimi_csr(path, threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
+    """read_fimi into CSR (offsets int64, items uint32, max id or -1) with the
+    native multi-threaded reader; lines the native reader does not accept
+    (errors or unusual forms) are handed to the reference-exact read_fimi,
+    which raises the same ParseError / InputError as the reference."""
+    import ctypes
+
+    from . import _native as nat
+
+    lib = nat.load()
+    h = ctypes.c_void_p()
+    n_tx, nnz, dups, bad = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    mx = ctypes.c_uint32()
+    rc = lib.crop_fimi_parse(os.fsencode(str(path)), int(threads), ctypes.byref(h), ctypes.byref(n_tx),
+                             ctypes.byref(nnz), ctypes.byref(mx), ctypes.byref(dups), ctypes.byref(bad))
+    if rc != 0:
+        rows = read_fimi(path)
+        offsets, items = _csr_from_lists(rows)
+        return offsets, items.astype(np.uint32), (int(items.max()) if items.size else -1)
+    try:
+        offsets = np.empty(n_tx.value + 1, dtype=np.int64)
+        items = np.empty(nnz.value, dtype=np.uint32)
+        nat.check(lib.crop_fimi_copy(h, offsets.ctypes.data, items.ctypes.data))
+    finally:
+        lib.crop_fimi_free(h)
+    if dups.value:
+        logger.warning("%s: dropped %d duplicate items within transactions", path, dups.value)
+    return offsets, items, (int(mx.value) if nnz.value else -1)
 
 
 def write_fimi(path, transactions: Iterable[Iterable[int]]) -> None:

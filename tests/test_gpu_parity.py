@@ -257,6 +257,28 @@ def test_interval_filter_matches_oracle_worker(kappa, workers, worker, count_mod
     assert int(got[2].sum()) == load
 
 
+def test_mine_fimi_file_matches_oracle(tmp_path):
+    """crop.mine over a FIMI file (native reader -> GPU) equals the oracle."""
+    cfg = workloads.CONFIGS["c1"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=5000)
+    off, items = dtx.to_host()
+    path = tmp_path / "c1.dat"
+    with open(path, "w") as fh:
+        for k in range(off.shape[0] - 1):
+            fh.write(" ".join(str(x) for x in items[off[k]:off[k + 1]].tolist()) + "\n")
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
+                               cs_enabled=True, seed=0)
+    state, report = crop.mine(path, config)
+    h = crop.make_hashes(crop.HashConfig(cfg.kappa, config.instance_seeds()[0]))
+    recs, loads = oracle.run(oracle.Stream(off, items), h.coefficients(), cfg.kappa, cfg.workers,
+                             upper_only=True, cs=True)
+    assert report.rows[0] == loads.tolist()
+    g = _gpu_pairs(state.device_result.entries)
+    o = oracle.sorted_pairs(recs.row, recs.col, recs.count)
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)
+
+
 def test_small_output_capacity_reruns():
     """An output capacity below the distinct count is detected and re-run."""
     cfg = workloads.CONFIGS["c2"]

@@ -401,6 +401,20 @@ def read_fimi(path) -> list[tuple[int, ...]]:
     return out
 
 
+def _host_array(n: int, dtype) -> np.ndarray:
+    """A numpy array in pinned (page-locked) memory when a GPU is present, so
+    the one host -> device copy of the stream runs at full DMA speed."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            tdt = {np.int64: torch.int64, np.uint32: torch.int32}[dtype]
+            return torch.empty(max(n, 1), dtype=tdt, pin_memory=True).numpy().view(dtype)[:n]
+    except Exception:
+        pass
+    return np.empty(n, dtype=dtype)
+
+
 def read_fimi_csr(path, threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
     """read_fimi into CSR (offsets int64, items uint32, max id or -1) with the
     native multi-threaded reader; lines the native reader does not accept
@@ -421,8 +435,8 @@ def read_fimi_csr(path, threads: int = 0) -> tuple[np.ndarray, np.ndarray, int]:
         offsets, items = _csr_from_lists(rows)
         return offsets, items.astype(np.uint32), (int(items.max()) if items.size else -1)
     try:
-        offsets = np.empty(n_tx.value + 1, dtype=np.int64)
-        items = np.empty(nnz.value, dtype=np.uint32)
+        offsets = _host_array(n_tx.value + 1, np.int64)
+        items = _host_array(nnz.value, np.uint32)
         nat.check(lib.crop_fimi_copy(h, offsets.ctypes.data, items.ctypes.data))
     finally:
         lib.crop_fimi_free(h)

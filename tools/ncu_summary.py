@@ -29,9 +29,11 @@ for r in rows[2:]:
         v = float(d[m].replace(",", ""))
         u = units[h.index(m)]
         if k == "ms":
-            v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(u, 1.0)
+            v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+                  "second": 1e3, "s": 1e3}.get(u, 1.0)
         if k.startswith("dram"):
-            v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1.0)
+            v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6,
+                  "GB": 1e9}.get(u, 1.0)
         rec[k] = v
     kernels.setdefault(name, []).append(rec)
 summary = {}

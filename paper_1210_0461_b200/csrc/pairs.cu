@@ -1297,6 +1297,21 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
 constexpr uint32_t kScatPark = 10240;   // parked rows (positions) per chunk
 constexpr uint32_t kScatMaxTx = 2048;   // transactions staged at once
 
+// 16-bit copy of the items (ids < 2^16) for the suffix gathers of the count
+// kernel; runs on a side stream while the single-CTA planner runs.
+__global__ void k_items16(const uint32_t* __restrict__ items, int64_t nnz, uint16_t* __restrict__ out) {
+  const int64_t n4 = nnz / 4;
+  const uint4* in4 = reinterpret_cast<const uint4*>(items);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n4; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcs(in4 + k);
+    const uint2 o = make_uint2(v.x | (v.y << 16), v.z | (v.w << 16));
+    reinterpret_cast<uint2*>(out)[k] = o;
+  }
+  for (int64_t k = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = (uint16_t)items[k];
+}
+
 __global__ void k_chunk_bounds(const int64_t* __restrict__ offsets, int64_t n_tx, uint32_t n_chunks,
                                uint32_t band, uint32_t* __restrict__ bounds) {
   // bounds[c] = first transaction whose start position lies in band >= c
@@ -1445,6 +1460,7 @@ struct StreamCountArgs {
   const unsigned long long* tile_words;
   const uint32_t* words;
   const uint32_t* items;
+  const uint16_t* items16;  // nullable: 16-bit copy written by k_stream_scatter
   unsigned int* unit_counter;
   uint32_t n_items, col_bits;
   int upper;
@@ -1499,7 +1515,8 @@ __device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint3
 // its quad. Two quads' loads are in flight while an older quad is counted
 // (the path is bound by memory-level parallelism, and registers cap it). Blocks of 32 entries go round-robin over the warps;
 // the next block's entries are loaded ahead.
-__device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict__ items,
+template <typename ItemT>
+__device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ items,
                                                      const uint2* __restrict__ ents, uint64_t e0,
                                                      uint64_t e1, uint32_t* table, uint32_t c0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1532,7 +1549,7 @@ __device__ __forceinline__ void count_suffix_entries(const uint32_t* __restrict_
       const uint32_t pos = Q * tt + d;
       uint32_t j[Q];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) j[k] = (tt < S && pos + k < e_end) ? __ldg(items + pos + k) : kNone;
+      for (int k = 0; k < Q; ++k) j[k] = (tt < S && pos + k < e_end) ? (uint32_t)__ldg(items + pos + k) : kNone;
       // count the quad loaded two steps ago while the newer ones are in flight
 #pragma unroll
       for (int k = 0; k < Q; ++k)
@@ -1604,8 +1621,12 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     __syncthreads();
     if (DBG) c1 = clock64();
     if (ents) {
-      count_suffix_entries(A.items, reinterpret_cast<const uint2*>(A.words + wb), w0, w1,
-                           table, T.c0);
+      // 16-bit copy of the items when ids fit (half the gathered bytes; an
+      // 80 MB copy of c2's items stays L2-resident)
+      if (A.items16)
+        count_suffix_entries(A.items16, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
+      else
+        count_suffix_entries(A.items, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
     } else {
     const uint32_t nb = (uint32_t)((w1 - w0 + BW - 1) / BW);
     const uint32_t* wp = A.words + wb + w0 + lane;
@@ -2391,6 +2412,8 @@ struct crop_pairs {
   uint32_t nt = 0, nu = 0;  // tiles, units (either planner)
   bool words_known = false;  // d_tile_words filled by the device planner
   uint32_t maxlen = 0;       // longest transaction (device planner path)
+  uint16_t* d_items16 = nullptr;  // 16-bit item copy (ids < 2^16), made on the side stream
+  cudaEvent_t ev_items16 = nullptr;
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
@@ -2439,7 +2462,8 @@ static inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 static void free_job(crop_pairs* j) {
   for (cudaEvent_t& e : j->ev)
     if (e) cudaEventDestroy(e);
-  void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words};
+  if (j->ev_items16) cudaEventDestroy(j->ev_items16);
+  void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words, j->d_items16};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
@@ -2762,6 +2786,20 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         J->n_reduce_chunks = ho->n_reduce_chunks;
         J->words_known = ho->words_known != 0;
         J->maxlen = *h_ml;
+        // 16-bit copy of the items for the count kernel's suffix gathers, on a
+        // side stream: it overlaps the write phase (latency-bound, little DRAM)
+        if (n_items <= 65536 && J->nnz > 0 && !getenv("CROP_NO_ITEMS16")) {
+          static cudaStream_t side = nullptr;
+          if (!side) JCUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+          JCUDA(cudaEventCreateWithFlags(&J->ev_items16, cudaEventDisableTiming));
+          JCUDA(cudaEventRecord(J->ev_items16, st));  // inputs ready (stream order)
+          JCUDA(cudaStreamWaitEvent(side, J->ev_items16, 0));
+          JCUDA(cudaMallocAsync(&J->d_items16, (size_t)J->nnz * 2, side));
+          k_items16<<<kNumSMs * 4, 256, 0, side>>>(items, J->nnz, J->d_items16);
+          JCUDA(cudaGetLastError());
+          crop_count_launches(1);
+          JCUDA(cudaEventRecord(J->ev_items16, side));
+        }
         J->entry_cap = 0;
         J->d_tiles = PA.tiles;
         J->d_units = PA.units;
@@ -3065,6 +3103,11 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.tile_words = J->d_tile_words;
     C.words = J->d_words;
     C.items = J->items;
+    C.items16 = nullptr;
+    if (J->d_items16) {
+      CROP_CUDA(cudaStreamWaitEvent(st, J->ev_items16, 0));
+      C.items16 = J->d_items16;
+    }
     C.unit_counter = J->d_unit_counter;
     C.n_items = J->n_items;
     C.col_bits = J->col_bits;

@@ -383,7 +383,7 @@ class SketchState:
 
         mask = self._candidate_mask()
         if d.integer:
-            count = e.count
+            count = None  # the raw counts: the fused top-k inputs apply
             if mask is not None:
                 count = torch.where(mask, e.count[: e.n], torch.zeros_like(e.count[: e.n]))
             idx = topk_indices(e, k, count=count)

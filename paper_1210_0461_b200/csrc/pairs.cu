@@ -971,7 +971,16 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(CountArgs A) {
 // model. The table is 57,344 u32 counters (224 KB), so c2's rows (50K
 // columns) need no windows and no counter can wrap.
 constexpr uint32_t kStreamDenseCap = 57344;
-constexpr uint32_t kStreamHashSlots = 28672;
+// Counting tables use half an SM's shared memory so two units run per SM
+// (one unit's clearing and compaction overlap the other's counting): dense
+// tables hold 16-bit counters, slot s in word s mod kSHalf, half s / kSHalf
+// (so neighbouring columns never share a word), <= 65,535 row occurrences
+// per unit keep them from wrapping; hash tables 14,336 64-bit slots.
+constexpr uint32_t kSHalf = kStreamDenseCap / 2;  // 28672 words = 112 KB
+constexpr int kSCThreads = 512;                     // count kernel threads (2 CTAs / SM)
+constexpr int kSCWarps = kSCThreads / 32;
+constexpr uint32_t kStreamUnitOcc = 65535;
+constexpr uint32_t kStreamHashSlots = 14336;
 
 // Stream-mode hash tiles size their table from their distinct-key bound
 // (load <= 1/2, multiple of 256 slots, at most kStreamHashSlots); the slot
@@ -981,8 +990,13 @@ __host__ __device__ __forceinline__ uint32_t stream_hash_slots(uint64_t key_boun
   if (s < 1024) s = 1024;
   return (uint32_t)(s < kStreamHashSlots ? s : kStreamHashSlots);
 }
-constexpr uint32_t kStreamHashCap = 18432;
-constexpr size_t kStreamSmem = (size_t)kStreamDenseCap * 4 + 64;
+constexpr uint32_t kStreamHashCap = 9216;
+constexpr size_t kStreamSmem = (size_t)kSHalf * 4 + 64;
+
+__device__ __forceinline__ void bump_half(uint32_t* t32, uint32_t slot) {
+  const uint32_t hi = slot >= kSHalf;
+  atomicAdd(&t32[slot - hi * kSHalf], 1u << (hi << 4));
+}
 constexpr uint32_t kStreamMeanMax = 64;
 
 // per-row constant of the word of (i, j) in tile T: dense word = base + j,
@@ -1531,9 +1545,10 @@ __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ i
   uint32_t pj[Q], qj[Q];  // the quads loaded two and one steps ago (kNone = none)
 #pragma unroll
   for (int k = 0; k < Q; ++k) pj[k] = qj[k] = kNone;
-  for (uint64_t blk = warp; blk < nblk; blk += kCountWarps) {
+  const uint32_t nwarps = blockDim.x >> 5;
+  for (uint64_t blk = warp; blk < nblk; blk += nwarps) {
     const uint2 en = nen;
-    if (blk + kCountWarps < nblk) nen = ld(blk + kCountWarps);
+    if (blk + nwarps < nblk) nen = ld(blk + nwarps);
     const uint32_t nq = (en.y + Q - 1) / Q;
     const uint32_t incl = warp_incl_scan(nq);
     const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
@@ -1553,7 +1568,7 @@ __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ i
       // count the quad loaded two steps ago while the newer ones are in flight
 #pragma unroll
       for (int k = 0; k < Q; ++k)
-        if (pj[k] != kNone) atomicAdd(&table[pj[k] - c0], 1u);
+        if (pj[k] != kNone) bump_half(table, pj[k] - c0);
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
         pj[k] = qj[k];
@@ -1563,8 +1578,8 @@ __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ i
   }
 #pragma unroll
   for (int k = 0; k < Q; ++k) {
-    if (pj[k] != kNone) atomicAdd(&table[pj[k] - c0], 1u);
-    if (qj[k] != kNone) atomicAdd(&table[qj[k] - c0], 1u);
+    if (pj[k] != kNone) bump_half(table, pj[k] - c0);
+    if (qj[k] != kNone) bump_half(table, qj[k] - c0);
   }
 }
 
@@ -1580,11 +1595,11 @@ __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ i
 constexpr unsigned long long kEmpty64 = ~0ull;
 
 template <bool DBG>
-__global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountArgs A) {
+__global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense counters
   unsigned long long* slot64 = reinterpret_cast<unsigned long long*>(smem);  // hash slots
-  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + (size_t)kStreamDenseCap * 4);
+  uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + (size_t)kSHalf * 4);
   __shared__ uint32_t s_warp[33];
   __shared__ unsigned long long s_base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1612,11 +1627,12 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     const uint32_t width = T.width;
     long long c0 = 0, c1 = 0, c2 = 0;
     if (DBG) c0 = clock64();
+    const uint32_t dwords = width < kSHalf ? width : kSHalf;  // dense: table words in use
     {
       uint4* t4 = reinterpret_cast<uint4*>(table);
-      const uint32_t n4 = dense ? (width + 3) / 4 : width / 2;  // hash: width = slots
+      const uint32_t n4 = dense ? (dwords + 3) / 4 : width / 2;  // hash: width = slots
       const uint32_t f = dense ? 0u : kEmpty32;
-      for (uint32_t s = threadIdx.x; s < n4; s += kCountThreads) t4[s] = make_uint4(f, f, f, f);
+      for (uint32_t s = threadIdx.x; s < n4; s += kSCThreads) t4[s] = make_uint4(f, f, f, f);
     }
     __syncthreads();
     if (DBG) c1 = clock64();
@@ -1643,12 +1659,12 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     };
     uint32_t cur[D], nxt[D];
     if ((uint32_t)warp < nb) fetch(warp, cur);
-    for (uint32_t blk = warp; blk < nb; blk += kCountWarps) {
-      if (blk + kCountWarps < nb) fetch(blk + kCountWarps, nxt);
+    for (uint32_t blk = warp; blk < nb; blk += kSCWarps) {
+      if (blk + kSCWarps < nb) fetch(blk + kSCWarps, nxt);
       if (dense) {
 #pragma unroll
         for (int k = 0; k < D; ++k)
-          if (cur[k] != kEmpty32) atomicAdd(&table[cur[k]], 1u);
+          if (cur[k] != kEmpty32) bump_half(table, cur[k]);
       } else {
         uint32_t sl[D];
         unsigned long long v[D];
@@ -1699,28 +1715,27 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
       }
     }
     if (dense && T.n_units > 1) {
-      uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * (uint64_t)kStreamDenseCap);
+      uint4* dst = reinterpret_cast<uint4*>(A.slabs + (T.slab_base + unit.local) * (uint64_t)kSHalf);
       const uint4* src = reinterpret_cast<const uint4*>(table);
-      for (uint32_t s = threadIdx.x; s < (width + 3) / 4; s += kCountThreads) __stcg(dst + s, src[s]);
+      for (uint32_t s = threadIdx.x; s < (dwords + 3) / 4; s += kSCThreads) __stcg(dst + s, src[s]);
       __syncthreads();
       continue;
     }
-    // compaction: count occupied slots (4 per lane per step), one output
-    // claim per unit, then emit
-    const uint32_t slots = width;  // counters, or hash slots
-    auto count_of = [&](uint32_t s) -> uint32_t {
-      if (dense) return table[s];
-      const unsigned long long x = slot64[s];
-      return x == kEmpty64 ? 0u : (uint32_t)x;
-    };
-    const uint32_t per_w = (((slots + kCountWarps - 1) / kCountWarps) + 127) & ~127u;
-    const uint32_t s_lo = min(slots, warp * per_w), s_hi = min(slots, s_lo + per_w);
+    // compaction: count occupied counters, one output claim per unit, emit.
+    // Dense: 4 table words per lane per step, each holding slots w and
+    // w + kSHalf; hash: 2 slots per lane per step.
+    const uint32_t span = dense ? dwords : width;
+    const uint32_t per_w = (((span + kSCWarps - 1) / kSCWarps) + 127) & ~127u;
+    const uint32_t s_lo = min(span, warp * per_w), s_hi = min(span, s_lo + per_w);
     uint32_t mine = 0;
     if (dense) {
       for (uint32_t s = s_lo + 4 * lane; s < s_hi; s += 128) {
         const uint4 c4 = *reinterpret_cast<const uint4*>(table + s);  // table padded to 4
-        mine += (c4.x != 0) + (s + 1 < s_hi && c4.y != 0) + (s + 2 < s_hi && c4.z != 0) +
-                (s + 3 < s_hi && c4.w != 0);
+        const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (s + q < s_hi)
+            mine += ((cw[q] & 0xFFFFu) != 0) + ((cw[q] >> 16) != 0 && s + q + kSHalf < width);
       }
     } else {
       for (uint32_t s = s_lo + 2 * lane; s < s_hi; s += 64) {
@@ -1737,21 +1752,20 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
     uint64_t pos = s_base + wbase;
     // past the output capacity: claim only (the host sees n > capacity)
     const bool fits = s_base + total <= A.out_cap;
-    // emit: each lane takes 4 (dense) or 2 (hash) consecutive slots per step;
-    // a warp prefix sum places the lane's entries
-    constexpr int V = 4;
-    const uint32_t step = dense ? 32 * V : 64;
     const bool single_row = dense && T.row1 - T.row0 == 1;
-    for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += step) {
-      uint32_t cv[V] = {0, 0, 0, 0}, kv[V] = {0, 0, 0, 0};
+    for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += dense ? 128 : 64) {
+      uint32_t cv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kv[2] = {0, 0};
       if (dense) {
-        const uint32_t s = s0 + V * lane;
+        const uint32_t s = s0 + 4 * lane;
         if (s < s_hi) {
           const uint4 c4 = *reinterpret_cast<const uint4*>(table + s);
-          cv[0] = c4.x;
-          cv[1] = s + 1 < s_hi ? c4.y : 0u;
-          cv[2] = s + 2 < s_hi ? c4.z : 0u;
-          cv[3] = s + 3 < s_hi ? c4.w : 0u;
+          const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (s + q < s_hi) {
+              cv[q] = cw[q] & 0xFFFFu;
+              cv[4 + q] = s + q + kSHalf < width ? cw[q] >> 16 : 0u;
+            }
         }
       } else {
         const uint32_t s = s0 + 2 * lane;
@@ -1767,22 +1781,27 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
           }
         }
       }
-      const uint32_t cnt = (cv[0] != 0) + (cv[1] != 0) + (cv[2] != 0) + (cv[3] != 0);
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cnt += cv[q] != 0;
       const uint32_t incl = warp_incl_scan(cnt);
       uint64_t o = pos + (incl - cnt);
 #pragma unroll
-      for (int q = 0; q < V; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const uint32_t c = cv[q];
         if (!c) continue;
         uint32_t i, j;
         if (!dense) {
-          i = T.row0 + (kv[q] >> A.col_bits);
-          j = kv[q] & ((1u << A.col_bits) - 1u);
-        } else if (single_row) {
-          i = T.row0;
-          j = s0 + V * lane + q + T.c0;
+          i = T.row0 + (kv[q & 1] >> A.col_bits);
+          j = kv[q & 1] & ((1u << A.col_bits) - 1u);
         } else {
-          dense_slot_pair(T, s0 + V * lane + q, n, A.upper != 0, i, j);
+          const uint32_t slot = s0 + 4 * lane + (q & 3) + (q >= 4 ? kSHalf : 0u);
+          if (single_row) {
+            i = T.row0;
+            j = slot + T.c0;
+          } else {
+            dense_slot_pair(T, slot, n, A.upper != 0, i, j);
+          }
         }
         A.out_row[o] = i;
         A.out_col[o] = j;
@@ -1806,42 +1825,36 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count_stream(StreamCountAr
 constexpr uint32_t kReduceSlots = 2048;
 __global__ void __launch_bounds__(256) k_reduce_slabs(StreamCountArgs A, const uint2* __restrict__ chunks,
                                                       uint32_t n_chunks) {
+  // chunk = (split tile, first table word): each thread owns 8 words = 16
+  // slots (w and w + kSHalf) and sums them over the tile's unit slabs
   __shared__ uint32_t s_warp[33];
   __shared__ unsigned long long s_base;
-  const int lane = threadIdx.x & 31;
   for (uint32_t ci = blockIdx.x; ci < n_chunks; ci += gridDim.x) {
     const uint2 ch = chunks[ci];
     const Tile T = A.tiles[ch.x];
-    const uint32_t s0 = ch.y + threadIdx.x * 8;
+    const uint32_t w0 = ch.y + threadIdx.x * 8;
     const uint32_t nu = T.n_units;
-    const uint32_t* base = A.slabs + (uint64_t)T.slab_base * kStreamDenseCap + s0;
-    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (s0 < T.width) {
-      uint32_t v = 0;
-      for (; v + 4 <= nu; v += 4) {
-        uint4 x[8];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4* p = reinterpret_cast<const uint4*>(base + (uint64_t)(v + q) * kStreamDenseCap);
-          x[2 * q] = __ldcs(p);
-          x[2 * q + 1] = __ldcs(p + 1);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int h = (q & 1) * 4;
-          c[h] += x[q].x; c[h + 1] += x[q].y; c[h + 2] += x[q].z; c[h + 3] += x[q].w;
-        }
-      }
-      for (; v < nu; ++v) {
-        const uint4* p = reinterpret_cast<const uint4*>(base + (uint64_t)v * kStreamDenseCap);
+    const uint32_t dwords = T.width < kSHalf ? T.width : kSHalf;
+    const uint32_t* base = A.slabs + (uint64_t)T.slab_base * kSHalf + w0;
+    uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0}, hi[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (w0 < dwords) {
+      for (uint32_t v = 0; v < nu; ++v) {
+        const uint4* p = reinterpret_cast<const uint4*>(base + (uint64_t)v * kSHalf);
         const uint4 a = __ldcs(p), b = __ldcs(p + 1);
-        c[0] += a.x; c[1] += a.y; c[2] += a.z; c[3] += a.w;
-        c[4] += b.x; c[5] += b.y; c[6] += b.z; c[7] += b.w;
+        const uint32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          lo[k] += x[k] & 0xFFFFu;
+          hi[k] += x[k] >> 16;
+        }
       }
     }
     uint32_t mine = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mine += (s0 + k < T.width && c[k] != 0);
+    for (int k = 0; k < 8; ++k) {
+      if (w0 + k >= dwords) break;
+      mine += (lo[k] != 0) + (hi[k] != 0 && w0 + k + kSHalf < T.width);
+    }
     uint32_t total;
     const uint32_t excl = block_excl_scan(mine, s_warp, total);
     if (threadIdx.x == 0) s_base = total ? atomicAdd(A.out_n, (unsigned long long)total) : 0ull;
@@ -1849,18 +1862,21 @@ __global__ void __launch_bounds__(256) k_reduce_slabs(StreamCountArgs A, const u
     uint64_t o = s_base + excl;
     const bool fits = s_base + total <= A.out_cap;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (fits && s0 + k < T.width && c[k] != 0) {
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t w = w0 + (k & 7);
+      const uint32_t slot = w + (k >= 8 ? kSHalf : 0u);
+      const uint32_t c = k >= 8 ? hi[k & 7] : lo[k & 7];
+      if (fits && w < dwords && slot < T.width && c != 0) {
         uint32_t i, j;
-        dense_slot_pair(T, s0 + k, A.n_items, A.upper != 0, i, j);
+        dense_slot_pair(T, slot, A.n_items, A.upper != 0, i, j);
         A.out_row[o] = i;
         A.out_col[o] = j;
-        A.out_count[o] = c[k];
-        note_high(A, c[k], o);
+        A.out_count[o] = c;
+        note_high(A, c, o);
         ++o;
       }
+    }
     __syncthreads();
-    (void)lane;
   }
 }
 
@@ -2028,8 +2044,12 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   const double inv_step = 1.0 / (double)step;
   auto bucket = [inv_step](unsigned long long p) { return (long long)((double)p * inv_step); };
   const uint64_t dense_cap = kStreamDenseCap, hash_cap = kStreamHashCap;
-  auto units_of = [&](uint64_t t) -> uint32_t {
-    const uint64_t u = (t + unit_terms - 1) / unit_terms;
+  // units: by terms for balance, and <= kStreamUnitOcc row occurrences each
+  // (16-bit dense counters)
+  auto units_of = [&](uint64_t t, uint64_t occ) -> uint32_t {
+    uint64_t u = (t + unit_terms - 1) / unit_terms;
+    const uint64_t uo = (occ + kStreamUnitOcc - 1) / kStreamUnitOcc;
+    if (uo > u) u = uo;
     return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
   };
   // carries across chunks
@@ -2139,7 +2159,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
             tl.c0 = P.upper ? i + 1 : 0;
             tl.mode = P.filter ? 0 : 2;
             tl.width = P.upper ? n - 1 - i : n;
-            tl.n_units = units_of(t);
+            tl.n_units = units_of(t, P.stats[i] >> 40);
           } else {
             tl.mode = 1;
             tl.n_units = 1;
@@ -2162,7 +2182,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
             tl.nwin = q == 0 ? nwin : 0;
             tl.width = tl.c1 - tl.c0;
             tl.terms = t / nwin + 1;
-            tl.n_units = units_of(tl.terms);
+            tl.n_units = units_of(tl.terms, P.stats[i] >> 40);
             P.tiles[id + q] = tl;
           }
           P.item_info[i] = make_uint2(id | kWinFlag, 0u);
@@ -2277,7 +2297,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     if (nu_t > 1) {
       a_slab += nu_t;
       a_split += 1;
-      a_rc += (wd + kReduceSlots - 1) / kReduceSlots;
+      a_rc += ((wd < kSHalf ? wd : kSHalf) + kReduceSlots - 1) / kReduceSlots;
     } else {
       a_single += 1;
     }
@@ -2306,7 +2326,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
         P.tiles[t].slab_base = sb;
         sb += nu_t;
         P.split[sp++] = t;
-        for (uint32_t c0 = 0; c0 < width; c0 += kReduceSlots) P.reduce_chunks[rc++] = make_uint2(t, c0);
+        const uint32_t dw = width < kSHalf ? width : kSHalf;
+        for (uint32_t c0 = 0; c0 < dw; c0 += kReduceSlots) P.reduce_chunks[rc++] = make_uint2(t, c0);
       }
     }
   }
@@ -2480,7 +2501,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   // stream mode: u32 counters (57,344 per tile)
   const uint64_t dense_cap = sm ? kStreamDenseCap : kDenseCap;
   const uint64_t hash_cap = sm ? kStreamHashCap : kHashCap;
-  const uint64_t occ_cap = sm ? ~0ull : (uint64_t)kUnitEntries;
+  const uint64_t occ_cap = sm ? (uint64_t)kStreamUnitOcc : (uint64_t)kUnitEntries;
   const bool upper = J->upper != 0;
   const uint64_t T = J->total_terms;
   const uint64_t unit_terms = std::max<uint64_t>(1ull << 16, T / ((uint64_t)kNumSMs * 8));
@@ -2816,7 +2837,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         J->d_unit_counter = reinterpret_cast<unsigned int*>(db + o_misc + 8);
         J->d_overflow = reinterpret_cast<uint32_t*>(db + o_misc + 16);
         if (J->n_slabs)
-          JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kStreamDenseCap * 4, st));
+          JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kSHalf * 4, st));
         JCUDA(cudaMallocAsync(&J->d_words, (J->total_terms + 2 * ho->occ_sum + 2 * (uint64_t)J->nt + 2) * 4, st));
         *job = J;
         return CROP_OK;
@@ -2884,7 +2905,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
     // reduce chunks (stream mode): (split tile, first slot)
     uint32_t nrc = 0;
     if (sm)
-      for (uint32_t t : J->split) nrc += (J->tiles[t].width + kReduceSlots - 1) / kReduceSlots;
+      for (uint32_t t : J->split) nrc += (std::min(J->tiles[t].width, kSHalf) + kReduceSlots - 1) / kReduceSlots;
     J->n_reduce_chunks = nrc;
     // one device block: [uploaded part | device-only part]
     const size_t o_tiles = 0;
@@ -2924,7 +2945,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       uint2* rcs = reinterpret_cast<uint2*>(hb + o_rc);
       uint32_t k = 0;
       for (uint32_t t : J->split)
-        for (uint32_t c0 = 0; c0 < J->tiles[t].width; c0 += kReduceSlots) rcs[k++] = make_uint2(t, c0);
+        for (uint32_t c0 = 0; c0 < std::min(J->tiles[t].width, kSHalf); c0 += kReduceSlots) rcs[k++] = make_uint2(t, c0);
       for (uint32_t t = 0; t < nt; ++t) h_base[t] = 0;
     } else {
       // entry capacity per tile: a row occurrence with a partner after it
@@ -2981,7 +3002,7 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       JCUDA(cudaEventRecord(g_pinned.done, st));
     }
     if (J->n_slabs)
-      JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)(sm ? kStreamDenseCap : kHalf) * 4, st));
+      JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)(sm ? kSHalf : kHalf) * 4, st));
     // words: <= one per term, or two per entry row occurrence, plus the even rounding per tile
     if (sm) JCUDA(cudaMallocAsync(&J->d_words, (J->total_terms + 2 * occ_sum + 2 * (uint64_t)nt + 2) * 4, st));
     else JCUDA(cudaMallocAsync(&J->d_entries, std::max<uint64_t>(1, J->entry_cap) * sizeof(uint2), st));
@@ -3132,7 +3153,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     auto kcs = C.dbg ? k_count_stream<true> : k_count_stream<false>;
     CROP_CUDA(cudaFuncSetAttribute(kcs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     mark(4);
-    kcs<<<std::min<int>(kNumSMs, (int)J->nu), kCountThreads, kStreamSmem, st>>>(C);
+    kcs<<<std::min<int>(2 * kNumSMs, (int)J->nu), kSCThreads, kStreamSmem, st>>>(C);
     CROP_LAUNCH_CHECK();
     const uint32_t nrc = J->n_reduce_chunks;
     if (nrc) {

@@ -1027,6 +1027,7 @@ struct StreamRouteArgs {
   const unsigned long long* tile_base;  // B2: first word of each tile
   int chunk_tx;                     // transactions per chunk (<= kChunkTx)
   uint32_t scat_ns;                 // k_stream_scatter: tiles with shared counters
+  int packed_filter;                // k_stream_scatter: bucket-filter the word rows' pairs
   uint32_t* words;
 };
 
@@ -1326,6 +1327,17 @@ __global__ void k_items16(const uint32_t* __restrict__ items, int64_t nnz, uint1
     out[k] = (uint16_t)items[k];
 }
 
+// Filtered jobs (multi-GPU bucket intervals): the items packed with their
+// column hash, item | h_col(item) << 16 (ids and kappa < 2^16), so the
+// count kernel tests bucket ownership of a pair without a table gather.
+__global__ void k_items_cls(const uint32_t* __restrict__ items, int64_t nnz,
+                            const uint32_t* __restrict__ h_col, uint32_t* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t it = __ldcs(items + k);
+    out[k] = it | (h_col[it] << 16);
+  }
+}
+
 __global__ void k_chunk_bounds(const int64_t* __restrict__ offsets, int64_t n_tx, uint32_t n_chunks,
                                uint32_t band, uint32_t* __restrict__ bounds) {
   // bounds[c] = first transaction whose start position lies in band >= c
@@ -1438,10 +1450,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             j_dst[r] = pos;
             j_src[r] = first;
             j_b[r] = s_bp[x];
-            j_n[r] = nw;
+            j_n[r] = nw | (A.packed_filter ? A.h_row[A.items[g]] << 16 : 0u);
           }
           __syncwarp();
-          const uint32_t my_n = lane < __popc(wm) ? j_n[lane] : 0u;
+          const uint32_t my_n = lane < __popc(wm) ? (j_n[lane] & 0xFFFFu) : 0u;  // n < 2^16 (maxlen)
           const uint32_t incl = warp_incl_scan(my_n);
           const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
           const uint32_t excl = incl - my_n;
@@ -1452,7 +1464,15 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o & 31);
             if (t < S) {
               const uint32_t loc = t - o_excl;
-              A.words[j_dst[o] + loc] = j_b[o] + A.items[j_src[o] + loc];
+              const uint32_t j = A.items[j_src[o] + loc];
+              uint32_t w = j_b[o] + j;
+              if (A.packed_filter) {
+                // pairs of other GPUs' buckets keep their place as empty words
+                uint32_t b = (j_n[o] >> 16) + A.h_col[j];
+                if (b >= A.kappa) b -= A.kappa;
+                if (b < A.start || b >= A.stop) w = kEmpty32;
+              }
+              A.words[j_dst[o] + loc] = w;
             }
           }
           __syncwarp();
@@ -1474,7 +1494,10 @@ struct StreamCountArgs {
   const unsigned long long* tile_words;
   const uint32_t* words;
   const uint32_t* items;
-  const uint16_t* items16;  // nullable: 16-bit copy written by k_stream_scatter
+  const uint16_t* items16;  // nullable: 16-bit copy of the items
+  const uint32_t* items_cls;  // nullable (filtered jobs): item | h_col << 16
+  const uint32_t* h_row;
+  uint32_t kappa, start, stop;
   unsigned int* unit_counter;
   uint32_t n_items, col_bits;
   int upper;
@@ -1529,10 +1552,20 @@ __device__ __forceinline__ void dense_slot_pair(const Tile& T, uint32_t s, uint3
 // its quad. Two quads' loads are in flight while an older quad is counted
 // (the path is bound by memory-level parallelism, and registers cap it). Blocks of 32 entries go round-robin over the warps;
 // the next block's entries are loaded ahead.
-template <typename ItemT>
+struct OwnFilter {  // packed items (item | h_col << 16): own pair iff (hr + h_col) mod kappa in [start, stop)
+  uint32_t hr, kappa, start, stop;
+  __device__ __forceinline__ bool own(uint32_t v) const {
+    uint32_t b = hr + (v >> 16);
+    if (b >= kappa) b -= kappa;
+    return b >= start && b < stop;
+  }
+};
+
+template <bool FILT, typename ItemT>
 __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ items,
                                                      const uint2* __restrict__ ents, uint64_t e0,
-                                                     uint64_t e1, uint32_t* table, uint32_t c0) {
+                                                     uint64_t e1, uint32_t* table, uint32_t c0,
+                                                     OwnFilter F = OwnFilter{}) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int Q = 4;
   const uint64_t nblk = (e1 - e0 + 31) / 32;
@@ -1564,7 +1597,10 @@ __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ i
       const uint32_t pos = Q * tt + d;
       uint32_t j[Q];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) j[k] = (tt < S && pos + k < e_end) ? (uint32_t)__ldg(items + pos + k) : kNone;
+      for (int k = 0; k < Q; ++k) {
+        j[k] = (tt < S && pos + k < e_end) ? (uint32_t)__ldg(items + pos + k) : kNone;
+        if (FILT && j[k] != kNone) j[k] = F.own(j[k]) ? (j[k] & 0xFFFFu) : kNone;
+      }
       // count the quad loaded two steps ago while the newer ones are in flight
 #pragma unroll
       for (int k = 0; k < Q; ++k)
@@ -1639,10 +1675,15 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
     if (ents) {
       // 16-bit copy of the items when ids fit (half the gathered bytes; an
       // 80 MB copy of c2's items stays L2-resident)
-      if (A.items16)
-        count_suffix_entries(A.items16, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
-      else
-        count_suffix_entries(A.items, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
+      if (A.items_cls) {
+        const OwnFilter F{A.h_row[T.row0], A.kappa, A.start, A.stop};
+        count_suffix_entries<true>(A.items_cls, reinterpret_cast<const uint2*>(A.words + wb), w0, w1,
+                                   table, T.c0, F);
+      } else if (A.items16) {
+        count_suffix_entries<false>(A.items16, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
+      } else {
+        count_suffix_entries<false>(A.items, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
+      }
     } else {
     const uint32_t nb = (uint32_t)((w1 - w0 + BW - 1) / BW);
     const uint32_t* wp = A.words + wb + w0 + lane;
@@ -2434,8 +2475,10 @@ struct crop_pairs {
   bool words_known = false;  // d_tile_words filled by the device planner
   uint32_t maxlen = 0;       // longest transaction (device planner path)
   uint16_t* d_items16 = nullptr;  // 16-bit item copy (ids < 2^16), made on the side stream
+  uint32_t* d_items_cls = nullptr;  // filtered jobs: item | h_col << 16 (side stream)
   cudaEvent_t ev_items16 = nullptr;
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
+  bool packed_filter = false;  // bucket filter applied on packed items (see k_items_cls)
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
   unsigned long long* hi_list = nullptr;
@@ -2484,7 +2527,8 @@ static void free_job(crop_pairs* j) {
   for (cudaEvent_t& e : j->ev)
     if (e) cudaEventDestroy(e);
   if (j->ev_items16) cudaEventDestroy(j->ev_items16);
-  void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words, j->d_items16};
+  void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words, j->d_items16,
+                  j->d_items_cls};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
@@ -2756,7 +2800,12 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       PA.n = n_items;
       PA.col_bits = J->col_bits;
       PA.upper = upper_only;
-      PA.filter = J->filter;
+      // filtered jobs whose ids and kappa fit 16 bits are planned like whole
+      // jobs: the bucket test moves into the scatter (words) and the count
+      // kernel (entries), on the packed items
+      J->packed_filter = J->filter && n_items <= 65536 && J->iv.kappa <= 65536 &&
+                         !getenv("CROP_NO_PACKED_FILTER");
+      PA.filter = J->filter && !J->packed_filter;
       PA.force = force;
       PA.tiles = reinterpret_cast<Tile*>(db + o_tiles);
       PA.tile_cap = (uint32_t)tile_cap;
@@ -2809,7 +2858,18 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
         J->maxlen = *h_ml;
         // 16-bit copy of the items for the count kernel's suffix gathers, on a
         // side stream: it overlaps the write phase (latency-bound, little DRAM)
-        if (n_items <= 65536 && J->nnz > 0 && !getenv("CROP_NO_ITEMS16")) {
+        if (J->packed_filter && J->nnz > 0) {
+          static cudaStream_t side2 = nullptr;
+          if (!side2) JCUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+          JCUDA(cudaEventCreateWithFlags(&J->ev_items16, cudaEventDisableTiming));
+          JCUDA(cudaEventRecord(J->ev_items16, st));
+          JCUDA(cudaStreamWaitEvent(side2, J->ev_items16, 0));
+          JCUDA(cudaMallocAsync(&J->d_items_cls, (size_t)J->nnz * 4, side2));
+          k_items_cls<<<kNumSMs * 4, 256, 0, side2>>>(items, J->nnz, J->iv.h_col, J->d_items_cls);
+          JCUDA(cudaGetLastError());
+          crop_count_launches(1);
+          JCUDA(cudaEventRecord(J->ev_items16, side2));
+        } else if (n_items <= 65536 && J->nnz > 0 && !getenv("CROP_NO_ITEMS16")) {
           static cudaStream_t side = nullptr;
           if (!side) JCUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
           JCUDA(cudaEventCreateWithFlags(&J->ev_items16, cudaEventDisableTiming));
@@ -3084,6 +3144,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     k_scan_u64<<<1, 1024, 0, st>>>(J->d_tile_words, nt, J->d_tile_ebase, J->d_tile_cursor);
     CROP_LAUNCH_CHECK();
     mark(1);
+    R.packed_filter = J->packed_filter ? 1 : 0;
     if (J->words_known && J->maxlen <= kScatPark / 2) {
       // single-walk scatter over position bands
       const uint32_t band = kScatPark - J->maxlen + 1;
@@ -3125,10 +3186,16 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.words = J->d_words;
     C.items = J->items;
     C.items16 = nullptr;
-    if (J->d_items16) {
+    C.items_cls = nullptr;
+    if (J->d_items16 || J->d_items_cls) {
       CROP_CUDA(cudaStreamWaitEvent(st, J->ev_items16, 0));
       C.items16 = J->d_items16;
+      C.items_cls = J->d_items_cls;
     }
+    C.h_row = J->iv.h_row;
+    C.kappa = J->iv.kappa;
+    C.start = J->iv.start;
+    C.stop = J->iv.stop;
     C.unit_counter = J->d_unit_counter;
     C.n_items = J->n_items;
     C.col_bits = J->col_bits;

@@ -6,7 +6,7 @@
 A step is one pass of the hot path over the whole synthetic workload of the
 configuration (default c2 = BASELINE.json configs[1], the 1-GPU exact pair
 count): per-item term scan + tile plan, routing, shared-memory counting of
-every pair term (i < j) of the GPU's bucket interval, and the top-k select.
+every pair term (i < j) of the GPU's tile share, and the top-k select.
 Inputs are resident in HBM; L2 is flushed (1 GiB write) before every timed
 step. `value` = all terms of the workload / (max over ranks of the summed
 per-step CUDA-event time). `e2e` runs the public API (`crop.run` +
@@ -18,7 +18,8 @@ C oracle (the reference algorithm restated, oracle/crop_oracle.c) on a
 bounded prefix, shared-nothing threads on the host cores.
 
 Under torchrun (N > 1) rank 0 generates the workload and broadcasts it once
-over NCCL; rank r counts the buckets split(kappa, N)[r] (no communication);
+over NCCL; every rank plans the same tiles and counts its 1/N share of them
+by terms (no communication; the shards are disjoint and cover the job);
 local top-k candidates are all-gathered and merged on rank 0.
 """
 
@@ -180,13 +181,11 @@ def run_ours(args, rank, world):
     config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
                                cs_enabled=False, seed=0)
     hasher = crop.make_hashes(crop.HashConfig(cfg.kappa, config.instance_seeds()[0]))
-    if world > cfg.kappa:
-        raise SystemExit(f"{world} GPUs > kappa={cfg.kappa} buckets")
-    asg = crop.WorkerAssignment.split(cfg.kappa, world)[rank]
     tables = kernels.hash_tables(hasher, cfg.n_items)
+    # rank r counts its 1/N share of the planned tiles (all buckets); the
+    # shards are disjoint and cover the job (crop_pairs_create_sharded)
     interval = None
-    if world > 1:
-        interval = kernels.interval_struct(cfg.kappa, asg.start, asg.stop, *tables)
+    shard = (rank, world)
     flush = torch.empty(1 << 28, dtype=torch.int32, device=dev)  # 1 GiB > 126 MB L2
 
     def step():
@@ -194,7 +193,7 @@ def run_ours(args, rank, world):
         # the job (per-item term scan) to the last counting kernel
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         p0.record()
-        job = kernels.PairCountJob(dtx, True, interval, keep=tables)
+        job = kernels.PairCountJob(dtx, True, interval, keep=tables, shard=shard)
         job.set_timing(True)
         ent = job.run(sync=False)
         p1.record()
@@ -266,7 +265,7 @@ def run_ours(args, rank, world):
     # the last counting kernel, host planning gap included). Own terms = terms
     # of this rank's buckets = the sum of its output counts.
     if world > 1:
-        job = kernels.PairCountJob(dtx, True, interval, keep=tables)
+        job = kernels.PairCountJob(dtx, True, interval, keep=tables, shard=shard)
         ent = job.run()
         own_terms = int(ent.weights_f64().sum().item())
         job.close()
@@ -309,9 +308,10 @@ def run_ours(args, rank, world):
             "data": "synthetic: seeded Zipf transactions (SURVEY.md §8d, data seed = config no.)",
             "config": {"workload": cfg.name, "n_tx": cfg.n_tx, "n_items": cfg.n_items,
                        "zipf_s": cfg.zipf_s, "length": list(cfg.length), "kappa": cfg.kappa,
-                       "buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})", "top_k": cfg.top_k,
+                       "sharding": f"tiles split by terms over {world} GPU(s), all {cfg.kappa} buckets",
+                       "top_k": cfg.top_k,
                        "terms": total_terms_all, "entries": own_entries if world == 1 else None,
-                       "tiles": stats[2], "units": stats[3], "parallelism": f"buckets{world}",
+                       "tiles": stats[2], "units": stats[3], "parallelism": f"tiles{world}",
                        "l2": "flushed (1 GiB write) before every timed step",
                        "broadcast_s": round(bcast_s, 4)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -92,6 +92,17 @@ typedef struct {
 int crop_pairs_create(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
                       uint32_t n_items, int upper_only, const crop_interval* interval,
                       void* stream, crop_pairs** job);
+/* Tile sharding across ranks (one GPU each): every rank plans the same tiles
+ * and keeps those whose term prefix falls in its 1/shard_world share (a
+ * split row's windows stay together), so the union of the ranks' outputs is
+ * the whole job's output, each pair on exactly one rank. The work, not the
+ * buckets, is what is split: bucket loads come from the entries
+ * (crop_entry_bucket_stats) and are summed across ranks. shard_world = 1 is
+ * crop_pairs_create. */
+int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                              uint32_t n_items, int upper_only, const crop_interval* interval,
+                              uint32_t shard_rank, uint32_t shard_world, void* stream,
+                              crop_pairs** job);
 /* host-side plan facts: output capacity, total terms (all buckets), tiles */
 int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* total_terms,
                     uint64_t* n_tiles, uint64_t* n_units);

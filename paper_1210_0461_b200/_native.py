@@ -35,6 +35,8 @@ _SIGS = {
     "crop_outer_bucket_loads": (i32, [P, P, P, P, i64, P, P, u32, i32, P, P]),
     "crop_pairs_create": (i32, [P, P, i64, u32, i32, ctypes.POINTER(Interval), P,
                                 ctypes.POINTER(P)]),
+    "crop_pairs_create_sharded": (i32, [P, P, i64, u32, i32, ctypes.POINTER(Interval), u32, u32, P,
+                                        ctypes.POINTER(P)]),
     "crop_pairs_info": (i32, [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
                               ctypes.POINTER(u64)]),
     "crop_pairs_run": (i32, [P, P, P, P, P, P]),

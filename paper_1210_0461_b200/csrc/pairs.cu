@@ -86,6 +86,15 @@ struct Unit {
   uint32_t tile, local;
 };
 
+// Counting-kernel cost of a tile for balancing tile shards across ranks, in
+// units of ~half a cycle (measured per-kind rates): 0.8 cycles
+// per word of a dense tile, ~5.5 per word of a hash tile, ~1.5 per table slot
+// cleared and compacted per unit.
+__host__ __device__ __forceinline__ uint64_t tile_cost(const Tile& t, uint32_t hash_room) {
+  const uint64_t room = t.mode == 1 ? hash_room : t.width;
+  return t.terms * (t.mode == 1 ? 11ull : 2ull) + 3ull * room * (t.n_units ? t.n_units : 1);
+}
+
 // Output capacity of a tile: a tile emits at most one entry per counter or
 // key and at most one per term (terms are exact except for column windows --
 // single rows narrower than the row -- whose terms are only an estimate).
@@ -1350,7 +1359,7 @@ __global__ void k_chunk_bounds(const int64_t* __restrict__ offsets, int64_t n_tx
   }
 }
 
-template <bool UPPER>
+template <bool UPPER, bool PF>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_stream_scatter(StreamRouteArgs A, const uint32_t* __restrict__ bounds, uint32_t n_chunks) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1450,10 +1459,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             j_dst[r] = pos;
             j_src[r] = first;
             j_b[r] = s_bp[x];
-            j_n[r] = nw | (A.packed_filter ? A.h_row[A.items[g]] << 16 : 0u);
+            j_n[r] = PF ? (nw | A.h_row[A.items[g]] << 16) : nw;
           }
           __syncwarp();
-          const uint32_t my_n = lane < __popc(wm) ? (j_n[lane] & 0xFFFFu) : 0u;  // n < 2^16 (maxlen)
+          const uint32_t my_n = lane < __popc(wm) ? (PF ? (j_n[lane] & 0xFFFFu) : j_n[lane]) : 0u;  // n < 2^16
           const uint32_t incl = warp_incl_scan(my_n);
           const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
           const uint32_t excl = incl - my_n;
@@ -1466,7 +1475,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
               const uint32_t loc = t - o_excl;
               const uint32_t j = A.items[j_src[o] + loc];
               uint32_t w = j_b[o] + j;
-              if (A.packed_filter) {
+              if (PF) {
                 // pairs of other GPUs' buckets keep their place as empty words
                 uint32_t b = (j_n[o] >> 16) + A.h_col[j];
                 if (b >= A.kappa) b -= A.kappa;
@@ -1495,9 +1504,6 @@ struct StreamCountArgs {
   const uint32_t* words;
   const uint32_t* items;
   const uint16_t* items16;  // nullable: 16-bit copy of the items
-  const uint32_t* items_cls;  // nullable (filtered jobs): item | h_col << 16
-  const uint32_t* h_row;
-  uint32_t kappa, start, stop;
   unsigned int* unit_counter;
   uint32_t n_items, col_bits;
   int upper;
@@ -1514,6 +1520,10 @@ struct StreamCountArgs {
   uint32_t* topk_hist;
   unsigned long long* hi_list;
   unsigned long long* hi_n;
+  // filtered jobs (packed bucket test, see k_items_cls)
+  const uint32_t* items_cls;  // nullable: item | h_col << 16
+  const uint32_t* h_row;
+  uint32_t kappa, start, stop;
 };
 
 // Record an emitted entry for the fused top-k (high counts only: rare).
@@ -1630,7 +1640,7 @@ __device__ __forceinline__ void count_suffix_entries(const ItemT* __restrict__ i
 // lane is issued at once.
 constexpr unsigned long long kEmpty64 = ~0ull;
 
-template <bool DBG>
+template <bool DBG, bool FILT>
 __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* table = reinterpret_cast<uint32_t*>(smem);  // dense counters
@@ -1675,7 +1685,7 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
     if (ents) {
       // 16-bit copy of the items when ids fit (half the gathered bytes; an
       // 80 MB copy of c2's items stays L2-resident)
-      if (A.items_cls) {
+      if (FILT) {
         const OwnFilter F{A.h_row[T.row0], A.kappa, A.start, A.stop};
         count_suffix_entries<true>(A.items_cls, reinterpret_cast<const uint2*>(A.words + wb), w0, w1,
                                    table, T.c0, F);
@@ -1994,6 +2004,7 @@ struct PlanArgs {
   uint32_t rc_cap;
   uint2* item_info;
   unsigned long long* tile_words;  // per-tile stream words, when knowable from the statistics
+  uint32_t shard_rank, shard_world;  // tile sharding: keep the tiles of this rank's term share
   PlanOut* out;
 };
 
@@ -2308,6 +2319,47 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   __threadfence_block();
   __syncthreads();
   const uint32_t nt = (uint32_t)c_tiles;
+  if (P.shard_world > 1) {
+    // tile sharding: rank r keeps the tiles whose cost prefix (tile_cost)
+    // falls in the r-th of shard_world equal shares (the windows of one row
+    // follow the row's first window); the others get no units, no words and
+    // no rows.
+    // The owner is parked in slab_base until the units phase.
+    const uint32_t ts = (nt + kPlanThreads - 1) / kPlanThreads;
+    const uint32_t a = min(nt, tid * ts), b = min(nt, a + ts);
+    auto cost = [&](const Tile& tl) {
+      return tile_cost(tl, stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap));
+    };
+    unsigned long long tsum = 0, all;
+    for (uint32_t t = a; t < b; ++t) tsum += cost(P.tiles[t]);
+    unsigned long long pre = plan_block_scan<unsigned long long>(tsum, s_u64, 0ull, add, all);
+    const unsigned long long share = all / P.shard_world + 1;
+    for (uint32_t t = a; t < b; ++t) {
+      const unsigned long long ow = (pre + cost(P.tiles[t]) / 2) / share;  // by the tile's midpoint
+      P.tiles[t].slab_base = ow < P.shard_world - 1 ? ow : P.shard_world - 1;
+      pre += cost(P.tiles[t]);
+    }
+    __threadfence_block();
+    __syncthreads();
+    auto is_window = [&](const Tile& tl) {
+      return tl.mode == 0 && tl.row1 - tl.row0 == 1 && tl.width < (P.upper ? n - 1 - tl.row0 : n);
+    };
+    for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+      uint32_t f = t;
+      if (is_window(P.tiles[t]))
+        while (P.tiles[f].nwin == 0 && f > 0) --f;  // the row's first window
+      if (P.tiles[f].slab_base != P.shard_rank) P.tiles[t].n_units = 0;
+    }
+    __threadfence_block();
+    __syncthreads();
+    for (uint32_t t = tid; t < nt; t += kPlanThreads) P.tiles[t].slab_base = 0;
+    for (uint32_t i = tid; i < n; i += kPlanThreads) {
+      const uint2 tv = P.item_info[i];
+      if (tv.x != kNone && P.tiles[tv.x & kTileMask].n_units == 0) P.item_info[i] = make_uint2(kNone, 0u);
+    }
+    __threadfence_block();
+    __syncthreads();
+  }
   // units, slabs, split list, reduce chunks, output capacity. Per-tile unit
   // counts and widths are cached in shared memory when they fit (hash tiles
   // report width 0 and count kStreamHashSlots output slots).
@@ -2333,6 +2385,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   unsigned long long a_slab = 0, a_split = 0, a_single = 0, a_rc = 0, a_cap = 0, a_units = 0;
   for (uint32_t t = tlo; t < thi; ++t) {
     const uint32_t nu_t = nu_of(t), wd = wd_of(t);
+    if (nu_t == 0) continue;  // another rank's tile
     a_cap += tile_out_cap(P.tiles[t], kStreamHashCap, n, P.upper != 0);
     a_units += nu_t;
     if (nu_t > 1) {
@@ -2395,7 +2448,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
         const uint32_t pos = atomicAdd(&s_cur[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
         P.units[pos] = Unit{t, u};
       }
-    } else {
+    } else if (nu_t == 1) {
       P.units[atomicAdd(&s_cur[kFracBins], 1u)] = Unit{t, 0};
     }
   }
@@ -2407,7 +2460,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   if (known)
     for (uint32_t t = tid; t < nt; t += kPlanThreads) {
       const Tile& tl = P.tiles[t];
-      P.tile_words[t] = tl.mode == 2 ? 2 * (P.stats[tl.row0] >> 40) : tl.terms;
+      P.tile_words[t] = tl.n_units == 0 ? 0ull : (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> 40) : tl.terms);
     }
   stamp(5);
   if (tid == 0) {
@@ -2479,6 +2532,7 @@ struct crop_pairs {
   cudaEvent_t ev_items16 = nullptr;
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
   bool packed_filter = false;  // bucket filter applied on packed items (see k_items_cls)
+  uint32_t shard_rank = 0, shard_world = 1;  // tile sharding across ranks
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
   unsigned long long* hi_list = nullptr;
@@ -2676,6 +2730,26 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   // Running units in order of that fraction keeps the ~148 concurrently
   // active units on nearby transactions, so the rows they re-read stay in
   // L2 (64 fraction bins, no sort). Single-unit tiles follow.
+  if (J->shard_world > 1) {
+    // tile sharding (see k_plan_stream): this rank keeps the tiles of its
+    // term share; a split row's windows follow the first window
+    const uint32_t hroom = sm ? kStreamHashSlots : kHashSlots;
+    uint64_t all = 0;
+    for (auto& t : tiles) all += tile_cost(t, hroom);
+    const uint64_t share = all / J->shard_world + 1;
+    uint64_t pre = 0;
+    uint32_t owner = 0;
+    for (uint32_t t = 0; t < tiles.size(); ++t) {
+      const bool cont = tiles[t].mode == 0 && tiles[t].nwin == 0 && tiles[t].row1 - tiles[t].row0 == 1 &&
+                        tiles[t].width < (upper ? n - 1 - tiles[t].row0 : n);
+      const uint64_t c = tile_cost(tiles[t], hroom);
+      if (!cont) owner = (uint32_t)std::min<uint64_t>(J->shard_world - 1, (pre + c / 2) / share);
+      pre += c;
+      if (owner != J->shard_rank) tiles[t].n_units = 0;
+    }
+    for (uint32_t i = 0; i < n; ++i)
+      if (item_tile[i] != kNone && tiles[item_tile[i] & ~kWinFlag].n_units == 0) item_tile[i] = kNone;
+  }
   J->units.clear();
   J->split.clear();
   J->n_slabs = 0;
@@ -2691,7 +2765,7 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
       J->split.push_back(t);
       for (uint32_t u = 0; u < tt.n_units; ++u)
         ++bin_count[(uint64_t)(2 * u + 1) * kFracBins / (2 * tt.n_units)];
-    } else {
+    } else if (tt.n_units == 1) {
       ++bin_count[kFracBins];
     }
   }
@@ -2703,20 +2777,37 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     if (tt.n_units > 1) {
       for (uint32_t u = 0; u < tt.n_units; ++u)
         J->units[bin_pos[(uint64_t)(2 * u + 1) * kFracBins / (2 * tt.n_units)]++] = Unit{t, u};
-    } else {
+    } else if (tt.n_units == 1) {
       J->units[bin_pos[kFracBins]++] = Unit{t, 0};
     }
   }
 
   uint64_t cap = 0;
-  for (auto& t : tiles) cap += tile_out_cap(t, (uint32_t)hash_cap, n, upper);
+  for (auto& t : tiles)
+    if (t.n_units) cap += tile_out_cap(t, (uint32_t)hash_cap, n, upper);
   J->max_entries = cap;
 }
+
+extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                                         uint32_t n_items, int upper_only, const crop_interval* interval,
+                                         uint32_t shard_rank, uint32_t shard_world, void* stream,
+                                         crop_pairs** job);
 
 extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
                                  uint32_t n_items, int upper_only, const crop_interval* interval,
                                  void* stream, crop_pairs** job) {
+  return crop_pairs_create_sharded(offsets, items, n_tx, n_items, upper_only, interval, 0, 1, stream, job);
+}
+
+extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                                         uint32_t n_items, int upper_only, const crop_interval* interval,
+                                         uint32_t shard_rank, uint32_t shard_world, void* stream,
+                                         crop_pairs** job) {
   *job = nullptr;
+  if (shard_world < 1 || shard_rank >= shard_world) {
+    crop_set_error(CROP_ECONFIG, "shard rank %u of %u", shard_rank, shard_world);
+    return CROP_ECONFIG;
+  }
   if (n_tx < 0 || n_items >= (1u << 31)) {
     crop_set_error(CROP_EINPUT, "need n_tx >= 0 and item ids < 2^31 (n_items=%u)", n_items);
     return CROP_EINPUT;
@@ -2724,6 +2815,8 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = crop_pool_setup()) return rc;
   crop_pairs* J = new crop_pairs();
+  J->shard_rank = shard_rank;
+  J->shard_world = shard_world;
   J->offsets = offsets;
   J->items = items;
   J->n_tx = n_tx;
@@ -2816,6 +2909,8 @@ extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, 
       PA.rc_cap = (uint32_t)rc_cap;
       PA.item_info = reinterpret_cast<uint2*>(db + o_item);
       PA.tile_words = reinterpret_cast<unsigned long long*>(db + o_twords);
+      PA.shard_rank = J->shard_rank;
+      PA.shard_world = J->shard_world;
       PA.out = reinterpret_cast<PlanOut*>(db + o_out);
       JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
       JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3158,7 +3253,8 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
       const size_t budget = 227 * 1024 - fixed;
       R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
       const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
-      auto kern = up ? k_stream_scatter<true> : k_stream_scatter<false>;
+      auto kern = J->packed_filter ? (up ? k_stream_scatter<true, true> : k_stream_scatter<false, true>)
+                                   : (up ? k_stream_scatter<true, false> : k_stream_scatter<false, false>);
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
       kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, bounds, n_chunks);
       CROP_LAUNCH_CHECK();
@@ -3217,7 +3313,8 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
       cudaMemsetAsync(dbg, 0, 20 * 8, st);
       C.dbg = dbg;
     }
-    auto kcs = C.dbg ? k_count_stream<true> : k_count_stream<false>;
+    auto kcs = C.items_cls ? (C.dbg ? k_count_stream<true, true> : k_count_stream<false, true>)
+                           : (C.dbg ? k_count_stream<true, false> : k_count_stream<false, false>);
     CROP_CUDA(cudaFuncSetAttribute(kcs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem));
     mark(4);
     kcs<<<std::min<int>(2 * kNumSMs, (int)J->nu), kSCThreads, kStreamSmem, st>>>(C);

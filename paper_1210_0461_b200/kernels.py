@@ -190,15 +190,17 @@ class PairCountJob:
     """K2 handle: plan on create (one stream sync), run on demand."""
 
     def __init__(self, dtx: DeviceTransactions, upper_only: bool, interval: nat.Interval | None,
-                 keep: tuple = ()):
+                 keep: tuple = (), shard: tuple[int, int] = (0, 1)):
+        """shard = (rank, world): keep this rank's share of the tiles (the union
+        over ranks is the whole job; crop_pairs_create_sharded)."""
         self._keep = (dtx, keep)  # tensors the native job points at
         self.dtx = dtx
         lib = nat.load()
         h = ctypes.c_void_p()
         iv = ctypes.byref(interval) if interval is not None else None
-        nat.check(lib.crop_pairs_create(nat.ptr(dtx.offsets), nat.ptr(dtx.items), dtx.n_tx,
-                                        dtx.n_items, int(upper_only), iv, nat.stream_ptr(),
-                                        ctypes.byref(h)))
+        nat.check(lib.crop_pairs_create_sharded(nat.ptr(dtx.offsets), nat.ptr(dtx.items), dtx.n_tx,
+                                                dtx.n_items, int(upper_only), iv, int(shard[0]),
+                                                int(shard[1]), nat.stream_ptr(), ctypes.byref(h)))
         self._h = h
         me, tt, nt, nu = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         nat.check(lib.crop_pairs_info(h, ctypes.byref(me), ctypes.byref(tt), ctypes.byref(nt),

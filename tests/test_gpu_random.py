@@ -70,3 +70,35 @@ def test_random_streams_bit_exact(case, monkeypatch):
     orow, ocol, ow = oracle.sorted_pairs(recs.row, recs.col, recs.count)
     assert np.array_equal(gr, orow) and np.array_equal(gc, ocol) and np.array_equal(gw, ow)
     assert int(gw.sum()) == load
+
+
+@pytest.mark.parametrize("name,n_tx,world,mode", [("c2", 50_000, 3, "auto"), ("c2", 50_000, 8, "auto"),
+                                                   ("c5", 2_000, 3, "auto"), ("c2", 30_000, 4, "entry"),
+                                                   ("c3", 20_000, 5, "stream")])
+def test_tile_shards_partition_the_job(name, n_tx, world, mode, monkeypatch):
+    """The ranks' tile shards are disjoint and together equal the whole job."""
+    from paper_1210_0461_b200 import workloads
+
+    if mode == "entry":
+        monkeypatch.setenv("CROP_FORCE_ENTRY_MODE", "1")
+    elif mode == "stream":
+        monkeypatch.setenv("CROP_FORCE_STREAM_MODE", "1")
+    dtx = workloads.generate_pairs_workload(workloads.CONFIGS[name], n_tx=n_tx)
+    off, items = dtx.to_host()
+    parts = []
+    for r in range(world):
+        job = kernels.PairCountJob(dtx, True, None, shard=(r, world))
+        try:
+            ent = job.run()
+        finally:
+            job.close()
+        parts.append(ent.to_numpy())
+    row = np.concatenate([p[0] for p in parts])
+    col = np.concatenate([p[1] for p in parts])
+    w = np.concatenate([p[2] for p in parts])
+    key = row.astype(np.int64) << 32 | col.astype(np.int64)
+    assert np.unique(key).shape[0] == key.shape[0]  # disjoint
+    g = oracle.sorted_pairs(row, col, w)
+    o = oracle.sorted_pairs(*oracle.pair_supports(off, items))
+    for x, y in zip(g, o):
+        assert np.array_equal(x, y)

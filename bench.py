@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 BASELINE_METRIC = "outer-product terms counted/sec at 1/2/4/8 B200; % of HBM roofline"
 HBM_FALLBACK_GBS = 6650.0
+SUB_SHARD_CAPACITY = 1_500_000_000  # output entries per sub-shard (c3), 18 GB
 
 
 def parse():
@@ -175,7 +176,7 @@ def run_ours(args, rank, world):
 
     cfg = workloads.CONFIGS[args.config]
     if not isinstance(cfg, workloads.PairConfig):
-        raise SystemExit(f"bench.py measures pair configs; {args.config} is a product config")
+        return run_product(args, rank, world)
     dev = torch.device("cuda", torch.cuda.current_device())
     dtx, bcast_s = load_workload(cfg, rank, world)
     config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
@@ -193,13 +194,22 @@ def run_ours(args, rank, world):
         # the job (per-item term scan) to the last counting kernel
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         p0.record()
-        job = kernels.PairCountJob(dtx, True, interval, keep=tables, shard=shard)
-        job.set_timing(True)
-        ent = job.run(sync=False)
-        p1.record()
-        ent.n = int(ent.n_dev.item())
-        if ent.n > ent.capacity or job.overflowed():
-            raise RuntimeError("pair engine overflow")
+        try:
+            job = kernels.PairCountJob(dtx, True, interval, keep=tables, shard=shard)
+        except crop.ResourceCapError:
+            # the shard's entry lists exceed one job's 2^32 limit (c3): count it
+            # as consecutive sub-shards (kernels.count_pairs_shard)
+            job = None
+            ent = kernels.count_pairs_shard(dtx, True, interval, keep=tables, shard=shard,
+                                            capacity=SUB_SHARD_CAPACITY)
+            p1.record()
+        if job is not None:
+            job.set_timing(True)
+            ent = job.run(sync=False)
+            p1.record()
+            ent.n = int(ent.n_dev.item())
+            if ent.n > ent.capacity or job.overflowed():
+                raise RuntimeError("pair engine overflow")
         idx = kernels.topk_indices(ent, cfg.top_k)
         top = (ent.row[idx], ent.col[idx], ent.count[idx])
         if world > 1:
@@ -212,10 +222,15 @@ def run_ours(args, rank, world):
             allb = [torch.empty_like(buf) for _ in range(world)]
             dist.all_gather(allb, buf)
             top = torch.cat(allb, dim=1)
+        if job is None:
+            phases = {"path": p0.elapsed_time(p1), "plan": float("nan"), "route": float("nan"),
+                      "write": float("nan"), "count": float("nan")}
+            stats = (ent.total_terms, ent.n, None, None, False, ent.sub_shards)
+            return phases, stats, top
         phases = job.phase_ms()
         phases["path"] = p0.elapsed_time(p1)
         phases["plan"] = phases["path"] - phases["route"] - phases["write"] - phases["count"]
-        stats = (job.total_terms, ent.n, job.n_tiles, job.n_units, job.stream_mode)
+        stats = (job.total_terms, ent.n, job.n_tiles, job.n_units, job.stream_mode, 1)
         job.close()
         return phases, stats, top
 
@@ -265,10 +280,10 @@ def run_ours(args, rank, world):
     # the last counting kernel, host planning gap included). Own terms = terms
     # of this rank's buckets = the sum of its output counts.
     if world > 1:
-        job = kernels.PairCountJob(dtx, True, interval, keep=tables, shard=shard)
-        ent = job.run()
+        ent = kernels.count_pairs_shard(dtx, True, interval, keep=tables, shard=shard,
+                                        capacity=SUB_SHARD_CAPACITY)
         own_terms = int(ent.weights_f64().sum().item())
-        job.close()
+        del ent
     else:
         own_terms = total_terms_all
     in_bytes = 4 * int(dtx.items.numel()) + 8 * int(dtx.offsets.numel())
@@ -277,6 +292,10 @@ def run_ours(args, rank, world):
     peak, peak_src = peaks()
     achieved = b_alg / (avg["path"] * 1e-3) / 1e9
     stream_mode = bool(stats[4])
+    if stats[5] > 1:
+        mode_name = f"entry, {stats[5]} sub-shards per GPU"
+    else:
+        mode_name = "stream" if stream_mode else "entry"
     kern = {"plan": "k_item_terms + host tile plan + uploads",
             "route": "k_stream_count + k_scan_u64" if stream_mode else "k_route",
             "write": "k_stream_write" if stream_mode else "k_tile_entries",
@@ -289,8 +308,8 @@ def run_ours(args, rank, world):
                 "avg_launch_ms": round(avg["path"], 4),
                 "phases": {k: {"kernels": kern[k], "ms": round(avg[k], 4),
                                "share_of_step": round(avg[k] / ms_per_step, 4)}
-                           for k in ("plan", "route", "write", "count")},
-                "mode": "stream" if stream_mode else "entry"}
+                           for k in ("plan", "route", "write", "count") if avg[k] == avg[k]},
+                "mode": mode_name}
 
     e2e = None
     if not args.no_e2e:
@@ -318,6 +337,110 @@ def run_ours(args, rank, world):
             "gpu_launches": int(launches), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+def run_product(args, rank, world):
+    """c4: real-valued C = A*B, entries hashed to kappa buckets; rank r owns the
+    bucket interval split(kappa, N)[r] (the reference's worker intervals)."""
+    import numpy as np
+    import torch
+
+    import paper_1210_0461_b200 as crop
+    from paper_1210_0461_b200 import kernels, workloads
+
+    cfg = workloads.CONFIGS[args.config]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s = workloads.generate_product_workload(cfg)  # same seed on every rank: no broadcast needed
+    ds = kernels.DeviceOuterStream.from_host(s)
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.kappa,
+                               cs_enabled=False, seed=0)
+    h = crop.make_hashes(crop.HashConfig(cfg.kappa, config.instance_seeds()[0]))
+    tab = kernels.hash_tables(h, cfg.n)
+    asg = crop.WorkerAssignment.split(cfg.kappa, world)[rank]
+    flush = torch.empty(1 << 28, dtype=torch.int32, device=dev)
+    total_terms = int((np.diff(s.a_ptr) * np.diff(s.b_ptr)).sum())
+
+    def step():
+        return kernels.outer_product(ds, False, cfg.kappa, asg.start, asg.stop, *tab)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = kernels.launch_counter()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    times = []
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ent = step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = kernels.launch_counter() - launches0
+    t_sum = sum(times)
+    if world > 1:
+        t = torch.tensor([t_sum], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_sum = float(t.item())
+    ms = t_sum / args.steps
+    own_terms = ent.total_terms if world == 1 else None
+    # B_alg (SURVEY.md §8d): 8 B per term + input (8 B per nnz per side +
+    # pointers) + output (row, col u32, value f64, bucket u32 = 20 B per entry)
+    nnz = int(s.a_idx.shape[0] + s.b_idx.shape[0])
+    in_bytes = 12 * nnz + 16 * (s.length + 1)
+    b_alg = 8 * ent.total_terms + in_bytes + 20 * ent.n
+    peak, peak_src = peaks()
+    achieved = b_alg / (statistics.mean(times) * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": total_terms / (ms * 1e-3), "unit": "terms/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded Pareto-nnz CSC/CSR, N(0,1) fp32 values (SURVEY.md §8d)",
+            "config": {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa,
+                       "buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})[rank]",
+                       "terms": total_terms, "entries": ent.n if world == 1 else None,
+                       "parallelism": f"buckets{world}",
+                       "l2": "flushed (1 GiB write) before every timed step"},
+            "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_outer_emit -> "
+                         "radix sort (row,col) + (bucket) -> k_outer_reduce",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,
+                         "avg_launch_ms": round(statistics.mean(times), 4)},
+            "cpu_baseline": (product_cpu_baseline(args, cfg, s) if world == 1 and not args.no_cpu
+                             else None),
+            "e2e": None,
+            "gpu_launches": int(launches), "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def product_cpu_baseline(args, cfg, s, n_products=None):
+    """C oracle exact_product (oracle.py:20-50 restated) on the first products, one thread."""
+    import numpy as np
+
+    import oracle
+
+    k = min(n_products or args.cpu_sample_tx or 100_000, s.length)
+    a1, b1 = int(s.a_ptr[k]), int(s.b_ptr[k])
+    st = oracle.Stream(s.a_ptr[: k + 1], s.a_idx[:a1], s.a_val[:a1],
+                       s.b_ptr[: k + 1], s.b_idx[:b1], s.b_val[:b1])
+    terms = int((np.diff(s.a_ptr[: k + 1]) * np.diff(s.b_ptr[: k + 1])).sum())
+    t0 = time.perf_counter()
+    oracle.exact_product(st)
+    t = time.perf_counter() - t0
+    return {"value": terms / t, "unit": "terms/s", "cores": 1, "kind": "port",
+            "sample": f"first {k} of {s.length} products ({terms} terms), exact_product "
+                      f"restatement (fp64 dict accumulation), one thread",
+            "seconds": round(t, 3)}
 
 
 def run_e2e(args, cfg, dtx, rank, world):
@@ -419,6 +542,22 @@ def run_reference(args, rank, world):
     from paper_1210_0461_b200 import workloads
 
     cfg = workloads.CONFIGS[args.config]
+    if not isinstance(cfg, workloads.PairConfig):
+        s = workloads.generate_product_workload(cfg)
+        vals = [product_cpu_baseline(args, cfg, s) for _ in range(args.warmup + args.steps)]
+        vals = vals[args.warmup:]
+        value = statistics.mean(v["value"] for v in vals)
+        print(json.dumps({
+            "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": "terms/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.mean(v["seconds"] for v in vals) * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8d)", "config": {"workload": cfg.name, "sample": vals[0]["sample"]},
+            "cpu_baseline": {"value": value, "unit": "terms/s", "cores": 1, "kind": "port",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     dtx = workloads.generate_pairs_workload(cfg, n_tx=args.cpu_sample_tx or default_sample(args.config))
     torch.cuda.synchronize()
     vals = []

@@ -2733,16 +2733,28 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   if (J->shard_world > 1) {
     // tile sharding (see k_plan_stream): this rank keeps the tiles of its
     // term share; a split row's windows follow the first window
+    // Entry mode re-reads a suffix per entry: its cost is per term and per
+    // entry (fit to the per-rank counting cycles of c5's 8 shards: ~0.23
+    // cycles per term, ~26 per entry; entries <= the rows' occurrences).
     const uint32_t hroom = sm ? kStreamHashSlots : kHashSlots;
+    std::vector<uint64_t> occ_pre;
+    if (!sm) {
+      occ_pre.assign(n + 1, 0);
+      for (uint32_t i = 0; i < n; ++i) occ_pre[i + 1] = occ_pre[i] + occ[i];
+    }
+    auto cost_of = [&](const Tile& tl) -> uint64_t {
+      if (sm) return tile_cost(tl, hroom);
+      return 2 * tl.terms + 220 * (occ_pre[tl.row1] - occ_pre[tl.row0]);
+    };
     uint64_t all = 0;
-    for (auto& t : tiles) all += tile_cost(t, hroom);
+    for (auto& t : tiles) all += cost_of(t);
     const uint64_t share = all / J->shard_world + 1;
     uint64_t pre = 0;
     uint32_t owner = 0;
     for (uint32_t t = 0; t < tiles.size(); ++t) {
       const bool cont = tiles[t].mode == 0 && tiles[t].nwin == 0 && tiles[t].row1 - tiles[t].row0 == 1 &&
                         tiles[t].width < (upper ? n - 1 - tiles[t].row0 : n);
-      const uint64_t c = tile_cost(tiles[t], hroom);
+      const uint64_t c = cost_of(tiles[t]);
       if (!cont) owner = (uint32_t)std::min<uint64_t>(J->shard_world - 1, (pre + c / 2) / share);
       pre += c;
       if (owner != J->shard_rank) tiles[t].n_units = 0;

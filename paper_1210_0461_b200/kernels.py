@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .errors import ConfigError, InputError
+from .errors import ConfigError, InputError, ResourceCapError
 
 TOPK_EXACT_BINS = 2048       # topk histogram: exact below, 2^-10 relative above
 TOPK_BINS = 2048 + 21 * 1024  # common.cuh kTopkBins
@@ -215,7 +215,7 @@ class PairCountJob:
         dev = self.dtx.offsets.device
         if capacity is None:
             capacity = min(self.max_entries, self.total_terms // 2 + (1 << 20))
-        m = max(int(capacity), 1)
+        m = max(min(int(capacity), self.max_entries), 1)
         nat.check(nat.load().crop_pairs_set_capacity(self._h, m))
         row = torch.empty(m, dtype=torch.int32, device=dev)
         col = torch.empty(m, dtype=torch.int32, device=dev)
@@ -242,8 +242,11 @@ class PairCountJob:
             if ent.n > m:
                 if m >= self.max_entries:
                     raise InputError(f"pair engine overflow: {ent.n} > {self.max_entries}")
+                # the counter claims every entry even past the capacity: the
+                # re-run needs exactly n slots
+                n_need = ent.n
                 del ent, row, col, cnt, fused
-                return self.run(True, self.max_entries)
+                return self.run(True, min(self.max_entries, n_need))
             if self.overflowed():
                 raise InputError("pair engine overflow: entry lists exceeded their bounds")
         return ent
@@ -289,11 +292,44 @@ def count_pairs(dtx: DeviceTransactions, upper_only: bool = True, kappa: int = 1
         if h_row is None or h_col is None:
             raise ConfigError("a partial interval needs the hash tables")
         iv = interval_struct(kappa, start, stop, h_row, h_col)
-    job = PairCountJob(dtx, upper_only, iv, keep=(h_row, h_col))
-    try:
-        return job.run()
-    finally:
-        job.close()
+    return count_pairs_shard(dtx, upper_only, iv, (h_row, h_col), (0, 1))
+
+
+def count_pairs_shard(dtx: DeviceTransactions, upper_only: bool, interval, keep=(),
+                      shard: tuple[int, int] = (0, 1), capacity: int | None = None,
+                      max_split: int = 64) -> DeviceEntries:
+    """Exact supports of one tile shard; a shard whose entry lists exceed one
+    job's 2^32 limit is counted as k consecutive sub-shards (r*k + s of N*k,
+    s < k -- together exactly the tiles of a finer split's shards, so the
+    union over all ranks is still the whole job, disjoint)."""
+    r, world = shard
+    k = 1
+    while True:
+        parts = []
+        try:
+            for s in range(k):
+                job = PairCountJob(dtx, upper_only, interval, keep=keep, shard=(r * k + s, world * k))
+                try:
+                    parts.append(job.run(capacity=capacity))
+                finally:
+                    job.close()
+        except ResourceCapError:
+            if k >= max_split:
+                raise
+            del parts
+            k *= 2
+            continue
+        break
+    if len(parts) == 1:
+        return parts[0]
+    n = sum(p.n for p in parts)
+    cat = lambda xs: torch.cat(xs) if xs else torch.empty(0, dtype=torch.int32, device=dtx.offsets.device)
+    ent = DeviceEntries(cat([p.row[: p.n] for p in parts]), cat([p.col[: p.n] for p in parts]),
+                        cat([p.count[: p.n] for p in parts]), None, n, parts[0].total_terms)
+    ent.n_dev = torch.tensor([n], dtype=torch.int64, device=dtx.offsets.device)
+    ent.capacity = n
+    ent.sub_shards = k
+    return ent
 
 
 def entry_bucket_stats(ent: DeviceEntries, tables: list, kappa: int, n_items: int,

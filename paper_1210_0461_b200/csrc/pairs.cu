@@ -64,7 +64,10 @@ constexpr size_t kOffBytes = (kChunkTx + 1) * 8;
 constexpr uint32_t kStatSmemItems = 24576;           // pass A privatised items (2 x u32, 192 KB)
 constexpr uint32_t kTileSmem = 24576;                // route shared tile counters (96 KB)
 constexpr uint32_t kStage = 4096;                    // route staging entries per chunk
-constexpr uint64_t kOccOne = 1ull << 40;             // pass A: occurrence count in bits 40+
+// pass A packs occ << 32 | terms: a row's terms (<= its transactions' total
+// length) and occurrences are both below nnz < 2^32 per job
+constexpr int kOccShift = 32;
+constexpr uint64_t kOccOne = 1ull << kOccShift;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kUnknown = 0xFFFFFFFEu;       // route: previous tile not known yet
 constexpr uint32_t kWinFlag = 0x80000000u;           // item_tile: row is split into windows
@@ -191,7 +194,7 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
 // ------------------------------------------------------------- pass A
 // Per row item i: terms_i (pairs with i as the row) and occ_i, the number of
 // transactions in which i has at least one partner after it (an upper bound
-// of the entries it creates). Output packed as occ << 40 | terms.
+// of the entries it creates). Output packed as occ << kOccShift | terms.
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_item_terms(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x)
     if (s_terms[i])
-      atomicAdd(&stats[i], ((unsigned long long)s_occ[i] << 40) | s_terms[i]);
+      atomicAdd(&stats[i], ((unsigned long long)s_occ[i] << kOccShift) | s_terms[i]);
 }
 
 // ------------------------------------------------------------- pass B
@@ -2071,7 +2074,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   for (uint32_t i = tid; i < n; i += kPlanThreads) {
     const unsigned long long x = P.stats[i];
     T += x & (kOccOne - 1);
-    O += x >> 40;
+    O += x >> kOccShift;
   }
   plan_block_scan<unsigned long long>(T, s_u64, 0ull, add, T);
   plan_block_scan<unsigned long long>(O, s_u64, 0ull, add, O);
@@ -2211,7 +2214,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
             tl.c0 = P.upper ? i + 1 : 0;
             tl.mode = P.filter ? 0 : 2;
             tl.width = P.upper ? n - 1 - i : n;
-            tl.n_units = units_of(t, P.stats[i] >> 40);
+            tl.n_units = units_of(t, P.stats[i] >> kOccShift);
           } else {
             tl.mode = 1;
             tl.n_units = 1;
@@ -2234,7 +2237,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
             tl.nwin = q == 0 ? nwin : 0;
             tl.width = tl.c1 - tl.c0;
             tl.terms = t / nwin + 1;
-            tl.n_units = units_of(tl.terms, P.stats[i] >> 40);
+            tl.n_units = units_of(tl.terms, P.stats[i] >> kOccShift);
             P.tiles[id + q] = tl;
           }
           P.item_info[i] = make_uint2(id | kWinFlag, 0u);
@@ -2333,9 +2336,11 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     unsigned long long tsum = 0, all;
     for (uint32_t t = a; t < b; ++t) tsum += cost(P.tiles[t]);
     unsigned long long pre = plan_block_scan<unsigned long long>(tsum, s_u64, 0ull, add, all);
-    const unsigned long long share = all / P.shard_world + 1;
+    // owner = floor(midpoint * world / all): a rank's k sub-shards of a
+    // k-times finer split (r*k + s of world*k) own exactly its tiles
     for (uint32_t t = a; t < b; ++t) {
-      const unsigned long long ow = (pre + cost(P.tiles[t]) / 2) / share;  // by the tile's midpoint
+      const unsigned long long ow =
+          all ? (pre + cost(P.tiles[t]) / 2) * P.shard_world / all : 0;  // by the tile's midpoint
       P.tiles[t].slab_base = ow < P.shard_world - 1 ? ow : P.shard_world - 1;
       pre += cost(P.tiles[t]);
     }
@@ -2460,7 +2465,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   if (known)
     for (uint32_t t = tid; t < nt; t += kPlanThreads) {
       const Tile& tl = P.tiles[t];
-      P.tile_words[t] = tl.n_units == 0 ? 0ull : (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> 40) : tl.terms);
+      P.tile_words[t] = tl.n_units == 0 ? 0ull : (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms);
     }
   stamp(5);
   if (tid == 0) {
@@ -2748,14 +2753,16 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     };
     uint64_t all = 0;
     for (auto& t : tiles) all += cost_of(t);
-    const uint64_t share = all / J->shard_world + 1;
+    // owner = floor(midpoint * world / all) (see k_plan_stream)
     uint64_t pre = 0;
     uint32_t owner = 0;
     for (uint32_t t = 0; t < tiles.size(); ++t) {
       const bool cont = tiles[t].mode == 0 && tiles[t].nwin == 0 && tiles[t].row1 - tiles[t].row0 == 1 &&
                         tiles[t].width < (upper ? n - 1 - tiles[t].row0 : n);
       const uint64_t c = cost_of(tiles[t]);
-      if (!cont) owner = (uint32_t)std::min<uint64_t>(J->shard_world - 1, (pre + c / 2) / share);
+      if (!cont)
+        owner = (uint32_t)std::min<uint64_t>(J->shard_world - 1,
+                                             all ? (unsigned __int128)(pre + c / 2) * J->shard_world / all : 0);
       pre += c;
       if (owner != J->shard_rank) tiles[t].n_units = 0;
     }
@@ -3049,7 +3056,7 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
     for (uint32_t i = 0; i < n_items; ++i) {
       const unsigned long long x = stats[i];
       terms[i] = x & (kOccOne - 1);
-      occ[i] = x >> 40;
+      occ[i] = x >> kOccShift;
       J->total_terms += terms[i];
       occ_sum += occ[i];
     }

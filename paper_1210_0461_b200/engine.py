@@ -410,9 +410,13 @@ class SketchState:
         rows, cols, ws = rows[keep], cols[keep], ws[keep]
         order = np.lexsort((cols, rows, -ws))[:k]
         cs = self.config.cs_enabled
-        return [TopEntry(Entry(int(r), int(c)), float(w), float(w),
-                         self._estimate(int(r), int(c)) if cs else None)
-                for r, c, w in zip(rows[order].tolist(), cols[order].tolist(), ws[order].tolist())]
+        rl, cl, wl = rows[order].tolist(), cols[order].tolist(), ws[order].tolist()
+        if cs:
+            return [TopEntry(Entry(r, c), w, w, self._estimate(r, c)) for r, c, w in zip(rl, cl, wl)]
+        # tuple.__new__ skips the NamedTuple constructor's argument parsing
+        # (k is 1,000-10,000 in the configs: this is the call's host cost)
+        tn = tuple.__new__
+        return [tn(TopEntry, (tn(Entry, (r, c)), w, w, None)) for r, c, w in zip(rl, cl, wl)]
 
     def recorded_weight(self) -> float:
         if self._dev is not None:

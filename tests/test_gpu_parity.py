@@ -360,6 +360,23 @@ def test_edge_cases():
         assert len(state.top_entries(5)) == min(5, len(sup))
 
 
+def test_row_with_more_than_2_24_occurrences(count_mode):
+    """A row item in more than 2^24 transactions (c3's heaviest rows have
+    4.4e7): its occurrence count must survive pass A's packing, or the units
+    are sized too few and the 16-bit counters wrap."""
+    n_tx = (1 << 24) + (1 << 20)
+    offsets = np.arange(0, 2 * n_tx + 1, 2, dtype=np.int64)
+    items = np.empty(2 * n_tx, dtype=np.uint32)
+    items[0::2] = 0
+    items[1::2] = 1 + (np.arange(n_tx) % 64)
+    dtx = kernels.DeviceTransactions.from_host(offsets, items, 65)
+    ent = kernels.count_pairs(dtx, True)
+    r, c, w = ent.to_numpy()
+    got = dict(zip(zip(r.tolist(), c.tolist()), w.tolist()))
+    want = np.bincount(np.arange(n_tx) % 64, minlength=64)
+    assert got == {(0, j + 1): float(want[j]) for j in range(64)}
+
+
 def test_long_transactions_and_wide_rows(count_mode):
     # lengths up to the 8192 limit; n > kDenseCap forces column windows
     rng = np.random.default_rng(0)

@@ -117,24 +117,46 @@ def test_c5_full_size_properties_and_shards():
     assert torch.equal(torch.cat(parts_c)[order.indices], wcnt)
 
 
+def _row_terms(dtx):
+    """Terms per row item (pairs (i, j > i)) from the positions, plain torch."""
+    want = torch.zeros(dtx.n_items, dtype=torch.int64, device=dtx.offsets.device)
+    step = 5_000_000
+    for t0 in range(0, dtx.n_tx, step):
+        off = dtx.offsets[t0: min(dtx.n_tx, t0 + step) + 1]
+        lens = off[1:] - off[:-1]
+        base = torch.repeat_interleave(off[:-1], lens)
+        L = torch.repeat_interleave(lens, lens)
+        g = torch.arange(int(off[0]), int(off[-1]), device=off.device, dtype=torch.int64)
+        want.index_add_(0, dtx.items[int(off[0]): int(off[-1])].to(torch.int64), L - 1 - (g - base))
+    return want
+
+
+def _unique_keys(ent):
+    # torch.sort is limited to 2^31 - 1 elements: check row classes mod 4
+    for q in range(4):
+        sel = (ent.row[: ent.n] & 3) == q
+        k = torch.sort(_keys(ent)[sel]).values
+        assert bool((k[1:] > k[:-1]).all().item())
+        del k, sel
+
+
 def test_c3_full_size_shard_conservation():
     """c3 (5e7 transactions, 1e6 items, 2.25e10 terms) as 8 tile shards run one
     after the other: every shard's keys are unique, and the counts of all
-    shards sum to the term count."""
+    shards sum, row by row, to the terms of each row item (rows 0-4 sit in
+    more than 2^24 transactions)."""
     cfg = workloads.CONFIGS["c3"]
     dtx = workloads.generate_pairs_workload(cfg)
-    terms = _terms(dtx)
-    total = 0
+    want = _row_terms(dtx)
+    assert int(want.sum().item()) == _terms(dtx)
+    got = torch.zeros_like(want)
     for r in range(8):
         e = kernels.count_pairs_shard(dtx, True, None, shard=(r, 8), capacity=1_500_000_000)
-        k = _keys(e)
-        sk = torch.sort(k).values
-        assert bool((sk[1:] > sk[:-1]).all().item())
-        del k, sk
-        total += int(e.count[: e.n].to(torch.int64).sum().item())
+        _unique_keys(e)
+        got.index_add_(0, e.row[: e.n].to(torch.int64), e.count[: e.n].to(torch.int64))
         del e
         torch.cuda.empty_cache()
-    assert total == terms
+    assert torch.equal(got, want)
 
 
 def test_c4_full_size_linearity_and_spot_entries():

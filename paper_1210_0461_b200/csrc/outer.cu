@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -62,11 +63,19 @@ __global__ void k_outer_count(const int64_t* __restrict__ a_ptr, const uint32_t*
   }
 }
 
+// Composite sort key (bucket << rc_bits | row << c_bits | col) when it fits
+// 64 bits (c4: 11 + 19 + 19 bits): ONE stable radix sort over end_bit bits
+// replaces the (row, col) sort + stable bucket sort + gather.
+struct CompositeKey {
+  int on, has_hash;
+  uint32_t c_bits, rc_bits, bits;
+};
+
 template <bool FILTER>
 __global__ void k_outer_emit(const int64_t* __restrict__ a_ptr, const uint32_t* __restrict__ a_idx,
                              const double* __restrict__ a_val, const int64_t* __restrict__ b_ptr,
                              const uint32_t* __restrict__ b_idx, const double* __restrict__ b_val,
-                             int64_t n, int upper, crop_interval iv,
+                             int64_t n, int upper, crop_interval iv, CompositeKey ck,
                              const unsigned long long* __restrict__ offs,
                              unsigned long long* __restrict__ keys, uint32_t* __restrict__ seq,
                              double* __restrict__ vals) {
@@ -82,8 +91,14 @@ __global__ void k_outer_emit(const int64_t* __restrict__ a_ptr, const uint32_t* 
       uint32_t i = 0, j = 0;
       int64_t p = 0, q = 0;
       if (t < la * lb) {
-        p = t / lb;
-        q = t - p * lb;
+        if (la * lb < (1ll << 32)) {  // 32-bit division (products up to 65,536^2 terms)
+          const uint32_t t32 = (uint32_t)t, l32 = (uint32_t)lb;
+          p = t32 / l32;
+          q = t32 - (uint32_t)p * l32;
+        } else {
+          p = t / lb;
+          q = t - p * lb;
+        }
         i = a_idx[a0 + p];
         j = b_idx[b0 + q];
         keep = own_term<FILTER>(i, j, upper, iv);
@@ -91,7 +106,18 @@ __global__ void k_outer_emit(const int64_t* __restrict__ a_ptr, const uint32_t* 
       const uint32_t m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const unsigned long long o = pos + __popc(m & ((1u << lane) - 1u));
-        keys[o] = ((unsigned long long)i << 32) | j;
+        if (ck.on) {
+          // composite key (bucket, row, col) in ck.bits bits: one sort orders
+          // the output per bucket by (row, col)
+          uint32_t b = 0;
+          if (ck.has_hash) {
+            b = iv.h_row[i] + iv.h_col[j];
+            if (b >= iv.kappa) b -= iv.kappa;
+          }
+          keys[o] = ((unsigned long long)b << ck.rc_bits) | ((unsigned long long)i << ck.c_bits) | j;
+        } else {
+          keys[o] = ((unsigned long long)i << 32) | j;
+        }
         seq[o] = (uint32_t)o;
         vals[o] = (a_val ? a_val[a0 + p] : 1.0) * (b_val ? b_val[b0 + q] : 1.0);
       }
@@ -161,6 +187,60 @@ __global__ void k_outer_reduce(const unsigned long long* __restrict__ keys,
   }
 }
 
+__global__ void k_outer_reduce_ck(const unsigned long long* __restrict__ keys,
+                                  const uint32_t* __restrict__ seq, const double* __restrict__ vals,
+                                  const uint32_t* __restrict__ head_pos, uint64_t n, CompositeKey ck,
+                                  uint32_t* __restrict__ out_row, uint32_t* __restrict__ out_col,
+                                  double* __restrict__ out_val, uint32_t* __restrict__ out_bucket) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[e];
+    if (e > 0 && keys[e - 1] == k) continue;  // not a segment head
+    // sum the run in stream order (the sort is stable): bit-identical to the
+    // reference's dict accumulation
+    double s = vals[seq[e]];
+    for (uint64_t f = e + 1; f < n && keys[f] == k; ++f) s = s + vals[seq[f]];
+    const uint32_t o = head_pos[e];
+    out_row[o] = (uint32_t)((k >> ck.c_bits) & ((1ull << (ck.rc_bits - ck.c_bits)) - 1));
+    out_col[o] = (uint32_t)(k & ((1ull << ck.c_bits) - 1));
+    out_val[o] = s;
+    out_bucket[o] = (uint32_t)(k >> ck.rc_bits);
+  }
+}
+
+__global__ void k_heads_count(const unsigned long long* __restrict__ keys, uint64_t n,
+                              uint32_t* __restrict__ head) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1u : 0u;
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ a, const int64_t* a_end,
+                          const uint32_t* __restrict__ b, const int64_t* b_end,
+                          unsigned int* __restrict__ out) {
+  const int64_t na = *a_end, nb = *b_end;
+  uint32_t ma = 0, mb = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < na; e += (int64_t)gridDim.x * blockDim.x)
+    ma = max(ma, a[e]);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nb; e += (int64_t)gridDim.x * blockDim.x)
+    mb = max(mb, b[e]);
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, d));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, ma);
+    atomicMax(out + 1, mb);
+  }
+}
+
+uint32_t bits_for(uint64_t v) {  // bits to hold values 0..v
+  uint32_t b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
 }  // namespace
 
 struct crop_outer {
@@ -173,6 +253,8 @@ struct crop_outer {
   crop_interval iv;
   uint64_t total_terms;  // own-interval terms
   uint64_t all_terms;
+  CompositeKey ck{};
+  cudaStream_t st = nullptr;  // creation stream: pool allocations are freed on it
   unsigned long long* d_counts = nullptr;
   unsigned long long* d_offs = nullptr;
 };
@@ -207,13 +289,15 @@ extern "C" int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, co
     J->iv = crop_interval{1, 0, 1, nullptr, nullptr};
   }
   const int64_t nn = std::max<int64_t>(n_products, 1);
-  cudaError_t e1 = cudaMalloc(&J->d_counts, nn * 8);
-  cudaError_t e2 = cudaMalloc(&J->d_offs, (nn + 1) * 8);
+  J->st = st;
+  // stream-ordered pool allocations (cudaMalloc / cudaFree would synchronise)
+  cudaError_t e1 = cudaMallocAsync(&J->d_counts, nn * 8, st);
+  cudaError_t e2 = cudaMallocAsync(&J->d_offs, (nn + 2) * 8, st);  // + 8 bytes: index maxima
   if (e1 != cudaSuccess || e2 != cudaSuccess) {
-    cudaFree(J->d_counts);
-    cudaFree(J->d_offs);
+    cudaFreeAsync(J->d_counts, st);
+    cudaFreeAsync(J->d_offs, st);
     delete J;
-    crop_set_error(CROP_ECUDA, "cudaMalloc failed");
+    crop_set_error(CROP_ECUDA, "cudaMallocAsync failed");
     return CROP_ECUDA;
   }
   J->total_terms = 0;
@@ -234,14 +318,30 @@ extern "C" int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, co
     // scanning only n and adding the last count below
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, J->d_counts, J->d_offs, n_products, st);
     cudaFreeAsync(tmp, st);
+    // largest row / column index (composite sort key width), same sync
+    unsigned int* d_mx = reinterpret_cast<unsigned int*>(J->d_offs + n_products + 1);
+    CROP_CUDA(cudaMemsetAsync(d_mx, 0, 8, st));
+    k_max_u32<<<2 * kNumSMs, 256, 0, st>>>(a_idx, a_ptr + n_products, b_idx, b_ptr + n_products, d_mx);
+    CROP_LAUNCH_CHECK();
     unsigned long long last_off = 0, last_cnt = 0;
+    unsigned int mx[2] = {0, 0};
     CROP_CUDA(cudaMemcpyAsync(&last_off, J->d_offs + n_products - 1, 8, cudaMemcpyDeviceToHost, st));
     CROP_CUDA(cudaMemcpyAsync(&last_cnt, J->d_counts + n_products - 1, 8, cudaMemcpyDeviceToHost, st));
+    CROP_CUDA(cudaMemcpyAsync(mx, d_mx, 8, cudaMemcpyDeviceToHost, st));
     CROP_CUDA(cudaStreamSynchronize(st));
     J->total_terms = last_off + last_cnt;
+    {
+      const uint32_t rb = bits_for(mx[0]), cb = bits_for(mx[1]);
+      const uint32_t bb = J->has_hash ? bits_for(J->iv.kappa - 1) : 0;
+      J->ck.has_hash = J->has_hash;
+      J->ck.c_bits = cb;
+      J->ck.rc_bits = rb + cb;
+      J->ck.bits = bb + rb + cb;
+      J->ck.on = J->ck.bits <= 64 && !getenv("CROP_OUTER_TWO_SORTS");
+    }
     if (J->total_terms >= (1ull << 32)) {
-      cudaFree(J->d_counts);
-      cudaFree(J->d_offs);
+      cudaFreeAsync(J->d_counts, st);
+      cudaFreeAsync(J->d_offs, st);
       delete J;
       crop_set_error(CROP_ERESOURCE, "more than 2^32 terms in one interval; split the stream");
       return CROP_ERESOURCE;
@@ -275,12 +375,14 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMallocAsync(&seq, n * 4, st));
   CROP_CUDA(cudaMallocAsync(&seq2, n * 4, st));
   CROP_CUDA(cudaMallocAsync(&vals, n * 8, st));
-  CROP_CUDA(cudaMallocAsync(&buck, n * 4, st));
-  CROP_CUDA(cudaMallocAsync(&buck2, n * 4, st));
-  CROP_CUDA(cudaMallocAsync(&iota, n * 4, st));
-  CROP_CUDA(cudaMallocAsync(&perm, n * 4, st));
-  CROP_CUDA(cudaMallocAsync(&keys_f, n * 8, st));
-  CROP_CUDA(cudaMallocAsync(&seq_f, n * 4, st));
+  if (!J->ck.on) {
+    CROP_CUDA(cudaMallocAsync(&buck, n * 4, st));
+    CROP_CUDA(cudaMallocAsync(&buck2, n * 4, st));
+    CROP_CUDA(cudaMallocAsync(&iota, n * 4, st));
+    CROP_CUDA(cudaMallocAsync(&perm, n * 4, st));
+    CROP_CUDA(cudaMallocAsync(&keys_f, n * 8, st));
+    CROP_CUDA(cudaMallocAsync(&seq_f, n * 4, st));
+  }
   CROP_CUDA(cudaMallocAsync(&head, n * 4, st));
   CROP_CUDA(cudaMallocAsync(&head_pos, n * 4, st));
   {
@@ -288,12 +390,40 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
     if (J->filter)
       k_outer_emit<true><<<(int)blocks, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr,
                                                      J->b_idx, J->b_val, J->n, J->upper, J->iv,
-                                                     J->d_offs, keys, seq, vals);
+                                                     J->ck, J->d_offs, keys, seq, vals);
     else
       k_outer_emit<false><<<(int)blocks, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr,
                                                       J->b_idx, J->b_val, J->n, J->upper, J->iv,
-                                                      J->d_offs, keys, seq, vals);
+                                                      J->ck, J->d_offs, keys, seq, vals);
     CROP_LAUNCH_CHECK();
+  }
+  if (J->ck.on) {
+    // one stable sort by (bucket, row, col) over the key's bits; ties keep
+    // emission (= stream) order
+    const int eb = (int)J->ck.bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, seq, seq2, (int64_t)n, 0, eb, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, head, head_pos, (int64_t)n, st);
+    tmp_bytes = std::max(tmp_bytes, t2);
+    cub::TransformInputIterator<unsigned long long, cub::CastOp<unsigned long long>, uint32_t*> hi(
+        head, cub::CastOp<unsigned long long>());
+    cub::DeviceReduce::Sum(nullptr, t2, hi, (unsigned long long*)d_n_entries, (int64_t)n, st);
+    tmp_bytes = std::max(tmp_bytes, t2);
+    CROP_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, seq, seq2, (int64_t)n, 0, eb, st);
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 16 * kNumSMs);
+    k_heads_count<<<(int)blocks, 256, 0, st>>>(keys2, n, head);
+    CROP_LAUNCH_CHECK();
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, head, head_pos, (int64_t)n, st);
+    k_outer_reduce_ck<<<(int)blocks, 256, 0, st>>>(keys2, seq2, vals, head_pos, n, J->ck, out_row,
+                                                   out_col, out_value, out_bucket);
+    CROP_LAUNCH_CHECK();
+    cub::DeviceReduce::Sum(tmp, tmp_bytes, hi, (unsigned long long*)d_n_entries, (int64_t)n, st);
+    for (void* p : {(void*)tmp, (void*)keys, (void*)keys2, (void*)seq, (void*)seq2, (void*)vals,
+                    (void*)head, (void*)head_pos})
+      cudaFreeAsync(p, st);
+    CROP_LAUNCH_CHECK();
+    crop_count_launches(5);
+    return CROP_OK;
   }
   // stable sort by (row, col): ties keep emission (= stream) order
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, seq, seq2, (int64_t)n, 0, 64, st);
@@ -350,7 +480,7 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
 
 extern "C" void crop_outer_destroy(crop_outer* J) {
   if (!J) return;
-  cudaFree(J->d_counts);
-  cudaFree(J->d_offs);
+  cudaFreeAsync(J->d_counts, J->st);
+  cudaFreeAsync(J->d_offs, J->st);
   delete J;
 }

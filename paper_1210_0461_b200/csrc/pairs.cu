@@ -2538,6 +2538,7 @@ struct crop_pairs {
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
   bool packed_filter = false;  // bucket filter applied on packed items (see k_items_cls)
   uint32_t shard_rank = 0, shard_world = 1;  // tile sharding across ranks
+  bool written = false;  // stream mode: the words were written by create (run counts only)
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
   unsigned long long* hi_list = nullptr;
@@ -2581,6 +2582,99 @@ struct PinnedArena {
 static PinnedArena g_pinned;
 
 static inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Stream mode, phases route + write: word totals (when unknown), tile bases,
+// then the scatter of every own pair into its tile's stream. Launched by
+// crop_pairs_create right after planning (so the caller's host work between
+// create and run overlaps the scatter), or by run after a re-run request.
+static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
+  const uint32_t nt = J->nt;
+  if (nt == 0 || J->n_tx == 0) return CROP_OK;
+  const bool up = J->upper != 0;
+  auto mark = [&](int k) {
+    if (rec) cudaEventRecord(J->ev[k], st);
+  };
+  mark(0);
+  {
+    StreamRouteArgs R{};
+    R.offsets = J->offsets;
+    R.items = J->items;
+    R.n_tx = J->n_tx;
+    R.item_info = J->d_item_info;
+    R.tiles = J->d_tiles;
+    R.n_tiles = nt;
+    R.n_items = J->n_items;
+    R.col_bits = J->col_bits;
+    R.filter = J->filter;
+    R.kappa = J->iv.kappa;
+    R.start = J->iv.start;
+    R.stop = J->iv.stop;
+    R.h_row = J->iv.h_row;
+    R.h_col = J->iv.h_col;
+    R.tile_words = J->d_tile_words;
+    R.tile_cursor = J->d_tile_cursor;
+    R.tile_base = J->d_tile_ebase;
+    R.words = J->d_words;
+    // about 12 chunks per CTA so the last wave's imbalance stays small
+    R.chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, J->n_tx / (kNumSMs * 12)));
+    const int64_t chunks = (J->n_tx + R.chunk_tx - 1) / R.chunk_tx;
+    const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
+    if (!J->words_known) {
+      CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
+      auto kern = up ? k_stream_count<true> : k_stream_count<false>;
+      const size_t smem = kOffBytes + (size_t)std::min(nt, kTileSmem) * 4;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kOffBytes + kTileSmem * 4)));
+      kern<<<grid, kPassThreads, smem, st>>>(R);
+      CROP_LAUNCH_CHECK();
+    }
+    k_scan_u64<<<1, 1024, 0, st>>>(J->d_tile_words, nt, J->d_tile_ebase, J->d_tile_cursor);
+    CROP_LAUNCH_CHECK();
+    mark(1);
+    R.packed_filter = J->packed_filter ? 1 : 0;
+    if (J->words_known && J->maxlen <= kScatPark / 2) {
+      // single-walk scatter over position bands
+      const uint32_t band = kScatPark - J->maxlen + 1;
+      const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
+      uint32_t* bounds = nullptr;
+      CROP_CUDA(cudaMallocAsync(&bounds, (size_t)(n_chunks + 1) * 4, st));
+      k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
+          J->offsets, J->n_tx, n_chunks, band, bounds);
+      CROP_LAUNCH_CHECK();
+      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 16 + 16 + kPassThreads / 32 * 128 * 4;
+      const size_t budget = 227 * 1024 - fixed;
+      R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
+      const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
+      auto kern = J->packed_filter ? (up ? k_stream_scatter<true, true> : k_stream_scatter<false, true>)
+                                   : (up ? k_stream_scatter<true, false> : k_stream_scatter<false, false>);
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
+      kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, bounds, n_chunks);
+      CROP_LAUNCH_CHECK();
+      cudaFreeAsync(bounds, st);
+      crop_count_launches(1);
+    } else {
+      auto kern = up ? k_stream_write<true> : k_stream_write<false>;
+      const size_t ns2 = (std::min(nt, kTileSmem) + 1) & ~1u;
+      const size_t smem = kOffBytes + ns2 * 6 + 16;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(kOffBytes + (size_t)kTileSmem * 6 + 16)));
+      kern<<<grid, kPassThreads, smem, st>>>(R);
+      CROP_LAUNCH_CHECK();
+    }
+    mark(2);
+  }
+  return CROP_OK;
+}
+
+// Launch the stream write from create (events recorded for phase_ms).
+static int early_write(crop_pairs* J, cudaStream_t st) {
+  if (getenv("CROP_LATE_WRITE")) return CROP_OK;
+  if (!J->ev[0])
+    for (cudaEvent_t& e : J->ev) CROP_CUDA(cudaEventCreate(&e));
+  if (int rc = stream_write(J, st, true)) return rc;
+  J->written = true;
+  return CROP_OK;
+}
 
 static void free_job(crop_pairs* j) {
   for (cudaEvent_t& e : j->ev)
@@ -3013,6 +3107,8 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
         if (J->n_slabs)
           JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kSHalf * 4, st));
         JCUDA(cudaMallocAsync(&J->d_words, (J->total_terms + 2 * ho->occ_sum + 2 * (uint64_t)J->nt + 2) * 4, st));
+        rc = early_write(J, st);
+        if (rc) goto fail;
         *job = J;
         return CROP_OK;
       }
@@ -3193,6 +3289,10 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
     }
   }
 #undef JCUDA
+  if (J->stream_mode) {
+    rc = early_write(J, st);
+    if (rc) goto fail;
+  }
   *job = J;
   return CROP_OK;
 fail:
@@ -3221,74 +3321,11 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
   auto mark = [&](int k) {
     if (J->timing) cudaEventRecord(J->ev[k], st);
   };
-  mark(0);
   if (J->stream_mode) {
-    StreamRouteArgs R{};
-    R.offsets = J->offsets;
-    R.items = J->items;
-    R.n_tx = J->n_tx;
-    R.item_info = J->d_item_info;
-    R.tiles = J->d_tiles;
-    R.n_tiles = nt;
-    R.n_items = J->n_items;
-    R.col_bits = J->col_bits;
-    R.filter = J->filter;
-    R.kappa = J->iv.kappa;
-    R.start = J->iv.start;
-    R.stop = J->iv.stop;
-    R.h_row = J->iv.h_row;
-    R.h_col = J->iv.h_col;
-    R.tile_words = J->d_tile_words;
-    R.tile_cursor = J->d_tile_cursor;
-    R.tile_base = J->d_tile_ebase;
-    R.words = J->d_words;
-    // about 12 chunks per CTA so the last wave's imbalance stays small
-    R.chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, J->n_tx / (kNumSMs * 12)));
-    const int64_t chunks = (J->n_tx + R.chunk_tx - 1) / R.chunk_tx;
-    const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
-    if (!J->words_known) {
-      CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
-      auto kern = up ? k_stream_count<true> : k_stream_count<false>;
-      const size_t smem = kOffBytes + (size_t)std::min(nt, kTileSmem) * 4;
-      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(kOffBytes + kTileSmem * 4)));
-      kern<<<grid, kPassThreads, smem, st>>>(R);
-      CROP_LAUNCH_CHECK();
+    if (!J->written) {
+      if (int rc = stream_write(J, st, J->timing)) return rc;
     }
-    k_scan_u64<<<1, 1024, 0, st>>>(J->d_tile_words, nt, J->d_tile_ebase, J->d_tile_cursor);
-    CROP_LAUNCH_CHECK();
-    mark(1);
-    R.packed_filter = J->packed_filter ? 1 : 0;
-    if (J->words_known && J->maxlen <= kScatPark / 2) {
-      // single-walk scatter over position bands
-      const uint32_t band = kScatPark - J->maxlen + 1;
-      const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
-      uint32_t* bounds = nullptr;
-      CROP_CUDA(cudaMallocAsync(&bounds, (size_t)(n_chunks + 1) * 4, st));
-      k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
-          J->offsets, J->n_tx, n_chunks, band, bounds);
-      CROP_LAUNCH_CHECK();
-      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 16 + 16 + kPassThreads / 32 * 128 * 4;
-      const size_t budget = 227 * 1024 - fixed;
-      R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
-      const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
-      auto kern = J->packed_filter ? (up ? k_stream_scatter<true, true> : k_stream_scatter<false, true>)
-                                   : (up ? k_stream_scatter<true, false> : k_stream_scatter<false, false>);
-      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
-      kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, bounds, n_chunks);
-      CROP_LAUNCH_CHECK();
-      cudaFreeAsync(bounds, st);
-      crop_count_launches(1);
-    } else {
-      auto kern = up ? k_stream_write<true> : k_stream_write<false>;
-      const size_t ns2 = (std::min(nt, kTileSmem) + 1) & ~1u;
-      const size_t smem = kOffBytes + ns2 * 6 + 16;
-      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(kOffBytes + (size_t)kTileSmem * 6 + 16)));
-      kern<<<grid, kPassThreads, smem, st>>>(R);
-      CROP_LAUNCH_CHECK();
-    }
-    mark(2);
+    J->written = false;  // a re-run (capacity) writes again
     mark(3);
     CROP_CUDA(cudaMemsetAsync(J->d_unit_counter, 0, 4, st));
     CROP_CUDA(cudaMemsetAsync(J->d_tile_done, 0, nt * 4, st));
@@ -3357,6 +3394,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     return CROP_OK;
   }
   // route: one walk, staged per chunk, ranges claimed per touched tile
+  mark(0);
   CROP_CUDA(cudaMemcpyAsync(J->d_tile_cursor, J->d_tile_ebase, nt * 8, cudaMemcpyDeviceToDevice, st));
   {
     auto kern = up ? k_route<true> : k_route<false>;

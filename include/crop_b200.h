@@ -106,6 +106,10 @@ int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int
 /* host-side plan facts: output capacity, total terms (all buckets), tiles */
 int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* total_terms,
                     uint64_t* n_tiles, uint64_t* n_units);
+/* terms of this job's own tiles (a tile shard's share; window tiles are
+ * estimates), 0 when unknown (host-planned jobs): sizes the output buffer of
+ * a shard (LoadReport units, engine.py:283) */
+int crop_pairs_own_terms(const crop_pairs* job, uint64_t* own_terms);
 int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32_t* out_count,
                    uint64_t* d_n_entries, void* stream);
 /* Per-phase CUDA-event timing of crop_pairs_run (off by default). out4 =

@@ -39,6 +39,7 @@ _SIGS = {
                                         ctypes.POINTER(P)]),
     "crop_pairs_info": (i32, [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
                               ctypes.POINTER(u64)]),
+    "crop_pairs_own_terms": (i32, [P, ctypes.POINTER(u64)]),
     "crop_pairs_run": (i32, [P, P, P, P, P, P]),
     "crop_pairs_set_timing": (i32, [P, i32]),
     "crop_pairs_phase_ms": (i32, [P, ctypes.POINTER(ctypes.c_float)]),

@@ -993,6 +993,7 @@ constexpr int kSCThreads = 512;                     // count kernel threads (2 C
 constexpr int kSCWarps = kSCThreads / 32;
 constexpr uint32_t kStreamUnitOcc = 65535;
 constexpr uint32_t kStreamHashSlots = 14336;
+constexpr uint32_t kSparseWindowWords = 7168;  // <= half the hash slots: load <= 1/2
 
 // Stream-mode hash tiles size their table from their distinct-key bound
 // (load <= 1/2, multiple of 256 slots, at most kStreamHashSlots); the slot
@@ -1672,8 +1673,13 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
     const uint64_t Wu = ents ? Wn / 2 : Wn;
     const uint64_t w0 = Wu * unit.local / T.n_units;
     const uint64_t w1 = Wu * (unit.local + 1) / T.n_units;
-    const bool dense = T.mode != 1;
-    const uint32_t width = T.width;
+    // a sparse column window (a mid-weight row's window holding few words,
+    // c3) counts in a hash table sized to its exact word total instead of
+    // clearing and compacting 57,344 dense counters: key = column - c0
+    const bool hwin = T.mode == 0 && T.n_units == 1 && T.row1 - T.row0 == 1 &&
+                      Wn <= kSparseWindowWords && T.width > 2 * kSparseWindowWords;
+    const bool dense = T.mode != 1 && !hwin;
+    const uint32_t width = hwin ? stream_hash_slots(Wn) : T.width;
     long long c0 = 0, c1 = 0, c2 = 0;
     if (DBG) c0 = clock64();
     const uint32_t dwords = width < kSHalf ? width : kSHalf;  // dense: table words in use
@@ -1845,7 +1851,10 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
         const uint32_t c = cv[q];
         if (!c) continue;
         uint32_t i, j;
-        if (!dense) {
+        if (hwin) {
+          i = T.row0;
+          j = kv[q & 1] + T.c0;
+        } else if (!dense) {
           i = T.row0 + (kv[q & 1] >> A.col_bits);
           j = kv[q & 1] & ((1u << A.col_bits) - 1u);
         } else {
@@ -1992,6 +2001,8 @@ struct PlanOut {
   uint32_t stream_mode, overflow, pad0, pad1;
   long long dbg[4];  // development: planner phase cycles
   uint32_t words_known, pad2;  // per-tile word totals written (no word-count pass needed)
+  unsigned long long own_words;  // bound on this shard's stream words (allocation; < 2^32)
+  unsigned long long own_terms;  // this shard's terms (window tiles: estimates)
 };
 
 struct PlanArgs {
@@ -2012,6 +2023,7 @@ struct PlanArgs {
 };
 
 constexpr int kPlanThreads = 1024;
+constexpr uint32_t kMaxShardCheck = 1024;  // owners tracked by the per-shard word check
 constexpr uint64_t kPlanS = 1ull << 24;  // fixed-point capacity of one light tile
 constexpr uint32_t kMinDenseWidth = 4096;
 
@@ -2078,15 +2090,20 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   }
   plan_block_scan<unsigned long long>(T, s_u64, 0ull, add, T);
   plan_block_scan<unsigned long long>(O, s_u64, 0ull, add, O);
-  const bool fits = T + 2 * O + 2ull * n + 2 < (1ull << 32);
-  bool sm = fits && O > 0 && T <= (unsigned long long)kStreamMeanMax * O;
+  // word positions are 32-bit: a whole job must fit; a shard is checked on
+  // its own words once the tiles are assigned (below)
+  const bool fits = P.shard_world > 1 || T + 2 * O + 2ull * n + 2 < (1ull << 32);
+  const bool short_rows = O > 0 && T <= (unsigned long long)kStreamMeanMax * O;
+  bool sm = fits && short_rows;
   if (P.force == 1) sm = false;
   if (P.force == 2) sm = fits;
   if (tid == 0) {
     P.out->total_terms = T;
     P.out->occ_sum = O;
     P.out->stream_mode = sm;
-    P.out->overflow = 0;
+    // short rows whose words do not fit one job: split into tile shards
+    // (every shard size is decided from the whole plan, so all ranks agree)
+    P.out->overflow = (!fits && short_rows && P.force == 0) ? 2u : 0u;
   }
   if (!sm) return;
   stamp(0);
@@ -2330,29 +2347,60 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     // The owner is parked in slab_base until the units phase.
     const uint32_t ts = (nt + kPlanThreads - 1) / kPlanThreads;
     const uint32_t a = min(nt, tid * ts), b = min(nt, a + ts);
-    auto cost = [&](const Tile& tl) {
-      return tile_cost(tl, stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap));
-    };
-    unsigned long long tsum = 0, all;
-    for (uint32_t t = a; t < b; ++t) tsum += cost(P.tiles[t]);
-    unsigned long long pre = plan_block_scan<unsigned long long>(tsum, s_u64, 0ull, add, all);
-    // owner = floor(midpoint * world / all): a rank's k sub-shards of a
-    // k-times finer split (r*k + s of world*k) own exactly its tiles
-    for (uint32_t t = a; t < b; ++t) {
-      const unsigned long long ow =
-          all ? (pre + cost(P.tiles[t]) / 2) * P.shard_world / all : 0;  // by the tile's midpoint
-      P.tiles[t].slab_base = ow < P.shard_world - 1 ? ow : P.shard_world - 1;
-      pre += cost(P.tiles[t]);
-    }
-    __threadfence_block();
-    __syncthreads();
     auto is_window = [&](const Tile& tl) {
       return tl.mode == 0 && tl.row1 - tl.row0 == 1 && tl.width < (P.upper ? n - 1 - tl.row0 : n);
     };
+    // stream words of a tile (bounds as in the units phase below): a window's
+    // words are bounded by its row's terms, carried by the row's first window
+    auto words_of = [&](const Tile& tl) -> unsigned long long {
+      if (is_window(tl)) return 2 + (tl.nwin ? (P.stats[tl.row0] & (kOccOne - 1)) : 0ull);
+      return 2 + (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms);
+    };
+    auto cost = [&](const Tile& tl) -> unsigned long long {
+      return tile_cost(tl, stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap));
+    };
+    __shared__ unsigned long long s_ow[kMaxShardCheck];
+    // pass 0: shares of the counting cost; if a share's words pass the
+    // 32-bit word positions, pass 1: shares of the words; if even those do
+    // not fit, every rank asks for a finer split (the decision depends only
+    // on the whole plan, so all ranks agree)
+    for (int pass = 0; pass < 2; ++pass) {
+      auto metric = [&](const Tile& tl) { return pass == 0 ? cost(tl) : words_of(tl); };
+      unsigned long long tsum = 0, all;
+      for (uint32_t t = a; t < b; ++t) tsum += metric(P.tiles[t]);
+      unsigned long long pre = plan_block_scan<unsigned long long>(tsum, s_u64, 0ull, add, all);
+      // owner = floor(midpoint * world / all): a rank's k sub-shards of a
+      // k-times finer split (r*k + s of world*k) own exactly its tiles
+      for (uint32_t t = a; t < b; ++t) {
+        const unsigned long long c = metric(P.tiles[t]);
+        const unsigned long long ow = all ? (pre + c / 2) * P.shard_world / all : 0;  // tile midpoint
+        P.tiles[t].slab_base = ow < P.shard_world - 1 ? ow : P.shard_world - 1;
+        pre += c;
+      }
+      for (uint32_t k = tid; k < kMaxShardCheck; k += kPlanThreads) s_ow[k] = 0;
+      __threadfence_block();
+      __syncthreads();
+      for (uint32_t t = tid; t < nt; t += kPlanThreads) {
+        uint32_t f = t;
+        if (is_window(P.tiles[t]))
+          while (P.tiles[f].nwin == 0 && f > 0) --f;  // the row's first window
+        const uint32_t ow = (uint32_t)P.tiles[f].slab_base;
+        atomicAdd(&s_ow[ow < kMaxShardCheck ? ow : kMaxShardCheck - 1], words_of(P.tiles[t]));
+      }
+      __syncthreads();
+      unsigned long long mxw = 0;
+      for (uint32_t k = tid; k < kMaxShardCheck; k += kPlanThreads) mxw = s_ow[k] > mxw ? s_ow[k] : mxw;
+      plan_block_scan<long long>((long long)mxw, s_i64, 0ll, mx, totl);
+      if (totl + 2 < (1ll << 32)) break;
+      if (pass == 1) {
+        if (tid == 0) P.out->overflow = 2;
+        return;
+      }
+    }
     for (uint32_t t = tid; t < nt; t += kPlanThreads) {
       uint32_t f = t;
       if (is_window(P.tiles[t]))
-        while (P.tiles[f].nwin == 0 && f > 0) --f;  // the row's first window
+        while (P.tiles[f].nwin == 0 && f > 0) --f;
       if (P.tiles[f].slab_base != P.shard_rank) P.tiles[t].n_units = 0;
     }
     __threadfence_block();
@@ -2388,9 +2436,22 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   const uint32_t tseg = (nt + kPlanThreads - 1) / kPlanThreads;
   const uint32_t tlo = min(nt, tid * tseg), thi = min(nt, tlo + tseg);
   unsigned long long a_slab = 0, a_split = 0, a_single = 0, a_rc = 0, a_cap = 0, a_units = 0;
+  unsigned long long a_words = 0, a_terms = 0;
   for (uint32_t t = tlo; t < thi; ++t) {
     const uint32_t nu_t = nu_of(t), wd = wd_of(t);
     if (nu_t == 0) continue;  // another rank's tile
+    {
+      // stream words: a window's words are bounded by its row's terms (counted
+      // once, at the row's first window), an entry tile stores 2 per row
+      // occurrence, other tiles one per term; + 2 for the even rounding
+      const Tile& tl = P.tiles[t];
+      const bool win = tl.mode == 0 && tl.row1 - tl.row0 == 1 &&
+                       tl.width < (P.upper ? n - 1 - tl.row0 : n);
+      if (win) a_words += tl.nwin ? (P.stats[tl.row0] & (kOccOne - 1)) : 0ull;
+      else a_words += tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms;
+      a_words += 2;
+      a_terms += tl.terms;
+    }
     a_cap += tile_out_cap(P.tiles[t], kStreamHashCap, n, P.upper != 0);
     a_units += nu_t;
     if (nu_t > 1) {
@@ -2408,7 +2469,10 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   const unsigned long long b_rc = plan_block_scan<unsigned long long>(a_rc, s_u64, 0ull, add, n_rc);
   plan_block_scan<unsigned long long>(a_cap, s_u64, 0ull, add, cap);
   plan_block_scan<unsigned long long>(a_units, s_u64, 0ull, add, nu);
-  if (nu > P.unit_cap || n_rc > P.rc_cap) {
+  unsigned long long own_words, own_terms;
+  plan_block_scan<unsigned long long>(a_words, s_u64, 0ull, add, own_words);
+  plan_block_scan<unsigned long long>(a_terms, s_u64, 0ull, add, own_terms);
+  if (nu > P.unit_cap || n_rc > P.rc_cap || own_words + 2 >= (1ull << 32)) {
     if (tid == 0) P.out->overflow = 1;
     return;
   }
@@ -2477,6 +2541,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
     P.out->dbg[2] = ck[4];
     P.out->dbg[3] = ck[5];
     P.out->max_entries = cap;
+    P.out->own_words = own_words + 2;
+    P.out->own_terms = own_terms;
     P.out->n_slabs = n_slabs;
     P.out->n_tiles = nt;
     P.out->n_units = (uint32_t)nu;
@@ -2539,6 +2605,8 @@ struct crop_pairs {
   bool packed_filter = false;  // bucket filter applied on packed items (see k_items_cls)
   uint32_t shard_rank = 0, shard_world = 1;  // tile sharding across ranks
   bool written = false;  // stream mode: the words were written by create (run counts only)
+  int64_t nnz_hint = 0;  // offsets[n_tx], read at creation
+  uint64_t own_terms = 0;  // this shard's terms (device planner; 0 = unknown)
   // fused top-k buffers (caller-owned, stream mode): see crop_pairs_set_topk
   uint32_t* topk_hist = nullptr;
   unsigned long long* hi_list = nullptr;
@@ -2963,6 +3031,20 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
   } while (0)
   {
     const uint32_t nn = std::max<uint32_t>(n_items, 1);
+    // (the pinned staging and the nnz read below are shared across jobs)
+    std::lock_guard<std::mutex> pin_lock(g_pinned.mu);
+    // nnz (= offsets[n_tx]) sizes the device planner's capacities: read on a
+    // side stream ordered after the inputs but not after pass A, so the host
+    // waits for it while pass A runs
+    static cudaStream_t s_nnz = nullptr;
+    static cudaEvent_t e_in = nullptr;
+    static int64_t* h_nnz_hint = nullptr;
+    if (!s_nnz) {
+      JCUDA(cudaStreamCreateWithFlags(&s_nnz, cudaStreamNonBlocking));
+      JCUDA(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
+      JCUDA(cudaMallocHost(&h_nnz_hint, 8));
+    }
+    if (n_tx > 0) JCUDA(cudaEventRecord(e_in, st));
     JCUDA(cudaMallocAsync(&J->d_terms, nn * sizeof(unsigned long long) + 16, st));
     J->d_maxlen = reinterpret_cast<unsigned int*>(J->d_terms + nn);
     JCUDA(cudaMemsetAsync(J->d_terms, 0, nn * sizeof(unsigned long long) + 16, st));
@@ -2978,14 +3060,25 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
     }
-    std::lock_guard<std::mutex> pin_lock(g_pinned.mu);
+    if (n_tx > 0) {
+      JCUDA(cudaStreamWaitEvent(s_nnz, e_in, 0));
+      JCUDA(cudaMemcpyAsync(h_nnz_hint, offsets + n_tx, 8, cudaMemcpyDeviceToHost, s_nnz));
+      JCUDA(cudaStreamSynchronize(s_nnz));
+      J->nnz_hint = *h_nnz_hint;
+    }
     // GPU planner first (stream mode); the host planner below handles entry
     // mode and the rare plans that exceed the device planner's bounds
     const int force = getenv("CROP_FORCE_ENTRY_MODE") ? 1 : (getenv("CROP_FORCE_STREAM_MODE") ? 2 : 0);
     if (n_tx > 0 && n_items > 0 && force != 1 && !getenv("CROP_HOST_PLANNER")) {
-      const size_t tile_cap = 2 * (size_t)nn + 64;
-      const size_t unit_cap = tile_cap + 1300;  // split units <= T / unit_terms <= 1184
-      const size_t rc_cap = 29 * 1200;          // <= 29 chunks per split tile
+      // capacities: rows wider than one table are cut into up to `wmax`
+      // column windows; units beyond one per tile come from terms (<= T /
+      // unit_terms <= 1184) or from row occurrences (<= 65,535 per unit of
+      // 16-bit counters, per window: <= wmax * nnz / 65,535)
+      const uint64_t wmax = ((uint64_t)nn + kStreamDenseCap - 1) / kStreamDenseCap;
+      const uint64_t occ_units = wmax * ((uint64_t)J->nnz_hint / kStreamUnitOcc + 1);
+      const size_t tile_cap = (wmax > 1 ? 3 : 2) * (size_t)nn + 64;
+      const size_t unit_cap = tile_cap + 1300 + occ_units;
+      const size_t rc_cap = 29 * (1200 + occ_units);  // <= 29 chunks per split tile
       const size_t o_tiles = 0;
       const size_t o_units = align16(o_tiles + tile_cap * sizeof(Tile));
       const size_t o_split = align16(o_units + unit_cap * sizeof(Unit));
@@ -3053,6 +3146,14 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       if (getenv("CROP_DEBUG_TIMING"))
         fprintf(stderr, "[k_plan_stream] kcyc: totals %u classify %u scans+walks %.0f tiles %.0f light %.0f units %.0f\n",
                 ho->pad0, ho->pad1, ho->dbg[0] / 1e3, ho->dbg[1] / 1e3, ho->dbg[2] / 1e3, ho->dbg[3] / 1e3);
+      if (ho->overflow == 2) {
+        // the stream words of this job (or of its largest tile shard) pass
+        // the 32-bit word positions: the caller splits into finer shards
+        crop_set_error(CROP_ERESOURCE, "%llu terms exceed one job's 2^32 stream words; "
+                       "split into tile shards", (unsigned long long)ho->total_terms);
+        rc = CROP_ERESOURCE;
+        goto fail;
+      }
       if (ho->stream_mode && !ho->overflow) {
         J->nnz = *h_nz;
         J->stream_mode = true;
@@ -3106,7 +3207,8 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
         J->d_overflow = reinterpret_cast<uint32_t*>(db + o_misc + 16);
         if (J->n_slabs)
           JCUDA(cudaMallocAsync(&J->d_slabs, J->n_slabs * (size_t)kSHalf * 4, st));
-        JCUDA(cudaMallocAsync(&J->d_words, (J->total_terms + 2 * ho->occ_sum + 2 * (uint64_t)J->nt + 2) * 4, st));
+        JCUDA(cudaMallocAsync(&J->d_words, ho->own_words * 4, st));
+        J->own_terms = ho->own_terms;
         rc = early_write(J, st);
         if (rc) goto fail;
         *job = J;
@@ -3307,6 +3409,11 @@ extern "C" int crop_pairs_info(const crop_pairs* J, uint64_t* max_entries, uint6
   if (total_terms) *total_terms = J->total_terms;
   if (n_tiles) *n_tiles = J->nt;
   if (n_units) *n_units = J->nu;
+  return CROP_OK;
+}
+
+extern "C" int crop_pairs_own_terms(const crop_pairs* J, uint64_t* own_terms) {
+  *own_terms = J->own_terms;
   return CROP_OK;
 }
 

@@ -207,6 +207,10 @@ class PairCountJob:
                                       ctypes.byref(nu)))
         self.max_entries, self.total_terms = int(me.value), int(tt.value)
         self.n_tiles, self.n_units = int(nt.value), int(nu.value)
+        ot = ctypes.c_uint64()
+        nat.check(lib.crop_pairs_own_terms(h, ctypes.byref(ot)))
+        self.own_terms = int(ot.value)  # 0: unknown
+        self.sharded = shard[1] > 1
 
     def run(self, sync: bool = True, capacity: int | None = None) -> DeviceEntries:
         """Count; output arrays hold `capacity` entries (default: a guess of half
@@ -214,7 +218,12 @@ class PairCountJob:
         fit is counted again with the full bound."""
         dev = self.dtx.offsets.device
         if capacity is None:
-            capacity = min(self.max_entries, self.total_terms // 2 + (1 << 20))
+            if self.sharded and self.own_terms:
+                # a shard emits at most one entry per own term (c3's light
+                # shards are almost all distinct pairs)
+                capacity = min(self.max_entries, self.own_terms + (1 << 20))
+            else:
+                capacity = min(self.max_entries, self.total_terms // 2 + (1 << 20))
         m = max(min(int(capacity), self.max_entries), 1)
         nat.check(nat.load().crop_pairs_set_capacity(self._h, m))
         row = torch.empty(m, dtype=torch.int32, device=dev)

@@ -302,7 +302,9 @@ extern "C" int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, co
   }
   J->total_terms = 0;
   if (n_products > 0) {
-    int64_t blocks = std::min<int64_t>((n_products + 7) / 8, 8 * kNumSMs);
+    // one warp per product (8 per block): enough warps in flight to hide the
+    // dependent pointer loads of short products
+    int64_t blocks = std::min<int64_t>((n_products + 7) / 8, 1 << 20);
     if (J->filter)
       k_outer_count<true><<<(int)blocks, 256, 0, st>>>(a_ptr, a_idx, b_ptr, b_idx, n_products,
                                                       upper_only, J->iv, J->d_counts);
@@ -386,7 +388,7 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMallocAsync(&head, n * 4, st));
   CROP_CUDA(cudaMallocAsync(&head_pos, n * 4, st));
   {
-    int64_t blocks = std::min<int64_t>((J->n + 7) / 8, 8 * kNumSMs);
+    int64_t blocks = std::min<int64_t>((J->n + 7) / 8, 1 << 20);
     if (J->filter)
       k_outer_emit<true><<<(int)blocks, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr,
                                                      J->b_idx, J->b_val, J->n, J->upper, J->iv,

@@ -1813,66 +1813,68 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
     // past the output capacity: claim only (the host sees n > capacity)
     const bool fits = s_base + total <= A.out_cap;
     const bool single_row = dense && T.row1 - T.row0 == 1;
-    for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += dense ? 128 : 64) {
-      uint32_t cv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kv[2] = {0, 0};
-      if (dense) {
-        const uint32_t s = s0 + 4 * lane;
-        if (s < s_hi) {
-          const uint4 c4 = *reinterpret_cast<const uint4*>(table + s);
-          const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (s + q < s_hi) {
-              cv[q] = cw[q] & 0xFFFFu;
-              cv[4 + q] = s + q + kSHalf < width ? cw[q] >> 16 : 0u;
-            }
-        }
-      } else {
-        const uint32_t s = s0 + 2 * lane;
-        if (s < s_hi) {
-          const ulonglong2 c2v = *reinterpret_cast<const ulonglong2*>(slot64 + s);
-          if (c2v.x != kEmpty64) {
-            cv[0] = (uint32_t)c2v.x;
-            kv[0] = (uint32_t)(c2v.x >> 32);
-          }
-          if (s + 1 < s_hi && c2v.y != kEmpty64) {
-            cv[1] = (uint32_t)c2v.y;
-            kv[1] = (uint32_t)(c2v.y >> 32);
-          }
-        }
-      }
-      uint32_t cnt = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) cnt += cv[q] != 0;
-      const uint32_t incl = warp_incl_scan(cnt);
-      uint64_t o = pos + (incl - cnt);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t c = cv[q];
-        if (!c) continue;
+    // emit: consecutive lanes own consecutive table words (dense: word w
+    // holds slots w and w + kSHalf) or hash slots, and a ballot compacts each
+    // step's non-zero counters to consecutive output positions -- every
+    // store instruction writes one contiguous run of entries
+    const uint32_t lt = (1u << lane) - 1u;
+    auto put = [&](uint64_t o, uint32_t i, uint32_t j, uint32_t c) {
+      A.out_row[o] = i;
+      A.out_col[o] = j;
+      A.out_count[o] = c;
+      note_high(A, c, o);
+    };
+    if (dense) {
+      for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += 32) {
+        const uint32_t w = s0 + lane;
+        const uint32_t cw = w < s_hi ? table[w] : 0u;
+        const uint32_t c_lo = cw & 0xFFFFu;
+        const uint32_t c_hi = w + kSHalf < width ? cw >> 16 : 0u;
+        const uint32_t m_lo = __ballot_sync(0xffffffffu, c_lo != 0);
+        const uint32_t m_hi = __ballot_sync(0xffffffffu, c_hi != 0);
         uint32_t i, j;
-        if (hwin) {
-          i = T.row0;
-          j = kv[q & 1] + T.c0;
-        } else if (!dense) {
-          i = T.row0 + (kv[q & 1] >> A.col_bits);
-          j = kv[q & 1] & ((1u << A.col_bits) - 1u);
-        } else {
-          const uint32_t slot = s0 + 4 * lane + (q & 3) + (q >= 4 ? kSHalf : 0u);
+        if (c_lo) {
+          if (single_row) {
+            i = T.row0;
+            j = w + T.c0;
+          } else {
+            dense_slot_pair(T, w, n, A.upper != 0, i, j);
+          }
+          put(pos + __popc(m_lo & lt), i, j, c_lo);
+        }
+        pos += __popc(m_lo);
+        if (c_hi) {
+          const uint32_t slot = w + kSHalf;
           if (single_row) {
             i = T.row0;
             j = slot + T.c0;
           } else {
             dense_slot_pair(T, slot, n, A.upper != 0, i, j);
           }
+          put(pos + __popc(m_hi & lt), i, j, c_hi);
         }
-        A.out_row[o] = i;
-        A.out_col[o] = j;
-        A.out_count[o] = c;
-        note_high(A, c, o);
-        ++o;
+        pos += __popc(m_hi);
       }
-      pos += __shfl_sync(0xffffffffu, incl, 31);
+    } else {
+      for (uint32_t s0 = s_lo; fits && s0 < s_hi; s0 += 32) {
+        const uint32_t sl = s0 + lane;
+        const unsigned long long v = sl < s_hi ? slot64[sl] : kEmpty64;
+        const bool occ = v != kEmpty64;
+        const uint32_t m = __ballot_sync(0xffffffffu, occ);
+        if (occ) {
+          const uint32_t key = (uint32_t)(v >> 32);
+          uint32_t i, j;
+          if (hwin) {
+            i = T.row0;
+            j = key + T.c0;
+          } else {
+            i = T.row0 + (key >> A.col_bits);
+            j = key & ((1u << A.col_bits) - 1u);
+          }
+          put(pos + __popc(m & lt), i, j, (uint32_t)v);
+        }
+        pos += __popc(m);
+      }
     }
     __syncthreads();
     if (DBG && threadIdx.x == 0) {

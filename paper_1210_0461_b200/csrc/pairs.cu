@@ -1192,7 +1192,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
       auto claim = [&](int t, int64_t tb, uint32_t L, uint32_t pc, uint32_t i, uint2 tv,
                        uint32_t& dest, uint32_t& bb) -> uint32_t {
         const uint32_t p = pc + lane;
-        bool fast = false;
+        bool fast = false, slow = false;
         if (p < L && (!UPPER || p + 1 < L) && tv.x != kNone) {
           const uint32_t n = UPPER ? L - 1 - p : L;
           if (tv.x & kEntFlag) {
@@ -1207,18 +1207,62 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
             dest = tv.x < ns ? atomicAdd(&s_cnt[tv.x], n)
                              : (uint32_t)atomicAdd(&A.tile_cursor[tv.x], (unsigned long long)n);
           } else {
-            Pos q;
-            q.base = tb;
-            q.p = p;
-            q.L = L;
-            q.tx = (uint32_t)t;
-            q.valid = true;
-            stream_row<UPPER>(A, i, q, tv, [&](uint32_t t2, uint32_t b, uint32_t first, uint32_t n2) {
-              const unsigned long long p0 =
-                  t2 < ns ? (unsigned long long)atomicAdd(&s_cnt[t2], n2)
-                          : atomicAdd(&A.tile_cursor[t2], (unsigned long long)n2);
-              for (uint32_t k = 0; k < n2; ++k) A.words[p0 + k] = b + A.items[first + k];
-            });
+            slow = true;
+          }
+        }
+        // split (column-window) and filtered rows: one row at a time across
+        // the warp -- lanes take 32 suffix columns, group by destination tile
+        // (windows of a sorted suffix are contiguous), one claim per group,
+        // and the group's words are stored to consecutive positions
+        uint32_t sm = __ballot_sync(0xffffffffu, slow);
+        while (sm) {
+          const int r = __ffs(sm) - 1;
+          sm &= sm - 1;
+          const uint32_t ir = __shfl_sync(0xffffffffu, i, r);
+          const uint32_t tx = __shfl_sync(0xffffffffu, tv.x, r);
+          const uint32_t ty = __shfl_sync(0xffffffffu, tv.y, r);
+          const uint32_t tile = tx & kTileMask;
+          uint32_t c0 = 0, nwin = 1;
+          if (tx & kWinFlag) {
+            const Tile T0 = A.tiles[tile];
+            c0 = T0.c0;
+            nwin = T0.nwin;
+          }
+          const uint32_t hr = A.filter ? A.h_row[ir] : 0u;
+          for (uint32_t k0 = UPPER ? pc + r + 1 : 0; k0 < L; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            uint32_t dst = kNone, word = 0;
+            if (k < L) {
+              const uint32_t j = A.items[tb + k];
+              dst = tile;
+              word = ty + j;
+              if (tx & kWinFlag) {
+                const uint32_t w = j >= c0 ? (j - c0) / kStreamDenseCap : nwin;
+                if (w >= nwin) {
+                  dst = kNone;
+                } else {
+                  dst = tile + w;
+                  word = j - (c0 + w * kStreamDenseCap);  // window w starts at c0 + w * cap
+                }
+              }
+              if (A.filter && dst != kNone) {
+                uint32_t bk = hr + A.h_col[j];
+                if (bk >= A.kappa) bk -= A.kappa;
+                if (bk < A.start || bk >= A.stop) dst = kNone;
+              }
+            }
+            const uint32_t grp = __match_any_sync(0xffffffffu, dst);
+            if (dst != kNone) {
+              const int lead = __ffs(grp) - 1;
+              uint32_t p0 = 0;
+              if (lane == lead) {
+                const uint32_t cnt = __popc(grp);
+                p0 = dst < ns ? atomicAdd(&s_cnt[dst], cnt)
+                              : (uint32_t)atomicAdd(&A.tile_cursor[dst], (unsigned long long)cnt);
+              }
+              p0 = __shfl_sync(grp, p0, lead);
+              A.words[p0 + __popc(grp & ((1u << lane) - 1u))] = word;
+            }
           }
         }
         return __ballot_sync(0xffffffffu, fast);
@@ -2382,12 +2426,31 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
       for (uint32_t k = tid; k < kMaxShardCheck; k += kPlanThreads) s_ow[k] = 0;
       __threadfence_block();
       __syncthreads();
-      for (uint32_t t = tid; t < nt; t += kPlanThreads) {
-        uint32_t f = t;
-        if (is_window(P.tiles[t]))
-          while (P.tiles[f].nwin == 0 && f > 0) --f;  // the row's first window
-        const uint32_t ow = (uint32_t)P.tiles[f].slab_base;
-        atomicAdd(&s_ow[ow < kMaxShardCheck ? ow : kMaxShardCheck - 1], words_of(P.tiles[t]));
+      {
+        // per thread a contiguous tile range: a continuation window takes the
+        // owner of the tile before it (its row's previous window); the owner
+        // rarely changes inside a range, so one shared atomic per change
+        uint32_t cur = kNone;
+        unsigned long long acc = 0;
+        for (uint32_t t = a; t < b; ++t) {
+          const Tile& tl = P.tiles[t];
+          uint32_t ow;
+          if (is_window(tl) && tl.nwin == 0 && t > a) {
+            ow = cur;
+          } else {
+            uint32_t f = t;
+            if (is_window(tl))
+              while (P.tiles[f].nwin == 0 && f > 0) --f;  // the row's first window
+            ow = (uint32_t)P.tiles[f].slab_base;
+          }
+          if (ow != cur) {
+            if (cur != kNone) atomicAdd(&s_ow[cur < kMaxShardCheck ? cur : kMaxShardCheck - 1], acc);
+            cur = ow;
+            acc = 0;
+          }
+          acc += words_of(tl);
+        }
+        if (cur != kNone) atomicAdd(&s_ow[cur < kMaxShardCheck ? cur : kMaxShardCheck - 1], acc);
       }
       __syncthreads();
       unsigned long long mxw = 0;
@@ -2399,11 +2462,20 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
         return;
       }
     }
-    for (uint32_t t = tid; t < nt; t += kPlanThreads) {
-      uint32_t f = t;
-      if (is_window(P.tiles[t]))
-        while (P.tiles[f].nwin == 0 && f > 0) --f;
-      if (P.tiles[f].slab_base != P.shard_rank) P.tiles[t].n_units = 0;
+    {
+      // drop the other ranks' tiles (the owner walk reads slab_base and the
+      // window fields only, never n_units)
+      uint32_t cur = kNone;
+      for (uint32_t t = a; t < b; ++t) {
+        Tile& tl = P.tiles[t];
+        if (!(is_window(tl) && tl.nwin == 0 && t > a)) {
+          uint32_t f = t;
+          if (is_window(tl))
+            while (P.tiles[f].nwin == 0 && f > 0) --f;
+          cur = (uint32_t)P.tiles[f].slab_base;
+        }
+        if (cur != P.shard_rank) tl.n_units = 0;
+      }
     }
     __threadfence_block();
     __syncthreads();
@@ -2519,11 +2591,15 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
         const uint32_t pos = atomicAdd(&s_cur[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
         P.units[pos] = Unit{t, u};
       }
-    } else if (nu_t == 1) {
-      P.units[atomicAdd(&s_cur[kFracBins], 1u)] = Unit{t, 0};
     }
   }
-  (void)b_single;
+  {
+    // single-unit tiles after the split units, in tile order (the exclusive
+    // prefix of each thread's contiguous range: no shared counter)
+    uint64_t pos = s_cur[kFracBins] + b_single;
+    for (uint32_t t = tlo; t < thi; ++t)
+      if (nu_of(t) == 1) P.units[pos++] = Unit{t, 0};
+  }
   // per-tile stream words from the statistics (unfiltered, no windows): an
   // entry tile stores 2 words per row occurrence with a partner after it,
   // a hash tile one word per term

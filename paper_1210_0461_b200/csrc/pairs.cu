@@ -1096,6 +1096,32 @@ __device__ __forceinline__ void stream_row(const StreamRouteArgs& A, uint32_t i,
   if (run_n) fn(run_tile, run_base, run_start, run_n);
 }
 
+// Destination tile and word of column j of a split (column-window) or
+// filtered row (tx, ty = the row's item_info; c0, nwin = its first window's
+// start and count; hr = h_row of the row item): dst = kNone when the column
+// is past the last window or in another bucket interval. Same rules as
+// stream_row.
+__device__ __forceinline__ void split_row_dest(const StreamRouteArgs& A, uint32_t tx, uint32_t ty,
+                                               uint32_t c0, uint32_t nwin, uint32_t hr, uint32_t j,
+                                               uint32_t& dst, uint32_t& word) {
+  dst = tx & kTileMask;
+  word = ty + j;
+  if (tx & kWinFlag) {
+    const uint32_t w = j >= c0 ? (j - c0) / kStreamDenseCap : nwin;
+    if (w >= nwin) {
+      dst = kNone;
+      return;
+    }
+    dst += w;
+    word = j - (c0 + w * kStreamDenseCap);  // window w starts at c0 + w * cap
+  }
+  if (A.filter) {
+    uint32_t bk = hr + A.h_col[j];
+    if (bk >= A.kappa) bk -= A.kappa;
+    if (bk < A.start || bk >= A.stop) dst = kNone;
+  }
+}
+
 // B1: words per tile (shared counters per CTA, flushed once)
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArgs A) {
@@ -1103,6 +1129,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kOffBytes);
   const uint32_t ns = min(A.n_tiles, kTileSmem);
+  const int lane = threadIdx.x & 31;
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
   const int64_t n_chunks = (A.n_tx + A.chunk_tx - 1) / A.chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
@@ -1110,13 +1137,44 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
     const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, A.chunk_tx);
     walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
-      if (!q.valid) return;
-      // an entry row stores one (first column position, count) pair
-      stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t, uint32_t, uint32_t n) {
-        if (tv.x & kEntFlag) n = 2;
+      const bool live = q.valid && tv.x != kNone && !(UPPER && q.p + 1 >= q.L);
+      const bool slow = live && !(tv.x & kEntFlag) && ((tv.x & kWinFlag) || A.filter);
+      if (live && !slow) {
+        // one run: a word row's suffix, or an entry row's (first, count) pair
+        const uint32_t t = tv.x & kTileMask;
+        const uint32_t n = (tv.x & kEntFlag) ? 2u : q.L - (UPPER ? q.p + 1 : 0u);
         if (t < ns) atomicAdd(&s_cnt[t], n);
         else atomicAdd(&A.tile_words[t], (unsigned long long)n);
-      });
+      }
+      // split / filtered rows one at a time across the warp (as k_stream_write)
+      uint32_t sm = __ballot_sync(0xffffffffu, slow);
+      while (sm) {
+        const int r = __ffs(sm) - 1;
+        sm &= sm - 1;
+        const uint32_t ir = __shfl_sync(0xffffffffu, i, r);
+        const uint32_t tx = __shfl_sync(0xffffffffu, tv.x, r);
+        const uint32_t ty = __shfl_sync(0xffffffffu, tv.y, r);
+        const int64_t tb = __shfl_sync(0xffffffffu, q.base, r);
+        const uint32_t pr = __shfl_sync(0xffffffffu, q.p, r);
+        const uint32_t L = __shfl_sync(0xffffffffu, q.L, r);
+        uint32_t c0 = 0, nwin = 1;
+        if (tx & kWinFlag) {
+          const Tile T0 = A.tiles[tx & kTileMask];
+          c0 = T0.c0;
+          nwin = T0.nwin;
+        }
+        const uint32_t hr = A.filter ? A.h_row[ir] : 0u;
+        for (uint32_t k0 = UPPER ? pr + 1 : 0; k0 < L; k0 += 32) {
+          const uint32_t k = k0 + lane;
+          uint32_t dst = kNone, word = 0;
+          if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
+          const uint32_t grp = __match_any_sync(0xffffffffu, dst);
+          if (dst != kNone && lane == __ffs(grp) - 1) {
+            if (dst < ns) atomicAdd(&s_cnt[dst], (uint32_t)__popc(grp));
+            else atomicAdd(&A.tile_words[dst], (unsigned long long)__popc(grp));
+          }
+        }
+      }
     });
     // flush per chunk: shared u32 counts never exceed one chunk's words
     __syncthreads();
@@ -1232,25 +1290,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
           for (uint32_t k0 = UPPER ? pc + r + 1 : 0; k0 < L; k0 += 32) {
             const uint32_t k = k0 + lane;
             uint32_t dst = kNone, word = 0;
-            if (k < L) {
-              const uint32_t j = A.items[tb + k];
-              dst = tile;
-              word = ty + j;
-              if (tx & kWinFlag) {
-                const uint32_t w = j >= c0 ? (j - c0) / kStreamDenseCap : nwin;
-                if (w >= nwin) {
-                  dst = kNone;
-                } else {
-                  dst = tile + w;
-                  word = j - (c0 + w * kStreamDenseCap);  // window w starts at c0 + w * cap
-                }
-              }
-              if (A.filter && dst != kNone) {
-                uint32_t bk = hr + A.h_col[j];
-                if (bk >= A.kappa) bk -= A.kappa;
-                if (bk < A.start || bk >= A.stop) dst = kNone;
-              }
-            }
+            if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
             const uint32_t grp = __match_any_sync(0xffffffffu, dst);
             if (dst != kNone) {
               const int lead = __ffs(grp) - 1;

@@ -1213,13 +1213,43 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
     const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, A.chunk_tx);
     walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
-      if (!q.valid) return;
-      stream_row<UPPER>(A, i, q, tv, [&](uint32_t t, uint32_t, uint32_t, uint32_t n) {
-        if (tv.x & kEntFlag) n = 2;
-        if (t < ns) {
-          if (atomicAdd(&s_cnt[t], n) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = t;
+      // words per shared-counter tile (ids < ns; a split row's windows follow
+      // its first window's id, so a row whose first tile is >= ns is skipped)
+      const bool live = q.valid && tv.x != kNone && !(UPPER && q.p + 1 >= q.L) &&
+                        (tv.x & kTileMask) < ns;
+      const bool slow = live && !(tv.x & kEntFlag) && ((tv.x & kWinFlag) || A.filter);
+      if (live && !slow) {
+        const uint32_t t = tv.x & kTileMask;
+        const uint32_t n = (tv.x & kEntFlag) ? 2u : q.L - (UPPER ? q.p + 1 : 0u);
+        if (atomicAdd(&s_cnt[t], n) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = t;
+      }
+      uint32_t sm = __ballot_sync(0xffffffffu, slow);
+      while (sm) {
+        const int r = __ffs(sm) - 1;
+        sm &= sm - 1;
+        const uint32_t ir = __shfl_sync(0xffffffffu, i, r);
+        const uint32_t tx = __shfl_sync(0xffffffffu, tv.x, r);
+        const uint32_t ty = __shfl_sync(0xffffffffu, tv.y, r);
+        const int64_t tb = __shfl_sync(0xffffffffu, q.base, r);
+        const uint32_t pr = __shfl_sync(0xffffffffu, q.p, r);
+        const uint32_t L = __shfl_sync(0xffffffffu, q.L, r);
+        uint32_t c0 = 0, nwin = 1;
+        if (tx & kWinFlag) {
+          const Tile T0 = A.tiles[tx & kTileMask];
+          c0 = T0.c0;
+          nwin = T0.nwin;
         }
-      });
+        const uint32_t hr = A.filter ? A.h_row[ir] : 0u;
+        for (uint32_t k0 = UPPER ? pr + 1 : 0; k0 < L; k0 += 32) {
+          const uint32_t k = k0 + lane;
+          uint32_t dst = kNone, word = 0;
+          if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
+          if (dst >= ns) dst = kNone;
+          const uint32_t grp = __match_any_sync(0xffffffffu, dst);
+          if (dst != kNone && lane == __ffs(grp) - 1)
+            if (atomicAdd(&s_cnt[dst], (uint32_t)__popc(grp)) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = dst;
+        }
+      }
     });
     __syncthreads();
     const uint32_t n_touch = s_misc[0];
@@ -2218,15 +2248,17 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   for (uint32_t base = 0; base < n; base += kPlanChunk) {
     const uint32_t cn = min(kPlanChunk, n - base);
     // classify: 1 H, 2 W (record = #windows), 3 L1, 4 L (record = weight), 0 none
-    unsigned long long st8[kPlanRowsPerThread];
+    // rows in batches of 8 loads in flight (registers: 64 per thread)
+    for (uint32_t qb = 0; qb < kPlanRowsPerThread; qb += 8) {
+    unsigned long long st8[8];
 #pragma unroll
-    for (uint32_t q = 0; q < kPlanRowsPerThread; ++q) {
-      const uint32_t k = tid + q * kPlanThreads;
+    for (uint32_t q = 0; q < 8; ++q) {
+      const uint32_t k = tid + (qb + q) * kPlanThreads;
       st8[q] = k < cn ? P.stats[base + k] : 0ull;
     }
 #pragma unroll
-    for (uint32_t q = 0; q < kPlanRowsPerThread; ++q) {
-      const uint32_t k = tid + q * kPlanThreads;
+    for (uint32_t q = 0; q < 8; ++q) {
+      const uint32_t k = tid + (qb + q) * kPlanThreads;
       if (k >= cn) break;
       const uint32_t i = base + k;
       const uint64_t t = st8[q] & (kOccOne - 1);
@@ -2249,6 +2281,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
         }
       }
       s_rec[k] = rec;
+    }
     }
     __syncthreads();
     stamp(1);

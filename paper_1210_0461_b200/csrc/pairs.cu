@@ -1818,23 +1818,30 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
         count_suffix_entries<false>(A.items, reinterpret_cast<const uint2*>(A.words + wb), w0, w1, table, T.c0);
       }
     } else {
-    const uint32_t nb = (uint32_t)((w1 - w0 + BW - 1) / BW);
-    const uint32_t* wp = A.words + wb + w0 + lane;
+    // CTA-wide blocks of kSCThreads * D words: lane (warp, lane) reads word
+    // warp * 32 + lane + k * kSCThreads of each block (coalesced per warp),
+    // so every warp gets an equal share even of a small unit (c3's sparse
+    // windows and light tiles hold a few thousand words)
+    constexpr uint32_t CB = kSCThreads * D;
+    const uint64_t nw = w1 - w0;
+    const uint32_t nb = (uint32_t)((nw + CB - 1) / CB);
+    const uint32_t* wp = A.words + wb + w0 + warp * 32 + lane;
     auto fetch = [&](uint32_t blk, uint32_t (&v)[D]) {
-      const uint32_t* p = wp + (uint64_t)blk * BW;
-      if ((uint64_t)(blk + 1) * BW <= w1 - w0) {
+      const uint32_t* p = wp + (uint64_t)blk * CB;
+      if ((uint64_t)(blk + 1) * CB <= nw) {
 #pragma unroll
-        for (int k = 0; k < D; ++k) v[k] = __ldcs(p + k * 32);
+        for (int k = 0; k < D; ++k) v[k] = __ldcs(p + k * kSCThreads);
       } else {
-        const uint64_t left = (w1 - w0) - (uint64_t)blk * BW;
+        const uint64_t left = nw - (uint64_t)blk * CB;
 #pragma unroll
-        for (int k = 0; k < D; ++k) v[k] = (uint64_t)(k * 32 + lane) < left ? __ldcs(p + k * 32) : kEmpty32;
+        for (int k = 0; k < D; ++k)
+          v[k] = (uint64_t)(k * kSCThreads + warp * 32 + lane) < left ? __ldcs(p + k * kSCThreads) : kEmpty32;
       }
     };
     uint32_t cur[D], nxt[D];
-    if ((uint32_t)warp < nb) fetch(warp, cur);
-    for (uint32_t blk = warp; blk < nb; blk += kSCWarps) {
-      if (blk + kSCWarps < nb) fetch(blk + kSCWarps, nxt);
+    if (nb > 0) fetch(0, cur);
+    for (uint32_t blk = 0; blk < nb; ++blk) {
+      if (blk + 1 < nb) fetch(blk + 1, nxt);
       if (dense) {
 #pragma unroll
         for (int k = 0; k < D; ++k)
@@ -2476,15 +2483,28 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
       return 2 + (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms);
     };
     auto cost = [&](const Tile& tl) -> unsigned long long {
+      // a sparse column window counts in a hash table sized to its words
+      // (k_count_stream hwin): cost it as a hash tile of its average words
+      if (is_window(tl) && tl.n_units == 1 && tl.terms <= kSparseWindowWords) {
+        Tile h = tl;
+        h.mode = 1;
+        return tile_cost(h, stream_hash_slots(tl.terms));
+      }
       return tile_cost(tl, stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap));
     };
     __shared__ unsigned long long s_ow[kMaxShardCheck];
     // pass 0: shares of the counting cost; if a share's words pass the
-    // 32-bit word positions, pass 1: shares of the words; if even those do
-    // not fit, every rank asks for a finer split (the decision depends only
+    // 32-bit word positions, shares of the words (plus a per-unit overhead,
+    // then without it); if even those do not fit, every rank asks for a
+    // finer split (the decision depends only
     // on the whole plan, so all ranks agree)
-    for (int pass = 0; pass < 2; ++pass) {
-      auto metric = [&](const Tile& tl) { return pass == 0 ? cost(tl) : words_of(tl); };
+    // (pass 1 adds a per-unit overhead to the words: ~2,048 words' worth of
+    // clearing, compaction and unit scheduling; pass 2 is words only)
+    for (int pass = 0; pass < 3; ++pass) {
+      auto metric = [&](const Tile& tl) -> unsigned long long {
+        if (pass == 0) return cost(tl);
+        return words_of(tl) + (pass == 1 ? 2048ull * (tl.n_units ? tl.n_units : 1) : 0ull);
+      };
       unsigned long long tsum = 0, all;
       for (uint32_t t = a; t < b; ++t) tsum += metric(P.tiles[t]);
       unsigned long long pre = plan_block_scan<unsigned long long>(tsum, s_u64, 0ull, add, all);
@@ -2530,7 +2550,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
       for (uint32_t k = tid; k < kMaxShardCheck; k += kPlanThreads) mxw = s_ow[k] > mxw ? s_ow[k] : mxw;
       plan_block_scan<long long>((long long)mxw, s_i64, 0ll, mx, totl);
       if (totl + 2 < (1ll << 32)) break;
-      if (pass == 1) {
+      if (pass == 2) {
         if (tid == 0) P.out->overflow = 2;
         return;
       }

@@ -144,6 +144,17 @@ int crop_topk_fused(const uint32_t* row, const uint32_t* col, const uint32_t* co
                     const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k, uint32_t* hist,
                     const uint64_t* hi_list, const uint64_t* hi_n, uint64_t* out_idx,
                     uint64_t* d_k_out, void* stream);
+/* Per-partition top-l select: the summaries of the bounded Space-Saving
+ * regime (spacesaving.py:39-63 with capacity l; engine.py:108-176 queries).
+ * For every bucket b = (h_row[row] + h_col[col]) mod kappa holding >= l
+ * entries: recorded[e] = 1 for its top-l entries by (count desc, row asc, col
+ * asc), 0 for the rest, bucket_min[b] = the count of its l-th entry; buckets
+ * with fewer entries record everything (bucket_min 0). bucket_total[b]
+ * (nullable) = entries per bucket. recorded may be NULL (minima only). */
+int crop_bucket_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
+                     const uint64_t* d_n_entries, uint64_t n_capacity, const uint32_t* h_row,
+                     const uint32_t* h_col, uint32_t kappa, uint32_t capacity, uint8_t* recorded,
+                     uint32_t* bucket_min, uint32_t* bucket_total, void* stream);
 void crop_pairs_destroy(crop_pairs* job);
 
 /* Per-instance bucket statistics of counted entries (the LoadReport rows,

@@ -53,6 +53,7 @@ _SIGS = {
     "crop_fimi_free": (None, [P]),
     "crop_pairs_set_topk": (i32, [P, P, P, P, u64]),
     "crop_topk_fused": (i32, [P, P, P, P, u64, u32, P, P, P, P, P, P]),
+    "crop_bucket_topk": (i32, [P, P, P, P, u64, P, P, u32, u32, P, P, P, P]),
     "crop_pairs_destroy": (None, [P]),
     "crop_entry_bucket_stats": (i32, [P, P, P, P, u64, i32, u32, P, P, u32, P, P, P, P, P]),
     "crop_entry_buckets": (i32, [P, P, u64, P, P, u32, P, P]),

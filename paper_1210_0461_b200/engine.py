@@ -176,6 +176,17 @@ class _DeviceResult:
             inst.bucket_min = np.zeros(self.kappa)
             if not full.any():
                 continue
+            if self.integer:
+                # native per-bucket top-l select (csrc/bucket_topk.cu): same
+                # order (weight desc, row, col), no 2^31-element sort limit
+                from .kernels import bucket_topk
+
+                mask, bmin, _ = bucket_topk(e, inst.tables[0], inst.tables[1], self.kappa, cap,
+                                            want_mask=bool(overflow.any()))
+                if overflow.any():
+                    inst.recorded = mask
+                inst.bucket_min = bmin.cpu().numpy().astype(np.float64)
+                continue
             w_all = e.weights_f64()
             from .kernels import entry_buckets
 

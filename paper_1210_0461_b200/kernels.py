@@ -398,6 +398,25 @@ def topk_indices(ent: DeviceEntries, k: int, count: torch.Tensor | None = None) 
     return out[: int(kout.item())]
 
 
+def bucket_topk(ent: DeviceEntries, h_row, h_col, kappa: int, capacity: int, want_mask: bool = True):
+    """Per-bucket top-`capacity` of integer entries by (count desc, row, col):
+    (recorded bool[n] or None, bucket_min int64[kappa], bucket_total int64[kappa])
+    -- the bounded Space-Saving summaries (csrc/bucket_topk.cu)."""
+    dev = ent.row.device
+    n_dev = getattr(ent, "n_dev", None)
+    if n_dev is None:
+        n_dev = torch.tensor([ent.n], dtype=torch.int64, device=dev)
+    cap = min(int(capacity), 0xFFFFFFFF)
+    rec = torch.empty(max(ent.n, 1), dtype=torch.uint8, device=dev) if want_mask else None
+    bmin = torch.empty(kappa, dtype=torch.int32, device=dev)
+    btot = torch.empty(kappa, dtype=torch.int32, device=dev)
+    nat.call("crop_bucket_topk", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev),
+             ent.row.shape[0], nat.ptr(h_row), nat.ptr(h_col), int(kappa), cap,
+             nat.ptr(rec) if rec is not None else None, nat.ptr(bmin), nat.ptr(btot), nat.stream_ptr())
+    mask = rec[: ent.n].to(torch.bool) if rec is not None else None
+    return mask, bmin.to(torch.int64) & U32_MASK, btot.to(torch.int64) & U32_MASK
+
+
 # ------------------------------------------------------------------ K5 outer
 
 def outer_product(ds: DeviceOuterStream, upper_only: bool = False, kappa: int = 1, start: int = 0,

@@ -1,0 +1,86 @@
+"""Per-partition top-l select (csrc/bucket_topk.cu) against a plain torch
+ranking of the same entries: per bucket, the top-l entries by (count desc,
+row asc, col asc) and the count of the l-th (engine.finalize_summaries'
+bounded Space-Saving regime, spacesaving.py:39-63)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1210_0461_b200 as crop  # noqa: E402
+from paper_1210_0461_b200 import kernels  # noqa: E402
+
+
+def _reference(row, col, cnt, b, kappa, cap):
+    """torch: stable sorts by col, row, count desc, bucket -> rank in bucket."""
+    n = row.shape[0]
+    order = torch.arange(n, device=row.device)
+    for key in (col.to(torch.int64), row.to(torch.int64)):
+        order = order[torch.sort(key[order], stable=True).indices]
+    order = order[torch.sort(cnt.to(torch.int64)[order], descending=True, stable=True).indices]
+    order = order[torch.sort(b[order], stable=True).indices]
+    bs = b[order]
+    first = torch.searchsorted(bs, bs, right=False)
+    rank = torch.arange(n, device=row.device) - first
+    rec = torch.zeros(n, dtype=torch.bool, device=row.device)
+    rec[order] = rank < cap
+    total = torch.bincount(b, minlength=kappa)
+    bmin = torch.zeros(kappa, dtype=torch.int64, device=row.device)
+    last = rank == cap - 1
+    bmin[bs[last]] = cnt.to(torch.int64)[order][last]
+    full = total >= cap
+    rec[~full[b]] = True
+    return rec, bmin, total
+
+
+@pytest.mark.parametrize("kappa,cap,n,maxc", [(1, 5, 1000, 3), (4, 50, 20_000, 10), (8, 1000, 200_000, 4),
+                                              (31, 7, 5000, 2), (33, 100, 50_000, 50),
+                                              (1184, 65, 300_000, 1000), (300, 1, 40_000, 6)])
+def test_bucket_topk_matches_torch_ranking(kappa, cap, n, maxc):
+    g = torch.Generator(device="cpu").manual_seed(kappa * 7 + cap)
+    n_items = 4096
+    # distinct (row, col) pairs, row < col; counts with many ties
+    keys = torch.unique(torch.randint(0, n_items * n_items, (n,), generator=g))
+    row, col = keys // n_items, keys % n_items
+    keep = row != col
+    row, col = torch.minimum(row, col)[keep], torch.maximum(row, col)[keep]
+    k2 = torch.unique(row * n_items + col)
+    row, col = (k2 // n_items).to(torch.int32), (k2 % n_items).to(torch.int32)
+    perm = torch.randperm(row.shape[0], generator=g)
+    row, col = row[perm].cuda(), col[perm].cuda()
+    cnt = (torch.randint(1, maxc + 1, (row.shape[0],), generator=g) ** 2).to(torch.int32).cuda()
+    h = crop.make_hashes(crop.HashConfig(kappa, 11))
+    hr, hc = kernels.hash_tables(h, n_items)
+    b = kernels.entry_buckets(row, col, row.shape[0], hr, hc, kappa).to(torch.int64)
+    ent = kernels.DeviceEntries(row, col, cnt, None, row.shape[0], int(cnt.sum()))
+    mask, bmin, btot = kernels.bucket_topk(ent, hr, hc, kappa, cap)
+    rec, want_min, want_tot = _reference(row, col, cnt, b, kappa, cap)
+    assert torch.equal(btot, want_tot)
+    assert torch.equal(bmin, want_min)
+    assert torch.equal(mask, rec)
+    # exactly min(cap, total) recorded per bucket
+    per = torch.bincount(b[mask], minlength=kappa)
+    assert torch.equal(per, torch.minimum(want_tot, torch.full_like(want_tot, cap)))
+
+
+def test_bounded_regime_through_the_api():
+    """crop.run with a small Space-Saving capacity: the summaries satisfy the
+    reference guarantees (sandwich, over <= m/l, capture of heavy entries)."""
+    rng = np.random.default_rng(3)
+    tx = [sorted(rng.choice(60, size=rng.integers(2, 12), replace=False).tolist()) for _ in range(3000)]
+    cfg = crop.EngineConfig(kappa=5, ss_capacity=40, workers=5, seed=2, cs_enabled=False)
+    state, report = crop.run(crop.transactions_to_stream(tx), cfg, upper_triangle_only=True)
+    sup = crop.exact_pair_supports(tx)
+    for inst in state.instances:
+        for bkt, s in inst.summaries.items():
+            m = s.total_weight
+            recs = s.records()
+            assert len(recs) <= cfg.ss_capacity
+            for item, c, over in recs:
+                assert c - over <= sup[item] <= c
+                assert over <= m / cfg.ss_capacity
+    for (i, j), true in sup.items():
+        lo, up, _ = state.query((i, j))
+        assert lo <= true <= up

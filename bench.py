@@ -6,7 +6,10 @@
 A step is one pass of the hot path over the whole synthetic workload of the
 configuration (default c2 = BASELINE.json configs[1], the 1-GPU exact pair
 count): per-item term scan + tile plan, routing, shared-memory counting of
-every pair term (i < j) of the GPU's tile share, and the top-k select.
+every pair term (i < j) of the GPU's tile share, the per-bucket top-l
+Space-Saving summaries when the config bounds them (c3: l = 65,536 per
+bucket), and the top-k select. `--config c3|c4|c5` measures the other
+configurations (c4 through the real-valued product path).
 Inputs are resident in HBM; L2 is flushed (1 GiB write) before every timed
 step. `value` = all terms of the workload / (max over ranks of the summed
 per-step CUDA-event time). `e2e` runs the public API (`crop.run` +
@@ -210,6 +213,10 @@ def run_ours(args, rank, world):
             ent.n = int(ent.n_dev.item())
             if ent.n > ent.capacity or job.overflowed():
                 raise RuntimeError("pair engine overflow")
+        if cfg.ss_capacity:
+            # bounded Space-Saving regime (c3): per-bucket top-l summaries
+            # (with N > 1, each rank's candidates for its share of every bucket)
+            kernels.bucket_topk(ent, tables[0], tables[1], cfg.kappa, cfg.ss_capacity)
         idx = kernels.topk_indices(ent, cfg.top_k)
         top = (ent.row[idx], ent.col[idx], ent.count[idx])
         if world > 1:
@@ -329,6 +336,7 @@ def run_ours(args, rank, world):
                        "zipf_s": cfg.zipf_s, "length": list(cfg.length), "kappa": cfg.kappa,
                        "sharding": f"tiles split by terms over {world} GPU(s), all {cfg.kappa} buckets",
                        "top_k": cfg.top_k,
+                       "ss_capacity": cfg.ss_capacity,
                        "terms": total_terms_all, "entries": own_entries if world == 1 else None,
                        "tiles": stats[2], "units": stats[3], "parallelism": f"tiles{world}",
                        "l2": "flushed (1 GiB write) before every timed step",

@@ -76,7 +76,7 @@ def test_bounded_regime_through_the_api():
     for inst in state.instances:
         for bkt, s in inst.summaries.items():
             m = s.total_weight
-            recs = s.records()
+            recs = list(s.records())
             assert len(recs) <= cfg.ss_capacity
             for item, c, over in recs:
                 assert c - over <= sup[item] <= c

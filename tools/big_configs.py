@@ -67,6 +67,17 @@ for r in ranks:
         if it < iters - 1:
             del ent
             torch.cuda.empty_cache()
+    if cfg.ss_capacity and n <= ent.capacity:
+        ent.n = n
+        for _ in range(2):
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record()
+            mask, bmin, btot = kernels.bucket_topk(ent, tab[0], tab[1], cfg.kappa, cfg.ss_capacity)
+            b1.record()
+            torch.cuda.synchronize()
+        print(f"  rank {r}: per-bucket top-{cfg.ss_capacity} summaries {b0.elapsed_time(b1):.3f} ms, "
+              f"recorded {int(mask.sum())}, full buckets {int((btot >= cfg.ss_capacity).sum())}", flush=True)
+        del mask
     if n <= ent.capacity:
         s = int(ent.count[:n].to(torch.int64).sum().item())
         mx = int(ent.count[:n].max().item())

@@ -21,8 +21,13 @@
 //                unique inside a bucket, so exactly l entries per full bucket)
 // Pass 0 also yields each bucket's distinct count: buckets with fewer than l
 // entries keep everything (bucket_min 0), buckets with exactly l are full.
+// That flat form serves kappa <= 32 (histograms privatised per CTA); for
+// 32 < kappa <= 4096 (c3: 1184) the entries of the full buckets are grouped
+// into per-bucket segments and each bucket is selected by one CTA with its
+// histogram in shared memory (k_bt_seg_*; CROP_BT_FLAT=1 forces the flat form).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -113,6 +118,10 @@ __global__ void __launch_bounds__(kBtThreads)
       if (bkt) bkt[e] = (uint16_t)b;
       a[0] &= kc; a[1] &= i; a[2] &= j;
       o[0] |= kc; o[1] |= i; o[2] |= j;
+    }
+    if (priv && kappa >= 256) {
+      if (b != 0xFFFFFFFFu) atomicAdd(&s_tot[b], 1u);
+      continue;
     }
     const uint32_t grp = __match_any_sync(0xffffffffu, b);
     if (b != 0xFFFFFFFFu && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) {
@@ -295,6 +304,333 @@ __global__ void k_bt_mark(const uint32_t* __restrict__ row, const uint32_t* __re
   }
 }
 
+// ---------------------------------------------------------------- segmented
+// kappa in (32, 4096]: the per-pass global histograms of the flat path take
+// one L2 atomic per entry (hot (bucket, digit) slots when most counts tie),
+// so the active buckets' entries are first grouped into one contiguous
+// segment per bucket and each bucket is then selected by one CTA with its
+// histogram in shared memory:
+//   k_bt_seg_scan    segment offsets of the active buckets (one block)
+//   k_bt_scatter     per CTA, a contiguous range of entries: count per
+//                    bucket in shared memory, one global claim per touched
+//                    bucket, then write (~count, row, col) into the claims
+//   k_bt_seg_select  one CTA per active bucket: MSD radix select of the
+//                    96-bit key over its segment; once the keys matching
+//                    the decided prefix fit in shared memory they are staged
+//                    there by the next pass and later passes read only them
+constexpr uint32_t kBtSegMaxKappa = 4096;
+constexpr int kBtSegThreads = 512;
+constexpr uint32_t kBtSegStage = 4096;  // staged keys (3 x u32: 48 KB)
+
+__global__ void __launch_bounds__(1024) k_bt_seg_scan(uint32_t kappa, const BtState* __restrict__ st,
+                                                      uint32_t* __restrict__ seg_off,
+                                                      uint32_t* __restrict__ seg_cur) {
+  __shared__ uint32_t s_part[1024];
+  const uint32_t per = (kappa + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = min(kappa, threadIdx.x * per), hi = min(kappa, lo + per);
+  uint32_t sum = 0;
+  for (uint32_t b = lo; b < hi; ++b) sum += st[b].active ? st[b].total : 0u;
+  s_part[threadIdx.x] = sum;
+  __syncthreads();
+  for (uint32_t d = 1; d < blockDim.x; d <<= 1) {
+    const uint32_t v = threadIdx.x >= d ? s_part[threadIdx.x - d] : 0u;
+    __syncthreads();
+    s_part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = s_part[threadIdx.x] - sum;
+  for (uint32_t b = lo; b < hi; ++b) {
+    seg_off[b] = run;
+    seg_cur[b] = run;
+    run += st[b].active ? st[b].total : 0u;
+  }
+}
+
+// tiles of kScTile entries are grouped by bucket in shared memory first, so
+// each bucket's entries of a tile leave as one contiguous run (consecutive
+// lanes, consecutive addresses) that continues the previous tile's run
+constexpr int kScThreads = 1024;
+constexpr uint32_t kScPer = 8;
+constexpr uint32_t kScTile = kScThreads * kScPer;
+constexpr size_t kScSmem = (size_t)(2 * kBtSegMaxKappa + 32 + kBtSegMaxKappa / 32 + 3 * kScTile) * 4 +
+                           (size_t)kScTile * 2;
+
+__global__ void __launch_bounds__(kScThreads, 1)
+    k_bt_scatter(const uint32_t* __restrict__ row, const uint32_t* __restrict__ col,
+                 const uint32_t* __restrict__ count, const uint64_t* __restrict__ d_n,
+                 const uint16_t* __restrict__ bkt, uint32_t kappa, const BtState* __restrict__ st,
+                 uint32_t* __restrict__ seg_cur, uint32_t* __restrict__ s_k0,
+                 uint32_t* __restrict__ s_row, uint32_t* __restrict__ s_col) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* s_cur = sm;                            // [kappa] this CTA's write cursor per bucket
+  uint32_t* s_cnt = s_cur + kBtSegMaxKappa;        // [kappa + 1] tile counts -> offsets
+  uint32_t* s_act = s_cnt + kBtSegMaxKappa + 32;   // [kappa / 32] active-bucket bits
+  uint32_t* stg = s_act + kBtSegMaxKappa / 32;     // [3][kScTile] staged keys
+  uint16_t* s_b = reinterpret_cast<uint16_t*>(stg + 3 * kScTile);  // [kScTile] their buckets
+  __shared__ uint32_t s_warp[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) s_cur[b] = 0;
+  for (uint32_t k = threadIdx.x; k < (kappa + 31) / 32; k += blockDim.x) {
+    uint32_t bits = 0;
+    for (uint32_t q = 0; q < 32 && k * 32 + q < kappa; ++q) bits |= (st[k * 32 + q].active ? 1u : 0u) << q;
+    s_act[k] = bits;
+  }
+  __syncthreads();
+  auto active = [&](uint32_t b) { return b < kappa && ((s_act[b >> 5] >> (b & 31)) & 1u); };
+  const uint64_t n = *d_n;
+  const uint64_t per = (((n + gridDim.x - 1) / gridDim.x) + 31) & ~31ull;
+  const uint64_t lo = min(n, blockIdx.x * per), hi = min(n, lo + per);
+  // 1: this CTA's entries per active bucket, one global claim per bucket
+  for (uint64_t e0 = lo; e0 < hi; e0 += kScTile) {
+    uint32_t bb[kScPer];
+#pragma unroll
+    for (uint32_t u = 0; u < kScPer; ++u) {
+      const uint64_t e = e0 + u * blockDim.x + threadIdx.x;
+      bb[u] = e < hi ? bkt[e] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kScPer; ++u)
+      if (active(bb[u])) atomicAdd(&s_cur[bb[u]], 1u);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) {
+    const uint32_t c = s_cur[b];
+    if (c) s_cur[b] = atomicAdd(&seg_cur[b], c);
+  }
+  // 2: per tile, group by bucket in shared memory, then write the runs
+  const uint32_t per_t = (kappa + blockDim.x - 1) / blockDim.x;  // scan elements per thread (<= 4)
+  for (uint64_t e0 = lo; e0 < hi; e0 += kScTile) {
+    for (uint32_t b = threadIdx.x; b <= kappa; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    uint32_t bb[kScPer], kc[kScPer], ii[kScPer], jj[kScPer], rk[kScPer];
+#pragma unroll
+    for (uint32_t u = 0; u < kScPer; ++u) {
+      const uint64_t e = e0 + u * blockDim.x + threadIdx.x;
+      const bool ok = e < hi;
+      bb[u] = ok ? bkt[e] : 0xFFFFFFFFu;
+      kc[u] = ok ? ~__ldcs(count + e) : 0u;
+      ii[u] = ok ? __ldcs(row + e) : 0u;
+      jj[u] = ok ? __ldcs(col + e) : 0u;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kScPer; ++u) {
+      if (!active(bb[u])) bb[u] = 0xFFFFFFFFu;
+      rk[u] = bb[u] != 0xFFFFFFFFu ? atomicAdd(&s_cnt[bb[u]], 1u) : 0u;
+    }
+    __syncthreads();
+    // exclusive scan of s_cnt[0, kappa) in place; s_cnt[kappa] = tile total
+    {
+      const uint32_t b0 = threadIdx.x * per_t;
+      uint32_t v[4] = {0u, 0u, 0u, 0u}, sum = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k)
+        if (k < per_t && b0 + k < kappa) {
+          v[k] = s_cnt[b0 + k];
+          sum += v[k];
+        }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t wv = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
+        uint32_t wi = wv;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
+          if (lane >= d) wi += t;
+        }
+        s_warp[lane] = wi - wv;
+        if (lane == 31) s_cnt[kappa] = wi;
+      }
+      __syncthreads();
+      uint32_t run = s_warp[warp] + incl - sum;
+#pragma unroll
+      for (uint32_t k = 0; k < 4; ++k)
+        if (k < per_t && b0 + k < kappa) {
+          s_cnt[b0 + k] = run;
+          run += v[k];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t u = 0; u < kScPer; ++u)
+      if (bb[u] != 0xFFFFFFFFu) {
+        const uint32_t t = s_cnt[bb[u]] + rk[u];
+        stg[t] = kc[u];
+        stg[kScTile + t] = ii[u];
+        stg[2 * kScTile + t] = jj[u];
+        s_b[t] = (uint16_t)bb[u];
+      }
+    __syncthreads();
+    const uint32_t total = s_cnt[kappa];
+    for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+      const uint32_t b = s_b[t];
+      const uint32_t dst = s_cur[b] + (t - s_cnt[b]);
+      s_k0[dst] = stg[t];
+      s_row[dst] = stg[kScTile + t];
+      s_col[dst] = stg[2 * kScTile + t];
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) {
+      const uint32_t nb = b + 1 < kappa ? s_cnt[b + 1] : total;
+      s_cur[b] += nb - s_cnt[b];
+    }
+    __syncthreads();
+  }
+}
+
+// does key word set kw agree with the prefix on the digits decided before p?
+// (register arrays indexed by constants only: no local memory)
+__device__ __forceinline__ uint32_t bt_pick(const uint32_t (&v)[3], uint32_t w) {
+  return w == 0 ? v[0] : (w == 1 ? v[1] : v[2]);
+}
+
+__device__ __forceinline__ bool bt_prefix_match(const uint32_t (&kw)[3], const uint32_t (&key)[3],
+                                                uint32_t p) {
+  const uint32_t w = p >> 2, q = p & 3;
+  if (w > 0 && kw[0] != key[0]) return false;
+  if (w > 1 && kw[1] != key[1]) return false;
+  if (q == 0) return true;
+  const uint32_t sh = 32 - 8 * q;
+  return (bt_pick(kw, w) >> sh) == (bt_pick(key, w) >> sh);
+}
+
+// one histogram add per lane; a warp whose lanes all hold the same digit
+// (the common case when most counts tie) adds once
+__device__ __forceinline__ void bt_hist_add(uint32_t* hist, uint32_t d) {
+  const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+  if (__all_sync(0xffffffffu, d == d0)) {
+    if ((threadIdx.x & 31) == 0 && d0 < 256) atomicAdd(&hist[d0], 32u);
+  } else if (d < 256) {
+    atomicAdd(&hist[d], 1u);
+  }
+}
+
+__global__ void __launch_bounds__(kBtSegThreads)
+    k_bt_seg_select(const uint32_t* __restrict__ s_k0g, const uint32_t* __restrict__ s_rowg,
+                    const uint32_t* __restrict__ s_colg, const uint32_t* __restrict__ seg_off,
+                    BtState* __restrict__ st, const uint32_t* __restrict__ andor) {
+  extern __shared__ __align__(16) uint32_t stage[];  // [3][kBtSegStage]
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_sel[3];
+  __shared__ uint32_t s_n;
+  const uint32_t b = blockIdx.x;
+  const BtState s = st[b];
+  if (!s.active) return;
+  const uint32_t off = seg_off[b], m = s.total;
+  const uint32_t* gk[3] = {s_k0g + off, s_rowg + off, s_colg + off};
+  uint32_t key[3] = {0u, 0u, 0u};
+  uint32_t need = s.need, match = m, ns = 0;
+  bool staged = false;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t p = 0; p < 12; ++p) {
+    const uint32_t w = p >> 2, sh = 24 - 8 * (p & 3);
+    if (bt_constant_digit(andor, p)) {
+      const uint32_t dg = ((andor[w] >> sh) & 0xFFu) << sh;
+      key[0] |= w == 0 ? dg : 0u;
+      key[1] |= w == 1 ? dg : 0u;
+      key[2] |= w == 2 ? dg : 0u;
+      continue;
+    }
+    for (uint32_t k = threadIdx.x; k < 256; k += blockDim.x) hist[k] = 0;
+    if (threadIdx.x == 0) s_n = 0;
+    const bool stage_now = !staged && match <= kBtSegStage;
+    __syncthreads();
+    if (staged) {
+      for (uint32_t e0 = 0; e0 < ns; e0 += blockDim.x) {
+        const uint32_t e = e0 + threadIdx.x;
+        uint32_t d = 0xFFFFFFFFu;
+        if (e < ns) {
+          const uint32_t kw[3] = {stage[e], stage[kBtSegStage + e], stage[2 * kBtSegStage + e]};
+          if (bt_prefix_match(kw, key, p)) d = (bt_pick(kw, w) >> sh) & 0xFFu;
+        }
+        bt_hist_add(hist, d);
+      }
+    } else {
+      // U entries per thread per step, all loads issued before any is used
+      constexpr uint32_t U = 4;
+      const uint32_t nw = stage_now ? 3 : w + 1;  // key words this pass reads
+      for (uint32_t e0 = 0; e0 < m; e0 += U * blockDim.x) {
+        uint32_t kw[U][3];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          const bool ok = e < m;
+          kw[u][0] = ok ? __ldcs(gk[0] + e) : 0u;
+          kw[u][1] = ok && nw > 1 ? __ldcs(gk[1] + e) : 0u;
+          kw[u][2] = ok && nw > 2 ? __ldcs(gk[2] + e) : 0u;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          uint32_t d = 0xFFFFFFFFu;
+          if (e < m && bt_prefix_match(kw[u], key, p)) {
+            d = (bt_pick(kw[u], w) >> sh) & 0xFFu;
+            if (stage_now) {
+              const uint32_t q = atomicAdd(&s_n, 1u);
+              stage[q] = kw[u][0];
+              stage[kBtSegStage + q] = kw[u][1];
+              stage[2 * kBtSegStage + q] = kw[u][2];
+            }
+          }
+          bt_hist_add(hist, d);
+        }
+      }
+    }
+    __syncthreads();
+    if (stage_now) {
+      staged = true;
+      ns = s_n;
+    }
+    if (threadIdx.x < 32) {
+      uint32_t v[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        v[k] = hist[lane * 8 + k];
+        sum += v[k];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += u;
+      }
+      const uint32_t excl = incl - sum;
+      if (excl < need && need <= incl) {
+        uint32_t c = excl;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (c < need && need <= c + v[k]) {
+            s_sel[0] = lane * 8 + k;
+            s_sel[1] = c;
+            s_sel[2] = v[k];
+          }
+          c += v[k];
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t dg = s_sel[0] << sh;
+    key[0] |= w == 0 ? dg : 0u;
+    key[1] |= w == 1 ? dg : 0u;
+    key[2] |= w == 2 ? dg : 0u;
+    need -= s_sel[1];
+    match = s_sel[2];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st[b].key[0] = key[0];
+    st[b].key[1] = key[1];
+    st[b].key[2] = key[2];
+    st[b].need = need;
+  }
+}
+
 __global__ void k_bt_out(uint32_t kappa, const BtState* __restrict__ st, uint32_t* __restrict__ bucket_min,
                          uint32_t* __restrict__ bucket_total) {
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < kappa; b += gridDim.x * blockDim.x) {
@@ -334,6 +670,50 @@ extern "C" int crop_bucket_topk(const uint32_t* row, const uint32_t* col, const 
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((n_capacity + kBtThreads - 1) / kBtThreads,
                                                                  (uint64_t)kNumSMs * 4));
   const int sel_grid = (int)((kappa + 7) / 8);
+  // segmented select (see k_bt_seg_select) when the buckets are too many
+  // for privatised histograms but few enough for per-CTA bucket counters
+  const bool segmented = kappa > kBtSmemBuckets && kappa <= kBtSegMaxKappa &&
+                         n_capacity < (1ull << 32) && !getenv("CROP_BT_FLAT");
+  if (segmented) {
+    uint16_t* bkt = nullptr;
+    uint32_t *seg = nullptr, *g_k0 = nullptr;
+    const uint64_t cap1 = std::max<uint64_t>(n_capacity, 1);
+    CROP_CUDA(cudaMallocAsync(&bkt, cap1 * 2, st));
+    CROP_CUDA(cudaMallocAsync(&seg, (size_t)kappa * 8, st));
+    CROP_CUDA(cudaMallocAsync(&g_k0, cap1 * 12, st));
+    uint32_t* g_row = g_k0 + cap1;
+    uint32_t* g_col = g_row + cap1;
+    k_bt_pre<<<grid, kBtThreads, 0, st>>>(row, col, count, d_n_entries, h_row, h_col, kappa, d_tot, d_ao,
+                                           bkt);
+    CROP_LAUNCH_CHECK();
+    k_bt_init<<<(kappa + 255) / 256, 256, 0, st>>>(kappa, capacity, d_tot, d_st);
+    CROP_LAUNCH_CHECK();
+    k_bt_seg_scan<<<1, 1024, 0, st>>>(kappa, d_st, seg, seg + kappa);
+    CROP_LAUNCH_CHECK();
+    CROP_CUDA(cudaFuncSetAttribute(k_bt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScSmem));
+    k_bt_scatter<<<kNumSMs, kScThreads, kScSmem, st>>>(row, col, count, d_n_entries, bkt, kappa, d_st,
+                                                     seg + kappa, g_k0, g_row, g_col);
+    CROP_LAUNCH_CHECK();
+    const size_t smem = (size_t)kBtSegStage * 12;
+    CROP_CUDA(cudaFuncSetAttribute(k_bt_seg_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bt_seg_select<<<kappa, kBtSegThreads, smem, st>>>(g_k0, g_row, g_col, seg, d_st, d_ao);
+    CROP_LAUNCH_CHECK();
+    cudaFreeAsync(g_k0, st);
+    cudaFreeAsync(seg, st);
+    if (recorded) {
+      k_bt_mark<<<grid, kBtThreads, 0, st>>>(row, col, count, d_n_entries, h_row, h_col, kappa, d_st,
+                                              recorded, bkt);
+      CROP_LAUNCH_CHECK();
+    }
+    k_bt_out<<<(kappa + 255) / 256, 256, 0, st>>>(kappa, d_st, bucket_min, bucket_total);
+    CROP_LAUNCH_CHECK();
+    cudaFreeAsync(bkt, st);
+    cudaFreeAsync(d_hist, st);
+    cudaFreeAsync(d_misc, st);
+    cudaFreeAsync(d_st, st);
+    crop_count_launches(recorded ? 7 : 6);
+    return CROP_OK;
+  }
   // count digits over all entries, then the row / column digits over the
   // compacted ties (entries whose count equals the bucket's threshold)
   uint32_t *c_row = nullptr, *c_col = nullptr;

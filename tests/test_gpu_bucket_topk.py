@@ -37,8 +37,16 @@ def _reference(row, col, cnt, b, kappa, cap):
 
 @pytest.mark.parametrize("kappa,cap,n,maxc", [(1, 5, 1000, 3), (4, 50, 20_000, 10), (8, 1000, 200_000, 4),
                                               (31, 7, 5000, 2), (33, 100, 50_000, 50),
-                                              (1184, 65, 300_000, 1000), (300, 1, 40_000, 6)])
-def test_bucket_topk_matches_torch_ranking(kappa, cap, n, maxc):
+                                              (1184, 65, 300_000, 1000), (300, 1, 40_000, 6),
+                                              # c3-like: every count ties (segmented select, keys
+                                              # staged in shared memory from the first pass)
+                                              (1184, 2000, 3_000_000, 1),
+                                              # buckets past the staging size: global passes first
+                                              (64, 5000, 2_000_000, 2), (40, 20_000, 1_500_000, 1)])
+@pytest.mark.parametrize("flat", [False, True])
+def test_bucket_topk_matches_torch_ranking(kappa, cap, n, maxc, flat, monkeypatch):
+    if flat:  # the flat (all buckets per pass) select, the only one for kappa <= 32
+        monkeypatch.setenv("CROP_BT_FLAT", "1")
     g = torch.Generator(device="cpu").manual_seed(kappa * 7 + cap)
     n_items = 4096
     # distinct (row, col) pairs, row < col; counts with many ties

@@ -22,7 +22,7 @@
 // Pass 0 also yields each bucket's distinct count: buckets with fewer than l
 // entries keep everything (bucket_min 0), buckets with exactly l are full.
 // That flat form serves kappa <= 32 (histograms privatised per CTA); for
-// 32 < kappa <= 4096 (c3: 1184) the entries of the full buckets are grouped
+// 32 < kappa <= 2048 (c3: 1184) the entries of the full buckets are grouped
 // into per-bucket segments and each bucket is selected by one CTA with its
 // histogram in shared memory (k_bt_seg_*; CROP_BT_FLAT=1 forces the flat form).
 #include <algorithm>
@@ -305,7 +305,7 @@ __global__ void k_bt_mark(const uint32_t* __restrict__ row, const uint32_t* __re
 }
 
 // ---------------------------------------------------------------- segmented
-// kappa in (32, 4096]: the per-pass global histograms of the flat path take
+// kappa in (32, 2048]: the per-pass global histograms of the flat path take
 // one L2 atomic per entry (hot (bucket, digit) slots when most counts tie),
 // so the active buckets' entries are first grouped into one contiguous
 // segment per bucket and each bucket is then selected by one CTA with its
@@ -318,13 +318,15 @@ __global__ void k_bt_mark(const uint32_t* __restrict__ row, const uint32_t* __re
 //                    96-bit key over its segment; once the keys matching
 //                    the decided prefix fit in shared memory they are staged
 //                    there by the next pass and later passes read only them
-constexpr uint32_t kBtSegMaxKappa = 4096;
+constexpr uint32_t kBtSegMaxKappa = 2048;
 constexpr int kBtSegThreads = 512;
 constexpr uint32_t kBtSegStage = 4096;  // staged keys (3 x u32: 48 KB)
 
 __global__ void __launch_bounds__(1024) k_bt_seg_scan(uint32_t kappa, const BtState* __restrict__ st,
                                                       uint32_t* __restrict__ seg_off,
-                                                      uint32_t* __restrict__ seg_cur) {
+                                                      uint32_t* __restrict__ seg_cur,
+                                                      uint32_t* __restrict__ grp_cur,
+                                                      uint64_t* __restrict__ n_active) {
   __shared__ uint32_t s_part[1024];
   const uint32_t per = (kappa + blockDim.x - 1) / blockDim.x;
   const uint32_t lo = min(kappa, threadIdx.x * per), hi = min(kappa, lo + per);
@@ -342,34 +344,43 @@ __global__ void __launch_bounds__(1024) k_bt_seg_scan(uint32_t kappa, const BtSt
   for (uint32_t b = lo; b < hi; ++b) {
     seg_off[b] = run;
     seg_cur[b] = run;
+    if ((b & 31) == 0) grp_cur[b >> 5] = run;  // group g = buckets [32 g, 32 g + 32)
     run += st[b].active ? st[b].total : 0u;
   }
+  if (threadIdx.x == blockDim.x - 1) *n_active = s_part[threadIdx.x];
 }
 
 // tiles of kScTile entries are grouped by bucket in shared memory first, so
 // each bucket's entries of a tile leave as one contiguous run (consecutive
 // lanes, consecutive addresses) that continues the previous tile's run
-constexpr int kScThreads = 1024;
+constexpr int kScThreads = 512;  // two CTAs per SM: one loads while the other groups
 constexpr uint32_t kScPer = 8;
 constexpr uint32_t kScTile = kScThreads * kScPer;
 constexpr size_t kScSmem = (size_t)(2 * kBtSegMaxKappa + 32 + kBtSegMaxKappa / 32 + 3 * kScTile) * 4 +
                            (size_t)kScTile * 2;
 
-__global__ void __launch_bounds__(kScThreads, 1)
-    k_bt_scatter(const uint32_t* __restrict__ row, const uint32_t* __restrict__ col,
-                 const uint32_t* __restrict__ count, const uint64_t* __restrict__ d_n,
-                 const uint16_t* __restrict__ bkt, uint32_t kappa, const BtState* __restrict__ st,
-                 uint32_t* __restrict__ seg_cur, uint32_t* __restrict__ s_k0,
-                 uint32_t* __restrict__ s_row, uint32_t* __restrict__ s_col) {
+// Grouping key = bucket >> shift. With many buckets the scatter runs twice
+// (shift 5, then 0 over the output of the first) so every tile's runs stay
+// long: a tile of 8,192 entries over 1,184 buckets leaves runs of ~7 entries
+// (partial sectors, ~2x DRAM write amplification), over 37 groups or the 32
+// buckets of one group runs of ~250.
+__global__ void __launch_bounds__(kScThreads, 2)
+    k_bt_scatter(const uint32_t* __restrict__ in0, const uint32_t* __restrict__ row,
+                 const uint32_t* __restrict__ col, const uint64_t* __restrict__ d_n,
+                 const uint16_t* __restrict__ bkt, bool invert, uint32_t shift, uint32_t kappa,
+                 const BtState* __restrict__ st, uint32_t* __restrict__ seg_cur,
+                 uint32_t* __restrict__ s_k0, uint32_t* __restrict__ s_row, uint32_t* __restrict__ s_col,
+                 uint16_t* __restrict__ out_bkt) {
   extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* s_cur = sm;                            // [kappa] this CTA's write cursor per bucket
-  uint32_t* s_cnt = s_cur + kBtSegMaxKappa;        // [kappa + 1] tile counts -> offsets
+  uint32_t* s_cur = sm;                            // [nkeys] this CTA's write cursor per key
+  uint32_t* s_cnt = s_cur + kBtSegMaxKappa;        // [nkeys + 1] tile counts -> offsets
   uint32_t* s_act = s_cnt + kBtSegMaxKappa + 32;   // [kappa / 32] active-bucket bits
   uint32_t* stg = s_act + kBtSegMaxKappa / 32;     // [3][kScTile] staged keys
   uint16_t* s_b = reinterpret_cast<uint16_t*>(stg + 3 * kScTile);  // [kScTile] their buckets
   __shared__ uint32_t s_warp[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) s_cur[b] = 0;
+  const uint32_t nkeys = (kappa + (1u << shift) - 1) >> shift;
+  for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x) s_cur[k] = 0;
   for (uint32_t k = threadIdx.x; k < (kappa + 31) / 32; k += blockDim.x) {
     uint32_t bits = 0;
     for (uint32_t q = 0; q < 32 && k * 32 + q < kappa; ++q) bits |= (st[k * 32 + q].active ? 1u : 0u) << q;
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(kScThreads, 1)
   const uint64_t n = *d_n;
   const uint64_t per = (((n + gridDim.x - 1) / gridDim.x) + 31) & ~31ull;
   const uint64_t lo = min(n, blockIdx.x * per), hi = min(n, lo + per);
-  // 1: this CTA's entries per active bucket, one global claim per bucket
+  // 1: this CTA's entries per key, one global claim per key
   for (uint64_t e0 = lo; e0 < hi; e0 += kScTile) {
     uint32_t bb[kScPer];
 #pragma unroll
@@ -390,17 +401,17 @@ __global__ void __launch_bounds__(kScThreads, 1)
     }
 #pragma unroll
     for (uint32_t u = 0; u < kScPer; ++u)
-      if (active(bb[u])) atomicAdd(&s_cur[bb[u]], 1u);
+      if (active(bb[u])) atomicAdd(&s_cur[bb[u] >> shift], 1u);
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) {
-    const uint32_t c = s_cur[b];
-    if (c) s_cur[b] = atomicAdd(&seg_cur[b], c);
+  for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x) {
+    const uint32_t c = s_cur[k];
+    if (c) s_cur[k] = atomicAdd(&seg_cur[k], c);
   }
-  // 2: per tile, group by bucket in shared memory, then write the runs
-  const uint32_t per_t = (kappa + blockDim.x - 1) / blockDim.x;  // scan elements per thread (<= 4)
+  // 2: per tile, group by key in shared memory, then write the runs
+  const uint32_t per_t = (nkeys + blockDim.x - 1) / blockDim.x;  // scan elements per thread (<= 4)
   for (uint64_t e0 = lo; e0 < hi; e0 += kScTile) {
-    for (uint32_t b = threadIdx.x; b <= kappa; b += blockDim.x) s_cnt[b] = 0;
+    for (uint32_t k = threadIdx.x; k <= nkeys; k += blockDim.x) s_cnt[k] = 0;
     __syncthreads();
     uint32_t bb[kScPer], kc[kScPer], ii[kScPer], jj[kScPer], rk[kScPer];
 #pragma unroll
@@ -408,23 +419,24 @@ __global__ void __launch_bounds__(kScThreads, 1)
       const uint64_t e = e0 + u * blockDim.x + threadIdx.x;
       const bool ok = e < hi;
       bb[u] = ok ? bkt[e] : 0xFFFFFFFFu;
-      kc[u] = ok ? ~__ldcs(count + e) : 0u;
+      kc[u] = ok ? __ldcs(in0 + e) : 0u;
+      if (invert) kc[u] = ~kc[u];
       ii[u] = ok ? __ldcs(row + e) : 0u;
       jj[u] = ok ? __ldcs(col + e) : 0u;
     }
 #pragma unroll
     for (uint32_t u = 0; u < kScPer; ++u) {
       if (!active(bb[u])) bb[u] = 0xFFFFFFFFu;
-      rk[u] = bb[u] != 0xFFFFFFFFu ? atomicAdd(&s_cnt[bb[u]], 1u) : 0u;
+      rk[u] = bb[u] != 0xFFFFFFFFu ? atomicAdd(&s_cnt[bb[u] >> shift], 1u) : 0u;
     }
     __syncthreads();
-    // exclusive scan of s_cnt[0, kappa) in place; s_cnt[kappa] = tile total
+    // exclusive scan of s_cnt[0, nkeys) in place; s_cnt[nkeys] = tile total
     {
       const uint32_t b0 = threadIdx.x * per_t;
       uint32_t v[4] = {0u, 0u, 0u, 0u}, sum = 0;
 #pragma unroll
       for (uint32_t k = 0; k < 4; ++k)
-        if (k < per_t && b0 + k < kappa) {
+        if (k < per_t && b0 + k < nkeys) {
           v[k] = s_cnt[b0 + k];
           sum += v[k];
         }
@@ -445,13 +457,13 @@ __global__ void __launch_bounds__(kScThreads, 1)
           if (lane >= d) wi += t;
         }
         s_warp[lane] = wi - wv;
-        if (lane == 31) s_cnt[kappa] = wi;
+        if (lane == 31) s_cnt[nkeys] = wi;
       }
       __syncthreads();
       uint32_t run = s_warp[warp] + incl - sum;
 #pragma unroll
       for (uint32_t k = 0; k < 4; ++k)
-        if (k < per_t && b0 + k < kappa) {
+        if (k < per_t && b0 + k < nkeys) {
           s_cnt[b0 + k] = run;
           run += v[k];
         }
@@ -460,25 +472,26 @@ __global__ void __launch_bounds__(kScThreads, 1)
 #pragma unroll
     for (uint32_t u = 0; u < kScPer; ++u)
       if (bb[u] != 0xFFFFFFFFu) {
-        const uint32_t t = s_cnt[bb[u]] + rk[u];
+        const uint32_t t = s_cnt[bb[u] >> shift] + rk[u];
         stg[t] = kc[u];
         stg[kScTile + t] = ii[u];
         stg[2 * kScTile + t] = jj[u];
         s_b[t] = (uint16_t)bb[u];
       }
     __syncthreads();
-    const uint32_t total = s_cnt[kappa];
+    const uint32_t total = s_cnt[nkeys];
     for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-      const uint32_t b = s_b[t];
-      const uint32_t dst = s_cur[b] + (t - s_cnt[b]);
+      const uint32_t bf = s_b[t], k = bf >> shift;
+      const uint32_t dst = s_cur[k] + (t - s_cnt[k]);
       s_k0[dst] = stg[t];
       s_row[dst] = stg[kScTile + t];
       s_col[dst] = stg[2 * kScTile + t];
+      if (out_bkt) out_bkt[dst] = (uint16_t)bf;
     }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < kappa; b += blockDim.x) {
-      const uint32_t nb = b + 1 < kappa ? s_cnt[b + 1] : total;
-      s_cur[b] += nb - s_cnt[b];
+    for (uint32_t k = threadIdx.x; k < nkeys; k += blockDim.x) {
+      const uint32_t nb = k + 1 < nkeys ? s_cnt[k + 1] : total;
+      s_cur[k] += nb - s_cnt[k];
     }
     __syncthreads();
   }
@@ -511,10 +524,14 @@ __device__ __forceinline__ void bt_hist_add(uint32_t* hist, uint32_t d) {
   }
 }
 
+// Per pass, the keys matching the decided prefix are read from the current
+// source: the bucket's segment, a compacted copy of the matching keys in the
+// scratch segment (written by the pass after the matches fell to a quarter
+// of the source; the two alternate), or shared memory (staged once they fit)
 __global__ void __launch_bounds__(kBtSegThreads)
-    k_bt_seg_select(const uint32_t* __restrict__ s_k0g, const uint32_t* __restrict__ s_rowg,
-                    const uint32_t* __restrict__ s_colg, const uint32_t* __restrict__ seg_off,
-                    BtState* __restrict__ st, const uint32_t* __restrict__ andor) {
+    k_bt_seg_select(uint32_t* __restrict__ seg_a, uint32_t* __restrict__ seg_b, uint32_t cap,
+                    const uint32_t* __restrict__ seg_off, BtState* __restrict__ st,
+                    const uint32_t* __restrict__ andor) {
   extern __shared__ __align__(16) uint32_t stage[];  // [3][kBtSegStage]
   __shared__ uint32_t hist[256];
   __shared__ uint32_t s_sel[3];
@@ -523,9 +540,11 @@ __global__ void __launch_bounds__(kBtSegThreads)
   const BtState s = st[b];
   if (!s.active) return;
   const uint32_t off = seg_off[b], m = s.total;
-  const uint32_t* gk[3] = {s_k0g + off, s_rowg + off, s_colg + off};
+  // key word k of source entry e: src + k * cap + e (three u32 arrays)
+  uint32_t* src = seg_a + off;
+  uint32_t* dst = seg_b + off;
   uint32_t key[3] = {0u, 0u, 0u};
-  uint32_t need = s.need, match = m, ns = 0;
+  uint32_t need = s.need, match = m, msrc = m, ns = 0;
   bool staged = false;
   const int lane = threadIdx.x & 31;
   for (uint32_t p = 0; p < 12; ++p) {
@@ -540,6 +559,7 @@ __global__ void __launch_bounds__(kBtSegThreads)
     for (uint32_t k = threadIdx.x; k < 256; k += blockDim.x) hist[k] = 0;
     if (threadIdx.x == 0) s_n = 0;
     const bool stage_now = !staged && match <= kBtSegStage;
+    const bool compact_now = !staged && !stage_now && match <= msrc / 4;
     __syncthreads();
     if (staged) {
       for (uint32_t e0 = 0; e0 < ns; e0 += blockDim.x) {
@@ -552,30 +572,38 @@ __global__ void __launch_bounds__(kBtSegThreads)
         bt_hist_add(hist, d);
       }
     } else {
-      // U entries per thread per step, all loads issued before any is used
+      // U entries per thread per step, all loads issued before any is used;
+      // the words after w are loaded only for matching keys that move
       constexpr uint32_t U = 4;
-      const uint32_t nw = stage_now ? 3 : w + 1;  // key words this pass reads
-      for (uint32_t e0 = 0; e0 < m; e0 += U * blockDim.x) {
+      for (uint32_t e0 = 0; e0 < msrc; e0 += U * blockDim.x) {
         uint32_t kw[U][3];
 #pragma unroll
         for (uint32_t u = 0; u < U; ++u) {
           const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
-          const bool ok = e < m;
-          kw[u][0] = ok ? __ldcs(gk[0] + e) : 0u;
-          kw[u][1] = ok && nw > 1 ? __ldcs(gk[1] + e) : 0u;
-          kw[u][2] = ok && nw > 2 ? __ldcs(gk[2] + e) : 0u;
+          const bool ok = e < msrc;
+          kw[u][0] = ok ? __ldcs(src + e) : 0u;
+          kw[u][1] = ok && w >= 1 ? __ldcs(src + (size_t)cap + e) : 0u;
+          kw[u][2] = ok && w >= 2 ? __ldcs(src + 2 * (size_t)cap + e) : 0u;
         }
 #pragma unroll
         for (uint32_t u = 0; u < U; ++u) {
           const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
           uint32_t d = 0xFFFFFFFFu;
-          if (e < m && bt_prefix_match(kw[u], key, p)) {
+          if (e < msrc && bt_prefix_match(kw[u], key, p)) {
             d = (bt_pick(kw[u], w) >> sh) & 0xFFu;
-            if (stage_now) {
+            if (stage_now || compact_now) {
+              if (w < 1) kw[u][1] = __ldcs(src + (size_t)cap + e);
+              if (w < 2) kw[u][2] = __ldcs(src + 2 * (size_t)cap + e);
               const uint32_t q = atomicAdd(&s_n, 1u);
-              stage[q] = kw[u][0];
-              stage[kBtSegStage + q] = kw[u][1];
-              stage[2 * kBtSegStage + q] = kw[u][2];
+              if (stage_now) {
+                stage[q] = kw[u][0];
+                stage[kBtSegStage + q] = kw[u][1];
+                stage[2 * kBtSegStage + q] = kw[u][2];
+              } else {
+                dst[q] = kw[u][0];
+                dst[(size_t)cap + q] = kw[u][1];
+                dst[2 * (size_t)cap + q] = kw[u][2];
+              }
             }
           }
           bt_hist_add(hist, d);
@@ -586,6 +614,11 @@ __global__ void __launch_bounds__(kBtSegThreads)
     if (stage_now) {
       staged = true;
       ns = s_n;
+    } else if (compact_now) {
+      uint32_t* t = src;
+      src = dst;
+      dst = t;
+      msrc = s_n;
     }
     if (threadIdx.x < 32) {
       uint32_t v[8], sum = 0;
@@ -677,10 +710,24 @@ extern "C" int crop_bucket_topk(const uint32_t* row, const uint32_t* col, const 
   if (segmented) {
     uint16_t* bkt = nullptr;
     uint32_t *seg = nullptr, *g_k0 = nullptr;
-    const uint64_t cap1 = std::max<uint64_t>(n_capacity, 1);
+    // the segments hold the entries (not the capacity): one 8-byte read-back
+    uint64_t n_host = 0;
+    CROP_CUDA(cudaMemcpyAsync(&n_host, d_n_entries, 8, cudaMemcpyDeviceToHost, st));
+    CROP_CUDA(cudaStreamSynchronize(st));
+    if (n_host > n_capacity) {
+      crop_set_error(CROP_EINPUT, "%llu entries exceed their arrays' capacity %llu",
+                     (unsigned long long)n_host, (unsigned long long)n_capacity);
+      cudaFreeAsync(d_st, st);
+      cudaFreeAsync(d_hist, st);
+      cudaFreeAsync(d_misc, st);
+      return CROP_EINPUT;
+    }
+    const uint64_t cap1 = std::max<uint64_t>(n_host, 1);
     CROP_CUDA(cudaMallocAsync(&bkt, cap1 * 2, st));
-    CROP_CUDA(cudaMallocAsync(&seg, (size_t)kappa * 8, st));
-    CROP_CUDA(cudaMallocAsync(&g_k0, cap1 * 12, st));
+    // offsets, cursors, group cursors, the active entry count
+    CROP_CUDA(cudaMallocAsync(&seg, ((size_t)2 * kappa + kBtSegMaxKappa / 32 + 4) * 4, st));
+    // segments + scratch segments (+ the group pass's 16-bit buckets)
+    CROP_CUDA(cudaMallocAsync(&g_k0, cap1 * 26, st));
     uint32_t* g_row = g_k0 + cap1;
     uint32_t* g_col = g_row + cap1;
     k_bt_pre<<<grid, kBtThreads, 0, st>>>(row, col, count, d_n_entries, h_row, h_col, kappa, d_tot, d_ao,
@@ -688,15 +735,32 @@ extern "C" int crop_bucket_topk(const uint32_t* row, const uint32_t* col, const 
     CROP_LAUNCH_CHECK();
     k_bt_init<<<(kappa + 255) / 256, 256, 0, st>>>(kappa, capacity, d_tot, d_st);
     CROP_LAUNCH_CHECK();
-    k_bt_seg_scan<<<1, 1024, 0, st>>>(kappa, d_st, seg, seg + kappa);
+    uint32_t* grp_cur = seg + 2 * kappa;
+    uint64_t* n_act = reinterpret_cast<uint64_t*>(seg + 2 * kappa + kBtSegMaxKappa / 32 + 2);
+    k_bt_seg_scan<<<1, 1024, 0, st>>>(kappa, d_st, seg, seg + kappa, grp_cur, n_act);
     CROP_LAUNCH_CHECK();
     CROP_CUDA(cudaFuncSetAttribute(k_bt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScSmem));
-    k_bt_scatter<<<kNumSMs, kScThreads, kScSmem, st>>>(row, col, count, d_n_entries, bkt, kappa, d_st,
-                                                     seg + kappa, g_k0, g_row, g_col);
+    uint32_t* g_scr = g_k0 + 3 * cap1;  // the select's scratch segments
+    if (kappa > 256) {
+      // by group of 32 buckets into the scratch (with the buckets), then by
+      // bucket into the segments
+      uint16_t* bkt2 = reinterpret_cast<uint16_t*>(g_scr + 3 * cap1);
+      k_bt_scatter<<<kNumSMs * 2, kScThreads, kScSmem, st>>>(count, row, col, d_n_entries, bkt, true, 5, kappa,
+                                                         d_st, grp_cur, g_scr, g_scr + cap1,
+                                                         g_scr + 2 * cap1, bkt2);
+      CROP_LAUNCH_CHECK();
+      k_bt_scatter<<<kNumSMs * 2, kScThreads, kScSmem, st>>>(g_scr, g_scr + cap1, g_scr + 2 * cap1, n_act, bkt2,
+                                                         false, 0, kappa, d_st, seg + kappa, g_k0, g_row,
+                                                         g_col, nullptr);
+    } else {
+      k_bt_scatter<<<kNumSMs * 2, kScThreads, kScSmem, st>>>(count, row, col, d_n_entries, bkt, true, 0, kappa,
+                                                         d_st, seg + kappa, g_k0, g_row, g_col, nullptr);
+    }
     CROP_LAUNCH_CHECK();
     const size_t smem = (size_t)kBtSegStage * 12;
     CROP_CUDA(cudaFuncSetAttribute(k_bt_seg_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bt_seg_select<<<kappa, kBtSegThreads, smem, st>>>(g_k0, g_row, g_col, seg, d_st, d_ao);
+    k_bt_seg_select<<<kappa, kBtSegThreads, smem, st>>>(g_k0, g_k0 + 3 * cap1, (uint32_t)cap1, seg, d_st,
+                                                         d_ao);
     CROP_LAUNCH_CHECK();
     cudaFreeAsync(g_k0, st);
     cudaFreeAsync(seg, st);
@@ -711,7 +775,7 @@ extern "C" int crop_bucket_topk(const uint32_t* row, const uint32_t* col, const 
     cudaFreeAsync(d_hist, st);
     cudaFreeAsync(d_misc, st);
     cudaFreeAsync(d_st, st);
-    crop_count_launches(recorded ? 7 : 6);
+    crop_count_launches((recorded ? 7 : 6) + (kappa > 256 ? 1 : 0));
     return CROP_OK;
   }
   // count digits over all entries, then the row / column digits over the

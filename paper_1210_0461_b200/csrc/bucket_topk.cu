@@ -304,6 +304,39 @@ __global__ void k_bt_mark(const uint32_t* __restrict__ row, const uint32_t* __re
   }
 }
 
+// k_bt_mark over 16-byte aligned columns with the bucket ids cached: four
+// entries per thread per step (uint4 loads, one 4-byte store of flags)
+__device__ __forceinline__ uint32_t bt_keep(const BtState& s, uint32_t c, uint32_t i, uint32_t j) {
+  if (!s.active) return 1u;
+  const uint32_t k0 = ~c;
+  return (k0 < s.key[0] || (k0 == s.key[0] && (i < s.key[1] || (i == s.key[1] && j <= s.key[2])))) ? 1u : 0u;
+}
+
+__global__ void k_bt_mark4(const uint4* __restrict__ row, const uint4* __restrict__ col,
+                           const uint4* __restrict__ count, const uint64_t* __restrict__ d_n,
+                           const BtState* __restrict__ st, uint32_t* __restrict__ recorded,
+                           const uint2* __restrict__ bkt) {
+  const uint64_t n = *d_n, nq = n / 4;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 i = __ldcs(row + q), j = __ldcs(col + q), c = __ldcs(count + q);
+    const uint2 bb = __ldcs(bkt + q);
+    const uint32_t f = bt_keep(st[bb.x & 0xFFFFu], c.x, i.x, j.x) |
+                       bt_keep(st[bb.x >> 16], c.y, i.y, j.y) << 8 |
+                       bt_keep(st[bb.y & 0xFFFFu], c.z, i.z, j.z) << 16 |
+                       bt_keep(st[bb.y >> 16], c.w, i.w, j.w) << 24;
+    __stcs(recorded + q, f);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const uint64_t e = nq * 4 + threadIdx.x;
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(row);
+    const uint32_t* cl = reinterpret_cast<const uint32_t*>(col);
+    const uint32_t* ct = reinterpret_cast<const uint32_t*>(count);
+    const uint16_t* bk = reinterpret_cast<const uint16_t*>(bkt);
+    reinterpret_cast<uint8_t*>(recorded)[e] = (uint8_t)bt_keep(st[bk[e]], ct[e], r[e], cl[e]);
+  }
+}
+
 // ---------------------------------------------------------------- segmented
 // kappa in (32, 2048]: the per-pass global histograms of the flat path take
 // one L2 atomic per entry (hot (bucket, digit) slots when most counts tie),
@@ -765,8 +798,16 @@ extern "C" int crop_bucket_topk(const uint32_t* row, const uint32_t* col, const 
     cudaFreeAsync(g_k0, st);
     cudaFreeAsync(seg, st);
     if (recorded) {
-      k_bt_mark<<<grid, kBtThreads, 0, st>>>(row, col, count, d_n_entries, h_row, h_col, kappa, d_st,
-                                              recorded, bkt);
+      auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+      if (al16(row) && al16(col) && al16(count) && al16(recorded)) {
+        k_bt_mark4<<<kNumSMs * 8, 256, 0, st>>>(
+            reinterpret_cast<const uint4*>(row), reinterpret_cast<const uint4*>(col),
+            reinterpret_cast<const uint4*>(count), d_n_entries, d_st, reinterpret_cast<uint32_t*>(recorded),
+            reinterpret_cast<const uint2*>(bkt));
+      } else {
+        k_bt_mark<<<grid, kBtThreads, 0, st>>>(row, col, count, d_n_entries, h_row, h_col, kappa, d_st,
+                                                recorded, bkt);
+      }
       CROP_LAUNCH_CHECK();
     }
     k_bt_out<<<(kappa + 255) / 256, 256, 0, st>>>(kappa, d_st, bucket_min, bucket_total);

@@ -198,7 +198,7 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_item_terms(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
-                 int64_t n_tx, uint32_t n_items, unsigned long long* __restrict__ stats,
+                 int64_t n_tx, uint32_t n_items, int chunk_tx, unsigned long long* __restrict__ stats,
                  unsigned int* __restrict__ max_len) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
@@ -210,10 +210,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     s_occ[i] = 0;
   }
   uint32_t my_max = 0;
-  const int64_t n_chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+  const int64_t n_chunks = (n_tx + chunk_tx - 1) / chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
-    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk, kChunkTx);
+    const int ntx = stage_offsets(s_off, offsets, n_tx, chunk, chunk_tx);
     walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr, [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
       if (!q.valid) return;
       my_max = max(my_max, q.L);
@@ -3216,6 +3216,15 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       JCUDA(cudaMallocHost(&h_nnz_hint, 8));
     }
     if (n_tx > 0) JCUDA(cudaEventRecord(e_in, st));
+    // CROP_DEBUG_TIMING: GPU time of pass A + planner and the idle gap
+    // between the planner and the first write kernel (host planning latency)
+    static cudaEvent_t dbg_ev[3] = {};
+    const bool dbg_t = getenv("CROP_DEBUG_TIMING") != nullptr;
+    if (dbg_t) {
+      if (!dbg_ev[0])
+        for (cudaEvent_t& e : dbg_ev) JCUDA(cudaEventCreate(&e));
+      JCUDA(cudaEventRecord(dbg_ev[0], st));
+    }
     JCUDA(cudaMallocAsync(&J->d_terms, nn * sizeof(unsigned long long) + 16, st));
     J->d_maxlen = reinterpret_cast<unsigned int*>(J->d_terms + nn);
     JCUDA(cudaMemsetAsync(J->d_terms, 0, nn * sizeof(unsigned long long) + 16, st));
@@ -3225,9 +3234,11 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       const size_t smem = kOffBytes + ns * 8;  // two u32 arrays
       JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(kOffBytes + kStatSmemItems * 8)));
-      const int64_t chunks = (n_tx + kChunkTx - 1) / kChunkTx;
+      // ~12 chunks per CTA: the last wave of chunks is a small share of the pass
+      const int chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, n_tx / (kNumSMs * 12)));
+      const int64_t chunks = (n_tx + chunk_tx - 1) / chunk_tx;
       const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
-      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, J->d_terms, J->d_maxlen);
+      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, chunk_tx, J->d_terms, J->d_maxlen);
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
     }
@@ -3292,9 +3303,11 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
       JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(kPlanChunk * 8)));
+      if (dbg_t) JCUDA(cudaEventRecord(dbg_ev[1], st));
       k_plan_stream<<<1, kPlanThreads, kPlanChunk * 8, st>>>(PA);
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
+      if (dbg_t) JCUDA(cudaEventRecord(dbg_ev[2], st));
       JCUDA(g_pinned.reserve(sizeof(PlanOut) + 64));
       PlanOut* ho = reinterpret_cast<PlanOut*>(g_pinned.p);
       unsigned int* h_ml = reinterpret_cast<unsigned int*>(g_pinned.p + sizeof(PlanOut));
@@ -3382,6 +3395,15 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
         J->own_terms = ho->own_terms;
         rc = early_write(J, st);
         if (rc) goto fail;
+        if (dbg_t && J->ev[0]) {
+          float a = 0, b = 0, c = 0;
+          JCUDA(cudaEventSynchronize(J->ev[0]));
+          cudaEventElapsedTime(&a, dbg_ev[0], dbg_ev[1]);
+          cudaEventElapsedTime(&b, dbg_ev[1], dbg_ev[2]);
+          cudaEventElapsedTime(&c, dbg_ev[2], J->ev[0]);
+          fprintf(stderr, "[create] pass A %.3f ms, planner %.3f ms, planner end -> write start %.3f ms\n",
+                  a, b, c);
+        }
         *job = J;
         return CROP_OK;
       }

@@ -244,7 +244,7 @@ __global__ void k_bt_select(uint32_t kappa, uint32_t p, BtState* __restrict__ st
 
 // after the count digits: the entries whose count equals their full
 // bucket's threshold count are the only ones the row / column digits can
-// still separate -- compact them (warp-aggregated claims)
+// still separate -- compact them (one output claim per block and step)
 __global__ void k_bt_compact(const uint32_t* __restrict__ row, const uint32_t* __restrict__ col,
                              const uint32_t* __restrict__ count, const uint64_t* __restrict__ d_n,
                              const uint32_t* __restrict__ h_row, const uint32_t* __restrict__ h_col,
@@ -253,8 +253,11 @@ __global__ void k_bt_compact(const uint32_t* __restrict__ row, const uint32_t* _
                              unsigned long long* __restrict__ c_n, uint32_t* __restrict__ c_andor,
                              const uint16_t* __restrict__ bkt, uint16_t* __restrict__ c_bkt) {
   const uint64_t n = *d_n;
-  const uint64_t n_round = (n + 31) & ~31ull;
-  const int lane = threadIdx.x & 31;
+  // uniform trip count per block: one output claim per block and step
+  const uint64_t n_round = (n + blockDim.x - 1) / blockDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t s_wcnt[32];
+  __shared__ unsigned long long s_base;
   // candidates' key words 1-2 (word 0 is each bucket's decided ~count: its
   // digits are never examined again, AND = OR = 0 marks them constant)
   uint32_t a[3] = {0u, ~0u, ~0u}, o[3] = {0u, 0u, 0u};
@@ -270,9 +273,26 @@ __global__ void k_bt_compact(const uint32_t* __restrict__ row, const uint32_t* _
       keep = s.active && ~count[e] == s.key[0];
     }
     const uint32_t m = __ballot_sync(0xffffffffu, keep);
-    unsigned long long base = 0;
-    if (lane == 0 && m) base = atomicAdd(c_n, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane == 0) s_wcnt[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t c = lane < (int)(blockDim.x >> 5) ? s_wcnt[lane] : 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += u;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      unsigned long long bb = 0;
+      if (lane == 0 && tot) bb = atomicAdd(c_n, (unsigned long long)tot);
+      bb = __shfl_sync(0xffffffffu, bb, 0);
+      if (lane == 0) s_base = bb;
+      s_wcnt[lane] = incl - c;
+    }
+    __syncthreads();
+    const unsigned long long base = s_base + s_wcnt[warp];
+    __syncthreads();  // s_wcnt / s_base are rewritten by the next step
     if (keep) {
       const uint64_t q = base + __popc(m & ((1u << lane) - 1u));
       c_row[q] = i;

@@ -10,8 +10,10 @@
 //   k_outer_count  per product: own-interval terms (warp per product)
 //   scan           exclusive offsets (CUB)
 //   k_outer_emit   (row<<32|col, term index) for own terms, in stream order;
-//                  values are a_k(i)*b_k(j) in fp64 (exact for fp32 inputs)
-//   sort           stable radix sort by (row, col), then stable by bucket (CUB)
+//                  values are a_k(i)*b_k(j) in fp64 (exact for fp32 inputs);
+//                  unfiltered full products: k_outer_emit_bal, warps over
+//                  fixed term chunks instead of whole products
+//   sort          stable radix sort by (row, col), then stable by bucket (CUB)
 //   k_outer_reduce segment heads sum their run IN STREAM ORDER in fp64 ->
 //                  bit-identical to the reference's dict accumulation; output
 //                  per-bucket sorted COO (row, col, value, bucket)
@@ -122,6 +124,74 @@ __global__ void k_outer_emit(const int64_t* __restrict__ a_ptr, const uint32_t* 
         vals[o] = (a_val ? a_val[a0 + p] : 1.0) * (b_val ? b_val[b0 + q] : 1.0);
       }
       pos += __popc(m);
+    }
+  }
+}
+
+// Unfiltered full products (every term is own: term t of product k lands at
+// offs[k] + t): warps take fixed chunks of terms instead of whole products,
+// so a 2,000 x 2,000 product no longer holds one warp for 125,000 steps
+// (c4's Pareto sizes) and every store run is 32 consecutive terms.
+constexpr uint32_t kEmitChunk = 1024;
+
+__global__ void __launch_bounds__(256) k_outer_emit_bal(
+    const int64_t* __restrict__ a_ptr, const uint32_t* __restrict__ a_idx, const double* __restrict__ a_val,
+    const int64_t* __restrict__ b_ptr, const uint32_t* __restrict__ b_idx, const double* __restrict__ b_val,
+    int64_t n, uint64_t total, crop_interval iv, CompositeKey ck, const unsigned long long* __restrict__ offs,
+    unsigned long long* __restrict__ keys, uint32_t* __restrict__ seq, double* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t n_chunks = (total + kEmitChunk - 1) / kEmitChunk;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  auto next_off = [&](int64_t k) -> uint64_t { return k + 1 < n ? offs[k + 1] : total; };
+  for (uint64_t c = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; c < n_chunks; c += warps) {
+    const uint64_t g0 = c * kEmitChunk, g1 = min(total, g0 + kEmitChunk);
+    // the product holding g0: the last k with offs[k] <= g0
+    int64_t k = 0;
+    if (lane == 0) {
+      int64_t lo = 0, hi = n;  // offs[lo] <= g0 < offs[hi] (offs[n] = total)
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (offs[mid] <= g0) lo = mid;
+        else hi = mid;
+      }
+      k = lo;
+    }
+    k = __shfl_sync(0xffffffffu, k, 0);
+    int64_t kc = -1, a0 = 0, b0 = 0;
+    uint64_t base = 0, lb = 1, terms = 0;
+    for (uint64_t g = g0 + lane; g < g1; g += 32) {
+      while (next_off(k) <= g) ++k;
+      if (k != kc) {
+        kc = k;
+        base = offs[k];
+        a0 = a_ptr[k];
+        b0 = b_ptr[k];
+        lb = (uint64_t)(b_ptr[k + 1] - b0);
+        terms = (uint64_t)(a_ptr[k + 1] - a0) * lb;
+      }
+      const uint64_t t = g - base;
+      uint64_t p, q;
+      if (terms < (1ull << 32)) {
+        const uint32_t t32 = (uint32_t)t, l32 = (uint32_t)lb;
+        p = t32 / l32;
+        q = t32 - (uint32_t)p * l32;
+      } else {
+        p = t / lb;
+        q = t - p * lb;
+      }
+      const uint32_t i = a_idx[a0 + p], j = b_idx[b0 + q];
+      if (ck.on) {
+        uint32_t b = 0;
+        if (ck.has_hash) {
+          b = iv.h_row[i] + iv.h_col[j];
+          if (b >= iv.kappa) b -= iv.kappa;
+        }
+        keys[g] = ((unsigned long long)b << ck.rc_bits) | ((unsigned long long)i << ck.c_bits) | j;
+      } else {
+        keys[g] = ((unsigned long long)i << 32) | j;
+      }
+      seq[g] = (uint32_t)g;
+      vals[g] = (a_val ? a_val[a0 + p] : 1.0) * (b_val ? b_val[b0 + q] : 1.0);
     }
   }
 }
@@ -389,7 +459,11 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMallocAsync(&head_pos, n * 4, st));
   {
     int64_t blocks = std::min<int64_t>((J->n + 7) / 8, 1 << 20);
-    if (J->filter)
+    if (!J->filter && !J->upper && n > 0 && !getenv("CROP_OUTER_EMIT_PER_PRODUCT"))
+      k_outer_emit_bal<<<kNumSMs * 8, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr, J->b_idx,
+                                                     J->b_val, J->n, (uint64_t)n, J->iv, J->ck, J->d_offs,
+                                                     keys, seq, vals);
+    else if (J->filter)
       k_outer_emit<true><<<(int)blocks, 256, 0, st>>>(J->a_ptr, J->a_idx, J->a_val, J->b_ptr,
                                                      J->b_idx, J->b_val, J->n, J->upper, J->iv,
                                                      J->ck, J->d_offs, keys, seq, vals);

@@ -13,7 +13,7 @@
 //                  values are a_k(i)*b_k(j) in fp64 (exact for fp32 inputs);
 //                  unfiltered full products: k_outer_emit_bal, warps over
 //                  fixed term chunks instead of whole products
-//   sort          stable radix sort by (row, col), then stable by bucket (CUB)
+//   sort           stable radix sort by (row, col), then stable by bucket (CUB)
 //   k_outer_reduce segment heads sum their run IN STREAM ORDER in fp64 ->
 //                  bit-identical to the reference's dict accumulation; output
 //                  per-bucket sorted COO (row, col, value, bucket)

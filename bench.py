@@ -135,6 +135,22 @@ def cpu_count():
         return os.cpu_count() or 1
 
 
+def config_dict(cfg, world):
+    """The workload description both arms print (identical dicts)."""
+    from paper_1210_0461_b200 import workloads
+
+    if isinstance(cfg, workloads.PairConfig):
+        return {"workload": cfg.name, "n_tx": cfg.n_tx, "n_items": cfg.n_items,
+                "zipf_s": cfg.zipf_s, "length": list(cfg.length), "kappa": cfg.kappa,
+                "top_k": cfg.top_k, "ss_capacity": cfg.ss_capacity, "data_seed": cfg.seed,
+                "engine_seed": 0, "upper_triangle_only": True,
+                "parallelism": f"tiles{world}",
+                "l2": "flushed (1 GiB write) before every timed step"}
+    return {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "data_seed": cfg.seed,
+            "engine_seed": 0, "parallelism": f"buckets{world}",
+            "l2": "flushed (1 GiB write) before every timed step"}
+
+
 # ------------------------------------------------------------------ workload
 
 def load_workload(cfg, rank, world):
@@ -293,6 +309,23 @@ def run_ours(args, rank, world):
         del ent
     else:
         own_terms = total_terms_all
+    # per-partition balance (BASELINE c5: max/mean terms per partition), the
+    # LoadReport.max_avg_ratio arithmetic (engine.py:207-216) over the kappa
+    # bucket loads of this rank's entries (summed over ranks)
+    ent_b = kernels.count_pairs_shard(dtx, True, interval, keep=tables, shard=shard,
+                                      capacity=SUB_SHARD_CAPACITY)
+    bl, _, _ = kernels.entry_bucket_stats(ent_b, [tables], cfg.kappa, cfg.n_items, None)
+    bl = bl[0]
+    if world > 1:
+        dist.all_reduce(bl)
+    del ent_b
+    bucket_loads = [int(x) for x in bl.cpu().tolist()]
+    balance = {"partitions": cfg.kappa,
+               "max_mean": crop.LoadReport(kappa=cfg.kappa, workers=cfg.kappa, rows=[bucket_loads],
+                                           input_pair_total=0).max_avg_ratio(),
+               "max_terms": max(bucket_loads), "mean_terms": sum(bucket_loads) / cfg.kappa,
+               "source": "exact bucket loads of the counted entries (sum of supports per "
+                         "bucket), LoadReport.max_avg_ratio arithmetic"}
     in_bytes = 4 * int(dtx.items.numel()) + 8 * int(dtx.offsets.numel())
     b_alg = 8 * own_terms + in_bytes + 12 * own_entries
     avg = {k: statistics.mean(p[k] for p in phase_log) for k in phase_log[0]}
@@ -332,15 +365,11 @@ def run_ours(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic: seeded Zipf transactions (SURVEY.md §8d, data seed = config no.)",
-            "config": {"workload": cfg.name, "n_tx": cfg.n_tx, "n_items": cfg.n_items,
-                       "zipf_s": cfg.zipf_s, "length": list(cfg.length), "kappa": cfg.kappa,
-                       "sharding": f"tiles split by terms over {world} GPU(s), all {cfg.kappa} buckets",
-                       "top_k": cfg.top_k,
-                       "ss_capacity": cfg.ss_capacity,
-                       "terms": total_terms_all, "entries": own_entries if world == 1 else None,
-                       "tiles": stats[2], "units": stats[3], "parallelism": f"tiles{world}",
-                       "l2": "flushed (1 GiB write) before every timed step",
-                       "broadcast_s": round(bcast_s, 4)},
+            "config": config_dict(cfg, world),
+            "details": {"sharding": f"tiles split by terms over {world} GPU(s), all {cfg.kappa} buckets",
+                        "terms": total_terms_all, "entries": own_entries if world == 1 else None,
+                        "tiles": stats[2], "units": stats[3], "broadcast_s": round(bcast_s, 4)},
+            "partition_balance": balance,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": sampler.summary(),
         }
@@ -412,11 +441,9 @@ def run_product(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded Pareto-nnz CSC/CSR, N(0,1) fp32 values (SURVEY.md §8d)",
-            "config": {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa,
-                       "buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})[rank]",
-                       "terms": total_terms, "entries": ent.n if world == 1 else None,
-                       "parallelism": f"buckets{world}",
-                       "l2": "flushed (1 GiB write) before every timed step"},
+            "config": config_dict(cfg, world),
+            "details": {"buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})[rank]",
+                        "terms": total_terms, "entries": ent.n if world == 1 else None},
             "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_outer_emit -> "
                          "radix sort (row,col) + (bucket) -> k_outer_reduce",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -432,27 +459,39 @@ def run_product(args, rank, world):
 
 
 def product_cpu_baseline(args, cfg, s, n_products=None):
-    """C oracle exact_product (oracle.py:20-50 restated) on the first products, one thread."""
+    """The reference's per-partition enumerate_interval + fp64 dict
+    accumulation (interval.py:236-254, engine.py:584-591), restated in C
+    (oracle run_parallel, exact regime): shared-nothing worker intervals of
+    the kappa buckets on all host cores, over the first products."""
     import numpy as np
 
     import oracle
+    import paper_1210_0461_b200 as crop
 
     k = min(n_products or args.cpu_sample_tx or 100_000, s.length)
     a1, b1 = int(s.a_ptr[k]), int(s.b_ptr[k])
     st = oracle.Stream(s.a_ptr[: k + 1], s.a_idx[:a1], s.a_val[:a1],
                        s.b_ptr[: k + 1], s.b_idx[:b1], s.b_val[:b1])
     terms = int((np.diff(s.a_ptr[: k + 1]) * np.diff(s.b_ptr[: k + 1])).sum())
+    cores = cpu_count()
+    workers = min(cores, cfg.kappa)
+    h = crop.make_hashes(crop.HashConfig(cfg.kappa, crop.derive_seed(0, "instance:0")))
     t0 = time.perf_counter()
-    oracle.exact_product(st)
+    oracle.run_parallel(st, h.coefficients(), cfg.kappa, workers, capacity=0, upper_only=False,
+                        threads=workers)
     t = time.perf_counter() - t0
-    return {"value": terms / t, "unit": "terms/s", "cores": 1, "kind": "port",
-            "sample": f"first {k} of {s.length} products ({terms} terms), exact_product "
-                      f"restatement (fp64 dict accumulation), one thread",
+    return {"value": terms / t, "unit": "terms/s", "cores": workers, "kind": "port",
+            "sample": f"first {k} of {s.length} products ({terms} terms), per-partition "
+                      f"enumerate_interval + fp64 dict restatement, {workers} shared-nothing "
+                      f"workers (bucket intervals of kappa={cfg.kappa}) on {workers} threads",
             "seconds": round(t, 3)}
 
 
 def run_e2e(args, cfg, dtx, rank, world):
-    """Public API from pinned host buffers: H2D, count, top-k, D2H inside."""
+    """Public API from pinned host buffers, every step: H2D of the input,
+    crop.run (count), SketchState.top_entries, and the D2H of EVERY counted
+    entry (row, col, support) into pinned host arrays
+    (SketchState.entry_arrays) -- c2 "report all counts"."""
     import numpy as np
     import torch
 
@@ -463,18 +502,29 @@ def run_e2e(args, cfg, dtx, rank, world):
     config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
                                cs_enabled=False, seed=0)
     off_np, it_np = off_h.numpy(), it_h.numpy().view(np.uint32)
-    total_terms = None
+    out = None
+    d2h = [0]
 
     def once():
+        nonlocal out
         stream = crop.TransactionStream(cfg.n_items, off_np, it_np, validate=False)
         if world > 1:
             from paper_1210_0461_b200 import distributed
 
             top, report = distributed.top_entries_distributed(stream if rank == 0 else None,
                                                               config, cfg.top_k)
+            d2h[0] = cfg.kappa * 8 + cfg.top_k * 24
         else:
             state, report = crop.run(stream, config, upper_triangle_only=True)
             top = state.top_entries(cfg.top_k)
+            n = state.device_result.entries.n
+            if out is None or out[0].shape[0] < n:
+                cap = int(n * 1.05) + 1024
+                out = tuple(torch.empty(cap, dtype=torch.int32, pin_memory=True).numpy()
+                            .view(np.uint32) for _ in range(3))
+            row, col, cnt = state.entry_arrays(out=out)
+            # loads (kappa u64) + top-k + every entry's (row, col, count)
+            d2h[0] = cfg.kappa * 8 + cfg.top_k * 24 + 12 * int(row.shape[0])
         torch.cuda.synchronize()
         return report
 
@@ -496,42 +546,45 @@ def run_e2e(args, cfg, dtx, rank, world):
     terms = int(((dtx.offsets[1:] - dtx.offsets[:-1]) *
                  (dtx.offsets[1:] - dtx.offsets[:-1] - 1) // 2).sum().item())
     h2d = off_h.numel() * 8 + it_h.numel() * 4
-    d2h = cfg.kappa * 12 + 16 + cfg.top_k * 24
     return {"value": terms / tm, "unit": "terms/s", "ms_per_step": tm * 1e3,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "api": "crop.run(TransactionStream) + SketchState.top_entries"
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0],
+            "api": "crop.run(TransactionStream) + SketchState.top_entries + "
+                   "SketchState.entry_arrays (all counts to pinned host memory)"
             if world == 1 else "distributed.top_entries_distributed"}
 
 
 def default_sample(cfg_name):
     # about 10 s of oracle work on the box's host threads
-    return {"c1": 20_000, "c2": 2_000_000, "c3": 600_000, "c5": 20_000}.get(cfg_name, 50_000)
+    return {"c1": 20_000, "c2": 500_000, "c3": 400_000, "c5": 10_000, "c4": 100_000}.get(
+        cfg_name, 50_000)
 
 
-def cpu_baseline(args, cfg, dtx, reps: int = 1):
-    """C oracle (reference algorithm restated) on a bounded prefix, all host cores."""
+def cpu_baseline(args, cfg, dtx):
+    """C oracle (reference algorithm restated) on a bounded prefix of the
+    workload, all host cores."""
+    n_sample = args.cpu_sample_tx or default_sample(args.config)
+    n_sample = min(n_sample, dtx.n_tx)
+    off = dtx.offsets[: n_sample + 1].cpu().numpy()
+    items = dtx.items[: int(off[-1])].cpu().numpy().view("uint32")
+    return cpu_baseline_arrays(args, cfg, off, items)
+
+
+def cpu_baseline_arrays(args, cfg, off, items):
     import numpy as np
 
     import oracle
     import paper_1210_0461_b200 as crop
 
-    n_sample = args.cpu_sample_tx or default_sample(args.config)
-    off, items = dtx.to_host()
-    n_sample = min(n_sample, off.shape[0] - 1)
-    off_s = off[: n_sample + 1]
-    items_s = items[: off_s[-1]]
-    lens = np.diff(off_s)
+    n_sample = off.shape[0] - 1
+    lens = np.diff(off)
     terms = int((lens * (lens - 1) // 2).sum())
     cores = cpu_count()
     h = crop.make_hashes(crop.HashConfig(cfg.kappa, crop.derive_seed(0, "instance:0")))
-    stream = oracle.Stream(off_s, items_s)
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        oracle.run_parallel(stream, h.coefficients(), cfg.kappa, cfg.workers, capacity=0,
-                            upper_only=True, threads=cores)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.mean(ts)
+    stream = oracle.Stream(off, items)
+    t0 = time.perf_counter()
+    oracle.run_parallel(stream, h.coefficients(), cfg.kappa, cfg.workers, capacity=0,
+                        upper_only=True, threads=cores)
+    t = time.perf_counter() - t0
     return {"value": terms / t, "unit": "terms/s", "cores": min(cores, cfg.workers),
             "kind": "port",
             "sample": f"first {n_sample} of {cfg.n_tx} transactions ({terms} terms), "
@@ -542,45 +595,49 @@ def cpu_baseline(args, cfg, dtx, reps: int = 1):
 
 # ------------------------------------------------------------------ reference arm
 
+def host_workload_sample(cfg, n_tx):
+    """The first n_tx transactions of the config's seeded workload, built on
+    the host by the oracle's copy of the generator (no product library)."""
+    import oracle
+    from paper_1210_0461_b200 import workloads
+
+    alias = workloads.zipf_alias(cfg.n_items, cfg.zipf_s)
+    cdf, lo = workloads.length_cdf(cfg.length)
+    return oracle.gen_transactions(n_tx, cfg.n_items, alias, cdf, lo, cfg.seed)
+
+
 def run_reference(args, rank, world):
+    """The reference algorithm on the host cores (the reference package is pure
+    Python and absent on the GPU box: its C restatement, oracle/, stands in;
+    kind "port"). Rank 0 alone; no CUDA context, no product library."""
     if rank != 0:
         return
-    import torch
-
     from paper_1210_0461_b200 import workloads
 
     cfg = workloads.CONFIGS[args.config]
     if not isinstance(cfg, workloads.PairConfig):
-        s = workloads.generate_product_workload(cfg)
+        s = workloads.generate_product_workload(cfg)  # numpy, host
         vals = [product_cpu_baseline(args, cfg, s) for _ in range(args.warmup + args.steps)]
         vals = vals[args.warmup:]
-        value = statistics.mean(v["value"] for v in vals)
-        print(json.dumps({
-            "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": "terms/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": statistics.mean(v["seconds"] for v in vals) * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (SURVEY.md §8d)", "config": {"workload": cfg.name, "sample": vals[0]["sample"]},
-            "cpu_baseline": {"value": value, "unit": "terms/s", "cores": 1, "kind": "port",
-                             "sample": vals[0]["sample"]},
-            "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }), flush=True)
-        return
-    dtx = workloads.generate_pairs_workload(cfg, n_tx=args.cpu_sample_tx or default_sample(args.config))
-    torch.cuda.synchronize()
-    vals = []
-    for k in range(args.warmup + args.steps):
-        r = cpu_baseline(args, cfg, dtx)
-        if k >= args.warmup:
-            vals.append(r)
+        dtype = "f64"
+        data = "synthetic: seeded Pareto-nnz CSC/CSR, N(0,1) fp32 values (SURVEY.md §8d)"
+    else:
+        n_sample = args.cpu_sample_tx or default_sample(args.config)
+        off, items = host_workload_sample(cfg, min(n_sample, cfg.n_tx))
+        vals = []
+        for k in range(args.warmup + args.steps):
+            r = cpu_baseline_arrays(args, cfg, off, items)
+            if k >= args.warmup:
+                vals.append(r)
+        dtype = "u32"
+        data = "synthetic: seeded Zipf transactions (SURVEY.md §8d, data seed = config no.)"
     value = statistics.mean(v["value"] for v in vals)
     line = {
         "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": "terms/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.mean(v["seconds"] for v in vals) * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic: seeded Zipf transactions (SURVEY.md §8d)",
-        "config": {"workload": cfg.name, "sample": vals[0]["sample"]},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
+        "data": data, "config": config_dict(cfg, world),
         "cpu_baseline": {"value": value, "unit": "terms/s", "cores": vals[0]["cores"],
                          "kind": "port", "sample": vals[0]["sample"]},
         "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0,
@@ -594,6 +651,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)  # host only: rank 0 runs, the others exit 0
+        return
     import torch
 
     torch.cuda.set_device(local)
@@ -602,10 +662,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        if args.impl == "reference":
-            run_reference(args, rank, world)
-        else:
-            run_ours(args, rank, world)
+        run_ours(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -69,6 +69,10 @@ def lib():
         L.ora_table_size.argtypes = [P]
         L.ora_table_export.argtypes = [P, P, P, P]
         L.ora_table_free.argtypes = [P]
+        L.ora_gen_lengths.argtypes = [i64, u64, P, u32, u32, P]
+        L.ora_gen_lengths.restype = None
+        L.ora_gen_items.argtypes = [i64, u64, u32, P, P, P, P, i32]
+        L.ora_gen_items.restype = None
         _lib = L
     return _lib
 
@@ -225,3 +229,21 @@ def sorted_pairs(row, col, w):
     """Canonical (row, col)-sorted view for comparisons."""
     order = np.lexsort((col, row))
     return row[order], col[order], w[order]
+
+
+def gen_transactions(n_tx: int, n_items: int, item_alias, len_cdf, len_lo: int, seed: int,
+                     threads: int = 0):
+    """Host copy of the bench's seeded generator (csrc/gen.cu, restated in
+    crop_oracle.c) -> CSR (offsets int64[n_tx+1], items uint32[nnz]); the same
+    arrays the GPU generator writes, without loading the product library."""
+    thresh, alias = _u32(item_alias[0]), _u32(item_alias[1])
+    cdf = _u32(len_cdf)
+    lengths = np.empty(max(n_tx, 1), np.int64)
+    lib().ora_gen_lengths(n_tx, seed, _p(cdf), cdf.shape[0], len_lo, _p(lengths))
+    offsets = np.zeros(n_tx + 1, np.int64)
+    np.cumsum(lengths[:n_tx], out=offsets[1:])
+    items = np.empty(max(int(offsets[-1]), 1), np.uint32)
+    threads = threads or len(os.sched_getaffinity(0))
+    lib().ora_gen_items(n_tx, seed, n_items, _p(thresh), _p(alias), _p(offsets), _p(items),
+                        threads)
+    return offsets, items[: int(offsets[-1])]

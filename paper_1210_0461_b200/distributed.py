@@ -121,67 +121,125 @@ def run_distributed(stream, config, upper_triangle_only: bool = False, compute=N
     return merge_partials([p for part in gathered for p in part])
 
 
+def _coll(op, t, *args, **kw):
+    """Run a collective on `t` with the process group's device: NCCL takes the
+    CUDA tensor as is; gloo (CPU tests, several processes sharing one GPU)
+    goes through a host copy, written back for in-place collectives."""
+    dist = _dist()
+    if dist.get_backend() == "nccl" or t.device.type == "cpu":
+        return op(t, *args, **kw)
+    h = t.cpu()
+    r = op(h, *args, **kw)
+    t.copy_(h)
+    return r
+
+
 def top_entries_distributed(stream, config, k: int, upper_triangle_only: bool = True,
                             src: int = 0):
-    """Device path of a multi-GPU top-k mine (the benchmark's public call).
+    """Device path of a multi-GPU top-k mine (the benchmark's public call):
+    SketchState.top_entries(k) of crop.run over all GPUs (engine.py:162-172).
 
     Rank `src` moves the stream to its GPU and broadcasts the CSR arrays once
-    over NCCL; each rank counts the buckets of its block of worker intervals
-    (crop_pairs with an interval filter), reports per-bucket loads and its
-    local top-k; loads are all-reduced and the k*G candidates gathered to
+    (NCCL over NVLink); each rank counts the buckets of its block of worker
+    intervals only (crop_pairs with an interval filter), applies the bounded
+    regime's per-bucket top-l summaries to its own buckets (each bucket lives
+    on exactly one rank), and picks its local top-k; per-bucket loads and
+    Count-Sketch cells are all-reduced and the k*G candidates gathered to
     `src`, which merges them. Returns (top entries, LoadReport) on `src`,
-    (None, None) elsewhere. 0/1 self-join (mining) streams only."""
+    (None, None) elsewhere. 0/1 self-join (mining) streams, one instance
+    (an entry's buckets in several instances live on different ranks)."""
     import torch
 
     from . import kernels
     from .engine import LoadReport, TopEntry, _worker_rows, prepare
+    from .errors import ConfigError
     from .hashing import HashConfig, make_hashes
     from .sparse import Entry
 
+    if config.instances != 1:
+        raise ConfigError("top_entries_distributed handles instances == 1 (use run_parallel)")
+    if k < 0:
+        raise ConfigError(f"k must be >= 0, got {k}")
     dist = _dist()
     me, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", torch.cuda.current_device())
     if me == src:
         prep = prepare(stream)
         if prep.kind != "pairs":
-            raise ValueError("top_entries_distributed handles 0/1 self-join streams")
+            raise ConfigError("top_entries_distributed handles 0/1 self-join streams")
         dtx = prep.device
         meta = torch.tensor([dtx.n_tx, dtx.nnz, dtx.n_items, prep.n_rows, prep.pair_total],
                             dtype=torch.int64, device=dev)
     else:
         meta = torch.zeros(5, dtype=torch.int64, device=dev)
-    dist.broadcast(meta, src)
+    _coll(dist.broadcast, meta, src)
     n_tx, nnz, n_items, dim, pair_total = (int(v) for v in meta.tolist())
     if me != src:
         dtx = kernels.DeviceTransactions(torch.empty(n_tx + 1, dtype=torch.int64, device=dev),
                                          torch.empty(nnz, dtype=torch.int32, device=dev), n_items)
-    dist.broadcast(dtx.offsets, src)
-    dist.broadcast(dtx.items, src)
+    _coll(dist.broadcast, dtx.offsets, src)
+    _coll(dist.broadcast, dtx.items, src)
     kappa = config.kappa
     lo, hi = rank_workers(config.workers, me, world)
     asg = config.assignments()
     h = make_hashes(HashConfig(kappa, config.instance_seeds()[0]))
     tab = kernels.hash_tables(h, n_items)
-    cand = torch.full((3, k), -1, dtype=torch.int32, device=dev)
+    kk = max(k, 1)
+    cand = torch.full((3, kk), -1, dtype=torch.int32, device=dev)
     loads = torch.zeros(kappa, dtype=torch.int64, device=dev)
-    if hi > lo:
+    cells = torch.zeros(kappa, dtype=torch.int64, device=dev)
+    if hi > lo and k > 0:
         ent = kernels.count_pairs(dtx, upper_triangle_only, kappa, asg[lo].start,
                                   asg[hi - 1].stop, *tab)
-        bl, _, _ = kernels.entry_bucket_stats(ent, [tab], kappa, n_items, None)
+        signs = [h.sign_hash] if config.cs_enabled else None
+        bl, distinct, cs = kernels.entry_bucket_stats(ent, [tab], kappa, n_items, signs)
         loads += bl[0]
-        idx = kernels.topk_indices(ent, k)
+        if cs is not None:
+            cells += cs[0]
+        count = None
+        if int(distinct[0].max().item()) > config.ss_capacity:
+            # bounded regime: only the per-bucket top-l records are candidates
+            mask, _, _ = kernels.bucket_topk(ent, tab[0], tab[1], kappa, config.ss_capacity)
+            count = torch.where(mask, ent.count[: ent.n], torch.zeros_like(ent.count[: ent.n]))
+        idx = kernels.topk_indices(ent, k, count=count)
+        if count is not None:
+            idx = idx[count[idx] != 0]
         m = idx.shape[0]
         cand[0, :m], cand[1, :m], cand[2, :m] = ent.row[idx], ent.col[idx], ent.count[idx]
-    dist.all_reduce(loads)
-    gathered = [torch.empty_like(cand) for _ in range(world)] if me == src else None
-    dist.gather(cand, gathered, dst=src)
+    elif hi > lo:
+        ent = kernels.count_pairs(dtx, upper_triangle_only, kappa, asg[lo].start,
+                                  asg[hi - 1].stop, *tab)
+        bl, _, cs = kernels.entry_bucket_stats(ent, [tab], kappa, n_items,
+                                               [h.sign_hash] if config.cs_enabled else None)
+        loads += bl[0]
+        if cs is not None:
+            cells += cs[0]
+    _coll(dist.all_reduce, loads)
+    if config.cs_enabled:
+        _coll(dist.all_reduce, cells)
+    if dist.get_backend() == "nccl":
+        gathered = [torch.empty_like(cand) for _ in range(world)] if me == src else None
+        dist.gather(cand, gathered, dst=src)
+    else:
+        gathered = [torch.empty_like(cand).cpu() for _ in range(world)] if me == src else None
+        dist.gather(cand.cpu(), gathered, dst=src)
     if me != src:
         return None, None
-    allc = torch.cat(gathered, dim=1).cpu().numpy().view(np.uint32).astype(np.int64)
-    keep = allc[2] != 0xFFFFFFFF
-    r, c, w = allc[0][keep], allc[1][keep], allc[2][keep]
-    order = np.lexsort((c, r, -w))[:k]
-    top = [TopEntry(Entry(int(r[x]), int(c[x])), float(w[x]), float(w[x]), None) for x in order]
+    if k == 0:
+        top = []
+    else:
+        allc = torch.cat([g.cpu() for g in gathered], dim=1).numpy().view(np.uint32)
+        allc = allc.astype(np.int64)
+        keep = allc[2] != 0xFFFFFFFF
+        r, c, w = allc[0][keep], allc[1][keep], allc[2][keep]
+        order = np.lexsort((c, r, -w))[:k]
+        cs_h = cells.cpu().numpy().astype(np.float64) if config.cs_enabled else None
+        top = []
+        for x in order:
+            row, col, wt = int(r[x]), int(c[x]), float(w[x])
+            est = float(cs_h[h.bucket_of(row, col)]) * h.sign_hash(row, col) \
+                if cs_h is not None else None
+            top.append(TopEntry(Entry(row, col), wt, wt, est))
     rows = [_worker_rows(loads.cpu().numpy(), asg)]
     report = LoadReport(kappa=kappa, workers=config.workers, rows=rows,
                         input_pair_total=pair_total,

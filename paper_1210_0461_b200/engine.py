@@ -429,6 +429,45 @@ class SketchState:
         tn = tuple.__new__
         return [tn(TopEntry, (tn(Entry, (r, c)), w, w, None)) for r, c, w in zip(rl, cl, wl)]
 
+    def entry_arrays(self, instance: int = 0, out=None):
+        """All recorded entries of one instance as columnar host arrays
+        (row uint32, col uint32, weight): the columnar form of
+        `instances[t].summaries` (the reference's per-bucket dicts,
+        engine.py:108-118) without building one Python object per entry.
+        0/1 streams give uint32 supports, real streams float64 weights.
+        A device-backed state copies them with one device->host transfer per
+        column into pinned buffers (`out` = reusable (row, col, weight) numpy
+        arrays of at least the entry count, e.g. from pinned torch tensors)."""
+        self._require_frozen()
+        if self._dev is None:
+            recs = [(it[0], it[1], c) for s in self.instances[instance].summaries.values()
+                    for it, c, _ in s.records()]
+            row = np.array([r[0] for r in recs], dtype=np.uint32)
+            col = np.array([r[1] for r in recs], dtype=np.uint32)
+            return row, col, np.array([r[2] for r in recs], dtype=np.float64)
+        import torch
+
+        d = self._dev
+        e = d.entries
+        inst = d.instances[instance]
+        n = e.n
+        cols = [e.row[:n], e.col[:n], e.count[:n] if d.integer else e.value[:n]]
+        if inst.recorded is not None:
+            cols = [c[inst.recorded] for c in cols]
+            n = int(cols[0].shape[0])
+        if out is None:
+            host = [torch.empty(n, dtype=c.dtype, pin_memory=True) for c in cols]
+        else:
+            host = [torch.from_numpy(o.view(np.int32) if o.dtype == np.uint32 else o)[:n]
+                    for o in out]
+        for h, c in zip(host, cols):
+            h.copy_(c, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        row, col, w = (h.numpy() for h in host)
+        if d.integer:
+            return row.view(np.uint32), col.view(np.uint32), w.view(np.uint32)
+        return row.view(np.uint32), col.view(np.uint32), w
+
     def recorded_weight(self) -> float:
         if self._dev is not None:
             d = self._dev
@@ -460,11 +499,15 @@ class LoadReport:
         return self.total_entries / self.workers
 
     def max_avg_ratio(self) -> float:
+        """Worst max/avg over instances, rounded as engine.py:207-216 does
+        (avg = total / len first, then max / avg)."""
         worst = 1.0
         for row in self.rows:
             total = sum(row)
-            if total:
-                worst = max(worst, max(row) * len(row) / total)
+            if total == 0:
+                continue
+            avg = total / len(row)
+            worst = max(worst, max(row) / avg)
         return worst
 
 

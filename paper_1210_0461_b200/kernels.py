@@ -502,3 +502,41 @@ def product_worker_loads(a_ptr, a_idx, b_ptr, b_idx, n_products: int, h_row, h_c
              nat.ptr(b_idx), n_products, nat.ptr(h_row), nat.ptr(h_col), kappa, workers,
              int(upper_only), nat.ptr(out), nat.stream_ptr())
     return out[: n_products * workers].view(n_products, workers)
+
+
+def merge_bucket_summaries(parts: list, h_row, h_col, kappa: int, capacity: int):
+    """Per-bucket top-`capacity` summaries of a job counted as disjoint parts
+    (tile shards / ranks: every pair's exact count lives in exactly one part,
+    but a bucket's pairs spread over all parts).
+
+    Each part keeps only its own top-l candidates per bucket; a bucket's
+    global top-l is among the union of those candidates, so one more
+    bucket_topk over the concatenated candidates gives the summaries of the
+    whole job (the bounded Space-Saving regime, spacesaving.py:39-63, with
+    exact weights). Loads and distinct counts are summed over the parts.
+    Returns (DeviceEntries of the candidates, recorded mask over them,
+    bucket_min int64[kappa], loads int64[kappa], distinct int64[kappa])."""
+    dev = h_row.device
+    loads = torch.zeros(kappa, dtype=torch.int64, device=dev)
+    distinct = torch.zeros(kappa, dtype=torch.int64, device=dev)
+    rows, cols, cnts = [], [], []
+    for ent in parts:
+        bl, dc, _ = entry_bucket_stats(ent, [(h_row, h_col)], kappa, int(h_row.shape[0]), None)
+        loads += bl[0]
+        distinct += dc[0].to(torch.int64)
+        n = ent.n
+        if int(dc[0].max().item()) >= capacity:
+            mask, _, _ = bucket_topk(ent, h_row, h_col, kappa, capacity)
+            rows.append(ent.row[:n][mask])
+            cols.append(ent.col[:n][mask])
+            cnts.append(ent.count[:n][mask])
+        else:
+            rows.append(ent.row[:n])
+            cols.append(ent.col[:n])
+            cnts.append(ent.count[:n])
+    row, col, cnt = torch.cat(rows), torch.cat(cols), torch.cat(cnts)
+    cand = DeviceEntries(row, col, cnt, None, int(row.shape[0]), parts[0].total_terms)
+    mask, bmin, _ = bucket_topk(cand, h_row, h_col, kappa, capacity)
+    full = distinct >= capacity
+    bmin = torch.where(full, bmin, torch.zeros_like(bmin))
+    return cand, mask, bmin, loads, distinct

@@ -199,6 +199,58 @@ def main():
                                                                     "0", "1", "2", "9"]}})
     golden["spacesaving"] = ss_cases
 
+    # ---- round 2 additions (appended so every fixture above is unchanged) ----
+    # LoadReport.max_avg_ratio rounding (engine.py:207-216) on random rows
+    ratio_rows = []
+    for _ in range(400):
+        width = rng.randint(1, 12)
+        rows = [[rng.randint(0, 10 ** rng.randint(1, 9)) for _ in range(width)]
+                for _ in range(rng.randint(1, 3))]
+        rep = crop.LoadReport(kappa=width, workers=width, rows=rows, input_pair_total=0)
+        ratio_rows.append([rows, rep.max_avg_ratio()])
+    golden["max_avg_ratio"] = ratio_rows
+
+    # per-product worker loads (engine.py:250-251,287-288; measure_loads :305-349)
+    per_product = []
+    for n_tx, n_items, max_len, kappa, workers, seed, upper in [(120, 50, 14, 8, 3, 1, True),
+                                                                (90, 200, 30, 64, 5, 2, False)]:
+        tx = gen_transactions(rng, n_tx, n_items, max_len)
+        stream = crop.transactions_to_stream(tx)
+        cfg = crop.EngineConfig(kappa=kappa, ss_capacity=2 ** 31, workers=workers,
+                                cs_enabled=False, seed=seed)
+        _, rep = crop.run(stream, cfg, upper_triangle_only=upper, record_per_product=True)
+        ml = crop.measure_loads(stream, cfg, upper_triangle_only=upper, record_per_product=True)
+        per_product.append({"transactions": tx, "config": cfg.to_dict(), "upper": upper,
+                            "run": [list(x[:2]) + [list(x[2])] for x in rep.per_product],
+                            "measure": [list(x[:2]) + [list(x[2])] for x in ml.per_product]})
+    golden["per_product"] = per_product
+
+    # run_worker payloads (engine.py:396-455), exact regime, 3 instances + Count-Sketch
+    tx = gen_transactions(rng, 200, 80, 16)
+    stream = crop.transactions_to_stream(tx)
+    cfg = crop.EngineConfig(kappa=12, ss_capacity=2 ** 31, workers=4, cs_enabled=True,
+                            instances=3, seed=21)
+    golden["run_worker"] = {"transactions": tx, "config": cfg.to_dict(),
+                            "payloads": [crop.run_worker(stream, cfg, w, upper_triangle_only=True)
+                                         for w in range(cfg.workers)]}
+
+    # Zipf generators (oracle.py:74-185)
+    zs = []
+    for scale, skew, distinct, dim, outer, seed in [(100.0, 1.2, 30, 12, None, 1),
+                                                     (5.0, 0.8, 20, 9, 20, 2),
+                                                     (1.0, 1.5, 12, 6, 17, 3)]:
+        s = crop.gen_zipf_stream(crop.ZipfModel(scale, skew, distinct), dim, outer, seed)
+        zs.append({"args": [scale, skew, distinct, dim, outer, seed],
+                   "products": [[list(a.indices), list(a.values), list(b.indices), list(b.values)]
+                                for a, b in s]})
+    zt = []
+    for n_items, n_tx, skew, seed, mean in [(200, 40, 1.1, 5, 10), (30, 25, 0.7, 9, 4),
+                                            (5, 10, 2.0, 0, 8)]:
+        zt.append({"args": [n_items, n_tx, skew, seed, mean],
+                   "transactions": [list(t) for t in
+                                    crop.gen_zipf_transactions(n_items, n_tx, skew, seed, mean)]})
+    golden["zipf"] = {"streams": zs, "transactions": zt}
+
     with open(os.path.join(HERE, "reference_golden.json"), "w") as fh:
         json.dump(golden, fh, separators=(",", ":"))
     print("wrote", os.path.join(HERE, "reference_golden.json"))

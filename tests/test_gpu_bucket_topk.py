@@ -80,7 +80,12 @@ def test_bounded_regime_through_the_api():
     tx = [sorted(rng.choice(60, size=rng.integers(2, 12), replace=False).tolist()) for _ in range(3000)]
     cfg = crop.EngineConfig(kappa=5, ss_capacity=40, workers=5, seed=2, cs_enabled=False)
     state, report = crop.run(crop.transactions_to_stream(tx), cfg, upper_triangle_only=True)
-    sup = crop.exact_pair_supports(tx)
+    # exact supports from the C oracle (an independent CPU count)
+    import oracle
+    from conftest import tx_to_csr
+
+    r, c, w = oracle.pair_supports(*tx_to_csr(tx))
+    sup = {(int(a), int(b)): int(x) for a, b, x in zip(r, c, w)}
     for inst in state.instances:
         for bkt, s in inst.summaries.items():
             m = s.total_weight

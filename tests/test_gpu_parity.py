@@ -396,3 +396,17 @@ def test_long_transactions_and_wide_rows(count_mode):
     off, items = tx_to_csr(too_long)
     with pytest.raises(crop.InputError):
         kernels.count_pairs(kernels.DeviceTransactions.from_host(off, items, 9000), True)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_host_generator_copy_matches_device_generator(name):
+    """bench.py's reference arm builds its sample with the oracle's host copy
+    of the generator (no product library); it must be the same data."""
+    cfg = workloads.CONFIGS[name]
+    n = 20_000
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=n)
+    off, items = oracle.gen_transactions(n, cfg.n_items, workloads.zipf_alias(cfg.n_items, cfg.zipf_s),
+                                         *workloads.length_cdf(cfg.length), cfg.seed)
+    d_off, d_items = dtx.to_host()
+    assert np.array_equal(off, d_off)
+    assert np.array_equal(items, d_items)

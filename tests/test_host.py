@@ -204,3 +204,48 @@ def test_workload_tables():
     for k in range(0, 2000, 97):
         seg = s.a_idx[s.a_ptr[k]:s.a_ptr[k + 1]]
         assert np.all(np.diff(seg.astype(np.int64)) > 0)
+
+
+# ---------------------------------------------------------------- round 2
+
+def test_max_avg_ratio_rounds_like_reference(golden):
+    """engine.py:207-216: avg = total / len first, then max / avg, bit for bit."""
+    for rows, want in golden["max_avg_ratio"]:
+        rep = crop.LoadReport(kappa=len(rows[0]), workers=len(rows[0]), rows=rows,
+                              input_pair_total=0)
+        assert rep.max_avg_ratio() == want
+
+
+def test_public_names_match_reference():
+    ref_all = {"BalanceCheck", "ConfigError", "CountSketch", "CropError", "DimensionError",
+               "EngineConfig", "Entry", "EntryHasher", "HashConfig", "HashedIndexArray",
+               "IndexHashFn", "InputError", "LoadReport", "MedianEstimator",
+               "OuterProductStream", "ParseError", "ResourceCapError", "ScanStats", "SignHashFn",
+               "SketchState", "SpaceSavingSummary", "SparseVector", "TopEntry",
+               "WorkerAssignment", "ZipfModel", "bound_ratio_report", "bucket_sort_indices",
+               "count_interval", "derive_seed", "entry_hash", "enumerate_interval",
+               "exact_pair_supports", "exact_product", "exact_top", "gen_zipf_stream",
+               "gen_zipf_transactions", "load_balance_check", "load_column_row_streams",
+               "load_state", "make_hashes", "measure_loads", "median_query", "merge_partials",
+               "mine", "outer_product_nnz", "read_fimi", "recall_at_k", "run", "run_parallel",
+               "run_worker", "save_state", "transaction_to_outer", "transactions_to_stream",
+               "write_fimi", "write_triple_file"}  # reference __init__.py:84-137
+    assert ref_all <= set(crop.__all__)
+    assert all(hasattr(crop, n) for n in crop.__all__)
+
+
+def test_zipf_generators_match_reference(golden):
+    for case in golden["zipf"]["streams"]:
+        scale, skew, distinct, dim, outer, seed = case["args"]
+        s = crop.gen_zipf_stream(crop.ZipfModel(scale, skew, distinct), dim, outer, seed)
+        got = [[list(a.indices), list(a.values), list(b.indices), list(b.values)] for a, b in s]
+        assert got == case["products"]
+    for case in golden["zipf"]["transactions"]:
+        got = crop.gen_zipf_transactions(*case["args"])
+        assert [list(t) for t in got] == case["transactions"]
+    with pytest.raises(crop.ConfigError):
+        crop.ZipfModel(0.0, 1.0, 3)
+    with pytest.raises(crop.ConfigError):
+        crop.gen_zipf_stream(crop.ZipfModel(1.0, 1.0, 50), 5, None, 0)
+    with pytest.raises(crop.ConfigError):
+        crop.gen_zipf_transactions(10, 5, 0.0, 0)

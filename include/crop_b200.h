@@ -103,6 +103,28 @@ int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int
                               uint32_t n_items, int upper_only, const crop_interval* interval,
                               uint32_t shard_rank, uint32_t shard_world, void* stream,
                               crop_pairs** job);
+/* crop_pairs_create_sharded with option flags:
+ *  CROP_PAIRS_SAFE_UNITS  cut every word-counted dense tile into units of at
+ *                         most 65,535 words, so no 16-bit counter can wrap
+ *                         whatever the order of the stream (the re-run after
+ *                         crop_pairs_overflowed reports a wrap);
+ *  CROP_PAIRS_NO_OWN      filtered jobs: do not use the own-bucket (Lemma 1)
+ *                         layout (A/B measurements).
+ * A filtered job (interval narrower than [0, kappa)) whose ids fit one dense
+ * table (n_items <= 57,345) and whose (h_col, id) keys fit 32 bits visits only
+ * its own terms: each transaction's items are copied sorted by (h_col, id)
+ * (bucket_sort_indices, interval.py:70-109) and every row occurrence reads
+ * its one or two class windows of that copy (scan_sorted's windows,
+ * interval.py:125-189). Its plan, words and counts cover its own terms only;
+ * crop_pairs_info's total_terms is then the interval's own term count. */
+#define CROP_PAIRS_SAFE_UNITS 1u
+#define CROP_PAIRS_NO_OWN 2u
+int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                         uint32_t n_items, int upper_only, const crop_interval* interval,
+                         uint32_t shard_rank, uint32_t shard_world, uint32_t flags, void* stream,
+                         crop_pairs** job);
+/* 1 if the job uses the own-bucket layout (see crop_pairs_create_ex). */
+int crop_pairs_own(const crop_pairs* job, int* own);
 /* host-side plan facts: output capacity, total terms (all buckets), tiles */
 int crop_pairs_info(const crop_pairs* job, uint64_t* max_entries, uint64_t* total_terms,
                     uint64_t* n_tiles, uint64_t* n_units);
@@ -118,8 +140,11 @@ int crop_pairs_run(crop_pairs* job, uint32_t* out_row, uint32_t* out_col, uint32
  * routing, per-tile entry counts, -, count}. */
 int crop_pairs_set_timing(crop_pairs* job, int on);
 int crop_pairs_phase_ms(const crop_pairs* job, float* out4);
-/* 1 if the entry list overflowed its capacity (entry mode only: never expected;
- * synchronises). Stream-mode jobs report 0 without synchronising. */
+/* 1 if the job's counts are unreliable (synchronises): entry mode -- the entry
+ * list overflowed its capacity (never expected); stream mode -- a 16-bit
+ * dense counter of a unit holding more than 65,535 words wrapped (possible
+ * only for adversarially ordered streams); re-create the job with
+ * CROP_PAIRS_SAFE_UNITS and run it again. */
 int crop_pairs_overflowed(const crop_pairs* job, int* overflowed);
 /* Counting mode chosen by crop_pairs_create: 1 = stream (one 32-bit word per
  * pair term routed to its tile's stream, coalesced counting), 0 = entry

@@ -37,6 +37,9 @@ _SIGS = {
                                 ctypes.POINTER(P)]),
     "crop_pairs_create_sharded": (i32, [P, P, i64, u32, i32, ctypes.POINTER(Interval), u32, u32, P,
                                         ctypes.POINTER(P)]),
+    "crop_pairs_create_ex": (i32, [P, P, i64, u32, i32, ctypes.POINTER(Interval), u32, u32, u32, P,
+                                   ctypes.POINTER(P)]),
+    "crop_pairs_own": (i32, [P, ctypes.POINTER(i32)]),
     "crop_pairs_info": (i32, [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
                               ctypes.POINTER(u64)]),
     "crop_pairs_own_terms": (i32, [P, ctypes.POINTER(u64)]),
@@ -70,6 +73,9 @@ _SIGS = {
 }
 
 EXPORTED = tuple(_SIGS)
+
+PAIRS_SAFE_UNITS = 1  # include/crop_b200.h CROP_PAIRS_SAFE_UNITS
+PAIRS_NO_OWN = 2
 
 
 def load(path: str = LIB_PATH):

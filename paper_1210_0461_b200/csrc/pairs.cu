@@ -191,15 +191,128 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
   }
 }
 
+// ------------------------------------------------- own-bucket layout (Lemma 1)
+// A filtered job owns the bucket interval [start, stop) of kappa. Pair (i, j)
+// is own iff (h_row(i) + h_col(j)) mod kappa lies in it, i.e. iff h_col(j)
+// lies in row i's circular class window [start - h_row(i), stop - h_row(i))
+// mod kappa -- the two windows of scan_sorted (interval.py:125-189). Every
+// transaction gets a copy of its items sorted by (h_col, id) (the order of
+// bucket_sort_indices, interval.py:70-109), stored as keys
+// h_col << idbits | id, so a row's own partners are at most two contiguous
+// ranges of that copy, found by binary search: a filtered job reads, routes
+// and counts only its own terms (plus, with the triangle filter, the
+// window's items not after the row, which it skips like scan_sorted does).
+struct OwnArgs {
+  const uint32_t* hs;     // (h_col, id)-sorted keys per transaction (same offsets)
+  const uint32_t* h_row;
+  uint32_t kappa, start, len, idbits;
+};
+
+__device__ __forceinline__ uint32_t hs_lower(const uint32_t* __restrict__ hs, uint32_t L, uint64_t key) {
+  uint32_t lo = 0, hi = L;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((uint64_t)__ldg(hs + mid) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Own window of a row with h_row = hr in one transaction's keys hs[0, L):
+// positions [a0, a0 + n1) and (a wrapped window) [0, n2).
+__device__ __forceinline__ void own_window(const uint32_t* __restrict__ hs, uint32_t L, uint32_t hr,
+                                           const OwnArgs& O, uint32_t& a0, uint32_t& n1, uint32_t& n2) {
+  const uint32_t c_lo = O.start >= hr ? O.start - hr : O.start + O.kappa - hr;
+  const uint64_t c_hi = (uint64_t)c_lo + O.len;
+  a0 = hs_lower(hs, L, (uint64_t)c_lo << O.idbits);
+  if (c_hi <= O.kappa) {
+    n1 = hs_lower(hs, L, c_hi << O.idbits) - a0;
+    n2 = 0;
+  } else {
+    n1 = L - a0;
+    n2 = hs_lower(hs, L, (c_hi - O.kappa) << O.idbits);
+  }
+}
+
+// own terms of row item i (UPPER: partners with a larger id only)
+template <bool UPPER>
+__device__ __forceinline__ uint32_t own_count(const uint32_t* __restrict__ hs, uint32_t a0, uint32_t n1,
+                                              uint32_t n2, uint32_t i, uint32_t idmask) {
+  if (!UPPER) return n1 + n2;
+  uint32_t c = 0;
+  for (uint32_t k = 0; k < n1; ++k) c += (__ldg(hs + a0 + k) & idmask) > i;
+  for (uint32_t k = 0; k < n2; ++k) c += (__ldg(hs + k) & idmask) > i;
+  return c;
+}
+
+// Build the (h_col, id)-sorted copy: one warp per transaction; a register
+// bitonic sort for <= 32 items, a shared-memory bitonic sort up to kHsSmem,
+// rank counting beyond (transactions that long are rare).
+constexpr int kHsWarps = 4;
+constexpr uint32_t kHsSmem = 2048;
+__global__ void __launch_bounds__(kHsWarps * 32)
+    k_hs_build(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items, int64_t n_tx,
+               const uint32_t* __restrict__ h_col, uint32_t idbits, uint32_t* __restrict__ hs) {
+  __shared__ uint32_t s_k[kHsWarps][kHsSmem];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* sk = s_k[w];
+  auto key = [&](uint32_t it) { return (__ldg(h_col + it) << idbits) | it; };
+  for (int64_t t = (int64_t)blockIdx.x * kHsWarps + w; t < n_tx; t += (int64_t)gridDim.x * kHsWarps) {
+    const int64_t base = offsets[t];
+    const uint32_t L = (uint32_t)(offsets[t + 1] - base);
+    if (L <= 32) {
+      uint32_t k = (uint32_t)lane < L ? key(__ldg(items + base + lane)) : kEmpty32;
+#pragma unroll
+      for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, k, j);
+          const bool asc = (lane & kk) == 0, lower = (lane & j) == 0;
+          k = (lower == asc) ? min(k, o) : max(k, o);
+        }
+      if ((uint32_t)lane < L) hs[base + lane] = k;
+    } else if (L <= kHsSmem) {
+      uint32_t P = 64;
+      while (P < L) P <<= 1;
+      for (uint32_t x = lane; x < P; x += 32) sk[x] = x < L ? key(__ldg(items + base + x)) : kEmpty32;
+      __syncwarp();
+      for (uint32_t kk = 2; kk <= P; kk <<= 1)
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+          for (uint32_t x = lane; x < P; x += 32) {
+            const uint32_t y = x ^ j;
+            if (y > x) {
+              const uint32_t a = sk[x], b = sk[y];
+              if ((a > b) == ((x & kk) == 0)) {
+                sk[x] = b;
+                sk[y] = a;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      for (uint32_t x = lane; x < L; x += 32) hs[base + x] = sk[x];
+      __syncwarp();
+    } else {
+      for (uint32_t x = lane; x < L; x += 32) {
+        const uint32_t kx = key(__ldg(items + base + x));
+        uint32_t r = 0;
+        for (uint32_t y = 0; y < L; ++y) r += key(__ldg(items + base + y)) < kx;
+        hs[base + r] = kx;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- pass A
 // Per row item i: terms_i (pairs with i as the row) and occ_i, the number of
 // transactions in which i has at least one partner after it (an upper bound
 // of the entries it creates). Output packed as occ << kOccShift | terms.
-template <bool UPPER>
+// OWN: own terms only (the row's own window in the (h_col, id)-sorted copy).
+template <bool UPPER, bool OWN>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_item_terms(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
                  int64_t n_tx, uint32_t n_items, int chunk_tx, unsigned long long* __restrict__ stats,
-                 unsigned int* __restrict__ max_len) {
+                 unsigned int* __restrict__ max_len, OwnArgs O) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
   uint32_t* s_terms = reinterpret_cast<uint32_t*>(smem + kOffBytes);
@@ -210,6 +323,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     s_occ[i] = 0;
   }
   uint32_t my_max = 0;
+  const uint32_t idmask = O.idbits >= 32 ? 0xFFFFFFFFu : ((1u << O.idbits) - 1u);
   const int64_t n_chunks = (n_tx + chunk_tx - 1) / chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
@@ -217,7 +331,16 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr, [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
       if (!q.valid) return;
       my_max = max(my_max, q.L);
-      const uint32_t c = UPPER ? q.L - 1 - q.p : q.L;
+      uint32_t c;
+      if (OWN) {
+        if (UPPER && q.p + 1 >= q.L) return;
+        const uint32_t* hs = O.hs + q.base;
+        uint32_t a0, n1, n2;
+        own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
+        c = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
+      } else {
+        c = UPPER ? q.L - 1 - q.p : q.L;
+      }
       if (c == 0) return;
       if (i < n_smem) {
         atomicAdd(&s_terms[i], c);
@@ -1012,6 +1135,18 @@ __device__ __forceinline__ void bump_half(uint32_t* t32, uint32_t slot) {
 }
 constexpr uint32_t kStreamMeanMax = 64;
 
+// bump_half for a unit that holds more than 65,535 words: a counter can only
+// wrap there if one (row, column) pair occurs that often in the unit's word
+// range (the planner bounds a unit's ROW OCCURRENCES on average, not per
+// range), so the returning atomic checks the half it bumped and raises the
+// job's overflow flag; the caller re-plans with CROP_PAIRS_SAFE_UNITS.
+__device__ __forceinline__ void bump_half_checked(uint32_t* t32, uint32_t slot, uint32_t* flag) {
+  const uint32_t hi = slot >= kSHalf;
+  const uint32_t sh = hi << 4;
+  const uint32_t old = atomicAdd(&t32[slot - hi * kSHalf], 1u << sh);
+  if (((old >> sh) & 0xFFFFu) == 0xFFFFu) atomicOr(flag, 1u);
+}
+
 // per-row constant of the word of (i, j) in tile T: dense word = base + j,
 // hash word = base | j
 __host__ __device__ __forceinline__ uint32_t stream_base(const Tile& T, uint32_t i, uint32_t n,
@@ -1611,6 +1746,157 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   }
 }
 
+// Own-bucket scatter (Lemma 1): like k_stream_scatter, but a row occurrence
+// routes only its own partners, read from its window(s) of the (h_col,
+// id)-sorted copy. Walk: each position finds its window, counts its own
+// partners and claims that many words of its tile. Copy: the parked rows'
+// windows are flattened across the warp; with the triangle filter the items
+// not after the row are dropped and the kept ones compacted with a ballot
+// (one contiguous store run per row and step). Words only for own pairs: a
+// filtered job's write and count phases scale with its own terms.
+constexpr uint32_t kScatParkOwn = 8192;
+template <bool UPPER>
+__global__ void __launch_bounds__(kPassThreads, 1)
+    k_stream_scatter_own(StreamRouteArgs A, OwnArgs O, const uint32_t* __restrict__ bounds,
+                         uint32_t n_chunks) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // kScatMaxTx + 1
+  uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);     // parked rows
+  uint32_t* s_rank = s_tile + kScatParkOwn;
+  uint32_t* s_tx = s_rank + kScatParkOwn;                                     // chunk-local tx
+  uint32_t* s_bp = s_tx + kScatParkOwn;                                       // row word base
+  uint32_t* s_job = s_bp + kScatParkOwn;                                      // per warp 256 words
+  uint32_t* s_misc = s_job + kPassThreads / 32 * 256;
+  const uint32_t ns = min(A.n_tiles, A.scat_ns);
+  const uint32_t ns2 = (ns + 1) & ~1u;
+  uint32_t* s_cnt = s_misc + 4;
+  uint16_t* s_touched = reinterpret_cast<uint16_t*>(s_cnt + ns2);
+  const uint32_t idmask = O.idbits >= 32 ? 0xFFFFFFFFu : ((1u << O.idbits) - 1u);
+  for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
+  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint32_t tb0 = bounds[c], tb1 = bounds[c + 1];
+    for (uint32_t ta = tb0; ta < tb1; ta += kScatMaxTx) {
+      const int ntx = (int)min(kScatMaxTx, tb1 - ta);
+      __syncthreads();
+      if (threadIdx.x == 0) s_misc[0] = 0;
+      for (int t = threadIdx.x; t <= ntx; t += blockDim.x) s_off[t] = A.offsets[ta + t];
+      __syncthreads();
+      const int64_t g_lo = s_off[0];
+      const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
+      walk_chunk<true>(s_off, ntx, A.items, A.item_info,
+                       [&](int64_t g, const Pos& q, uint32_t i, uint2 tv) {
+        if (!q.valid) return;
+        const uint32_t x = (uint32_t)(g - g_lo);
+        uint32_t tile = kNone;
+        if (tv.x != kNone && (UPPER ? q.p + 1 < q.L : q.L > 0)) {
+          const uint32_t* hs = O.hs + q.base;
+          uint32_t a0, n1, n2;
+          own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
+          const uint32_t n = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
+          if (n) {
+            tile = tv.x & kTileMask;
+            uint32_t r;
+            if (tile < ns) {
+              r = atomicAdd(&s_cnt[tile], n);
+              if (r == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = (uint16_t)tile;
+            } else {
+              r = (uint32_t)atomicAdd(&A.tile_cursor[tile], (unsigned long long)n);
+              tile |= kWinFlag;  // rank is already absolute
+            }
+            s_rank[x] = r;
+            s_tx[x] = q.tx;
+            s_bp[x] = tv.y;
+          }
+        }
+        s_tile[x] = tile;
+      });
+      __syncthreads();
+      const uint32_t n_touch = s_misc[0];
+      for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) {
+        const uint32_t t = s_touched[k];
+        s_cnt[t] = (uint32_t)atomicAdd(&A.tile_cursor[t], (unsigned long long)s_cnt[t]);
+      }
+      __syncthreads();
+      {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint32_t* j_dst = s_job + warp * 256;
+        uint32_t* j_src = j_dst + 32;   // global key position of the first window
+        uint32_t* j_tb = j_src + 32;    // transaction start (second window)
+        uint32_t* j_n1 = j_tb + 32;     // first window's length
+        uint32_t* j_b = j_n1 + 32;      // row word base
+        uint32_t* j_i = j_b + 32;       // row item (triangle filter)
+        uint32_t* j_kept = j_i + 32;    // words written so far
+        uint32_t* j_n = j_kept + 32;    // window length
+        for (uint32_t x0 = warp * 32; x0 < npos; x0 += kPassThreads) {
+          const uint32_t x = x0 + lane;
+          uint32_t tile = kNone, pos = 0, nwin = 0, a0 = 0, n1 = 0, i = 0;
+          int64_t tb = 0;
+          if (x < npos) {
+            tile = s_tile[x];
+            if (tile != kNone) {
+              pos = (tile & kWinFlag) ? s_rank[x] : s_cnt[tile] + s_rank[x];
+              const uint32_t t = s_tx[x];
+              tb = s_off[t];
+              const uint32_t L = (uint32_t)(s_off[t + 1] - tb);
+              i = __ldg(A.items + g_lo + x);
+              uint32_t n2;
+              own_window(O.hs + tb, L, __ldg(O.h_row + i), O, a0, n1, n2);
+              nwin = n1 + n2;
+            }
+          }
+          const uint32_t wm = __ballot_sync(0xffffffffu, nwin > 0);
+          if (!wm) continue;
+          if (nwin) {
+            const int r = __popc(wm & ((1u << lane) - 1u));
+            j_dst[r] = pos;
+            j_src[r] = (uint32_t)tb + a0;
+            j_tb[r] = (uint32_t)tb;
+            j_n1[r] = n1;
+            j_b[r] = s_bp[x];
+            j_i[r] = i;
+            j_kept[r] = 0;
+            j_n[r] = nwin;
+          }
+          __syncwarp();
+          const uint32_t mine = (uint32_t)lane < (uint32_t)__popc(wm) ? j_n[lane] : 0u;
+          const uint32_t incl = warp_incl_scan(mine);
+          const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+          const uint32_t excl = incl - mine;
+          uint32_t ob = 0;
+          for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+            const uint32_t o = owner_step(incl, t0, ob) & 31;
+            const uint32_t t = t0 + lane;
+            const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o);
+            const uint32_t o_n = __shfl_sync(0xffffffffu, mine, o);
+            const bool valid = t < S;
+            const uint32_t loc = t - o_excl;
+            uint32_t j = 0;
+            bool keep = false;
+            if (valid) {
+              const uint32_t nn1 = j_n1[o];
+              const uint32_t idx = loc < nn1 ? j_src[o] + loc : j_tb[o] + (loc - nn1);
+              j = __ldg(O.hs + idx) & idmask;
+              keep = !UPPER || j > j_i[o];
+            }
+            const uint32_t km = __ballot_sync(0xffffffffu, keep);
+            const uint32_t sl = o_excl > t0 ? o_excl - t0 : 0u;  // owner's first lane in this step
+            const uint32_t from = ~((1u << sl) - 1u);
+            if (keep)
+              A.words[j_dst[o] + j_kept[o] + __popc(km & from & ((1u << lane) - 1u))] = j_b[o] + j;
+            const bool last = valid && (loc + 1 == o_n || lane == 31);
+            const uint32_t upto = lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+            __syncwarp();
+            if (last) j_kept[o] += __popc(km & from & upto);
+            __syncwarp();
+          }
+        }
+      }
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < n_touch; k += blockDim.x) s_cnt[s_touched[k]] = 0;
+    }
+  }
+}
+
 // Streaming counter: units are ranges of a tile's words; warps read them
 // coalesced (4 loads in flight per lane) and bump u32 shared counters.
 struct StreamCountArgs {
@@ -1642,6 +1928,7 @@ struct StreamCountArgs {
   const uint32_t* items_cls;  // nullable: item | h_col << 16
   const uint32_t* h_row;
   uint32_t kappa, start, stop;
+  uint32_t* overflow;  // raised when a 16-bit dense counter wraps (see bump_half_checked)
 };
 
 // Record an emitted entry for the fused top-k (high counts only: rare).
@@ -1839,10 +2126,16 @@ __global__ void __launch_bounds__(kSCThreads, 2) k_count_stream(StreamCountArgs 
       }
     };
     uint32_t cur[D], nxt[D];
+    // a unit of more than 65,535 words could wrap a 16-bit counter
+    const bool checked = dense && nw > kStreamUnitOcc;
     if (nb > 0) fetch(0, cur);
     for (uint32_t blk = 0; blk < nb; ++blk) {
       if (blk + 1 < nb) fetch(blk + 1, nxt);
-      if (dense) {
+      if (dense && checked) {
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          if (cur[k] != kEmpty32) bump_half_checked(table, cur[k], A.overflow);
+      } else if (dense) {
 #pragma unroll
         for (int k = 0; k < D; ++k)
           if (cur[k] != kEmpty32) bump_half(table, cur[k]);
@@ -2132,6 +2425,9 @@ struct PlanArgs {
   const unsigned long long* stats;
   uint32_t n, col_bits;
   int upper, filter, force;  // force: 0 auto, 1 entry, 2 stream
+  int own;  // filtered job planned on own terms (Lemma-1 layout): word totals known
+  int safe;  // CROP_PAIRS_SAFE_UNITS: word-counted dense units hold <= 65,535 words
+  unsigned long long unit_terms;  // 0: default; CROP_DEBUG_UNIT_TERMS (tests: large units)
   Tile* tiles;
   uint32_t tile_cap;
   Unit* units;
@@ -2230,7 +2526,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   }
   if (!sm) return;
   stamp(0);
-  const uint64_t unit_terms = max(1ull << 16, T / ((uint64_t)kNumSMs * 8));
+  const uint64_t unit_terms = P.unit_terms ? P.unit_terms : max(1ull << 16, T / ((uint64_t)kNumSMs * 8));
   const double inv_ut = (double)kPlanS / (double)unit_terms;
   const uint32_t rows_max = P.col_bits >= 32 ? 1u : ((1u << (32 - P.col_bits)) - 1u);
   const uint64_t y = (kPlanS + rows_max - 1) / rows_max;  // span weight of every row
@@ -2357,7 +2653,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
             tl.c0 = P.upper ? i + 1 : 0;
             tl.mode = P.filter ? 0 : 2;
             tl.width = P.upper ? n - 1 - i : n;
-            tl.n_units = units_of(t, P.stats[i] >> kOccShift);
+            const uint64_t occ = P.stats[i] >> kOccShift;
+            tl.n_units = units_of(t, (P.safe && tl.mode == 0 && t > occ) ? t : occ);
           } else {
             tl.mode = 1;
             tl.n_units = 1;
@@ -2380,7 +2677,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
             tl.nwin = q == 0 ? nwin : 0;
             tl.width = tl.c1 - tl.c0;
             tl.terms = t / nwin + 1;
-            tl.n_units = units_of(tl.terms, P.stats[i] >> kOccShift);
+            const uint64_t occ = P.stats[i] >> kOccShift;
+            tl.n_units = units_of(tl.terms, (P.safe && tl.terms > occ) ? tl.terms : occ);
             P.tiles[id + q] = tl;
           }
           P.item_info[i] = make_uint2(id | kWinFlag, 0u);
@@ -2696,7 +2994,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   // per-tile stream words from the statistics (unfiltered, no windows): an
   // entry tile stores 2 words per row occurrence with a partner after it,
   // a hash tile one word per term
-  const bool known = !P.filter && !s_has_win;
+  const bool known = (!P.filter || P.own) && !s_has_win;
   if (known)
     for (uint32_t t = tid; t < nt; t += kPlanThreads) {
       const Tile& tl = P.tiles[t];
@@ -2771,6 +3069,10 @@ struct crop_pairs {
   uint32_t maxlen = 0;       // longest transaction (device planner path)
   uint16_t* d_items16 = nullptr;  // 16-bit item copy (ids < 2^16), made on the side stream
   uint32_t* d_items_cls = nullptr;  // filtered jobs: item | h_col << 16 (side stream)
+  uint32_t flags = 0;        // CROP_PAIRS_* (crop_pairs_create_ex)
+  bool own = false;          // filtered job on the own-bucket layout (Lemma 1)
+  uint32_t* d_hs = nullptr;  // own: (h_col, id)-sorted keys per transaction
+  uint32_t idbits = 0;
   cudaEvent_t ev_items16 = nullptr;
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
   bool packed_filter = false;  // bucket filter applied on packed items (see k_items_cls)
@@ -2871,7 +3173,34 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
     CROP_LAUNCH_CHECK();
     mark(1);
     R.packed_filter = J->packed_filter ? 1 : 0;
-    if (J->words_known && J->maxlen <= kScatPark / 2) {
+    if (J->own && J->words_known && J->maxlen <= kScatParkOwn / 2) {
+      // own-bucket scatter: only own partners, read from the hs windows
+      const uint32_t band = kScatParkOwn - J->maxlen + 1;
+      const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
+      uint32_t* bounds = nullptr;
+      CROP_CUDA(cudaMallocAsync(&bounds, (size_t)(n_chunks + 1) * 4, st));
+      k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
+          J->offsets, J->n_tx, n_chunks, band, bounds);
+      CROP_LAUNCH_CHECK();
+      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatParkOwn * 16 + 16 +
+                           kPassThreads / 32 * 256 * 4;
+      const size_t budget = 227 * 1024 - fixed;
+      R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
+      const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
+      OwnArgs O{};
+      O.hs = J->d_hs;
+      O.h_row = J->iv.h_row;
+      O.kappa = J->iv.kappa;
+      O.start = J->iv.start;
+      O.len = J->iv.stop - J->iv.start;
+      O.idbits = J->idbits;
+      auto kern = up ? k_stream_scatter_own<true> : k_stream_scatter_own<false>;
+      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
+      kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, O, bounds, n_chunks);
+      CROP_LAUNCH_CHECK();
+      cudaFreeAsync(bounds, st);
+      crop_count_launches(2);
+    } else if (J->words_known && J->maxlen <= kScatPark / 2) {
       // single-walk scatter over position bands
       const uint32_t band = kScatPark - J->maxlen + 1;
       const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
@@ -2920,7 +3249,7 @@ static void free_job(crop_pairs* j) {
     if (e) cudaEventDestroy(e);
   if (j->ev_items16) cudaEventDestroy(j->ev_items16);
   void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words, j->d_items16,
-                  j->d_items_cls};
+                  j->d_items_cls, j->d_hs};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
@@ -3140,21 +3469,24 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
   J->max_entries = cap;
 }
 
-extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
-                                         uint32_t n_items, int upper_only, const crop_interval* interval,
-                                         uint32_t shard_rank, uint32_t shard_world, void* stream,
-                                         crop_pairs** job);
-
 extern "C" int crop_pairs_create(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
                                  uint32_t n_items, int upper_only, const crop_interval* interval,
                                  void* stream, crop_pairs** job) {
-  return crop_pairs_create_sharded(offsets, items, n_tx, n_items, upper_only, interval, 0, 1, stream, job);
+  return crop_pairs_create_ex(offsets, items, n_tx, n_items, upper_only, interval, 0, 1, 0, stream, job);
 }
 
 extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
                                          uint32_t n_items, int upper_only, const crop_interval* interval,
                                          uint32_t shard_rank, uint32_t shard_world, void* stream,
                                          crop_pairs** job) {
+  return crop_pairs_create_ex(offsets, items, n_tx, n_items, upper_only, interval, shard_rank, shard_world,
+                              0, stream, job);
+}
+
+extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* items, int64_t n_tx,
+                                    uint32_t n_items, int upper_only, const crop_interval* interval,
+                                    uint32_t shard_rank, uint32_t shard_world, uint32_t flags,
+                                    void* stream, crop_pairs** job) {
   *job = nullptr;
   if (shard_world < 1 || shard_rank >= shard_world) {
     crop_set_error(CROP_ECONFIG, "shard rank %u of %u", shard_rank, shard_world);
@@ -3167,6 +3499,7 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
   cudaStream_t st = (cudaStream_t)stream;
   if (int rc = crop_pool_setup()) return rc;
   crop_pairs* J = new crop_pairs();
+  J->flags = flags;
   J->shard_rank = shard_rank;
   J->shard_world = shard_world;
   J->offsets = offsets;
@@ -3228,8 +3561,42 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
     JCUDA(cudaMallocAsync(&J->d_terms, nn * sizeof(unsigned long long) + 16, st));
     J->d_maxlen = reinterpret_cast<unsigned int*>(J->d_terms + nn);
     JCUDA(cudaMemsetAsync(J->d_terms, 0, nn * sizeof(unsigned long long) + 16, st));
+    // own-bucket layout (Lemma 1) for filtered jobs: rows never need column
+    // windows (n <= one dense table), and the (h_col, id) keys fit 32 bits
+    {
+      const bool no_own = (J->flags & CROP_PAIRS_NO_OWN) || getenv("CROP_NO_OWN") ||
+                          getenv("CROP_FORCE_ENTRY_MODE") || getenv("CROP_HOST_PLANNER");
+      uint32_t kb = 0;
+      while (kb < 32 && (1ull << kb) < (uint64_t)J->iv.kappa) ++kb;
+      J->own = J->filter && !no_own && n_tx > 0 && n_items > 0 && n_items <= kStreamDenseCap + 1 &&
+               cb + kb <= 32 && J->iv.h_row && J->iv.h_col;
+      J->idbits = cb;
+    }
+    OwnArgs OA{};
+    if (J->own) {
+      int64_t nz = 0;
+      JCUDA(cudaMemcpyAsync(&nz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
+      JCUDA(cudaStreamSynchronize(st));
+      if ((uint64_t)nz >= (1ull << 32)) {
+        J->own = false;  // the 2^32 check below reports it
+      } else {
+        JCUDA(cudaMallocAsync(&J->d_hs, (size_t)std::max<int64_t>(nz, 1) * 4, st));
+        const int64_t blocks = std::min<int64_t>((n_tx + kHsWarps - 1) / kHsWarps, (int64_t)kNumSMs * 16);
+        k_hs_build<<<(int)blocks, kHsWarps * 32, 0, st>>>(offsets, items, n_tx, J->iv.h_col, J->idbits,
+                                                          J->d_hs);
+        JCUDA(cudaGetLastError());
+        crop_count_launches(1);
+        OA.hs = J->d_hs;
+        OA.h_row = J->iv.h_row;
+        OA.kappa = J->iv.kappa;
+        OA.start = J->iv.start;
+        OA.len = J->iv.stop - J->iv.start;
+        OA.idbits = J->idbits;
+      }
+    }
     if (n_tx > 0 && n_items > 0) {
-      auto kern = upper_only ? k_item_terms<true> : k_item_terms<false>;
+      auto kern = J->own ? (upper_only ? k_item_terms<true, true> : k_item_terms<false, true>)
+                         : (upper_only ? k_item_terms<true, false> : k_item_terms<false, false>);
       const uint32_t ns = std::min<uint32_t>(n_items, kStatSmemItems);
       const size_t smem = kOffBytes + ns * 8;  // two u32 arrays
       JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3238,7 +3605,8 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       const int chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, n_tx / (kNumSMs * 12)));
       const int64_t chunks = (n_tx + chunk_tx - 1) / chunk_tx;
       const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
-      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, chunk_tx, J->d_terms, J->d_maxlen);
+      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, chunk_tx, J->d_terms, J->d_maxlen,
+                                              OA);
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
     }
@@ -3284,10 +3652,14 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
       // filtered jobs whose ids and kappa fit 16 bits are planned like whole
       // jobs: the bucket test moves into the scatter (words) and the count
       // kernel (entries), on the packed items
-      J->packed_filter = J->filter && n_items <= 65536 && J->iv.kappa <= 65536 &&
+      J->packed_filter = J->filter && !J->own && n_items <= 65536 && J->iv.kappa <= 65536 &&
                          !getenv("CROP_NO_PACKED_FILTER");
       PA.filter = J->filter && !J->packed_filter;
-      PA.force = force;
+      // the own layout routes own words only: stream mode whatever the row length
+      PA.force = J->own ? 2 : force;
+      PA.own = J->own ? 1 : 0;
+      PA.safe = (J->flags & CROP_PAIRS_SAFE_UNITS) ? 1 : 0;
+      if (const char* ut = getenv("CROP_DEBUG_UNIT_TERMS")) PA.unit_terms = strtoull(ut, nullptr, 10);
       PA.tiles = reinterpret_cast<Tile*>(db + o_tiles);
       PA.tile_cap = (uint32_t)tile_cap;
       PA.units = reinterpret_cast<Unit*>(db + o_units);
@@ -3334,6 +3706,12 @@ extern "C" int crop_pairs_create_sharded(const int64_t* offsets, const uint32_t*
         // the stream words of this job (or of its largest tile shard) pass
         // the 32-bit word positions: the caller splits into finer shards
         crop_set_error(CROP_ERESOURCE, "%llu terms exceed one job's 2^32 stream words; "
+                       "split into tile shards", (unsigned long long)ho->total_terms);
+        rc = CROP_ERESOURCE;
+        goto fail;
+      }
+      if (J->own && !(ho->stream_mode && !ho->overflow)) {
+        crop_set_error(CROP_ERESOURCE, "%llu own terms exceed one job's 2^32 stream words; "
                        "split into tile shards", (unsigned long long)ho->total_terms);
         rc = CROP_ERESOURCE;
         goto fail;
@@ -3639,6 +4017,7 @@ extern "C" int crop_pairs_run(crop_pairs* J, uint32_t* out_row, uint32_t* out_co
     C.items = J->items;
     C.items16 = nullptr;
     C.items_cls = nullptr;
+    C.overflow = J->d_overflow;
     if (J->d_items16 || J->d_items_cls) {
       CROP_CUDA(cudaStreamWaitEvent(st, J->ev_items16, 0));
       C.items16 = J->d_items16;
@@ -3828,11 +4207,13 @@ extern "C" int crop_pairs_mode(const crop_pairs* J, int* stream_mode) {
   return CROP_OK;
 }
 
+extern "C" int crop_pairs_own(const crop_pairs* J, int* own) {
+  *own = J->own ? 1 : 0;
+  return CROP_OK;
+}
+
 extern "C" int crop_pairs_overflowed(const crop_pairs* J, int* overflowed) {
-  if (J->stream_mode) {  // stream ranges are exact (no capacity estimate to overflow)
-    *overflowed = 0;
-    return CROP_OK;
-  }
+  // stream mode: the count kernel raises the flag when a 16-bit counter wraps
   uint32_t h = 0;
   CROP_CUDA(cudaMemcpyAsync(&h, J->d_overflow, 4, cudaMemcpyDeviceToHost, J->stream));
   CROP_CUDA(cudaStreamSynchronize(J->stream));

@@ -190,18 +190,24 @@ class PairCountJob:
     """K2 handle: plan on create (one stream sync), run on demand."""
 
     def __init__(self, dtx: DeviceTransactions, upper_only: bool, interval: nat.Interval | None,
-                 keep: tuple = (), shard: tuple[int, int] = (0, 1)):
+                 keep: tuple = (), shard: tuple[int, int] = (0, 1), flags: int = 0):
         """shard = (rank, world): keep this rank's share of the tiles (the union
-        over ranks is the whole job; crop_pairs_create_sharded)."""
+        over ranks is the whole job; crop_pairs_create_sharded). flags:
+        CROP_PAIRS_* of crop_pairs_create_ex."""
         self._keep = (dtx, keep)  # tensors the native job points at
         self.dtx = dtx
+        self._args = (upper_only, interval, keep, shard, flags)
         lib = nat.load()
         h = ctypes.c_void_p()
         iv = ctypes.byref(interval) if interval is not None else None
-        nat.check(lib.crop_pairs_create_sharded(nat.ptr(dtx.offsets), nat.ptr(dtx.items), dtx.n_tx,
-                                                dtx.n_items, int(upper_only), iv, int(shard[0]),
-                                                int(shard[1]), nat.stream_ptr(), ctypes.byref(h)))
+        nat.check(lib.crop_pairs_create_ex(nat.ptr(dtx.offsets), nat.ptr(dtx.items), dtx.n_tx,
+                                           dtx.n_items, int(upper_only), iv, int(shard[0]),
+                                           int(shard[1]), int(flags), nat.stream_ptr(),
+                                           ctypes.byref(h)))
         self._h = h
+        own = ctypes.c_int()
+        nat.check(lib.crop_pairs_own(h, ctypes.byref(own)))
+        self.own = bool(own.value)
         me, tt, nt, nu = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         nat.check(lib.crop_pairs_info(h, ctypes.byref(me), ctypes.byref(tt), ctypes.byref(nt),
                                       ctypes.byref(nu)))
@@ -257,7 +263,18 @@ class PairCountJob:
                 del ent, row, col, cnt, fused
                 return self.run(True, min(self.max_entries, n_need))
             if self.overflowed():
-                raise InputError("pair engine overflow: entry lists exceeded their bounds")
+                upper_only, interval, keep, shard, flags = self._args
+                if self.stream_mode and not flags & nat.PAIRS_SAFE_UNITS:
+                    # a 16-bit counter wrapped (adversarial stream order):
+                    # re-plan with units of <= 65,535 words and count again
+                    del ent, row, col, cnt, fused
+                    safe = PairCountJob(self.dtx, upper_only, interval, keep, shard,
+                                        flags | nat.PAIRS_SAFE_UNITS)
+                    try:
+                        return safe.run(True, capacity)
+                    finally:
+                        safe.close()
+                raise InputError("pair engine overflow: counts exceeded their bounds")
         return ent
 
     def set_timing(self, on: bool = True) -> None:

@@ -73,6 +73,7 @@ constexpr uint32_t kUnknown = 0xFFFFFFFEu;       // route: previous tile not kno
 constexpr uint32_t kWinFlag = 0x80000000u;           // item_tile: row is split into windows
 constexpr uint32_t kEntFlag = 0x40000000u;           // stream item_info: row counted from entries
 constexpr uint32_t kTileMask = 0x3FFFFFFFu;
+constexpr uint32_t kScatMaxTx = 2048;             // transactions staged at once (scatter, own pass A)
 
 struct Tile {
   uint32_t row0, row1;  // rows [row0, row1)
@@ -208,11 +209,11 @@ struct OwnArgs {
   uint32_t kappa, start, len, idbits;
 };
 
-__device__ __forceinline__ uint32_t hs_lower(const uint32_t* __restrict__ hs, uint32_t L, uint64_t key) {
+__device__ __forceinline__ uint32_t hs_lower(const uint32_t* hs, uint32_t L, uint64_t key) {
   uint32_t lo = 0, hi = L;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if ((uint64_t)__ldg(hs + mid) < key) lo = mid + 1;
+    if ((uint64_t)hs[mid] < key) lo = mid + 1;
     else hi = mid;
   }
   return lo;
@@ -220,7 +221,7 @@ __device__ __forceinline__ uint32_t hs_lower(const uint32_t* __restrict__ hs, ui
 
 // Own window of a row with h_row = hr in one transaction's keys hs[0, L):
 // positions [a0, a0 + n1) and (a wrapped window) [0, n2).
-__device__ __forceinline__ void own_window(const uint32_t* __restrict__ hs, uint32_t L, uint32_t hr,
+__device__ __forceinline__ void own_window(const uint32_t* hs, uint32_t L, uint32_t hr,
                                            const OwnArgs& O, uint32_t& a0, uint32_t& n1, uint32_t& n2) {
   const uint32_t c_lo = O.start >= hr ? O.start - hr : O.start + O.kappa - hr;
   const uint64_t c_hi = (uint64_t)c_lo + O.len;
@@ -236,12 +237,12 @@ __device__ __forceinline__ void own_window(const uint32_t* __restrict__ hs, uint
 
 // own terms of row item i (UPPER: partners with a larger id only)
 template <bool UPPER>
-__device__ __forceinline__ uint32_t own_count(const uint32_t* __restrict__ hs, uint32_t a0, uint32_t n1,
+__device__ __forceinline__ uint32_t own_count(const uint32_t* hs, uint32_t a0, uint32_t n1,
                                               uint32_t n2, uint32_t i, uint32_t idmask) {
   if (!UPPER) return n1 + n2;
   uint32_t c = 0;
-  for (uint32_t k = 0; k < n1; ++k) c += (__ldg(hs + a0 + k) & idmask) > i;
-  for (uint32_t k = 0; k < n2; ++k) c += (__ldg(hs + k) & idmask) > i;
+  for (uint32_t k = 0; k < n1; ++k) c += (hs[a0 + k] & idmask) > i;
+  for (uint32_t k = 0; k < n2; ++k) c += (hs[k] & idmask) > i;
   return c;
 }
 
@@ -252,14 +253,17 @@ constexpr int kHsWarps = 4;
 constexpr uint32_t kHsSmem = 2048;
 __global__ void __launch_bounds__(kHsWarps * 32)
     k_hs_build(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items, int64_t n_tx,
-               const uint32_t* __restrict__ h_col, uint32_t idbits, uint32_t* __restrict__ hs) {
+               const uint32_t* __restrict__ h_col, uint32_t idbits, uint32_t* __restrict__ hs,
+               unsigned int* __restrict__ max_len) {
   __shared__ uint32_t s_k[kHsWarps][kHsSmem];
+  uint32_t my_max = 0;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* sk = s_k[w];
   auto key = [&](uint32_t it) { return (__ldg(h_col + it) << idbits) | it; };
   for (int64_t t = (int64_t)blockIdx.x * kHsWarps + w; t < n_tx; t += (int64_t)gridDim.x * kHsWarps) {
     const int64_t base = offsets[t];
     const uint32_t L = (uint32_t)(offsets[t + 1] - base);
+    my_max = max(my_max, L);
     if (L <= 32) {
       uint32_t k = (uint32_t)lane < L ? key(__ldg(items + base + lane)) : kEmpty32;
 #pragma unroll
@@ -301,18 +305,74 @@ __global__ void __launch_bounds__(kHsWarps * 32)
       }
     }
   }
+  if (lane == 0) atomicMax(max_len, my_max);
+}
+
+// Pass A of an own-bucket job: own terms per row. Chunks are the position
+// bands of k_chunk_bounds (<= kOwnStage positions); the chunk's sorted keys
+// are staged in shared memory so every row's window search (two binary
+// searches) and own-partner count run on shared memory.
+constexpr uint32_t kOwnStage = 8192;        // staged positions per band
+constexpr uint32_t kOwnStatItems = 20480;   // items with shared-memory counters
+template <bool UPPER>
+__global__ void __launch_bounds__(kPassThreads, 1)
+    k_item_terms_own(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
+                     uint32_t n_items, const uint32_t* __restrict__ bounds, uint32_t n_chunks,
+                     unsigned long long* __restrict__ stats, OwnArgs O) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);                       // kScatMaxTx + 1
+  uint32_t* s_hs = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);    // kOwnStage
+  uint32_t* s_terms = s_hs + kOwnStage;
+  const uint32_t n_smem = min(n_items, kOwnStatItems);
+  uint32_t* s_occ = s_terms + n_smem;
+  for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x) {
+    s_terms[i] = 0;
+    s_occ[i] = 0;
+  }
+  const uint32_t idmask = O.idbits >= 32 ? 0xFFFFFFFFu : ((1u << O.idbits) - 1u);
+  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint32_t tb0 = bounds[c], tb1 = bounds[c + 1];
+    for (uint32_t ta = tb0; ta < tb1; ta += kScatMaxTx) {
+      const int ntx = (int)min(kScatMaxTx, tb1 - ta);
+      __syncthreads();
+      for (int t = threadIdx.x; t <= ntx; t += blockDim.x) s_off[t] = offsets[ta + t];
+      __syncthreads();
+      const int64_t g_lo = s_off[0];
+      const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
+      for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) s_hs[x] = __ldg(O.hs + g_lo + x);
+      __syncthreads();
+      walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr,
+                        [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
+        if (!q.valid || (UPPER && q.p + 1 >= q.L)) return;
+        const uint32_t* hs = s_hs + (q.base - g_lo);
+        uint32_t a0, n1, n2;
+        own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
+        const uint32_t cnt = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
+        if (cnt == 0) return;
+        if (i < n_smem) {
+          atomicAdd(&s_terms[i], cnt);
+          atomicAdd(&s_occ[i], 1u);
+        } else {
+          atomicAdd(&stats[i], kOccOne | cnt);
+        }
+      });
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x)
+    if (s_terms[i])
+      atomicAdd(&stats[i], ((unsigned long long)s_occ[i] << kOccShift) | s_terms[i]);
 }
 
 // ------------------------------------------------------------- pass A
 // Per row item i: terms_i (pairs with i as the row) and occ_i, the number of
 // transactions in which i has at least one partner after it (an upper bound
 // of the entries it creates). Output packed as occ << kOccShift | terms.
-// OWN: own terms only (the row's own window in the (h_col, id)-sorted copy).
-template <bool UPPER, bool OWN>
+template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_item_terms(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
                  int64_t n_tx, uint32_t n_items, int chunk_tx, unsigned long long* __restrict__ stats,
-                 unsigned int* __restrict__ max_len, OwnArgs O) {
+                 unsigned int* __restrict__ max_len) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);
   uint32_t* s_terms = reinterpret_cast<uint32_t*>(smem + kOffBytes);
@@ -323,7 +383,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     s_occ[i] = 0;
   }
   uint32_t my_max = 0;
-  const uint32_t idmask = O.idbits >= 32 ? 0xFFFFFFFFu : ((1u << O.idbits) - 1u);
   const int64_t n_chunks = (n_tx + chunk_tx - 1) / chunk_tx;
   for (int64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
     __syncthreads();
@@ -331,16 +390,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr, [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
       if (!q.valid) return;
       my_max = max(my_max, q.L);
-      uint32_t c;
-      if (OWN) {
-        if (UPPER && q.p + 1 >= q.L) return;
-        const uint32_t* hs = O.hs + q.base;
-        uint32_t a0, n1, n2;
-        own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
-        c = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
-      } else {
-        c = UPPER ? q.L - 1 - q.p : q.L;
-      }
+      const uint32_t c = UPPER ? q.L - 1 - q.p : q.L;
       if (c == 0) return;
       if (i < n_smem) {
         atomicAdd(&s_terms[i], c);
@@ -1572,7 +1622,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
 // tile the parked rows are scattered: an 8-byte entry per entry-tile row,
 // the suffix words for a hash / multi-row tile row.
 constexpr uint32_t kScatPark = 10240;   // parked rows (positions) per chunk
-constexpr uint32_t kScatMaxTx = 2048;   // transactions staged at once
 
 // 16-bit copy of the items (ids < 2^16) for the suffix gathers of the count
 // kernel; runs on a side stream while the single-CTA planner runs.
@@ -1754,7 +1803,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 // not after the row are dropped and the kept ones compacted with a ballot
 // (one contiguous store run per row and step). Words only for own pairs: a
 // filtered job's write and count phases scale with its own terms.
-constexpr uint32_t kScatParkOwn = 8192;
+constexpr uint32_t kScatParkOwn = kOwnStage;
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_stream_scatter_own(StreamRouteArgs A, OwnArgs O, const uint32_t* __restrict__ bounds,
@@ -1763,8 +1812,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // kScatMaxTx + 1
   uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);     // parked rows
   uint32_t* s_rank = s_tile + kScatParkOwn;
-  uint32_t* s_tx = s_rank + kScatParkOwn;                                     // chunk-local tx
-  uint32_t* s_bp = s_tx + kScatParkOwn;                                       // row word base
+  uint32_t* s_hs = s_rank + kScatParkOwn;                                     // the band's keys
+  uint32_t* s_bp = s_hs + kScatParkOwn;                                       // row word base
   uint32_t* s_job = s_bp + kScatParkOwn;                                      // per warp 256 words
   uint32_t* s_misc = s_job + kPassThreads / 32 * 256;
   const uint32_t ns = min(A.n_tiles, A.scat_ns);
@@ -1783,13 +1832,15 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       __syncthreads();
       const int64_t g_lo = s_off[0];
       const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
+      for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) s_hs[x] = __ldg(O.hs + g_lo + x);
+      __syncthreads();
       walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                        [&](int64_t g, const Pos& q, uint32_t i, uint2 tv) {
         if (!q.valid) return;
         const uint32_t x = (uint32_t)(g - g_lo);
         uint32_t tile = kNone;
         if (tv.x != kNone && (UPPER ? q.p + 1 < q.L : q.L > 0)) {
-          const uint32_t* hs = O.hs + q.base;
+          const uint32_t* hs = s_hs + (q.base - g_lo);
           uint32_t a0, n1, n2;
           own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
           const uint32_t n = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
@@ -1804,7 +1855,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
               tile |= kWinFlag;  // rank is already absolute
             }
             s_rank[x] = r;
-            s_tx[x] = q.tx;
             s_bp[x] = tv.y;
           }
         }
@@ -1820,8 +1870,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         uint32_t* j_dst = s_job + warp * 256;
-        uint32_t* j_src = j_dst + 32;   // global key position of the first window
-        uint32_t* j_tb = j_src + 32;    // transaction start (second window)
+        uint32_t* j_src = j_dst + 32;   // staged key position of the first window
+        uint32_t* j_tb = j_src + 32;    // staged transaction start (second window)
         uint32_t* j_n1 = j_tb + 32;     // first window's length
         uint32_t* j_b = j_n1 + 32;      // row word base
         uint32_t* j_i = j_b + 32;       // row item (triangle filter)
@@ -1835,12 +1885,19 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             tile = s_tile[x];
             if (tile != kNone) {
               pos = (tile & kWinFlag) ? s_rank[x] : s_cnt[tile] + s_rank[x];
-              const uint32_t t = s_tx[x];
-              tb = s_off[t];
-              const uint32_t L = (uint32_t)(s_off[t + 1] - tb);
-              i = __ldg(A.items + g_lo + x);
+              // the row's transaction: last t with s_off[t] <= its position
+              const int64_t g = g_lo + x;
+              int lo = 0, hi = ntx;
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_off[mid] <= g) lo = mid;
+                else hi = mid;
+              }
+              tb = s_off[lo] - g_lo;
+              const uint32_t L = (uint32_t)(s_off[lo + 1] - s_off[lo]);
+              i = __ldg(A.items + g);
               uint32_t n2;
-              own_window(O.hs + tb, L, __ldg(O.h_row + i), O, a0, n1, n2);
+              own_window(s_hs + tb, L, __ldg(O.h_row + i), O, a0, n1, n2);
               nwin = n1 + n2;
             }
           }
@@ -1875,7 +1932,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             if (valid) {
               const uint32_t nn1 = j_n1[o];
               const uint32_t idx = loc < nn1 ? j_src[o] + loc : j_tb[o] + (loc - nn1);
-              j = __ldg(O.hs + idx) & idmask;
+              j = s_hs[idx] & idmask;
               keep = !UPPER || j > j_i[o];
             }
             const uint32_t km = __ballot_sync(0xffffffffu, keep);
@@ -3072,6 +3129,8 @@ struct crop_pairs {
   uint32_t flags = 0;        // CROP_PAIRS_* (crop_pairs_create_ex)
   bool own = false;          // filtered job on the own-bucket layout (Lemma 1)
   uint32_t* d_hs = nullptr;  // own: (h_col, id)-sorted keys per transaction
+  uint32_t* d_own_bounds = nullptr;  // own: first transaction of each position band
+  uint32_t own_chunks = 0;
   uint32_t idbits = 0;
   cudaEvent_t ev_items16 = nullptr;
   uint64_t out_cap = 0;      // caller's output capacity (0: max_entries)
@@ -3173,15 +3232,11 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
     CROP_LAUNCH_CHECK();
     mark(1);
     R.packed_filter = J->packed_filter ? 1 : 0;
-    if (J->own && J->words_known && J->maxlen <= kScatParkOwn / 2) {
-      // own-bucket scatter: only own partners, read from the hs windows
-      const uint32_t band = kScatParkOwn - J->maxlen + 1;
-      const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
-      uint32_t* bounds = nullptr;
-      CROP_CUDA(cudaMallocAsync(&bounds, (size_t)(n_chunks + 1) * 4, st));
-      k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
-          J->offsets, J->n_tx, n_chunks, band, bounds);
-      CROP_LAUNCH_CHECK();
+    if (J->own && J->words_known && J->d_own_bounds) {
+      // own-bucket scatter: only own partners, read from the staged windows
+      // (the position bands of pass A)
+      const uint32_t n_chunks = J->own_chunks;
+      const uint32_t* bounds = J->d_own_bounds;
       const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatParkOwn * 16 + 16 +
                            kPassThreads / 32 * 256 * 4;
       const size_t budget = 227 * 1024 - fixed;
@@ -3198,8 +3253,7 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
       kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, O, bounds, n_chunks);
       CROP_LAUNCH_CHECK();
-      cudaFreeAsync(bounds, st);
-      crop_count_launches(2);
+      crop_count_launches(1);
     } else if (J->words_known && J->maxlen <= kScatPark / 2) {
       // single-walk scatter over position bands
       const uint32_t band = kScatPark - J->maxlen + 1;
@@ -3249,7 +3303,7 @@ static void free_job(crop_pairs* j) {
     if (e) cudaEventDestroy(e);
   if (j->ev_items16) cudaEventDestroy(j->ev_items16);
   void* ptrs[] = {j->d_terms, j->d_block, j->d_entries, j->d_slabs, j->d_words, j->d_items16,
-                  j->d_items_cls, j->d_hs};
+                  j->d_items_cls, j->d_hs, j->d_own_bounds};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, j->stream);
 }
@@ -3574,29 +3628,53 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
     }
     OwnArgs OA{};
     if (J->own) {
+      // nnz sizes the key copy; the longest transaction sizes the position bands
       int64_t nz = 0;
       JCUDA(cudaMemcpyAsync(&nz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
       JCUDA(cudaStreamSynchronize(st));
-      if ((uint64_t)nz >= (1ull << 32)) {
-        J->own = false;  // the 2^32 check below reports it
-      } else {
+      if ((uint64_t)nz >= (1ull << 32)) J->own = false;  // the 2^32 check below reports it
+      if (J->own) {
         JCUDA(cudaMallocAsync(&J->d_hs, (size_t)std::max<int64_t>(nz, 1) * 4, st));
         const int64_t blocks = std::min<int64_t>((n_tx + kHsWarps - 1) / kHsWarps, (int64_t)kNumSMs * 16);
         k_hs_build<<<(int)blocks, kHsWarps * 32, 0, st>>>(offsets, items, n_tx, J->iv.h_col, J->idbits,
-                                                          J->d_hs);
+                                                          J->d_hs, J->d_maxlen);
         JCUDA(cudaGetLastError());
         crop_count_launches(1);
-        OA.hs = J->d_hs;
-        OA.h_row = J->iv.h_row;
-        OA.kappa = J->iv.kappa;
-        OA.start = J->iv.start;
-        OA.len = J->iv.stop - J->iv.start;
-        OA.idbits = J->idbits;
+        unsigned int ml = 0;
+        JCUDA(cudaMemcpyAsync(&ml, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
+        JCUDA(cudaStreamSynchronize(st));
+        if (ml > kOwnStage / 2) {
+          // too long for the staged bands: the plain filter path counts it
+          J->own = false;
+          JCUDA(cudaFreeAsync(J->d_hs, st));
+          J->d_hs = nullptr;
+        } else {
+          const uint32_t band = kOwnStage - ml + 1;
+          J->own_chunks = (uint32_t)((uint64_t)nz / band + 1);
+          JCUDA(cudaMallocAsync(&J->d_own_bounds, (size_t)(J->own_chunks + 1) * 4, st));
+          k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (n_tx + 256) / 256), 256, 0, st>>>(
+              offsets, n_tx, J->own_chunks, band, J->d_own_bounds);
+          JCUDA(cudaGetLastError());
+          OA.hs = J->d_hs;
+          OA.h_row = J->iv.h_row;
+          OA.kappa = J->iv.kappa;
+          OA.start = J->iv.start;
+          OA.len = J->iv.stop - J->iv.start;
+          OA.idbits = J->idbits;
+          auto kern = upper_only ? k_item_terms_own<true> : k_item_terms_own<false>;
+          const uint32_t ns = std::min<uint32_t>(n_items, kOwnStatItems);
+          const size_t smem = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kOwnStage * 4 + (size_t)ns * 8;
+          JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((kScatMaxTx + 1) * 8 + kOwnStage * 4 + kOwnStatItems * 8)));
+          kern<<<(int)std::min<uint32_t>(kNumSMs, J->own_chunks), kPassThreads, smem, st>>>(
+              offsets, items, n_items, J->d_own_bounds, J->own_chunks, J->d_terms, OA);
+          JCUDA(cudaGetLastError());
+          crop_count_launches(2);
+        }
       }
     }
-    if (n_tx > 0 && n_items > 0) {
-      auto kern = J->own ? (upper_only ? k_item_terms<true, true> : k_item_terms<false, true>)
-                         : (upper_only ? k_item_terms<true, false> : k_item_terms<false, false>);
+    if (n_tx > 0 && n_items > 0 && !J->own) {
+      auto kern = upper_only ? k_item_terms<true> : k_item_terms<false>;
       const uint32_t ns = std::min<uint32_t>(n_items, kStatSmemItems);
       const size_t smem = kOffBytes + ns * 8;  // two u32 arrays
       JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3605,8 +3683,7 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
       const int chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, n_tx / (kNumSMs * 12)));
       const int64_t chunks = (n_tx + chunk_tx - 1) / chunk_tx;
       const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
-      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, chunk_tx, J->d_terms, J->d_maxlen,
-                                              OA);
+      kern<<<grid, kPassThreads, smem, st>>>(offsets, items, n_tx, n_items, chunk_tx, J->d_terms, J->d_maxlen);
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
     }

@@ -13,7 +13,13 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
 want = {"gpu__time_duration.sum": "ms", "dram__bytes_read.sum": "dram_read", "dram__bytes_write.sum": "dram_write",
-        "lts__t_sector_hit_rate.pct": "l2_hit_pct", "sm__inst_executed.sum": "warp_instructions",
+        "lts__t_sector_hit_rate.pct": "l2_hit_pct", "smsp__inst_executed.sum": "warp_instructions",
+        "smsp__inst_executed_op_shared_atom.sum": "smem_atom_inst",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum": "smem_atom_wavefronts",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum": "smem_atom_bank_conflicts",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+        "lts__t_sectors_op_atom.sum": "l2_atom_sectors", "lts__t_sectors_op_red.sum": "l2_red_sectors",
+        "sm__cycles_elapsed.avg": "sm_cycles",
         "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
         "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
         "launch__registers_per_thread": "registers", "launch__grid_size": "grid", "launch__block_size": "block"}
@@ -50,6 +56,13 @@ for name, v in sorted(kernels.items(), key=lambda kv: -sum(x["ms"] for x in kv[1
                      "issue_active_pct": round(agg.get("issue_active_pct", 0), 1),
                      "occupancy_pct": round(agg.get("occupancy_pct", 0), 1),
                      "warp_instructions": int(agg.get("warp_instructions", 0)),
+                     "smem_atom_inst": int(agg.get("smem_atom_inst", 0)),
+                     "smem_atom_wavefronts": int(agg.get("smem_atom_wavefronts", 0)),
+                     "smem_atom_bank_conflicts": int(agg.get("smem_atom_bank_conflicts", 0)),
+                     "smem_bank_conflicts": int(agg.get("smem_bank_conflicts", 0)),
+                     "l2_atom_sectors": int(agg.get("l2_atom_sectors", 0)),
+                     "l2_red_sectors": int(agg.get("l2_red_sectors", 0)),
+                     "sm_cycles": int(agg.get("sm_cycles", 0)),
                      "registers": int(agg.get("registers", 0))}
     if not name.startswith("k_topk"):
         path += (agg["dram_read"] + agg["dram_write"]) * n

@@ -246,85 +246,64 @@ __device__ __forceinline__ uint32_t own_count(const uint32_t* hs, uint32_t a0, u
   return c;
 }
 
-// Build the (h_col, id)-sorted copy: one warp per transaction; a register
-// bitonic sort for <= 32 items, a shared-memory bitonic sort up to kHsSmem,
-// rank counting beyond (transactions that long are rare).
-constexpr int kHsWarps = 4;
-constexpr uint32_t kHsSmem = 2048;
-__global__ void __launch_bounds__(kHsWarps * 32)
-    k_hs_build(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items, int64_t n_tx,
-               const uint32_t* __restrict__ h_col, uint32_t idbits, uint32_t* __restrict__ hs,
-               unsigned int* __restrict__ max_len) {
-  __shared__ uint32_t s_k[kHsWarps][kHsSmem];
-  uint32_t my_max = 0;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* sk = s_k[w];
-  auto key = [&](uint32_t it) { return (__ldg(h_col + it) << idbits) | it; };
-  for (int64_t t = (int64_t)blockIdx.x * kHsWarps + w; t < n_tx; t += (int64_t)gridDim.x * kHsWarps) {
-    const int64_t base = offsets[t];
-    const uint32_t L = (uint32_t)(offsets[t + 1] - base);
-    my_max = max(my_max, L);
-    if (L <= 32) {
-      uint32_t k = (uint32_t)lane < L ? key(__ldg(items + base + lane)) : kEmpty32;
-#pragma unroll
-      for (int kk = 2; kk <= 32; kk <<= 1)
-#pragma unroll
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-          const uint32_t o = __shfl_xor_sync(0xffffffffu, k, j);
-          const bool asc = (lane & kk) == 0, lower = (lane & j) == 0;
-          k = (lower == asc) ? min(k, o) : max(k, o);
-        }
-      if ((uint32_t)lane < L) hs[base + lane] = k;
-    } else if (L <= kHsSmem) {
-      uint32_t P = 64;
-      while (P < L) P <<= 1;
-      for (uint32_t x = lane; x < P; x += 32) sk[x] = x < L ? key(__ldg(items + base + x)) : kEmpty32;
-      __syncwarp();
-      for (uint32_t kk = 2; kk <= P; kk <<= 1)
-        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
-          for (uint32_t x = lane; x < P; x += 32) {
-            const uint32_t y = x ^ j;
-            if (y > x) {
-              const uint32_t a = sk[x], b = sk[y];
-              if ((a > b) == ((x & kk) == 0)) {
-                sk[x] = b;
-                sk[y] = a;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      for (uint32_t x = lane; x < L; x += 32) hs[base + x] = sk[x];
-      __syncwarp();
-    } else {
-      for (uint32_t x = lane; x < L; x += 32) {
-        const uint32_t kx = key(__ldg(items + base + x));
-        uint32_t r = 0;
-        for (uint32_t y = 0; y < L; ++y) r += key(__ldg(items + base + y)) < kx;
-        hs[base + r] = kx;
-      }
-    }
+// Own partners of row item i in one transaction's keys hs[0, L): the count,
+// and, for a single-bucket interval (one class per row: the window is one
+// class segment whose ids ascend), the first key position -- the own
+// partners are then the contiguous range [src, src + count). General
+// intervals return src = kNone (the caller walks the window and filters).
+template <bool UPPER>
+__device__ __forceinline__ uint32_t own_partners(const uint32_t* hs, uint32_t L, uint32_t i, uint32_t hr,
+                                                 const OwnArgs& O, uint32_t idmask, uint32_t& src) {
+  if (O.len == 1) {
+    const uint32_t c = O.start >= hr ? O.start - hr : O.start + O.kappa - hr;
+    const uint64_t ck = (uint64_t)c << O.idbits;
+    const uint32_t lo = hs_lower(hs, L, UPPER ? (ck | (i + 1)) : ck);
+    const uint32_t hi = hs_lower(hs, L, ck + (1ull << O.idbits));
+    src = lo;
+    return hi - lo;
   }
-  if (lane == 0) atomicMax(max_len, my_max);
+  uint32_t a0, n1, n2;
+  own_window(hs, L, hr, O, a0, n1, n2);
+  src = kNone;
+  return own_count<UPPER>(hs, a0, n1, n2, i, idmask);
 }
 
-// Pass A of an own-bucket job: own terms per row. Chunks are the position
-// bands of k_chunk_bounds (<= kOwnStage positions); the chunk's sorted keys
-// are staged in shared memory so every row's window search (two binary
-// searches) and own-partner count run on shared memory.
+// Longest transaction (sizes the position bands of the own-bucket kernels).
+__global__ void k_max_len(const int64_t* __restrict__ offsets, int64_t n_tx, unsigned int* __restrict__ out) {
+  uint32_t m = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tx; t += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (uint32_t)(offsets[t + 1] - offsets[t]));
+#pragma unroll
+  for (int d = 16; d; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Pass A of an own-bucket job, fused with building the (h_col, id)-sorted
+// copy. Chunks are the position bands of k_chunk_bounds (<= kOwnStage
+// positions). Per band: the items are read coalesced and their keys
+// h_col << idbits | id staged in shared memory; each warp sorts its
+// transactions there (a register bitonic sort for <= 32 items, a shared
+// bitonic sort in a per-warp scratch up to kOwnSortMax, rank counting
+// beyond); the sorted band is written back (coalesced) for the scatter, and
+// every row occurrence counts its own partners with binary searches on the
+// staged keys.
 constexpr uint32_t kOwnStage = 8192;        // staged positions per band
-constexpr uint32_t kOwnStatItems = 20480;   // items with shared-memory counters
+constexpr uint32_t kOwnSortMax = 512;       // per-warp bitonic scratch
+constexpr uint32_t kOwnStatItems = 12288;   // items with shared-memory counters
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
-    k_item_terms_own(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
-                     uint32_t n_items, const uint32_t* __restrict__ bounds, uint32_t n_chunks,
-                     unsigned long long* __restrict__ stats, OwnArgs O) {
+    k_own_prep(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
+               uint32_t n_items, const uint32_t* __restrict__ h_col, const uint32_t* __restrict__ bounds,
+               uint32_t n_chunks, unsigned long long* __restrict__ stats, uint32_t* __restrict__ hs_out,
+               OwnArgs O) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);                       // kScatMaxTx + 1
   uint32_t* s_hs = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);    // kOwnStage
-  uint32_t* s_terms = s_hs + kOwnStage;
+  uint32_t* s_sort = s_hs + kOwnStage;                                     // 32 x kOwnSortMax
+  uint32_t* s_terms = s_sort + (kPassThreads / 32) * kOwnSortMax;
   const uint32_t n_smem = min(n_items, kOwnStatItems);
   uint32_t* s_occ = s_terms + n_smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t i = threadIdx.x; i < n_smem; i += blockDim.x) {
     s_terms[i] = 0;
     s_occ[i] = 0;
@@ -339,15 +318,97 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       __syncthreads();
       const int64_t g_lo = s_off[0];
       const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
-      for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) s_hs[x] = __ldg(O.hs + g_lo + x);
+      // keys, four gathers in flight per thread
+      for (uint32_t x0 = threadIdx.x; x0 < npos; x0 += 4 * blockDim.x) {
+        uint32_t it[4], hc[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t x = x0 + k * blockDim.x;
+          it[k] = x < npos ? __ldg(items + g_lo + x) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) hc[k] = __ldg(h_col + it[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t x = x0 + k * blockDim.x;
+          if (x < npos) s_hs[x] = (hc[k] << O.idbits) | it[k];
+        }
+      }
       __syncthreads();
+      // sort each transaction's keys in place
+      uint32_t* sc = s_sort + warp * kOwnSortMax;
+      for (int t = warp; t < ntx; t += kPassThreads / 32) {
+        const uint32_t b0 = (uint32_t)(s_off[t] - g_lo), L = (uint32_t)(s_off[t + 1] - s_off[t]);
+        uint32_t* seg = s_hs + b0;
+        if (L <= 32) {
+          uint32_t k = (uint32_t)lane < L ? seg[lane] : kEmpty32;
+#pragma unroll
+          for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+              const uint32_t o = __shfl_xor_sync(0xffffffffu, k, j);
+              const bool asc = (lane & kk) == 0, lower = (lane & j) == 0;
+              k = (lower == asc) ? min(k, o) : max(k, o);
+            }
+          if ((uint32_t)lane < L) seg[lane] = k;
+        } else if (L <= kOwnSortMax) {
+          uint32_t P = 64;
+          while (P < L) P <<= 1;
+          for (uint32_t x = lane; x < P; x += 32) sc[x] = x < L ? seg[x] : kEmpty32;
+          __syncwarp();
+          for (uint32_t kk = 2; kk <= P; kk <<= 1)
+            for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+              for (uint32_t x = lane; x < P; x += 32) {
+                const uint32_t y = x ^ j;
+                if (y > x) {
+                  const uint32_t a = sc[x], bb = sc[y];
+                  if ((a > bb) == ((x & kk) == 0)) {
+                    sc[x] = bb;
+                    sc[y] = a;
+                  }
+                }
+              }
+              __syncwarp();
+            }
+          for (uint32_t x = lane; x < L; x += 32) seg[x] = sc[x];
+        } else {
+          // rank counting through the scratch, kOwnSortMax keys at a time
+          for (uint32_t x0 = 0; x0 < L; x0 += kOwnSortMax) {
+            const uint32_t m = min(kOwnSortMax, L - x0);
+            uint32_t r[kOwnSortMax / 32];
+#pragma unroll
+            for (uint32_t q = 0; q < kOwnSortMax / 32; ++q) {
+              const uint32_t x = x0 + q * 32 + lane;
+              r[q] = 0;
+              if (q * 32 + lane < m) {
+                const uint32_t kx = seg[x];
+                for (uint32_t y = 0; y < L; ++y) r[q] += seg[y] < kx;
+              }
+            }
+            __syncwarp();
+            // the ranks of keys past this block still read the original keys:
+            // park the block's keys in the scratch, write them after all ranks
+            // of the transaction are known is not needed -- ranks are final,
+            // so stage the sorted block in the scratch by rank offset
+            for (uint32_t q = 0; q < kOwnSortMax / 32; ++q) {
+              const uint32_t x = x0 + q * 32 + lane;
+              if (q * 32 + lane < m) hs_out[g_lo + b0 + r[q]] = seg[x];
+            }
+          }
+          __syncwarp();
+          for (uint32_t x = lane; x < L; x += 32) seg[x] = hs_out[g_lo + b0 + x];
+          __threadfence_block();
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) hs_out[g_lo + x] = s_hs[x];
       walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr,
                         [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
         if (!q.valid || (UPPER && q.p + 1 >= q.L)) return;
-        const uint32_t* hs = s_hs + (q.base - g_lo);
-        uint32_t a0, n1, n2;
-        own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
-        const uint32_t cnt = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
+        uint32_t src;
+        const uint32_t cnt = own_partners<UPPER>(s_hs + (q.base - g_lo), q.L, i, __ldg(O.h_row + i), O,
+                                                 idmask, src);
         if (cnt == 0) return;
         if (i < n_smem) {
           atomicAdd(&s_terms[i], cnt);
@@ -1803,8 +1864,16 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 // not after the row are dropped and the kept ones compacted with a ballot
 // (one contiguous store run per row and step). Words only for own pairs: a
 // filtered job's write and count phases scale with its own terms.
+// SINGLE (single-bucket intervals): a row's own partners are one contiguous
+// range of the sorted keys (own_partners), parked at walk time and copied
+// like the plain scatter's suffixes; no filter, no compaction.
 constexpr uint32_t kScatParkOwn = kOwnStage;
-template <bool UPPER>
+template <bool SINGLE>
+__host__ __device__ constexpr size_t scatter_own_fixed() {
+  return (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatParkOwn * 4 * (SINGLE ? 5 : 4) + 16 +
+         (size_t)(kPassThreads / 32) * (SINGLE ? 128 : 256) * 4;
+}
+template <bool UPPER, bool SINGLE>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_stream_scatter_own(StreamRouteArgs A, OwnArgs O, const uint32_t* __restrict__ bounds,
                          uint32_t n_chunks) {
@@ -1814,8 +1883,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   uint32_t* s_rank = s_tile + kScatParkOwn;
   uint32_t* s_hs = s_rank + kScatParkOwn;                                     // the band's keys
   uint32_t* s_bp = s_hs + kScatParkOwn;                                       // row word base
-  uint32_t* s_job = s_bp + kScatParkOwn;                                      // per warp 256 words
-  uint32_t* s_misc = s_job + kPassThreads / 32 * 256;
+  uint32_t* s_src = s_bp + kScatParkOwn;                                      // SINGLE: first partner
+  uint32_t* s_job = s_src + (SINGLE ? kScatParkOwn : 0);                      // per warp 128 / 256 words
+  uint32_t* s_misc = s_job + kPassThreads / 32 * (SINGLE ? 128 : 256);
   const uint32_t ns = min(A.n_tiles, A.scat_ns);
   const uint32_t ns2 = (ns + 1) & ~1u;
   uint32_t* s_cnt = s_misc + 4;
@@ -1840,10 +1910,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         const uint32_t x = (uint32_t)(g - g_lo);
         uint32_t tile = kNone;
         if (tv.x != kNone && (UPPER ? q.p + 1 < q.L : q.L > 0)) {
-          const uint32_t* hs = s_hs + (q.base - g_lo);
-          uint32_t a0, n1, n2;
-          own_window(hs, q.L, __ldg(O.h_row + i), O, a0, n1, n2);
-          const uint32_t n = own_count<UPPER>(hs, a0, n1, n2, i, idmask);
+          const uint32_t b0 = (uint32_t)(q.base - g_lo);
+          uint32_t src;
+          const uint32_t n = own_partners<UPPER>(s_hs + b0, q.L, i, __ldg(O.h_row + i), O, idmask, src);
+          if (SINGLE) s_src[x] = (b0 + src) | (n << 16);  // < 2^16 each (band <= 8192)
           if (n) {
             tile = tv.x & kTileMask;
             uint32_t r;
@@ -1867,7 +1937,52 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         s_cnt[t] = (uint32_t)atomicAdd(&A.tile_cursor[t], (unsigned long long)s_cnt[t]);
       }
       __syncthreads();
-      {
+      if (SINGLE) {
+        // contiguous partner ranges, flattened across the warp (one store
+        // instruction per 32 words), as the plain scatter copies suffixes
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint32_t* j_dst = s_job + warp * 128;
+        uint32_t* j_src = j_dst + 32;
+        uint32_t* j_b = j_src + 32;
+        uint32_t* j_n = j_b + 32;
+        for (uint32_t x0 = warp * 32; x0 < npos; x0 += kPassThreads) {
+          const uint32_t x = x0 + lane;
+          uint32_t nw = 0, pos = 0, sp = 0;
+          if (x < npos) {
+            const uint32_t tile = s_tile[x];
+            if (tile != kNone) {
+              pos = (tile & kWinFlag) ? s_rank[x] : s_cnt[tile] + s_rank[x];
+              sp = s_src[x];
+              nw = sp >> 16;
+            }
+          }
+          const uint32_t wm = __ballot_sync(0xffffffffu, nw > 0);
+          if (!wm) continue;
+          if (nw) {
+            const int r = __popc(wm & ((1u << lane) - 1u));
+            j_dst[r] = pos;
+            j_src[r] = sp & 0xFFFFu;
+            j_b[r] = s_bp[x];
+            j_n[r] = nw;
+          }
+          __syncwarp();
+          const uint32_t my_n = lane < __popc(wm) ? j_n[lane] : 0u;
+          const uint32_t incl = warp_incl_scan(my_n);
+          const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+          const uint32_t excl = incl - my_n;
+          uint32_t ob = 0;
+          for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+            const uint32_t o = owner_step(incl, t0, ob) & 31;
+            const uint32_t t = t0 + lane;
+            const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o);
+            if (t < S) {
+              const uint32_t loc = t - o_excl;
+              A.words[j_dst[o] + loc] = j_b[o] + (s_hs[j_src[o] + loc] & idmask);
+            }
+          }
+          __syncwarp();
+        }
+      } else {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         uint32_t* j_dst = s_job + warp * 256;
         uint32_t* j_src = j_dst + 32;   // staged key position of the first window
@@ -3237,8 +3352,8 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
       // (the position bands of pass A)
       const uint32_t n_chunks = J->own_chunks;
       const uint32_t* bounds = J->d_own_bounds;
-      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatParkOwn * 16 + 16 +
-                           kPassThreads / 32 * 256 * 4;
+      const bool single = J->iv.stop - J->iv.start == 1;
+      const size_t fixed = single ? scatter_own_fixed<true>() : scatter_own_fixed<false>();
       const size_t budget = 227 * 1024 - fixed;
       R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
       const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
@@ -3249,7 +3364,8 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
       O.start = J->iv.start;
       O.len = J->iv.stop - J->iv.start;
       O.idbits = J->idbits;
-      auto kern = up ? k_stream_scatter_own<true> : k_stream_scatter_own<false>;
+      auto kern = single ? (up ? k_stream_scatter_own<true, true> : k_stream_scatter_own<false, true>)
+                         : (up ? k_stream_scatter_own<true, false> : k_stream_scatter_own<false, false>);
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
       kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, O, bounds, n_chunks);
       CROP_LAUNCH_CHECK();
@@ -3630,25 +3746,19 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
     if (J->own) {
       // nnz sizes the key copy; the longest transaction sizes the position bands
       int64_t nz = 0;
+      unsigned int ml = 0;
+      k_max_len<<<(int)std::min<int64_t>((n_tx + 255) / 256, kNumSMs * 8), 256, 0, st>>>(offsets, n_tx,
+                                                                                        J->d_maxlen);
+      JCUDA(cudaGetLastError());
       JCUDA(cudaMemcpyAsync(&nz, offsets + n_tx, 8, cudaMemcpyDeviceToHost, st));
+      JCUDA(cudaMemcpyAsync(&ml, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
       JCUDA(cudaStreamSynchronize(st));
       if ((uint64_t)nz >= (1ull << 32)) J->own = false;  // the 2^32 check below reports it
       if (J->own) {
-        JCUDA(cudaMallocAsync(&J->d_hs, (size_t)std::max<int64_t>(nz, 1) * 4, st));
-        const int64_t blocks = std::min<int64_t>((n_tx + kHsWarps - 1) / kHsWarps, (int64_t)kNumSMs * 16);
-        k_hs_build<<<(int)blocks, kHsWarps * 32, 0, st>>>(offsets, items, n_tx, J->iv.h_col, J->idbits,
-                                                          J->d_hs, J->d_maxlen);
-        JCUDA(cudaGetLastError());
-        crop_count_launches(1);
-        unsigned int ml = 0;
-        JCUDA(cudaMemcpyAsync(&ml, J->d_maxlen, 4, cudaMemcpyDeviceToHost, st));
-        JCUDA(cudaStreamSynchronize(st));
         if (ml > kOwnStage / 2) {
-          // too long for the staged bands: the plain filter path counts it
-          J->own = false;
-          JCUDA(cudaFreeAsync(J->d_hs, st));
-          J->d_hs = nullptr;
+          J->own = false;  // too long for the staged bands: the plain filter path counts it
         } else {
+          JCUDA(cudaMallocAsync(&J->d_hs, (size_t)std::max<int64_t>(nz, 1) * 4, st));
           const uint32_t band = kOwnStage - ml + 1;
           J->own_chunks = (uint32_t)((uint64_t)nz / band + 1);
           JCUDA(cudaMallocAsync(&J->d_own_bounds, (size_t)(J->own_chunks + 1) * 4, st));
@@ -3661,15 +3771,16 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
           OA.start = J->iv.start;
           OA.len = J->iv.stop - J->iv.start;
           OA.idbits = J->idbits;
-          auto kern = upper_only ? k_item_terms_own<true> : k_item_terms_own<false>;
+          auto kern = upper_only ? k_own_prep<true> : k_own_prep<false>;
           const uint32_t ns = std::min<uint32_t>(n_items, kOwnStatItems);
-          const size_t smem = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kOwnStage * 4 + (size_t)ns * 8;
+          const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kOwnStage * 4 +
+                               (size_t)(kPassThreads / 32) * kOwnSortMax * 4;
           JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((kScatMaxTx + 1) * 8 + kOwnStage * 4 + kOwnStatItems * 8)));
-          kern<<<(int)std::min<uint32_t>(kNumSMs, J->own_chunks), kPassThreads, smem, st>>>(
-              offsets, items, n_items, J->d_own_bounds, J->own_chunks, J->d_terms, OA);
+                                     (int)(fixed + kOwnStatItems * 8)));
+          kern<<<(int)std::min<uint32_t>(kNumSMs, J->own_chunks), kPassThreads, fixed + (size_t)ns * 8, st>>>(
+              offsets, items, n_items, J->iv.h_col, J->d_own_bounds, J->own_chunks, J->d_terms, J->d_hs, OA);
           JCUDA(cudaGetLastError());
-          crop_count_launches(2);
+          crop_count_launches(3);
         }
       }
     }

@@ -305,6 +305,320 @@ __global__ void k_max_u32(const uint32_t* __restrict__ a, const int64_t* a_end,
   }
 }
 
+// ---------------------------------------------------------------- partition path
+// The default path (no library sort): every own term goes to a PARTITION =
+// (bucket, row >> rs), sized so a partition (~1.5k terms on c4) sorts in one
+// CTA's shared memory. A term is stored as one 64-bit word
+//   row & (2^rs - 1) | col | seq   (seq = the term's index in stream order)
+// plus its fp64 value, so sorting a partition's words orders its entries by
+// (row, col) and the terms of one entry by stream order: the run sum is the
+// reference's dict accumulation, bit for bit (interval.py:236-254).
+//   k_part_count   terms per partition (shared-memory histogram)
+//   k_part_scan    partition offsets (one CTA)
+//   k_part_scatter words + values into their partitions
+//   k_part_sort    per partition: bitonic sort in shared memory, ordered run
+//                  sums, distinct entries written at the partition's offset
+//   k_part_scan    + k_part_compact: distinct entries to the output
+struct PartGeo {
+  uint32_t S_bits, rs, cb, sb;  // partitions per bucket (log2), row shift, col bits, seq bits
+  uint32_t nb;                  // buckets owned (stop - start)
+  uint32_t P;                   // partitions
+  int has_hash;
+};
+
+__device__ __forceinline__ uint32_t part_of(uint32_t i, uint32_t j, const crop_interval& iv,
+                                            const PartGeo& G) {
+  uint32_t b = 0;
+  if (G.has_hash) {
+    b = iv.h_row[i] + iv.h_col[j];
+    if (b >= iv.kappa) b -= iv.kappa;
+    b -= iv.start;
+  }
+  return (b << G.S_bits) | (i >> G.rs);
+}
+
+// Visit the own terms in stream order: fn(g, i, j, a_pos, b_pos) with g the
+// term's global index. Unfiltered full products: warps over fixed chunks of
+// terms; otherwise one warp per product with ballot-compacted indices.
+template <typename Fn>
+__device__ __forceinline__ void visit_balanced(const int64_t* __restrict__ a_ptr, const uint32_t* __restrict__ a_idx,
+                                               const int64_t* __restrict__ b_ptr, const uint32_t* __restrict__ b_idx,
+                                               int64_t n, uint64_t total, const unsigned long long* __restrict__ offs,
+                                               Fn&& fn) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t n_chunks = (total + kEmitChunk - 1) / kEmitChunk;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  auto next_off = [&](int64_t k) -> uint64_t { return k + 1 < n ? offs[k + 1] : total; };
+  for (uint64_t c = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; c < n_chunks; c += warps) {
+    const uint64_t g0 = c * kEmitChunk, g1 = min(total, g0 + kEmitChunk);
+    int64_t k = 0;
+    if (lane == 0) {
+      int64_t lo = 0, hi = n;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (offs[mid] <= g0) lo = mid;
+        else hi = mid;
+      }
+      k = lo;
+    }
+    k = __shfl_sync(0xffffffffu, k, 0);
+    int64_t kc = -1, a0 = 0, b0 = 0;
+    uint64_t base = 0, lb = 1, terms = 0;
+    for (uint64_t g = g0 + lane; g < g1; g += 32) {
+      while (next_off(k) <= g) ++k;
+      if (k != kc) {
+        kc = k;
+        base = offs[k];
+        a0 = a_ptr[k];
+        b0 = b_ptr[k];
+        lb = (uint64_t)(b_ptr[k + 1] - b0);
+        terms = (uint64_t)(a_ptr[k + 1] - a0) * lb;
+      }
+      const uint64_t t = g - base;
+      uint64_t p, q;
+      if (terms < (1ull << 32)) {
+        const uint32_t t32 = (uint32_t)t, l32 = (uint32_t)lb;
+        p = t32 / l32;
+        q = t32 - (uint32_t)p * l32;
+      } else {
+        p = t / lb;
+        q = t - p * lb;
+      }
+      fn(g, a_idx[a0 + p], b_idx[b0 + q], (uint64_t)(a0 + p), (uint64_t)(b0 + q));
+    }
+  }
+}
+
+template <bool FILTER, typename Fn>
+__device__ __forceinline__ void visit_products(const int64_t* __restrict__ a_ptr, const uint32_t* __restrict__ a_idx,
+                                               const int64_t* __restrict__ b_ptr, const uint32_t* __restrict__ b_idx,
+                                               int64_t n, int upper, const crop_interval& iv,
+                                               const unsigned long long* __restrict__ offs, Fn&& fn) {
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int64_t k = (int64_t)blockIdx.x * warps + threadIdx.x / 32; k < n; k += (int64_t)gridDim.x * warps) {
+    const int64_t a0 = a_ptr[k], la = a_ptr[k + 1] - a0;
+    const int64_t b0 = b_ptr[k], lb = b_ptr[k + 1] - b0;
+    unsigned long long pos = offs[k];
+    for (int64_t t0 = 0; t0 < la * lb; t0 += 32) {
+      const int64_t t = t0 + lane;
+      bool keep = false;
+      uint32_t i = 0, j = 0;
+      int64_t p = 0, q = 0;
+      if (t < la * lb) {
+        p = t / lb;
+        q = t - p * lb;
+        i = a_idx[a0 + p];
+        j = b_idx[b0 + q];
+        keep = own_term<FILTER>(i, j, upper, iv);
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) fn(pos + __popc(m & ((1u << lane) - 1u)), i, j, (uint64_t)(a0 + p), (uint64_t)(b0 + q));
+      pos += __popc(m);
+    }
+  }
+}
+
+constexpr uint32_t kPartSmemBins = 40960;  // shared histogram bins (160 KB)
+constexpr uint32_t kPartCap = 4096;        // terms a partition sorts in shared memory
+
+struct PartStream {
+  const int64_t *a_ptr, *b_ptr;
+  const uint32_t *a_idx, *b_idx;
+  const double *a_val, *b_val;
+  int64_t n;
+  uint64_t total;
+  int upper, balanced, filter;
+  const unsigned long long* offs;
+};
+
+template <typename Fn>
+__device__ __forceinline__ void visit_all(const PartStream& S, const crop_interval& iv, Fn&& fn) {
+  if (S.balanced) visit_balanced(S.a_ptr, S.a_idx, S.b_ptr, S.b_idx, S.n, S.total, S.offs, fn);
+  else if (S.filter) visit_products<true>(S.a_ptr, S.a_idx, S.b_ptr, S.b_idx, S.n, S.upper, iv, S.offs, fn);
+  else visit_products<false>(S.a_ptr, S.a_idx, S.b_ptr, S.b_idx, S.n, S.upper, iv, S.offs, fn);
+}
+
+__global__ void __launch_bounds__(256) k_part_count(PartStream S, crop_interval iv, PartGeo G,
+                                                    unsigned int* __restrict__ counts) {
+  extern __shared__ unsigned int s_h[];
+  const bool sm = G.P <= kPartSmemBins;
+  if (sm)
+    for (uint32_t x = threadIdx.x; x < G.P; x += blockDim.x) s_h[x] = 0;
+  __syncthreads();
+  visit_all(S, iv, [&](uint64_t, uint32_t i, uint32_t j, uint64_t, uint64_t) {
+    const uint32_t p = part_of(i, j, iv, G);
+    if (sm) atomicAdd(&s_h[p], 1u);
+    else atomicAdd(&counts[p], 1u);
+  });
+  __syncthreads();
+  if (sm)
+    for (uint32_t x = threadIdx.x; x < G.P; x += blockDim.x)
+      if (s_h[x]) atomicAdd(&counts[x], s_h[x]);
+}
+
+// exclusive scan of n u32 into u64 (one CTA of 1024 threads); out[n] = total;
+// *max_out (nullable) = the largest input
+__global__ void __launch_bounds__(1024) k_part_scan(const unsigned int* __restrict__ in, uint32_t n,
+                                                    unsigned long long* __restrict__ out,
+                                                    unsigned int* __restrict__ max_out) {
+  __shared__ unsigned long long s_w[32];
+  __shared__ unsigned long long s_carry;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  uint32_t mx = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += 1024) {
+    const uint32_t x = base + threadIdx.x;
+    const unsigned long long v = x < n ? in[x] : 0ull;
+    mx = max(mx, (uint32_t)v);
+    unsigned long long incl = warp_incl_scan(v);
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long t = s_w[lane];
+      const unsigned long long ti = warp_incl_scan(t);
+      s_w[lane] = ti - t;
+    }
+    __syncthreads();
+    const unsigned long long ex = s_carry + s_w[w] + incl - v;
+    if (x < n) out[x] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = ex + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = s_carry;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  if (lane == 0 && max_out) atomicMax(max_out, mx);
+}
+
+__global__ void __launch_bounds__(256) k_part_scatter(PartStream S, crop_interval iv, PartGeo G,
+                                                      unsigned int* __restrict__ cursor,
+                                                      const unsigned long long* __restrict__ part_off,
+                                                      unsigned long long* __restrict__ words,
+                                                      double* __restrict__ vals) {
+  const uint64_t rmask = (1ull << G.rs) - 1;
+  visit_all(S, iv, [&](uint64_t g, uint32_t i, uint32_t j, uint64_t pa, uint64_t pb) {
+    const uint32_t p = part_of(i, j, iv, G);
+    const uint64_t pos = part_off[p] + atomicAdd(&cursor[p], 1u);
+    words[pos] = (((uint64_t)i & rmask) << (G.cb + G.sb)) | ((uint64_t)j << G.sb) | g;
+    vals[pos] = (S.a_val ? S.a_val[pa] : 1.0) * (S.b_val ? S.b_val[pb] : 1.0);
+  });
+}
+
+// One CTA per partition (grid-stride): bitonic sort of (word, value) in
+// shared memory, then per run of equal (row, col): the sum in stream order.
+// Distinct entries are written at the partition's input offset (compacted
+// afterwards); dcount[p] = distinct entries. A partition larger than
+// kPartCap raises *overflow (the host falls back to the radix-sort path).
+__global__ void __launch_bounds__(512) k_part_sort(const unsigned long long* __restrict__ part_off, PartGeo G,
+                                                   uint32_t start, const unsigned long long* __restrict__ words,
+                                                   const double* __restrict__ vals,
+                                                   unsigned int* __restrict__ dcount,
+                                                   uint32_t* __restrict__ t_row, uint32_t* __restrict__ t_col,
+                                                   double* __restrict__ t_val, uint32_t* __restrict__ t_bucket,
+                                                   unsigned int* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(smem);
+  double* sv = reinterpret_cast<double*>(sw + kPartCap);
+  uint32_t* s_scan = reinterpret_cast<uint32_t*>(sv + kPartCap);  // 16 warp partials
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned long long smask = (1ull << G.sb) - 1;
+  for (uint32_t p = blockIdx.x; p < G.P; p += gridDim.x) {
+    const uint64_t o0 = part_off[p];
+    const uint32_t m = (uint32_t)(part_off[p + 1] - o0);
+    if (m == 0) {
+      if (threadIdx.x == 0) dcount[p] = 0;
+      continue;
+    }
+    if (m > kPartCap) {
+      if (threadIdx.x == 0) {
+        atomicOr(overflow, 1u);
+        dcount[p] = 0;
+      }
+      continue;
+    }
+    uint32_t P2 = 2;
+    while (P2 < m) P2 <<= 1;
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < P2; x += blockDim.x) {
+      sw[x] = x < m ? words[o0 + x] : ~0ull;
+      sv[x] = x < m ? vals[o0 + x] : 0.0;
+    }
+    __syncthreads();
+    for (uint32_t kk = 2; kk <= P2; kk <<= 1)
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        for (uint32_t x = threadIdx.x; x < P2 / 2; x += blockDim.x) {
+          // pair (a, a + j) with a's j-bit clear
+          const uint32_t a = ((x & ~(j - 1)) << 1) | (x & (j - 1));
+          const uint32_t b = a + j;
+          const unsigned long long wa = sw[a], wb = sw[b];
+          if ((wa > wb) == ((a & kk) == 0)) {
+            sw[a] = wb;
+            sw[b] = wa;
+            const double t = sv[a];
+            sv[a] = sv[b];
+            sv[b] = t;
+          }
+        }
+        __syncthreads();
+      }
+    // run heads and their distinct index (block scan over m elements)
+    uint32_t carry = 0;
+    const uint32_t bucket = start + (p >> G.S_bits);
+    const uint32_t row_hi = (p & ((1u << G.S_bits) - 1)) << G.rs;
+    for (uint32_t x0 = 0; x0 < m; x0 += blockDim.x) {
+      const uint32_t x = x0 + threadIdx.x;
+      const bool head = x < m && (x == 0 || (sw[x] >> G.sb) != (sw[x - 1] >> G.sb));
+      const uint32_t bal = __ballot_sync(0xffffffffu, head);
+      if (lane == 0) s_scan[w] = __popc(bal);
+      __syncthreads();
+      uint32_t before = carry;
+      for (int q = 0; q < w; ++q) before += s_scan[q];
+      uint32_t tot = 0;
+      for (int q = 0; q < (int)(blockDim.x / 32); ++q) tot += s_scan[q];
+      if (head) {
+        const uint32_t d = before + __popc(bal & ((1u << lane) - 1u));
+        const unsigned long long key = sw[x] >> G.sb;
+        double acc = sv[x];
+        for (uint32_t f = x + 1; f < m && (sw[f] >> G.sb) == key; ++f) acc = acc + sv[f];
+        const uint64_t o = o0 + d;
+        t_row[o] = row_hi | (uint32_t)(key >> G.cb);
+        t_col[o] = (uint32_t)(key & ((1ull << G.cb) - 1));
+        t_val[o] = acc;
+        t_bucket[o] = bucket;
+      }
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) dcount[p] = carry;
+    (void)smask;
+  }
+}
+
+// distinct entries of partition p: temp [part_off[p], + dcount[p]) -> out [dout[p], ...)
+__global__ void __launch_bounds__(256) k_part_compact(const unsigned long long* __restrict__ part_off,
+                                                      const unsigned long long* __restrict__ dout, uint32_t P,
+                                                      const uint32_t* __restrict__ t_row, const uint32_t* __restrict__ t_col,
+                                                      const double* __restrict__ t_val, const uint32_t* __restrict__ t_bucket,
+                                                      uint32_t* __restrict__ out_row, uint32_t* __restrict__ out_col,
+                                                      double* __restrict__ out_val, uint32_t* __restrict__ out_bucket,
+                                                      unsigned long long* __restrict__ n_out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t p = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; p < P; p += warps) {
+    const uint64_t s0 = part_off[p], d0 = dout[p];
+    const uint32_t c = (uint32_t)(dout[p + 1] - d0);
+    for (uint32_t x = lane; x < c; x += 32) {
+      out_row[d0 + x] = t_row[s0 + x];
+      out_col[d0 + x] = t_col[s0 + x];
+      out_val[d0 + x] = t_val[s0 + x];
+      out_bucket[d0 + x] = t_bucket[s0 + x];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = dout[P];
+}
+
 uint32_t bits_for(uint64_t v) {  // bits to hold values 0..v
   uint32_t b = 1;
   while (b < 64 && (v >> b)) ++b;
@@ -324,6 +638,9 @@ struct crop_outer {
   uint64_t total_terms;  // own-interval terms
   uint64_t all_terms;
   CompositeKey ck{};
+  PartGeo geo{};
+  bool part = false;                          // partition path (no library sort)
+  unsigned long long* d_part_off = nullptr;   // partition offsets [P + 1]
   cudaStream_t st = nullptr;  // creation stream: pool allocations are freed on it
   unsigned long long* d_counts = nullptr;
   unsigned long long* d_offs = nullptr;
@@ -418,6 +735,51 @@ extern "C" int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, co
       crop_set_error(CROP_ERESOURCE, "more than 2^32 terms in one interval; split the stream");
       return CROP_ERESOURCE;
     }
+    // partition geometry: (bucket, row >> rs) partitions of ~1.5k terms
+    if (J->total_terms > 0 && !getenv("CROP_OUTER_RADIX")) {
+      PartGeo G{};
+      G.has_hash = J->has_hash;
+      G.nb = J->has_hash ? J->iv.stop - J->iv.start : 1;
+      const uint32_t rb = bits_for(mx[0]);
+      G.cb = bits_for(mx[1]);
+      G.sb = bits_for(J->total_terms - 1);
+      const uint64_t want = (J->total_terms + (uint64_t)G.nb * 1536 - 1) / ((uint64_t)G.nb * 1536);
+      uint32_t sbits = 0;
+      while (sbits < rb && (1ull << sbits) < want) ++sbits;
+      G.S_bits = sbits;
+      G.rs = rb - sbits;
+      const uint64_t P = (uint64_t)G.nb << sbits;
+      if (G.rs + G.cb + G.sb <= 64 && P < (1ull << 26)) {
+        G.P = (uint32_t)P;
+        unsigned int* d_cnt = nullptr;
+        CROP_CUDA(cudaMallocAsync(&d_cnt, (P + 1) * 4, st));
+        CROP_CUDA(cudaMallocAsync(&J->d_part_off, (P + 1) * 8, st));
+        CROP_CUDA(cudaMemsetAsync(d_cnt, 0, (P + 1) * 4, st));
+        PartStream S{a_ptr, b_ptr, a_idx, b_idx, a_val, b_val, n_products, J->total_terms, upper_only,
+                     (!J->filter && !upper_only) ? 1 : 0, J->filter ? 1 : 0, J->d_offs};
+        const size_t sm = G.P <= kPartSmemBins ? (size_t)G.P * 4 : 0;
+        CROP_CUDA(cudaFuncSetAttribute(k_part_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kPartSmemBins * 4)));
+        const int grid = S.balanced ? kNumSMs * 2 : (int)std::min<int64_t>((n_products + 7) / 8, kNumSMs * 8);
+        k_part_count<<<grid, 256, sm, st>>>(S, J->iv, G, d_cnt);
+        CROP_LAUNCH_CHECK();
+        unsigned int* d_max = d_cnt + P;
+        k_part_scan<<<1, 1024, 0, st>>>(d_cnt, G.P, J->d_part_off, d_max);
+        CROP_LAUNCH_CHECK();
+        unsigned int hmax = 0;
+        CROP_CUDA(cudaMemcpyAsync(&hmax, d_max, 4, cudaMemcpyDeviceToHost, st));
+        CROP_CUDA(cudaStreamSynchronize(st));
+        cudaFreeAsync(d_cnt, st);
+        crop_count_launches(2);
+        if (hmax <= kPartCap) {
+          J->part = true;
+          J->geo = G;
+        } else {
+          cudaFreeAsync(J->d_part_off, st);
+          J->d_part_off = nullptr;
+        }
+      }
+    }
   }
   *job = J;
   return CROP_OK;
@@ -436,6 +798,45 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
   CROP_CUDA(cudaMemsetAsync(d_n_entries, 0, 8, st));
   const uint64_t n = J->total_terms;
   if (n == 0) return CROP_OK;
+  if (J->part) {
+    const PartGeo G = J->geo;
+    unsigned int *cursor = nullptr, *dcount = nullptr;
+    unsigned long long *words = nullptr, *dout = nullptr;
+    double *vals = nullptr, *t_val = nullptr;
+    uint32_t *t_row = nullptr, *t_col = nullptr, *t_bucket = nullptr;
+    CROP_CUDA(cudaMallocAsync(&cursor, (size_t)(G.P + 1) * 4 * 2, st));
+    dcount = cursor + G.P + 1;
+    CROP_CUDA(cudaMallocAsync(&dout, (size_t)(G.P + 1) * 8, st));
+    CROP_CUDA(cudaMallocAsync(&words, n * 8, st));
+    CROP_CUDA(cudaMallocAsync(&vals, n * 8, st));
+    CROP_CUDA(cudaMallocAsync(&t_val, n * 8, st));
+    CROP_CUDA(cudaMallocAsync(&t_row, n * 12, st));
+    t_col = t_row + n;
+    t_bucket = t_col + n;
+    CROP_CUDA(cudaMemsetAsync(cursor, 0, (size_t)(G.P + 1) * 4 * 2, st));
+    PartStream S{J->a_ptr, J->b_ptr, J->a_idx, J->b_idx, J->a_val, J->b_val, J->n, n, J->upper,
+                 (!J->filter && !J->upper) ? 1 : 0, J->filter ? 1 : 0, J->d_offs};
+    const int grid = S.balanced ? kNumSMs * 8 : (int)std::min<int64_t>((J->n + 7) / 8, 1 << 20);
+    k_part_scatter<<<grid, 256, 0, st>>>(S, J->iv, G, cursor, J->d_part_off, words, vals);
+    CROP_LAUNCH_CHECK();
+    const size_t sm = (size_t)kPartCap * 16 + 64;
+    CROP_CUDA(cudaFuncSetAttribute(k_part_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    unsigned int* d_ovf = cursor + G.P;  // spare slot (cursor has P + 1 entries)
+    k_part_sort<<<(int)std::min<uint32_t>(G.P, kNumSMs * 3), 512, sm, st>>>(
+        J->d_part_off, G, J->has_hash ? J->iv.start : 0, words, vals, dcount, t_row, t_col, t_val, t_bucket,
+        d_ovf);
+    CROP_LAUNCH_CHECK();
+    k_part_scan<<<1, 1024, 0, st>>>(dcount, G.P, dout, nullptr);
+    CROP_LAUNCH_CHECK();
+    k_part_compact<<<kNumSMs * 4, 256, 0, st>>>(J->d_part_off, dout, G.P, t_row, t_col, t_val, t_bucket,
+                                               out_row, out_col, out_value, out_bucket,
+                                               (unsigned long long*)d_n_entries);
+    CROP_LAUNCH_CHECK();
+    for (void* p : {(void*)cursor, (void*)dout, (void*)words, (void*)vals, (void*)t_val, (void*)t_row})
+      cudaFreeAsync(p, st);
+    crop_count_launches(4);
+    return CROP_OK;
+  }
   unsigned long long *keys = nullptr, *keys2 = nullptr, *keys_f = nullptr;
   uint32_t *seq = nullptr, *seq2 = nullptr, *seq_f = nullptr, *buck = nullptr, *buck2 = nullptr;
   uint32_t *iota = nullptr, *perm = nullptr, *head = nullptr, *head_pos = nullptr;
@@ -556,6 +957,7 @@ extern "C" int crop_outer_run(crop_outer* J, uint32_t* out_row, uint32_t* out_co
 
 extern "C" void crop_outer_destroy(crop_outer* J) {
   if (!J) return;
+  if (J->d_part_off) cudaFreeAsync(J->d_part_off, J->st);
   cudaFreeAsync(J->d_counts, J->st);
   cudaFreeAsync(J->d_offs, J->st);
   delete J;

@@ -206,17 +206,19 @@ __device__ __forceinline__ void walk_chunk(const int64_t* s_off, int ntx,
 struct OwnArgs {
   const uint32_t* hs;     // (h_col, id)-sorted keys per transaction (same offsets)
   const uint32_t* h_row;
-  uint32_t kappa, start, len, idbits;
+  uint32_t kappa, start, len, idbits, cbits;
+  uint32_t* pos_rec;      // per position: own partners | first partner << 16 (single bucket)
 };
 
+// lower bound of key in hs[0, L): branch-free steps (predicated adds), the
+// same trip count for every lane of a transaction
 __device__ __forceinline__ uint32_t hs_lower(const uint32_t* hs, uint32_t L, uint64_t key) {
-  uint32_t lo = 0, hi = L;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if ((uint64_t)hs[mid] < key) lo = mid + 1;
-    else hi = mid;
+  uint32_t pos = 0;
+  for (uint32_t step = L ? 1u << (31 - __clz(L)) : 0u; step; step >>= 1) {
+    const uint32_t q = pos + step;
+    if (q <= L && (uint64_t)hs[q - 1] < key) pos = q;
   }
-  return lo;
+  return pos;
 }
 
 // Own window of a row with h_row = hr in one transaction's keys hs[0, L):
@@ -289,7 +291,7 @@ __global__ void k_max_len(const int64_t* __restrict__ offsets, int64_t n_tx, uns
 // staged keys.
 constexpr uint32_t kOwnStage = 8192;        // staged positions per band
 constexpr uint32_t kOwnSortMax = 512;       // per-warp bitonic scratch
-constexpr uint32_t kOwnStatItems = 12288;   // items with shared-memory counters
+constexpr uint32_t kOwnStatItems = 8192;    // items with shared-memory counters
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1)
     k_own_prep(const int64_t* __restrict__ offsets, const uint32_t* __restrict__ items,
@@ -299,7 +301,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);                       // kScatMaxTx + 1
   uint32_t* s_hs = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);    // kOwnStage
-  uint32_t* s_sort = s_hs + kOwnStage;                                     // 32 x kOwnSortMax
+  uint32_t* s_hr = s_hs + kOwnStage;                                       // row class per position
+  uint32_t* s_sort = s_hr + kOwnStage;                                     // 32 x kOwnSortMax
   uint32_t* s_terms = s_sort + (kPassThreads / 32) * kOwnSortMax;
   const uint32_t n_smem = min(n_items, kOwnStatItems);
   uint32_t* s_occ = s_terms + n_smem;
@@ -318,20 +321,26 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       __syncthreads();
       const int64_t g_lo = s_off[0];
       const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
-      // keys, four gathers in flight per thread
+      // keys and row classes, four gathers of each in flight per thread
       for (uint32_t x0 = threadIdx.x; x0 < npos; x0 += 4 * blockDim.x) {
-        uint32_t it[4], hc[4];
+        uint32_t it[4], hc[4], hr[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t x = x0 + k * blockDim.x;
           it[k] = x < npos ? __ldg(items + g_lo + x) : 0u;
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) hc[k] = __ldg(h_col + it[k]);
+        for (int k = 0; k < 4; ++k) {
+          hc[k] = __ldg(h_col + it[k]);
+          hr[k] = __ldg(O.h_row + it[k]);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t x = x0 + k * blockDim.x;
-          if (x < npos) s_hs[x] = (hc[k] << O.idbits) | it[k];
+          if (x < npos) {
+            s_hs[x] = (hc[k] << O.idbits) | it[k];
+            s_hr[x] = hr[k];
+          }
         }
       }
       __syncthreads();
@@ -341,16 +350,25 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         const uint32_t b0 = (uint32_t)(s_off[t] - g_lo), L = (uint32_t)(s_off[t + 1] - s_off[t]);
         uint32_t* seg = s_hs + b0;
         if (L <= 32) {
-          uint32_t k = (uint32_t)lane < L ? seg[lane] : kEmpty32;
-#pragma unroll
-          for (int kk = 2; kk <= 32; kk <<= 1)
-#pragma unroll
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-              const uint32_t o = __shfl_xor_sync(0xffffffffu, k, j);
-              const bool asc = (lane & kk) == 0, lower = (lane & j) == 0;
-              k = (lower == asc) ? min(k, o) : max(k, o);
+          // stable rank by class (the items ascend with the lane): one ballot
+          // per class bit, most significant first
+          const bool v = (uint32_t)lane < L;
+          const uint32_t k = v ? seg[lane] : 0u;
+          const uint32_t cls = k >> O.idbits;
+          uint32_t eq = __ballot_sync(0xffffffffu, v), lt = 0;
+          for (int bt = (int)O.cbits - 1; bt >= 0; --bt) {
+            const bool bit = (cls >> bt) & 1u;
+            const uint32_t B = __ballot_sync(0xffffffffu, v && bit);
+            if (bit) {
+              lt += __popc(eq & ~B);
+              eq &= B;
+            } else {
+              eq &= ~B;
             }
-          if ((uint32_t)lane < L) seg[lane] = k;
+          }
+          const uint32_t r = lt + __popc(eq & ((1u << lane) - 1u));
+          __syncwarp();
+          if (v) seg[r] = k;
         } else if (L <= kOwnSortMax) {
           uint32_t P = 64;
           while (P < L) P <<= 1;
@@ -405,10 +423,15 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) hs_out[g_lo + x] = s_hs[x];
       walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr,
                         [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
-        if (!q.valid || (UPPER && q.p + 1 >= q.L)) return;
+        if (!q.valid) return;
+        if (UPPER && q.p + 1 >= q.L) {
+          O.pos_rec[g] = 0;
+          return;
+        }
         uint32_t src;
-        const uint32_t cnt = own_partners<UPPER>(s_hs + (q.base - g_lo), q.L, i, __ldg(O.h_row + i), O,
+        const uint32_t cnt = own_partners<UPPER>(s_hs + (q.base - g_lo), q.L, i, s_hr[g - g_lo], O,
                                                  idmask, src);
+        O.pos_rec[g] = cnt | (src << 16);  // src < 2^16 (kNone for general intervals: 0xFFFF)
         if (cnt == 0) return;
         if (i < n_smem) {
           atomicAdd(&s_terms[i], cnt);
@@ -1870,7 +1893,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 constexpr uint32_t kScatParkOwn = kOwnStage;
 template <bool SINGLE>
 __host__ __device__ constexpr size_t scatter_own_fixed() {
-  return (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatParkOwn * 4 * (SINGLE ? 5 : 4) + 16 +
+  return (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatParkOwn * 4 * 5 + 16 +
          (size_t)(kPassThreads / 32) * (SINGLE ? 128 : 256) * 4;
 }
 template <bool UPPER, bool SINGLE>
@@ -1881,10 +1904,12 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // kScatMaxTx + 1
   uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);     // parked rows
   uint32_t* s_rank = s_tile + kScatParkOwn;
-  uint32_t* s_hs = s_rank + kScatParkOwn;                                     // the band's keys
-  uint32_t* s_bp = s_hs + kScatParkOwn;                                       // row word base
-  uint32_t* s_src = s_bp + kScatParkOwn;                                      // SINGLE: first partner
-  uint32_t* s_job = s_src + (SINGLE ? kScatParkOwn : 0);                      // per warp 128 / 256 words
+  uint32_t* s_rec = s_rank + kScatParkOwn;                                    // pass A position records
+  uint32_t* s_bp = s_rec + kScatParkOwn;                                      // row word base
+  // SINGLE: first partner | count per parked row; general: the band's keys
+  uint32_t* s_src = s_bp + kScatParkOwn;
+  uint32_t* s_hs = s_src;
+  uint32_t* s_job = s_src + kScatParkOwn;                                     // per warp 128 / 256 words
   uint32_t* s_misc = s_job + kPassThreads / 32 * (SINGLE ? 128 : 256);
   const uint32_t ns = min(A.n_tiles, A.scat_ns);
   const uint32_t ns2 = (ns + 1) & ~1u;
@@ -1902,7 +1927,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       __syncthreads();
       const int64_t g_lo = s_off[0];
       const uint32_t npos = (uint32_t)(s_off[ntx] - g_lo);
-      for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) s_hs[x] = __ldg(O.hs + g_lo + x);
+      for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) {
+        s_rec[x] = __ldg(O.pos_rec + g_lo + x);
+        if (!SINGLE) s_hs[x] = __ldg(O.hs + g_lo + x);
+      }
       __syncthreads();
       walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                        [&](int64_t g, const Pos& q, uint32_t i, uint2 tv) {
@@ -1910,10 +1938,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         const uint32_t x = (uint32_t)(g - g_lo);
         uint32_t tile = kNone;
         if (tv.x != kNone && (UPPER ? q.p + 1 < q.L : q.L > 0)) {
-          const uint32_t b0 = (uint32_t)(q.base - g_lo);
-          uint32_t src;
-          const uint32_t n = own_partners<UPPER>(s_hs + b0, q.L, i, __ldg(O.h_row + i), O, idmask, src);
-          if (SINGLE) s_src[x] = (b0 + src) | (n << 16);  // < 2^16 each (band <= 8192)
+          // own partners counted by pass A (k_own_prep)
+          const uint32_t rec = s_rec[x];
+          const uint32_t n = rec & 0xFFFFu;
+          if (SINGLE) s_src[x] = (uint32_t)(q.base - g_lo + (rec >> 16)) | (n << 16);  // < 2^16 each
           if (n) {
             tile = tv.x & kTileMask;
             uint32_t r;
@@ -1977,7 +2005,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, o);
             if (t < S) {
               const uint32_t loc = t - o_excl;
-              A.words[j_dst[o] + loc] = j_b[o] + (s_hs[j_src[o] + loc] & idmask);
+              A.words[j_dst[o] + loc] = j_b[o] + (__ldg(O.hs + g_lo + j_src[o] + loc) & idmask);
             }
           }
           __syncwarp();
@@ -3245,6 +3273,7 @@ struct crop_pairs {
   bool own = false;          // filtered job on the own-bucket layout (Lemma 1)
   uint32_t* d_hs = nullptr;  // own: (h_col, id)-sorted keys per transaction
   uint32_t* d_own_bounds = nullptr;  // own: first transaction of each position band
+  uint32_t* d_pos_rec = nullptr;     // own: per-position partner records (inside d_hs)
   uint32_t own_chunks = 0;
   uint32_t idbits = 0;
   cudaEvent_t ev_items16 = nullptr;
@@ -3364,6 +3393,7 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
       O.start = J->iv.start;
       O.len = J->iv.stop - J->iv.start;
       O.idbits = J->idbits;
+      O.pos_rec = J->d_pos_rec;
       auto kern = single ? (up ? k_stream_scatter_own<true, true> : k_stream_scatter_own<false, true>)
                          : (up ? k_stream_scatter_own<true, false> : k_stream_scatter_own<false, false>);
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
@@ -3758,7 +3788,8 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
         if (ml > kOwnStage / 2) {
           J->own = false;  // too long for the staged bands: the plain filter path counts it
         } else {
-          JCUDA(cudaMallocAsync(&J->d_hs, (size_t)std::max<int64_t>(nz, 1) * 4, st));
+          JCUDA(cudaMallocAsync(&J->d_hs, (size_t)std::max<int64_t>(nz, 1) * 8, st));
+          J->d_pos_rec = J->d_hs + std::max<int64_t>(nz, 1);
           const uint32_t band = kOwnStage - ml + 1;
           J->own_chunks = (uint32_t)((uint64_t)nz / band + 1);
           JCUDA(cudaMallocAsync(&J->d_own_bounds, (size_t)(J->own_chunks + 1) * 4, st));
@@ -3771,9 +3802,12 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
           OA.start = J->iv.start;
           OA.len = J->iv.stop - J->iv.start;
           OA.idbits = J->idbits;
+          OA.cbits = 0;
+          while (OA.cbits < 32 && (1ull << OA.cbits) < (uint64_t)J->iv.kappa) ++OA.cbits;
+          OA.pos_rec = J->d_pos_rec;
           auto kern = upper_only ? k_own_prep<true> : k_own_prep<false>;
           const uint32_t ns = std::min<uint32_t>(n_items, kOwnStatItems);
-          const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kOwnStage * 4 +
+          const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kOwnStage * 8 +
                                (size_t)(kPassThreads / 32) * kOwnSortMax * 4;
           JCUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(fixed + kOwnStatItems * 8)));

@@ -435,6 +435,7 @@ def run_product(args, rank, world):
     b_alg = 8 * ent.total_terms + in_bytes + 20 * ent.n
     peak, peak_src = peaks()
     achieved = b_alg / (statistics.mean(times) * 1e-3) / 1e9
+    e2e = None if args.no_e2e else product_e2e(args, cfg, s, rank, world, total_terms)
     if rank == 0:
         line = {
             "metric": BASELINE_METRIC, "value": total_terms / (ms * 1e-3), "unit": "terms/s",
@@ -444,18 +445,71 @@ def run_product(args, rank, world):
             "config": config_dict(cfg, world),
             "details": {"buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})[rank]",
                         "terms": total_terms, "entries": ent.n if world == 1 else None},
-            "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_outer_emit -> "
-                         "radix sort (row,col) + (bucket) -> k_outer_reduce",
+            "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_part_count -> "
+                         "k_part_scan -> k_part_scatter -> k_part_sort -> k_part_compact",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,
                          "avg_launch_ms": round(statistics.mean(times), 4)},
             "cpu_baseline": (product_cpu_baseline(args, cfg, s) if world == 1 and not args.no_cpu
                              else None),
-            "e2e": None,
+            "e2e": e2e,
             "gpu_launches": int(launches), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+def product_e2e(args, cfg, s, rank, world, total_terms):
+    """Public API from pinned host buffers, every step: H2D of A (CSC) and B
+    (CSR), crop.partition_product for this rank's bucket interval, and the
+    D2H of every entry (row, col, value, bucket) into pinned host arrays."""
+    import numpy as np
+    import torch
+
+    import paper_1210_0461_b200 as crop
+
+    def pin(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    host = [pin(x) for x in (s.a_ptr, s.a_idx, s.a_val, s.b_ptr, s.b_idx, s.b_val)]
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=world,
+                               cs_enabled=False, seed=0)
+    out = None
+    d2h = [0]
+
+    def once():
+        nonlocal out
+        st = crop.ColumnRowStream(cfg.n, cfg.n, *host)
+        part = crop.partition_product(st, config, worker=rank if world > 1 else None)
+        n = len(part)
+        if out is None or out[0].shape[0] < n:
+            cap = int(n * 1.05) + 1024
+            out = tuple(torch.empty(cap, dtype=dt, pin_memory=True).numpy().view(nd)
+                        for dt, nd in ((torch.int32, np.uint32), (torch.int32, np.uint32),
+                                       (torch.float64, np.float64), (torch.int32, np.uint32)))
+        row, col, val, buck = part.arrays(out=out)
+        d2h[0] = 20 * int(row.shape[0])
+        torch.cuda.synchronize()
+
+    for _ in range(max(1, args.warmup // 2)):
+        once()
+    times = []
+    for _ in range(max(1, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        once()
+        times.append(time.perf_counter() - t0)
+    tm = statistics.mean(times)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([tm], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tm = float(t.item())
+    h2d = sum(int(x.nbytes) for x in host)
+    return {"value": total_terms / tm, "unit": "terms/s", "ms_per_step": tm * 1e3,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0],
+            "api": "crop.partition_product(ColumnRowStream) + ProductPartition.arrays "
+                   "(every entry to pinned host memory)"}
 
 
 def product_cpu_baseline(args, cfg, s, n_products=None):

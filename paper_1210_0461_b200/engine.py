@@ -786,6 +786,75 @@ def measure_loads(stream: OuterProductStream, config: EngineConfig,
                       assignments=[(a.start, a.stop) for a in assignments])
 
 
+# ============================================================ partitioned products
+
+class ProductPartition:
+    """Exact entries of buckets [start, stop) of a real-valued stream: the
+    columnar result of running enumerate_interval (interval.py:236-254) over
+    every outer product and accumulating each entry's terms in stream order
+    (the reference's per-worker dict, or exact_product restricted by bucket,
+    oracle.py:20-50). Entries are grouped by bucket ascending and sorted by
+    (row, col) inside; values are fp64 sums, bit-identical to the reference's
+    accumulation. Signed weights are allowed (no Space-Saving involved).
+    Results stay on the device; `arrays()` copies them to host memory."""
+
+    def __init__(self, entries, start: int, stop: int, total_terms: int):
+        self.entries = entries
+        self.start, self.stop = start, stop
+        self.total_terms = total_terms
+
+    def __len__(self) -> int:
+        return self.entries.n
+
+    def arrays(self, out=None):
+        """(row uint32, col uint32, value float64, bucket uint32) host arrays,
+        one device->host copy per column (into `out`, e.g. pinned buffers of
+        at least len(self) entries, when given)."""
+        import torch
+
+        e = self.entries
+        n = e.n
+        cols = [e.row[:n], e.col[:n], e.value[:n], e.bucket[:n]]
+        if out is None:
+            host = [torch.empty(n, dtype=c.dtype, pin_memory=True) for c in cols]
+        else:
+            host = [torch.from_numpy(o.view(np.int32) if o.dtype == np.uint32 else o)[:n] for o in out]
+        for h, c in zip(host, cols):
+            h.copy_(c, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        row, col, val, buck = (h.numpy() for h in host)
+        return row.view(np.uint32), col.view(np.uint32), val, buck.view(np.uint32)
+
+
+def partition_product(stream, config: EngineConfig, worker: int | None = None,
+                      upper_triangle_only: bool = False) -> ProductPartition:
+    """Exact per-partition accumulation of a (real-valued) stream on the GPU:
+    the entries of `worker`'s bucket interval (all kappa buckets when None)
+    under the config's first instance hash. This is the workload the
+    reference's per-partition enumerate_interval + dict loop computes; the
+    kernels (csrc/outer.cu) sort each (bucket, row-range) partition in shared
+    memory and sum every entry's terms in stream order."""
+    from . import kernels
+
+    _check_stream(stream)
+    prep = prepare(stream)
+    if prep.kind != "outer":
+        cr = ColumnRowStream.from_stream(stream)
+        prep = _Prepared("outer", kernels.DeviceOuterStream.from_host(cr), stream.n_rows,
+                         stream.n_cols, prep.n_items, cr.total_pair_count(), cr)
+    h = make_hashes(HashConfig(config.kappa, config.instance_seeds()[0]))
+    tab = kernels.hash_tables(h, prep.n_items)
+    if worker is None:
+        start, stop = 0, config.kappa
+    else:
+        if not 0 <= worker < config.workers:
+            raise ConfigError(f"worker index {worker} out of range for {config.workers}")
+        a = config.assignments()[worker]
+        start, stop = a.start, a.stop
+    ent = kernels.outer_product(prep.device, upper_triangle_only, config.kappa, start, stop, *tab)
+    return ProductPartition(ent, start, stop, ent.total_terms)
+
+
 # ============================================================ partial states
 
 def _summary_lines(capacity, total, rows, cols, weights) -> list[str]:

@@ -269,6 +269,22 @@ int crop_fimi_parse(const char* path, int threads, crop_fimi** out, int64_t* n_t
 int crop_fimi_copy(const crop_fimi* parsed, int64_t* offsets, uint32_t* items);
 void crop_fimi_free(crop_fimi* parsed);
 
+/* Read one triple file (read_triple_file, sparse.py:173-225: header
+ * "n_rows n_cols kcount", then "k index value" lines with k non-decreasing;
+ * explicit zeros dropped and counted; each k's entries sorted by index,
+ * duplicates rejected) on `threads` host threads into CSR over k. dims =
+ * {n_rows, n_cols, kcount}. Plain form only (ASCII decimal integers and
+ * decimal/exponent floats, '\n' or "\r\n"); anything else -- and every
+ * error the reference reports -- returns CROP_EINPUT with *bad_line (0 for a
+ * duplicate index), and the caller re-reads the file with the
+ * reference-exact reader (which raises ParseError). */
+typedef struct crop_triples crop_triples;
+int crop_triple_parse(const char* path, int threads, crop_triples** out, int64_t* dims,
+                      int64_t* nnz, int64_t* zeros, int64_t* bad_line);
+/* Copy into caller buffers: ptr[kcount + 1], idx[nnz], val[nnz]. */
+int crop_triple_copy(const crop_triples* parsed, int64_t* ptr, uint32_t* idx, double* val);
+void crop_triple_free(crop_triples* parsed);
+
 #ifdef __cplusplus
 }
 #endif

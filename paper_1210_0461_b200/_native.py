@@ -54,6 +54,10 @@ _SIGS = {
                               ctypes.POINTER(i64)]),
     "crop_fimi_copy": (i32, [P, P, P]),
     "crop_fimi_free": (None, [P]),
+    "crop_triple_parse": (i32, [ctypes.c_char_p, i32, ctypes.POINTER(P), P, ctypes.POINTER(i64),
+                                ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    "crop_triple_copy": (i32, [P, P, P, P]),
+    "crop_triple_free": (None, [P]),
     "crop_pairs_set_topk": (i32, [P, P, P, P, u64]),
     "crop_topk_fused": (i32, [P, P, P, P, u64, u32, P, P, P, P, P, P]),
     "crop_bucket_topk": (i32, [P, P, P, P, u64, P, P, u32, u32, P, P, P, P]),

@@ -22,7 +22,7 @@ from typing import Callable, Iterable, Iterator, NamedTuple
 
 import numpy as np
 
-from .errors import DimensionError, InputError, ParseError
+from .errors import CropError, DimensionError, InputError, ParseError
 
 logger = logging.getLogger(__name__)
 
@@ -342,7 +342,64 @@ def read_triple_file(path):
     return n_rows, n_cols, groups, zeros
 
 
+def read_triple_csr(path, threads: int = 0):
+    """read_triple_file into CSR over k: (n_rows, n_cols, ptr int64[kcount+1],
+    idx uint32, val float64, zeros dropped), parsed by the native
+    multi-threaded reader (csrc/ingest.cu). Files it does not accept -- every
+    error and every unusual spelling -- are re-read by the reference-exact
+    read_triple_file, which raises the reference's ParseError / InputError."""
+    import ctypes
+
+    from . import _native as nat
+
+    try:
+        lib = nat.load()
+    except CropError:
+        lib = None
+    if lib is not None:
+        h = ctypes.c_void_p()
+        dims = (ctypes.c_int64 * 3)()
+        nnz, zeros, bad = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        rc = lib.crop_triple_parse(os.fsencode(str(path)), int(threads), ctypes.byref(h), dims,
+                                   ctypes.byref(nnz), ctypes.byref(zeros), ctypes.byref(bad))
+        if rc == 0:
+            try:
+                ptr = _host_array(dims[2] + 1, np.int64)
+                idx = _host_array(nnz.value, np.uint32)
+                val = np.empty(nnz.value, dtype=np.float64)
+                nat.check(lib.crop_triple_copy(h, ptr.ctypes.data, idx.ctypes.data, val.ctypes.data))
+            finally:
+                lib.crop_triple_free(h)
+            if zeros.value:
+                logger.warning("%s: dropped %d explicit-zero triples", path, zeros.value)
+            return int(dims[0]), int(dims[1]), ptr, idx, val, int(zeros.value)
+    n_rows, n_cols, groups, z = read_triple_file(path)
+    ptr, idx = _csr_from_lists([[i for i, _ in g] for g in groups])
+    val = np.array([v for g in groups for _, v in g], dtype=np.float64)
+    return n_rows, n_cols, ptr, idx.astype(np.uint32), val, z
+
+
 def load_column_row_streams(path_a, path_b) -> ColumnRowStream:
+    """Load A's columns and B's rows (sparse.py:228-254) as one columnar
+    stream, both files parsed by the native reader."""
+    ar, ac, a_ptr, a_idx, a_val, za = read_triple_csr(path_a)
+    br, bc, b_ptr, b_idx, b_val, zb = read_triple_csr(path_b)
+    if a_ptr.shape[0] != b_ptr.shape[0]:
+        raise DimensionError(f"k-count mismatch: {path_a} has {a_ptr.shape[0] - 1}, "
+                             f"{path_b} has {b_ptr.shape[0] - 1}")
+    if (ar, ac) != (br, bc):
+        raise DimensionError(f"header mismatch: {path_a} says {ar}x{ac}, {path_b} says {br}x{bc}")
+    for ptr, idx, dim in ((a_ptr, a_idx, ar), (b_ptr, b_idx, bc)):
+        if idx.size and int(idx.max()) >= dim:
+            k = int(np.searchsorted(ptr, int(np.argmax(idx >= dim)), side="right")) - 1
+            last = int(idx[ptr[k]:ptr[k + 1]].max())
+            raise DimensionError(f"k={k}: index {last} out of range for dim {dim}")
+    s = ColumnRowStream(ar, bc, a_ptr, a_idx, a_val, b_ptr, b_idx, b_val)
+    s.zero_values_dropped = za + zb
+    return s
+
+
+def _load_column_row_streams_lists(path_a, path_b) -> ColumnRowStream:
     ar, ac, ga, za = read_triple_file(path_a)
     br, bc, gb, zb = read_triple_file(path_b)
     if len(ga) != len(gb):

@@ -251,6 +251,81 @@ def main():
                                     crop.gen_zipf_transactions(n_items, n_tx, skew, seed, mean)]})
     golden["zipf"] = {"streams": zs, "transactions": zt}
 
+    # triple files (sparse.py:173-254): valid files through load_column_row_streams
+    # and malformed ones with the reference's ParseError line numbers
+    import tempfile
+
+    def triple_text(vectors, n_rows, n_cols, blank_every=0, crlf=False, shuffle_within=False):
+        lines = [f"{n_rows} {n_cols} {len(vectors)}"]
+        for k, vec in enumerate(vectors):
+            pairs = list(vec)
+            if shuffle_within:
+                rng.shuffle(pairs)
+            for idx, val in pairs:
+                lines.append(f"{k} {idx} {val!r}")
+                if blank_every and rng.random() < 1.0 / blank_every:
+                    lines.append("   ")
+        nl = "\r\n" if crlf else "\n"
+        return nl.join(lines) + nl
+
+    def rand_vectors(n_vec, dim, max_nnz, zero_prob=0.0):
+        out = []
+        for _ in range(n_vec):
+            idx = sorted(rng.sample(range(dim), rng.randint(0, max_nnz)))
+            vals = [0.0 if rng.random() < zero_prob else
+                    rng.choice([1.5, -2.25, 3e-7, 1e22, -0.125, 7.0, 2.5e-300]) *
+                    (1 + rng.randint(0, 999) / 1000) for _ in idx]
+            out.append(list(zip(idx, vals)))
+        return out
+
+    triples = []
+    with tempfile.TemporaryDirectory() as td:
+        for n_vec, dim, max_nnz, kw in [(40, 60, 8, {}), (25, 30, 5, {"blank_every": 4}),
+                                        (30, 500, 12, {"crlf": True, "shuffle_within": True}),
+                                        (10, 20, 6, {"zero": 0.3})]:
+            zero = kw.pop("zero", 0.0)
+            va = rand_vectors(n_vec, dim, max_nnz, zero)
+            vb = rand_vectors(n_vec, dim, max_nnz, zero)
+            ta = triple_text(va, dim, dim, **kw)
+            tb = triple_text(vb, dim, dim, **kw)
+            pa, pb = os.path.join(td, "a.t"), os.path.join(td, "b.t")
+            with open(pa, "w", newline="") as fh:
+                fh.write(ta)
+            with open(pb, "w", newline="") as fh:
+                fh.write(tb)
+            s = crop.load_column_row_streams(pa, pb)
+            triples.append({"a": ta, "b": tb, "ok": True,
+                            "zeros": s.zero_values_dropped,
+                            "products": [[list(a.indices), list(a.values), list(b.indices),
+                                          list(b.values)] for a, b in s]})
+        bad_cases = [
+            "3 3\n",                                   # header fields
+            "3 3 2\n0 1 1.0\n1 2 x\n",                 # malformed value
+            "3 3 2\n1 1 1.0\n0 2 2.0\n",               # unsorted k
+            "3 3 2\n0 1 1.0\n2 2 2.0\n",               # k out of range
+            "3 3 2\n0 -1 1.0\n",                       # negative index
+            "3 3 2\n0 1 nan\n",                        # NaN
+            "3 3 2\n0 1 1.0 5\n",                      # four fields
+            "3 3 2\n0 1 2.0\n0 1 3.0\n",               # duplicate index (line 0)
+            "",                                        # missing header
+            "3 3 2\n0 1 1_000.5\n1 2 +2\n",            # unusual but valid spelling
+            "3 3 2\n\n0 1 inf\n1 0 -0.0\n",            # inf kept, -0.0 dropped
+        ]
+        for text in bad_cases:
+            pa = os.path.join(td, "bad.t")
+            with open(pa, "w", newline="") as fh:
+                fh.write(text)
+            try:
+                r, c, groups, zeros = crop.sparse.read_triple_file(pa)
+                triples.append({"a": text, "ok": True, "side_only": True, "header": [r, c],
+                                "groups": [[list(p) for p in g] for g in groups],
+                                "zeros": zeros})
+            except crop.ParseError as exc:
+                triples.append({"a": text, "ok": False, "side_only": True,
+                                "line_no": exc.line_no,
+                                "message": str(exc).split(": ", 1)[1]})
+    golden["triples"] = triples
+
     with open(os.path.join(HERE, "reference_golden.json"), "w") as fh:
         json.dump(golden, fh, separators=(",", ":"))
     print("wrote", os.path.join(HERE, "reference_golden.json"))

@@ -42,8 +42,17 @@ def _check(part_arrays, want):
     assert np.all(np.diff(key.astype(np.int64)) > 0)  # per-bucket sorted, distinct
 
 
+@pytest.fixture(params=["radix", "partition"])
+def outer_path(request, monkeypatch):
+    """Both sort paths of csrc/outer.cu: the radix sort (default) and the
+    shared-memory partition sort (CROP_OUTER_PARTITION=1)."""
+    if request.param == "partition":
+        monkeypatch.setenv("CROP_OUTER_PARTITION", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("workers", [1, 8])
-def test_partition_product_c4_prefix(workers, monkeypatch):
+def test_partition_product_c4_prefix(workers, outer_path, monkeypatch):
     cfg = workloads.CONFIGS["c4"]
     s = workloads.generate_product_workload(cfg, n_products=30_000)
     s = crop.ColumnRowStream(cfg.n, cfg.n, s.a_ptr, s.a_idx, s.a_val, s.b_ptr, s.b_idx, s.b_val)
@@ -55,7 +64,7 @@ def test_partition_product_c4_prefix(workers, monkeypatch):
         a = config.assignments()[0 if w is None else w]
         start, stop = (0, cfg.kappa) if w is None else (a.start, a.stop)
         _check(part.arrays(), _want(s, h, cfg.kappa, start, stop))
-    # the library radix-sort path gives the same arrays
+    # the radix-sort path gives the same arrays
     monkeypatch.setenv("CROP_OUTER_RADIX", "1")
     ref = crop.partition_product(s, config, worker=None if workers == 1 else 5).arrays()
     monkeypatch.delenv("CROP_OUTER_RADIX")
@@ -64,7 +73,7 @@ def test_partition_product_c4_prefix(workers, monkeypatch):
         assert np.array_equal(x, y)
 
 
-def test_partition_product_skewed_rows_fall_back():
+def test_partition_product_skewed_rows_fall_back(outer_path):
     """One row holding far more terms than a shared-memory partition: the
     job takes the radix-sort path and is still exact."""
     rng = np.random.default_rng(2)
@@ -92,7 +101,7 @@ def test_partition_product_skewed_rows_fall_back():
             _check(part.arrays(), _want(s, h, kappa, a_.start, a_.stop))
 
 
-def test_partition_product_upper_and_errors():
+def test_partition_product_upper_and_errors(outer_path):
     cfg = workloads.CONFIGS["c4"]
     s = workloads.generate_product_workload(cfg, n_products=5_000)
     s = crop.ColumnRowStream(cfg.n, cfg.n, s.a_ptr, s.a_idx, s.a_val, s.b_ptr, s.b_idx, s.b_val)

@@ -69,3 +69,68 @@ def test_fimi_stream_matches_transactions_to_stream(tmp_path):
     assert np.array_equal(a.items, b.items)
     with pytest.raises(crop.InputError):
         mining.fimi_stream(p, dim=3)
+
+
+# ---------------------------------------------------------------- triple files
+
+def _write(path, text):
+    with open(path, "w", newline="") as fh:
+        fh.write(text)
+
+
+def test_native_triple_reader_matches_reference(golden, tmp_path):
+    """load_column_row_streams through the native reader (csrc/ingest.cu)
+    gives the reference's stream; malformed files raise the reference's
+    ParseError (same line number and message) through the fallback."""
+    from paper_1210_0461_b200 import sparse
+
+    for n, case in enumerate(golden["triples"]):
+        pa, pb = tmp_path / f"a{n}.t", tmp_path / f"b{n}.t"
+        _write(pa, case["a"])
+        if not case.get("side_only"):
+            _write(pb, case["b"])
+            s = crop.load_column_row_streams(pa, pb)
+            got = [[list(a.indices), list(a.values), list(b.indices), list(b.values)] for a, b in s]
+            assert got == case["products"]
+            assert s.zero_values_dropped == case["zeros"]
+            continue
+        if case["ok"]:
+            r, c, ptr, idx, val, zeros = sparse.read_triple_csr(pa)
+            assert [r, c] == case["header"] and zeros == case["zeros"]
+            groups = [[[int(i), float(v)] for i, v in zip(idx[ptr[k]:ptr[k + 1]], val[ptr[k]:ptr[k + 1]])]
+                      for k in range(ptr.shape[0] - 1)]
+            assert groups == case["groups"]
+        else:
+            with pytest.raises(crop.ParseError) as exc:
+                sparse.read_triple_csr(pa)
+            assert exc.value.line_no == case["line_no"]
+            assert str(exc.value).split(": ", 1)[1] == case["message"]
+
+
+def test_native_triple_reader_large_multithreaded(tmp_path):
+    """A file big enough to be cut into many thread chunks: the CSR equals
+    the reference-exact Python reader's groups."""
+    from paper_1210_0461_b200 import sparse
+
+    rng = np.random.default_rng(4)
+    n_vec, dim = 30_000, 5_000
+    lines = [f"{dim} {dim} {n_vec}"]
+    for k in range(n_vec):
+        idx = rng.choice(dim, rng.integers(0, 9), replace=False)
+        for i in idx:  # unsorted within k, sorted by the reader
+            lines.append(f"{k} {int(i)} {float(rng.standard_normal())!r}")
+    p = tmp_path / "big.t"
+    _write(p, "\n".join(lines) + "\n")
+    r, c, ptr, idx, val, zeros = sparse.read_triple_csr(p, threads=8)
+    r2, c2, groups, z2 = sparse.read_triple_file(p)
+    assert (r, c, zeros) == (r2, c2, z2)
+    assert ptr.shape[0] == n_vec + 1
+    for k in range(0, n_vec, 997):
+        g = groups[k]
+        assert idx[ptr[k]:ptr[k + 1]].tolist() == [i for i, _ in g]
+        assert val[ptr[k]:ptr[k + 1]].tolist() == [v for _, v in g]
+    # an unsorted k far into the file is found through the fallback
+    lines.insert(len(lines) // 2, f"0 1 1.0")
+    _write(p, "\n".join(lines) + "\n")
+    with pytest.raises(crop.ParseError):
+        sparse.read_triple_csr(p, threads=8)

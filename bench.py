@@ -229,22 +229,42 @@ def run_ours(args, rank, world):
             ent.n = int(ent.n_dev.item())
             if ent.n > ent.capacity or job.overflowed():
                 raise RuntimeError("pair engine overflow")
+        src, cnt = ent, None
         if cfg.ss_capacity:
-            # bounded Space-Saving regime (c3): per-bucket top-l summaries
-            # (with N > 1, each rank's candidates for its share of every bucket)
-            kernels.bucket_topk(ent, tables[0], tables[1], cfg.kappa, cfg.ss_capacity)
-        idx = kernels.topk_indices(ent, cfg.top_k)
-        top = (ent.row[idx], ent.col[idx], ent.count[idx])
+            # bounded Space-Saving regime (c3): per-bucket top-l summaries. With
+            # N > 1 every bucket's pairs are spread over the tile shards: each
+            # rank sends its per-bucket candidates to the bucket's owner (one
+            # all-to-all) and the owner selects the bucket's top-l
+            if world > 1:
+                from paper_1210_0461_b200 import distributed
+
+                cand, mask, _, _, _ = distributed.merge_bucket_summaries_distributed(
+                    ent, tables[0], tables[1], cfg.kappa, cfg.ss_capacity)
+                src = cand
+                cnt = torch.where(mask, cand.count[: cand.n], torch.zeros_like(cand.count[: cand.n]))
+            else:
+                mask, _, _ = kernels.bucket_topk(ent, tables[0], tables[1], cfg.kappa, cfg.ss_capacity)
+                cnt = torch.where(mask, ent.count[: ent.n], torch.zeros_like(ent.count[: ent.n]))
+        idx = kernels.topk_indices(src, cfg.top_k, count=cnt)
+        top = (src.row[idx], src.col[idx], src.count[idx])
         if world > 1:
             import torch.distributed as dist
 
+            # gather every rank's local top-k; rank 0 selects the global top-k
+            # (count desc, row, col) with the same device select
             k = cfg.top_k
             buf = torch.full((3, k), -1, dtype=torch.int32, device=dev)
             m = idx.shape[0]
             buf[0, :m], buf[1, :m], buf[2, :m] = top
             allb = [torch.empty_like(buf) for _ in range(world)]
             dist.all_gather(allb, buf)
-            top = torch.cat(allb, dim=1)
+            if rank == 0:
+                g = torch.cat(allb, dim=1)
+                valid = g[2] != -1
+                ge = kernels.DeviceEntries(g[0][valid].contiguous(), g[1][valid].contiguous(),
+                                           g[2][valid].contiguous(), None, int(valid.sum().item()), 0)
+                gi = kernels.topk_indices(ge, k)
+                top = (ge.row[gi], ge.col[gi], ge.count[gi])
         if job is None:
             phases = {"path": p0.elapsed_time(p1), "plan": float("nan"), "route": float("nan"),
                       "write": float("nan"), "count": float("nan")}
@@ -445,8 +465,8 @@ def run_product(args, rank, world):
             "config": config_dict(cfg, world),
             "details": {"buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})[rank]",
                         "terms": total_terms, "entries": ent.n if world == 1 else None},
-            "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_part_count -> "
-                         "k_part_scan -> k_part_scatter -> k_part_sort -> k_part_compact",
+            "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_outer_emit_bal -> "
+                         "radix sort (bucket, row, col) -> k_outer_reduce_ck",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,

@@ -245,3 +245,76 @@ def top_entries_distributed(stream, config, k: int, upper_triangle_only: bool = 
                         input_pair_total=pair_total,
                         assignments=[(a.start, a.stop) for a in asg])
     return top, report
+
+
+def _a2a(out, inp, out_splits, in_splits):
+    """all_to_all_single on the group's device (host copies under gloo)."""
+    dist = _dist()
+    if dist.get_backend() == "nccl" or inp.device.type == "cpu":
+        dist.all_to_all_single(out, inp, out_splits, in_splits)
+        return
+    o = out.cpu()
+    dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits)
+    out.copy_(o)
+
+
+def merge_bucket_summaries_distributed(ent, h_row, h_col, kappa: int, capacity: int):
+    """Bounded-regime summaries of a job counted as tile shards across ranks
+    (bench.py's N-GPU path): every rank holds exact counts of its tiles, and
+    every bucket's pairs are spread over all ranks. Each rank keeps its own
+    top-l candidates per bucket, sends them to the bucket's owner (rank r owns
+    the buckets of split(kappa, world)[r], the reference's worker intervals,
+    interval.py:37-45) with one all-to-all, and the owner selects the bucket's
+    top-l among the union -- the same summary as one GPU counting everything
+    (kernels.merge_bucket_summaries). Loads are all-reduced.
+
+    Returns, for the caller's own buckets: (DeviceEntries of the received
+    candidates, recorded mask, bucket_min int64[kappa] (zero outside the own
+    interval), loads int64[kappa] (all buckets), distinct int64[kappa])."""
+    import torch
+
+    from . import kernels
+
+    dist = _dist()
+    me, world = dist.get_rank(), dist.get_world_size()
+    dev = h_row.device
+    n_items = int(h_row.shape[0])
+    bl, dc, _ = kernels.entry_bucket_stats(ent, [(h_row, h_col)], kappa, n_items, None)
+    loads, distinct = bl[0].clone(), dc[0].to(torch.int64)
+    _coll(dist.all_reduce, loads)
+    _coll(dist.all_reduce, distinct)
+    n = ent.n
+    row, col, cnt = ent.row[:n], ent.col[:n], ent.count[:n]
+    if n and int(dc[0].max().item()) >= capacity:
+        mask, _, _ = kernels.bucket_topk(ent, h_row, h_col, kappa, capacity)
+        row, col, cnt = row[mask], col[mask], cnt[mask]
+    b = kernels.entry_buckets(row, col, int(row.shape[0]), h_row, h_col, kappa).to(torch.int64)
+    # the owner of bucket b is the rank whose split(kappa, world) interval holds it
+    starts = torch.tensor([rank_workers(kappa, r, world)[0] for r in range(world)],
+                          dtype=torch.int64, device=dev)
+    owner = torch.bucketize(b, starts, right=True) - 1
+    order = torch.argsort(owner, stable=True)
+    row, col, cnt, owner = row[order], col[order], cnt[order], owner[order]
+    send = torch.bincount(owner, minlength=world).to(torch.int64)
+    recv = torch.empty_like(send)
+    _a2a(recv, send, None, None)
+    s_l, r_l = send.cpu().tolist(), recv.cpu().tolist()
+    total = int(sum(r_l))
+    packed = torch.stack([row, col, cnt])  # int32 [3, m]
+    out = torch.empty((3, max(total, 1)), dtype=torch.int32, device=dev)
+    for k in range(3):
+        buf = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        _a2a(buf[:total], packed[k].contiguous(), r_l, s_l)
+        out[k] = buf
+    cand = kernels.DeviceEntries(out[0, :total].contiguous(), out[1, :total].contiguous(),
+                                 out[2, :total].contiguous(), None, total, ent.total_terms)
+    if total:
+        mask, bmin, _ = kernels.bucket_topk(cand, h_row, h_col, kappa, capacity)
+    else:
+        mask = torch.zeros(0, dtype=torch.bool, device=dev)
+        bmin = torch.zeros(kappa, dtype=torch.int64, device=dev)
+    lo, hi = rank_workers(kappa, me, world)
+    own = torch.zeros(kappa, dtype=torch.bool, device=dev)
+    own[lo:hi] = True
+    bmin = torch.where(own & (distinct >= capacity), bmin, torch.zeros_like(bmin))
+    return cand, mask, bmin, loads, distinct

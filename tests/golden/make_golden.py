@@ -326,6 +326,39 @@ def main():
                                 "message": str(exc).split(": ", 1)[1]})
     golden["triples"] = triples
 
+    # the reference CLI (cli.py): mine and generate outputs on small inputs
+    from crop_ref import cli as ref_cli
+
+    cli_cases = {}
+    with tempfile.TemporaryDirectory() as td:
+        gen_dir = os.path.join(td, "gen")
+        assert ref_cli.main(["generate", "transactions", "--items", "120", "--count", "300",
+                             "--skew", "1.1", "--mean-size", "9", "--seed", "4",
+                             "--out", gen_dir]) == 0
+        with open(os.path.join(gen_dir, "transactions.fimi")) as fh:
+            fimi = fh.read()
+        with open(os.path.join(gen_dir, "pair_supports.csv")) as fh:
+            supports_csv = fh.read()
+        cli_cases["generate_transactions"] = {
+            "args": ["--items", "120", "--count", "300", "--skew", "1.1", "--mean-size", "9",
+                     "--seed", "4"], "fimi": fimi, "pair_supports": supports_csv}
+        mine_dir = os.path.join(td, "mine")
+        margs = ["--kappa", "8", "--workers", "4", "--ss-capacity", "1000000", "--seed", "3",
+                 "--top", "30", "--exact-oracle"]
+        assert ref_cli.main(["mine", "--fimi", os.path.join(gen_dir, "transactions.fimi"),
+                             "--out", mine_dir] + margs) == 0
+        outs = {}
+        for name in ("topk.csv", "load_report.json", "bound_ratios.csv", "state.json"):
+            with open(os.path.join(mine_dir, name)) as fh:
+                outs[name] = fh.read()
+        cli_cases["mine"] = {"args": margs, "outputs": outs}
+        rc_bad = ref_cli.main(["mine", "--fimi", os.path.join(td, "missing.fimi"), "--kappa", "4",
+                               "--out", os.path.join(td, "x")])
+        rc_cfg = ref_cli.main(["mine", "--fimi", os.path.join(gen_dir, "transactions.fimi"),
+                               "--kappa", "4", "--workers", "9", "--out", os.path.join(td, "y")])
+        cli_cases["exit_codes"] = {"missing_input": rc_bad, "bad_workers": rc_cfg}
+    golden["cli"] = cli_cases
+
     with open(os.path.join(HERE, "reference_golden.json"), "w") as fh:
         json.dump(golden, fh, separators=(",", ":"))
     print("wrote", os.path.join(HERE, "reference_golden.json"))

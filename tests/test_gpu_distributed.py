@@ -103,3 +103,65 @@ def test_distributed_gpu_matches_single_process(golden, workers, kappa, instance
     if instances == 1:
         assert got["top"] == _top(state.top_entries(40))
         assert got["rows2"] == report.rows
+
+
+def _merge_worker(rank, world, port, n_tx, cap, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1210_0461_b200 import kernels, workloads
+
+        cfg = workloads.CONFIGS["c3"]
+        dtx = workloads.generate_pairs_workload(cfg, n_tx=n_tx)
+        h = crop.make_hashes(crop.HashConfig(cfg.kappa, crop.derive_seed(0, "instance:0")))
+        tab = kernels.hash_tables(h, cfg.n_items)
+        ent = kernels.count_pairs_shard(dtx, True, None, keep=tab, shard=(rank, world))
+        cand, mask, bmin, loads, distinct = distributed.merge_bucket_summaries_distributed(
+            ent, tab[0], tab[1], cfg.kappa, cap)
+        rec = torch.stack([cand.row[mask], cand.col[mask]]).cpu().numpy().view("uint32")
+        q.put((rank, rec.astype("int64").tolist(), bmin.cpu().tolist(), loads.cpu().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tile_shard_summaries_merge_across_ranks():
+    """Bounded-regime summaries of 3 tile-shard ranks merged with the
+    bucket-owner all-to-all equal the single-GPU summaries (c3 prefix)."""
+    import numpy as np
+
+    from paper_1210_0461_b200 import kernels, workloads
+
+    n_tx, cap, world = 20_000, 256, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_merge_worker, args=(r, world, port, n_tx, cap, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (rec, bmin, loads)) for r, rec, bmin, loads in
+               (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = workloads.CONFIGS["c3"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=n_tx)
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=cap, workers=world, seed=0,
+                               cs_enabled=False)
+    state, _ = crop.run(dtx, config, upper_triangle_only=True)
+    d = state.device_result
+    e, inst = d.entries, d.instances[0]
+    m = inst.recorded
+    whole = np.stack([kernels.u32_to_numpy(e.row[: e.n][m]), kernels.u32_to_numpy(e.col[: e.n][m])])
+    whole_keys = set(map(tuple, whole.T.astype(np.int64).tolist()))
+    got_keys = set()
+    bmin = np.zeros(cfg.kappa, np.int64)
+    for r in range(world):
+        rec, bm, loads = res[r]
+        got_keys |= set(zip(rec[0], rec[1]))
+        bmin += np.array(bm)
+        assert loads == inst.loads.astype(np.int64).tolist()
+    assert got_keys == whole_keys
+    assert bmin.tolist() == inst.bucket_min.astype(np.int64).tolist()

@@ -249,3 +249,19 @@ def test_zipf_generators_match_reference(golden):
         crop.gen_zipf_stream(crop.ZipfModel(1.0, 1.0, 50), 5, None, 0)
     with pytest.raises(crop.ConfigError):
         crop.gen_zipf_transactions(10, 5, 0.0, 0)
+
+
+def test_cli_exit_codes_match_reference(golden, tmp_path):
+    """cli.py:391-404 exit codes: a missing input is 2, a bad config is 3
+    (both raised before any device work)."""
+    from paper_1210_0461_b200 import cli
+
+    codes = golden["cli"]["exit_codes"]
+    fimi = tmp_path / "t.fimi"
+    fimi.write_text(golden["cli"]["generate_transactions"]["fimi"])
+    assert cli.main(["mine", "--fimi", str(tmp_path / "missing.fimi"), "--kappa", "4",
+                     "--out", str(tmp_path / "x")]) == codes["missing_input"]
+    assert cli.main(["mine", "--fimi", str(fimi), "--kappa", "4", "--workers", "9",
+                     "--out", str(tmp_path / "y")]) == codes["bad_workers"]
+    assert cli.main(["bench", "--kappa", "4", "--out", str(tmp_path / "z")]) == 2  # no input
+    assert not (tmp_path / "x").exists() and not (tmp_path / "y").exists()

@@ -1706,6 +1706,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
 // tile the parked rows are scattered: an 8-byte entry per entry-tile row,
 // the suffix words for a hash / multi-row tile row.
 constexpr uint32_t kScatPark = 10240;   // parked rows (positions) per chunk
+constexpr uint32_t kScatPark2 = 5120;   // two CTAs per SM: half the band
+constexpr uint32_t kScatMaxTx2 = 1024;
 
 // 16-bit copy of the items (ids < 2^16) for the suffix gathers of the count
 // kernel; runs on a side stream while the single-CTA planner runs.
@@ -1745,17 +1747,21 @@ __global__ void k_chunk_bounds(const int64_t* __restrict__ offsets, int64_t n_tx
   }
 }
 
-template <bool UPPER, bool PF>
-__global__ void __launch_bounds__(kPassThreads, 1)
+// THREADS / PARK / MAXTX: one 1024-thread CTA per SM with 10,240-position
+// bands, or two 512-thread CTAs per SM with half the bands (one CTA's
+// returning tile claims and barriers overlap the other's walk and copy).
+template <bool UPPER, bool PF, int THREADS = kPassThreads, uint32_t PARK = kScatPark,
+          uint32_t MAXTX = kScatMaxTx>
+__global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 2)
     k_stream_scatter(StreamRouteArgs A, const uint32_t* __restrict__ bounds, uint32_t n_chunks) {
   extern __shared__ __align__(16) unsigned char smem[];
-  int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // kScatMaxTx + 1
-  uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + kScatMaxTx + 1);     // parked rows
-  uint32_t* s_rank = s_tile + kScatPark;
-  uint32_t* s_meta = s_rank + kScatPark;                                      // n | entry << 31
-  uint32_t* s_bp = s_meta + kScatPark;                                        // word rows: base
-  uint32_t* s_job = s_bp + kScatPark;                                         // per warp 128 words
-  uint32_t* s_misc = s_job + kPassThreads / 32 * 128;
+  int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // MAXTX + 1
+  uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + MAXTX + 1);     // parked rows
+  uint32_t* s_rank = s_tile + PARK;
+  uint32_t* s_meta = s_rank + PARK;                                      // n | entry << 31
+  uint32_t* s_bp = s_meta + PARK;                                        // word rows: base
+  uint32_t* s_job = s_bp + PARK;                                         // per warp 128 words
+  uint32_t* s_misc = s_job + THREADS / 32 * 128;
   const uint32_t ns = min(A.n_tiles, A.scat_ns);
   const uint32_t ns2 = (ns + 1) & ~1u;
   uint32_t* s_cnt = s_misc + 4;
@@ -1763,8 +1769,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
   for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) s_cnt[t] = 0;
   for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     const uint32_t tb0 = bounds[c], tb1 = bounds[c + 1];
-    for (uint32_t ta = tb0; ta < tb1; ta += kScatMaxTx) {
-      const int ntx = (int)min(kScatMaxTx, tb1 - ta);
+    for (uint32_t ta = tb0; ta < tb1; ta += MAXTX) {
+      const int ntx = (int)min(MAXTX, tb1 - ta);
       __syncthreads();
       if (threadIdx.x == 0) s_misc[0] = 0;
       for (int t = threadIdx.x; t <= ntx; t += blockDim.x) s_off[t] = A.offsets[ta + t];
@@ -1812,7 +1818,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         uint32_t* j_src = j_dst + 32;
         uint32_t* j_b = j_src + 32;
         uint32_t* j_n = j_b + 32;
-        for (uint32_t x0 = warp * 32; x0 < npos; x0 += kPassThreads) {
+        for (uint32_t x0 = warp * 32; x0 < npos; x0 += THREADS) {
           const uint32_t x = x0 + lane;
           uint32_t tile = kNone, pos = 0, meta = 0;
           if (x < npos) {
@@ -3402,21 +3408,36 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
       crop_count_launches(1);
     } else if (J->words_known && J->maxlen <= kScatPark / 2) {
       // single-walk scatter over position bands
-      const uint32_t band = kScatPark - J->maxlen + 1;
+      const bool two = J->maxlen <= kScatPark2 / 2 && !getenv("CROP_SCATTER_ONE_CTA");
+      const uint32_t band = (two ? kScatPark2 : kScatPark) - J->maxlen + 1;
       const uint32_t n_chunks = (uint32_t)((uint64_t)J->nnz / band + 1);
       uint32_t* bounds = nullptr;
       CROP_CUDA(cudaMallocAsync(&bounds, (size_t)(n_chunks + 1) * 4, st));
       k_chunk_bounds<<<(int)std::min<int64_t>(kNumSMs * 8, (J->n_tx + 256) / 256), 256, 0, st>>>(
           J->offsets, J->n_tx, n_chunks, band, bounds);
       CROP_LAUNCH_CHECK();
-      const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 16 + 16 + kPassThreads / 32 * 128 * 4;
-      const size_t budget = 227 * 1024 - fixed;
-      R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
-      const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
-      auto kern = J->packed_filter ? (up ? k_stream_scatter<true, true> : k_stream_scatter<false, true>)
-                                   : (up ? k_stream_scatter<true, false> : k_stream_scatter<false, false>);
-      CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
-      kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, bounds, n_chunks);
+      if (two) {
+        const size_t fixed = (size_t)(kScatMaxTx2 + 1) * 8 + (size_t)kScatPark2 * 16 + 16 + 512 / 32 * 128 * 4;
+        const size_t budget = 112 * 1024 - fixed;
+        R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
+        const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
+        auto kern = J->packed_filter
+                        ? (up ? k_stream_scatter<true, true, 512, kScatPark2, kScatMaxTx2>
+                              : k_stream_scatter<false, true, 512, kScatPark2, kScatMaxTx2>)
+                        : (up ? k_stream_scatter<true, false, 512, kScatPark2, kScatMaxTx2>
+                              : k_stream_scatter<false, false, 512, kScatPark2, kScatMaxTx2>);
+        CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(112 * 1024)));
+        kern<<<(int)std::min<uint32_t>(2 * kNumSMs, n_chunks), 512, smem, st>>>(R, bounds, n_chunks);
+      } else {
+        const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 16 + 16 + kPassThreads / 32 * 128 * 4;
+        const size_t budget = 227 * 1024 - fixed;
+        R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
+        const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
+        auto kern = J->packed_filter ? (up ? k_stream_scatter<true, true> : k_stream_scatter<false, true>)
+                                     : (up ? k_stream_scatter<true, false> : k_stream_scatter<false, false>);
+        CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024)));
+        kern<<<(int)std::min<uint32_t>(kNumSMs, n_chunks), kPassThreads, smem, st>>>(R, bounds, n_chunks);
+      }
       CROP_LAUNCH_CHECK();
       cudaFreeAsync(bounds, st);
       crop_count_launches(1);

@@ -45,9 +45,9 @@ def test_bench_reports_gpu_rows(golden, tmp_path):
     fimi = tmp_path / "t.fimi"
     fimi.write_text(golden["cli"]["generate_transactions"]["fimi"])
     out = tmp_path / "bench"
-    assert cli.main(["bench", "--fimi", str(fimi), "--kappa", "8", "--workers-list", "1,64",
+    assert cli.main(["bench", "--fimi", str(fimi), "--kappa", "8", "--workers-list", "1,4096",
                      "--out", str(out)]) == 0
     rows = json.loads((out / "manifest.json").read_text())["rows"]
     assert rows[0]["gpus"] == 1 and rows[0]["terms_per_second"] > 0
     assert 0 < rows[0]["hbm_roofline_fraction"] < 1
-    assert rows[1]["gpus"] == 64 and "unavailable" in rows[1]
+    assert rows[1]["gpus"] == 4096 and "unavailable" in rows[1]

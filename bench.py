@@ -465,8 +465,10 @@ def run_product(args, rank, world):
             "config": config_dict(cfg, world),
             "details": {"buckets_per_gpu": f"split(kappa={cfg.kappa}, {world})[rank]",
                         "terms": total_terms, "entries": ent.n if world == 1 else None},
-            "roofline": {"bound": "hbm", "kernel": "k_outer_count -> scan -> k_outer_emit_bal -> "
-                         "radix sort (bucket, row, col) -> k_outer_reduce_ck",
+            "roofline": {"bound": "hbm", "kernel": "scan (all-term offsets) -> k_nnz_hash -> k_bm_hist -> "
+                         "k_bm_colscan -> scan (partition offsets) -> k_bm_scatter -> k_bm_sort "
+                         "(bucket-major partitions sorted in shared memory, ordered fp64 run "
+                         "sums, look-back output offsets)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,

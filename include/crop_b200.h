@@ -232,13 +232,32 @@ int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
  * the per-partition sorted COO: row/col uint32, value float64, bucket
  * uint32, grouped by bucket ascending, (row, col) ascending inside. Zero sums
  * are kept (the caller decides, exact_product drops them, oracle.py:50).
- * crop_outer_create synchronises once to size the term buffer. */
+ * crop_outer_create synchronises to learn the stream's shape and the own
+ * term count; crop_outer_create_ex with a shape does not synchronise. */
 typedef struct crop_outer crop_outer;
 int crop_outer_create(const int64_t* a_ptr, const uint32_t* a_idx, const double* a_val,
                       const int64_t* b_ptr, const uint32_t* b_idx, const double* b_val,
                       int64_t n_products, int upper_only, const crop_interval* interval,
                       void* stream, crop_outer** job);
+/* Shape of an outer-product stream, known to the caller once per stream
+ * (e.g. computed at upload): with it crop_outer_create_ex plans without
+ * synchronising the stream; crop_outer_info then reports max_entries as the
+ * upper bound all_terms (the own-interval count is only known on the
+ * device, as *d_n_entries after the run). */
+typedef struct {
+    uint64_t all_terms;       /* sum over products of |a_k| * |b_k| */
+    uint32_t max_row;         /* largest a_idx (0 if none) */
+    uint32_t max_col;         /* largest b_idx (0 if none) */
+    int64_t nnz_a, nnz_b;     /* a_ptr[n], b_ptr[n] */
+} crop_outer_shape;
+int crop_outer_create_ex(const int64_t* a_ptr, const uint32_t* a_idx, const double* a_val,
+                         const int64_t* b_ptr, const uint32_t* b_idx, const double* b_val,
+                         int64_t n_products, int upper_only, const crop_interval* interval,
+                         const crop_outer_shape* shape, void* stream, crop_outer** job);
 int crop_outer_info(const crop_outer* job, uint64_t* max_entries, uint64_t* total_terms);
+/* Own-interval term count into device memory (stream-ordered; exact also
+ * when crop_outer_create_ex planned without synchronising). */
+int crop_outer_own_terms(const crop_outer* job, uint64_t* d_out, void* stream);
 int crop_outer_run(crop_outer* job, uint32_t* out_row, uint32_t* out_col, double* out_value,
                    uint32_t* out_bucket, uint64_t* d_n_entries, void* stream);
 void crop_outer_destroy(crop_outer* job);

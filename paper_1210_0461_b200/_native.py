@@ -25,6 +25,12 @@ class Interval(ctypes.Structure):
     _fields_ = [("kappa", u32), ("start", u32), ("stop", u32), ("h_row", P), ("h_col", P)]
 
 
+class OuterShape(ctypes.Structure):
+    """crop_outer_shape: what crop_outer_create_ex needs to plan without a sync."""
+
+    _fields_ = [("all_terms", u64), ("max_row", u32), ("max_col", u32), ("nnz_a", i64), ("nnz_b", i64)]
+
+
 _SIGS = {
     "crop_abi_version": (i32, []),
     "crop_last_error": (ctypes.c_char_p, []),
@@ -69,7 +75,10 @@ _SIGS = {
     "crop_topk": (i32, [P, P, P, P, u64, u32, P, P, P]),
     "crop_outer_create": (i32, [P, P, P, P, P, P, i64, i32, ctypes.POINTER(Interval), P,
                                 ctypes.POINTER(P)]),
+    "crop_outer_create_ex": (i32, [P, P, P, P, P, P, i64, i32, ctypes.POINTER(Interval),
+                                   ctypes.POINTER(OuterShape), P, ctypes.POINTER(P)]),
     "crop_outer_info": (i32, [P, ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+    "crop_outer_own_terms": (i32, [P, P, P]),
     "crop_outer_run": (i32, [P, P, P, P, P, P, P]),
     "crop_outer_destroy": (None, [P]),
     "crop_gen_lengths": (i32, [i64, u64, P, u32, u32, P, P]),

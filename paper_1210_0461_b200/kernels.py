@@ -84,6 +84,26 @@ class DeviceOuterStream:
     def n_products(self) -> int:
         return self.a_ptr.shape[0] - 1
 
+    def shape(self) -> "nat.OuterShape":
+        """All terms, largest row / column index and nonzero counts, reduced on
+        the device once per stream (one read-back) and cached: every job over
+        this stream then plans without synchronising."""
+        cached = getattr(self, "_shape", None)
+        if cached is None:
+            n = self.n_products
+            if n > 0 and self.a_idx.numel() and self.b_idx.numel():
+                la = self.a_ptr[1:] - self.a_ptr[:-1]
+                lb = self.b_ptr[1:] - self.b_ptr[:-1]
+                mask = 0xFFFFFFFF
+                vals = torch.stack([(la * lb).sum(), self.a_idx.to(torch.int64).bitwise_and(mask).max(),
+                                    self.b_idx.to(torch.int64).bitwise_and(mask).max()]).tolist()
+            else:
+                vals = [0, 0, 0]
+            cached = nat.OuterShape(int(vals[0]), int(vals[1]), int(vals[2]), int(self.a_idx.numel()),
+                                    int(self.b_idx.numel()))
+            object.__setattr__(self, "_shape", cached)
+        return cached
+
     @classmethod
     def from_host(cls, s, non_blocking: bool = False) -> "DeviceOuterStream":
         dev = _dev()
@@ -445,11 +465,12 @@ def outer_product(ds: DeviceOuterStream, upper_only: bool = False, kappa: int = 
         raise ConfigError("a partial interval needs the hash tables")
     lib = nat.load()
     h = ctypes.c_void_p()
-    nat.check(lib.crop_outer_create(nat.ptr(ds.a_ptr), nat.ptr(ds.a_idx), nat.ptr(ds.a_val),
-                                    nat.ptr(ds.b_ptr), nat.ptr(ds.b_idx), nat.ptr(ds.b_val),
-                                    ds.n_products, int(upper_only),
-                                    ctypes.byref(iv) if iv is not None else None,
-                                    nat.stream_ptr(), ctypes.byref(h)))
+    shape = ds.shape()
+    nat.check(lib.crop_outer_create_ex(nat.ptr(ds.a_ptr), nat.ptr(ds.a_idx), nat.ptr(ds.a_val),
+                                       nat.ptr(ds.b_ptr), nat.ptr(ds.b_idx), nat.ptr(ds.b_val),
+                                       ds.n_products, int(upper_only),
+                                       ctypes.byref(iv) if iv is not None else None,
+                                       ctypes.byref(shape), nat.stream_ptr(), ctypes.byref(h)))
     try:
         me, tt = ctypes.c_uint64(), ctypes.c_uint64()
         nat.check(lib.crop_outer_info(h, ctypes.byref(me), ctypes.byref(tt)))
@@ -459,13 +480,14 @@ def outer_product(ds: DeviceOuterStream, upper_only: bool = False, kappa: int = 
         col = torch.empty(m, dtype=torch.int32, device=dev)
         val = torch.empty(m, dtype=torch.float64, device=dev)
         buck = torch.empty(m, dtype=torch.int32, device=dev)
-        n_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        n_dev = torch.zeros(2, dtype=torch.int64, device=dev)
         nat.check(lib.crop_outer_run(h, nat.ptr(row), nat.ptr(col), nat.ptr(val), nat.ptr(buck),
                                      nat.ptr(n_dev), nat.stream_ptr()))
-        n = int(n_dev.item())
+        nat.check(lib.crop_outer_own_terms(h, ctypes.c_void_p(n_dev.data_ptr() + 8), nat.stream_ptr()))
+        n, own = n_dev.tolist()
     finally:
         lib.crop_outer_destroy(h)
-    ent = DeviceEntries(row, col, None, val, n, int(tt.value), bucket=buck)
+    ent = DeviceEntries(row, col, None, val, n, own, bucket=buck)
     ent.n_dev = n_dev
     return ent
 

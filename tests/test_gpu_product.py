@@ -1,9 +1,10 @@
-"""Real-valued partitioned products (csrc/outer.cu partition path) against the
-C oracle's exact_product (oracle.py:20-50 restated): per-bucket sorted COO,
-fp64 sums in stream order (bit-exact; BASELINE's tolerance rel 1e-5 / abs
-1e-6 is asserted too), every bucket interval, the triangle filter, the
-radix-sort fallback (partitions too large for shared memory) and the public
-crop.partition_product surface."""
+"""Real-valued partitioned products (csrc/outer.cu bucket-major path) against
+the C oracle's exact_product (oracle.py:20-50 restated): per-bucket sorted
+COO, fp64 sums in stream order (bit-exact; BASELINE's tolerance rel 1e-5 /
+abs 1e-6 is asserted too), every bucket interval, the triangle filter,
+partitions too large for shared memory (the in-CTA global-memory radix
+sort), the radix-sort fallback for keys wider than 64 bits (forced with
+CROP_OUTER_RADIX=1) and the public crop.partition_product surface."""
 
 import numpy as np
 import pytest
@@ -42,12 +43,12 @@ def _check(part_arrays, want):
     assert np.all(np.diff(key.astype(np.int64)) > 0)  # per-bucket sorted, distinct
 
 
-@pytest.fixture(params=["radix", "partition"])
+@pytest.fixture(params=["bucket-major", "radix"])
 def outer_path(request, monkeypatch):
-    """Both sort paths of csrc/outer.cu: the radix sort (default) and the
-    shared-memory partition sort (CROP_OUTER_PARTITION=1)."""
-    if request.param == "partition":
-        monkeypatch.setenv("CROP_OUTER_PARTITION", "1")
+    """Both sort paths of csrc/outer.cu: the bucket-major partition sort
+    (default) and the library radix-sort fallback (CROP_OUTER_RADIX=1)."""
+    if request.param == "radix":
+        monkeypatch.setenv("CROP_OUTER_RADIX", "1")
     return request.param
 
 
@@ -73,9 +74,9 @@ def test_partition_product_c4_prefix(workers, outer_path, monkeypatch):
         assert np.array_equal(x, y)
 
 
-def test_partition_product_skewed_rows_fall_back(outer_path):
+def test_partition_product_skewed_rows(outer_path):
     """One row holding far more terms than a shared-memory partition: the
-    job takes the radix-sort path and is still exact."""
+    partitions refine into column ranges of the row and stay exact."""
     rng = np.random.default_rng(2)
     n = 4000
     a, b = [], []
@@ -117,3 +118,45 @@ def test_partition_product_upper_and_errors(outer_path):
     _check(arrs, _want(s, h, 16, a_.start, a_.stop, upper=True))
     with pytest.raises(crop.ConfigError):
         crop.partition_product(s, config, worker=4)
+
+
+def test_partition_product_heavy_entry(outer_path):
+    """One (row, col) entry with more terms than a shared-memory partition
+    holds (6,000 products share it): that partition sorts in global memory
+    (stable LSD radix inside one CTA) and its sum is still in stream order."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    a, b = [], []
+    for k in range(6000):
+        ra = np.unique(np.concatenate([[11], rng.choice(n, 3, replace=False)]))
+        cb = np.unique(np.concatenate([[29], rng.choice(n, 3, replace=False)]))
+        a.append((ra.tolist(), rng.standard_normal(ra.size).astype(np.float32).astype(np.float64).tolist()))
+        b.append((cb.tolist(), rng.standard_normal(cb.size).astype(np.float32).astype(np.float64).tolist()))
+    ap, ai, av = vectors_to_csr(a)
+    bp, bi, bv = vectors_to_csr(b)
+    s = crop.ColumnRowStream(n, n, ap, ai, av, bp, bi, bv)
+    for kappa, workers in [(1, 1), (4, 2)]:
+        config = crop.EngineConfig(kappa=kappa, ss_capacity=2 ** 31, workers=workers, seed=2,
+                                   cs_enabled=False)
+        h = crop.make_hashes(crop.HashConfig(kappa, config.instance_seeds()[0]))
+        for w in range(workers):
+            a_ = config.assignments()[w]
+            part = crop.partition_product(s, config, worker=w if workers > 1 else None)
+            _check(part.arrays(), _want(s, h, kappa, a_.start, a_.stop))
+
+
+def test_outer_product_edge_streams(outer_path):
+    """Empty products, single-term products and an empty stream."""
+    a = [([], []), ([3], [2.0]), ([0, 5], [1.0, -1.0]), ([], []), ([7], [0.5])]
+    b = [([1], [1.0]), ([4], [3.0]), ([], []), ([2, 6], [1.0, 2.0]), ([7], [4.0])]
+    ap, ai, av = vectors_to_csr(a)
+    bp, bi, bv = vectors_to_csr(b)
+    s = crop.ColumnRowStream(8, 8, ap, ai, av, bp, bi, bv)
+    config = crop.EngineConfig(kappa=3, ss_capacity=2 ** 31, workers=3, seed=4, cs_enabled=False)
+    h = crop.make_hashes(crop.HashConfig(3, config.instance_seeds()[0]))
+    for w in range(3):
+        a_ = config.assignments()[w]
+        _check(crop.partition_product(s, config, worker=w).arrays(), _want(s, h, 3, a_.start, a_.stop))
+    e = crop.ColumnRowStream(8, 8, np.zeros(3, np.int64), np.zeros(0, np.uint32), np.zeros(0),
+                             np.zeros(3, np.int64), np.zeros(0, np.uint32), np.zeros(0))
+    assert len(crop.partition_product(e, config)) == 0

@@ -674,50 +674,40 @@ struct BmOut {
 };
 
 // Decoupled look-back over the partitions (taken in ticket order, so every
-// predecessor is running or done): publish the aggregate, then one warp reads
-// 32 predecessors' status words at a time and sums them back to the nearest
-// inclusive prefix, then publish the prefix. Called by warp 0.
-__device__ unsigned long long bm_lookback(unsigned long long* status, uint32_t p, unsigned long long agg) {
+// predecessor is running or done): publish the aggregate, then every thread
+// of the CTA reads one predecessor's status word (a CTA's worth of
+// predecessors per round: about one CTA per SM is in flight, so the nearest
+// inclusive prefix is usually within one round), the nearest inclusive
+// prefix is found with a block minimum and the aggregates up to it summed,
+// then the prefix is published. Called by the whole CTA.
+__device__ unsigned long long bm_lookback(unsigned long long* status, uint32_t p, unsigned long long agg,
+                                          unsigned long long* s_w, unsigned long long* s_red) {
   constexpr unsigned long long AGG = 1ull << 62, INC = 2ull << 62, VAL = (1ull << 62) - 1;
-  const int lane = threadIdx.x & 31;
   volatile unsigned long long* vs = status;
-  if (p == 0) {
-    if (lane == 0) {
-      __threadfence();
-      vs[0] = INC | agg;
-    }
-    return 0;
-  }
-  if (lane == 0) {
-    __threadfence();
-    vs[p] = AGG | agg;
-  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) vs[p] = (p == 0 ? INC : AGG) | agg;
+  if (p == 0) return 0;
   unsigned long long excl = 0;
-  int64_t top = (int64_t)p - 1;  // highest predecessor not yet summed
+  int64_t top = (int64_t)p - 1;
   for (;;) {
-    const int64_t q = top - lane;
+    const int64_t q = top - threadIdx.x;
     unsigned long long sv = q >= 0 ? vs[q] : INC;  // before partition 0: prefix 0
-    unsigned long long f = sv >> 62;
-    // wait until every lane's predecessor has published something
-    while (__any_sync(0xffffffffu, f == 0)) {
-      if (f == 0) {
-        sv = vs[q];
-        f = sv >> 62;
-      }
-    }
-    const uint32_t inc = __ballot_sync(0xffffffffu, f == 2);
-    // lanes up to and including the first (nearest) inclusive prefix
-    const int stop = inc ? __ffs(inc) - 1 : 31;
-    unsigned long long v = lane <= stop ? (sv & VAL) : 0ull;
-    v = warp_sum(v);
-    excl += v;
-    if (inc) break;
-    top -= 32;
+    while ((sv >> 62) == 0) sv = vs[q];
+    // nearest inclusive prefix = the smallest thread index holding one
+    unsigned int near = (sv >> 62) == 2 ? threadIdx.x : 0xFFFFFFFFu;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) near = min(near, __shfl_xor_sync(0xffffffffu, near, d));
+    if (lane == 0) s_red[warp] = near;
+    __syncthreads();
+    near = 0xFFFFFFFFu;
+    for (int w = 0; w < nw; ++w) near = min(near, (unsigned int)s_red[w]);
+    unsigned long long tot;
+    block_excl_scan(threadIdx.x <= near ? (sv & VAL) : 0ull, s_w, &tot);
+    excl += tot;
+    if (near != 0xFFFFFFFFu) break;
+    top -= blockDim.x;
   }
-  if (lane == 0) {
-    __threadfence();
-    vs[p] = INC | (excl + agg);
-  }
+  if (threadIdx.x == 0) vs[p] = INC | (excl + agg);
   return excl;
 }
 
@@ -741,15 +731,9 @@ __device__ __forceinline__ void bm_emit(uint32_t p, uint32_t m, const BmGeo& G, 
   }
   unsigned long long D;
   const unsigned long long d_w = block_excl_scan(lane == 0 ? heads : 0u, s_w, &D);
-  if (threadIdx.x < 32) {
-    const unsigned long long ex = bm_lookback(status, p, D);
-    if (threadIdx.x == 0) {
-      *s_excl = ex;
-      if (p == G.P - 1) *O.n_out = ex + D;
-    }
-  }
-  __syncthreads();
-  unsigned long long d = *s_excl + __shfl_sync(0xffffffffu, d_w, 0);
+  const unsigned long long ex = bm_lookback(status, p, D, s_w, s_excl + 1);
+  if (threadIdx.x == 0 && p == G.P - 1) *O.n_out = ex + D;
+  unsigned long long d = ex + __shfl_sync(0xffffffffu, d_w, 0);
   const uint32_t bucket = G.start + (p >> G.S_bits);
   const uint64_t c_hi = (uint64_t)(p & ((1u << G.S_bits) - 1)) << G.shift;
   const uint64_t lmask = (1ull << G.shift) - 1;
@@ -846,7 +830,7 @@ __global__ void __launch_bounds__(kBmSortThreads, 2) k_bm_sort(const unsigned lo
   uint16_t* idx2 = idx1 + kBmCap;                                         // kBmCap (ranks first)
   uint16_t* rk = idx2;
   __shared__ unsigned long long s_w[33];
-  __shared__ unsigned long long s_excl;
+  __shared__ unsigned long long s_excl[33];  // [1..32]: look-back reduction scratch
   __shared__ uint32_t s_p;
   const uint32_t bsh = G.sb + G.bin_shift;
   const uint32_t bmask = (G.shift - G.bin_shift >= 11) ? kBmBins - 1 : (1u << (G.shift - G.bin_shift)) - 1;
@@ -863,7 +847,7 @@ __global__ void __launch_bounds__(kBmSortThreads, 2) k_bm_sort(const unsigned lo
                                     reinterpret_cast<unsigned int*>(smem));
       const ulonglong2* tt = (fl ? terms2 : terms) + o0;
       bm_emit(p, m, G, [&](uint32_t q) { return tt[q].x; },
-              [&](uint32_t q) { return __longlong_as_double((long long)tt[q].y); }, status, O, s_w, &s_excl);
+              [&](uint32_t q) { return __longlong_as_double((long long)tt[q].y); }, status, O, s_w, s_excl);
       continue;
     }
     for (uint32_t x = threadIdx.x; x <= kBmBins; x += blockDim.x) cnt[x] = 0;
@@ -909,7 +893,7 @@ __global__ void __launch_bounds__(kBmSortThreads, 2) k_bm_sort(const unsigned lo
     }
     __syncthreads();
     bm_emit(p, m, G, [&](uint32_t q) { return sk[idx2[q]]; }, [&](uint32_t q) { return sv[idx2[q]]; }, status, O,
-            s_w, &s_excl);
+            s_w, s_excl);
   }
 }
 

@@ -224,6 +224,29 @@ int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
               const uint64_t* d_n_entries, uint64_t max_entries, uint32_t k, uint64_t* out_idx,
               uint64_t* d_k_out, void* stream);
 
+/* Streaming, mergeable per-bucket Space-Saving (spacesaving.py:39-63 with
+ * O(l) state per bucket; csrc/ss_stream.cu). The caller keeps the summary
+ * records of every bucket as flat device arrays (row, col, count, over) and
+ * merges each chunk's exact entries into them:
+ *   crop_ss_index  builds an open-addressing index over the n record keys
+ *                  (keys uint64[slots], idx uint32[slots]; slots a power of
+ *                  two >= 2n)
+ *   crop_ss_probe  for each chunk entry (row, col, e): a recorded key adds e
+ *                  to rec_count; an unrecorded key is appended to out_* as a
+ *                  candidate (mu[b] + e, over mu[b]) at position *d_n_out
+ *                  (incremented), b = (h_row[row] + h_col[col]) mod kappa.
+ *                  *d_saturated is set when a count would pass 2^32 - 1.
+ * The caller then keeps each bucket's l largest of records + candidates
+ * (crop_bucket_topk) and sets mu[b] to the l-th count of full buckets. */
+int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t n, unsigned long long* keys,
+                  uint32_t* idx, uint64_t slots, void* stream);
+int crop_ss_probe(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
+                  const uint64_t* d_n_entries, uint64_t max_entries, const unsigned long long* keys,
+                  const uint32_t* idx, uint64_t slots, const uint32_t* h_row, const uint32_t* h_col,
+                  uint32_t kappa, const uint32_t* mu, uint32_t* rec_count, uint32_t* out_row,
+                  uint32_t* out_col, uint32_t* out_count, uint32_t* out_over, uint64_t* d_n_out,
+                  unsigned int* d_saturated, void* stream);
+
 /* K5 -- general outer-product stream (real values), restricted to buckets
  * [start, stop): the per-partition enumerate_interval + accumulate loop
  * (interval.py:236-254; exact_product, oracle.py:20-50). Terms are emitted,

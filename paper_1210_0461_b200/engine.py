@@ -131,16 +131,31 @@ class _DeviceInstance:
         self.bucket_weight = None     # np.float64[kappa]: summary total_weight
 
 
+def torch_int64():
+    import torch
+
+    return torch.int64
+
+
 class _DeviceResult:
     """Exact entries of a run plus everything needed to answer queries."""
 
-    def __init__(self, entries, integer: bool, instances: list, capacity: int, kappa: int):
+    def __init__(self, entries, integer: bool, instances: list, capacity: int, kappa: int, over=None):
         self.entries = entries        # kernels.DeviceEntries
         self.integer = integer
         self.instances = instances
         self.capacity = capacity
         self.kappa = kappa
+        self.over = over              # streaming summaries: uint32 over-estimation per record
         self._index = None
+        self._over_host = None
+
+    def over_of(self, idx: int) -> float:
+        if self.over is None or idx < 0:
+            return 0.0
+        if self._over_host is None:
+            self._over_host = (self.over[: self.entries.n].to(torch_int64()) & 0xFFFFFFFF).cpu().numpy()
+        return float(self._over_host[idx])
 
     # -- host index for point queries (built on first use) -------------------
     def index(self):
@@ -296,7 +311,7 @@ class SketchState:
                 summaries[int(bucket)].total_weight = float(tot[bucket])
             order = np.lexsort((col, row, b))
             for x in order[keep[order]]:
-                summaries[int(b[x])]._load_record((int(row[x]), int(col[x])), float(w[x]), 0.0)
+                summaries[int(b[x])]._load_record((int(row[x]), int(col[x])), float(w[x]), d.over_of(int(x)))
             sketch = None
             if self.config.cs_enabled:
                 sketch = CountSketch(inst.hasher, [float(c) for c in inst.cs])
@@ -322,7 +337,7 @@ class SketchState:
             if inst.distinct[b] == 0:
                 lo, up = 0.0, 0.0
             elif idx >= 0 and d.recorded_of(inst, idx):
-                lo, up = w, w
+                lo, up = w - d.over_of(idx), w
             elif inst.distinct[b] >= d.capacity:
                 lo, up = 0.0, float(inst.bucket_min[b])
             else:
@@ -393,6 +408,8 @@ class SketchState:
         from .kernels import topk_indices, u32_to_numpy
 
         mask = self._candidate_mask()
+        if d.over is not None:
+            return self._top_entries_over(k)
         if d.integer:
             count = None  # the raw counts: the fused top-k inputs apply
             if mask is not None:
@@ -428,6 +445,27 @@ class SketchState:
         # (k is 1,000-10,000 in the configs: this is the call's host cost)
         tn = tuple.__new__
         return [tn(TopEntry, (tn(Entry, (r, c)), w, w, None)) for r, c, w in zip(rl, cl, wl)]
+
+    def _top_entries_over(self, k: int) -> list[TopEntry]:
+        """Streaming summaries (one instance): rank the records by (upper desc,
+        lower desc, row, col) with upper = count, lower = count - over
+        (engine.py:162-172)."""
+        import torch
+
+        d = self._dev
+        e = d.entries
+        n = e.n
+        up = e.count[:n].to(torch.int64) & 0xFFFFFFFF
+        lo = up - (d.over[:n].to(torch.int64) & 0xFFFFFFFF)
+        order = torch.arange(n, device=up.device)
+        for key, desc in ((e.col[:n].to(torch.int64) & 0xFFFFFFFF, False),
+                          (e.row[:n].to(torch.int64) & 0xFFFFFFFF, False), (lo, True), (up, True)):
+            order = order[torch.sort(key[order], stable=True, descending=desc).indices]
+        idx = order[:k]
+        h = torch.stack([(e.row[idx].to(torch.int64) & 0xFFFFFFFF), (e.col[idx].to(torch.int64) & 0xFFFFFFFF),
+                         up[idx], lo[idx]]).cpu().numpy()
+        return [TopEntry(Entry(int(r), int(c)), float(l), float(u), self._estimate(int(r), int(c)))
+                for r, c, u, l in zip(h[0], h[1], h[2], h[3])]
 
     def entry_arrays(self, instance: int = 0, out=None):
         """All recorded entries of one instance as columnar host arrays
@@ -753,6 +791,97 @@ def run(stream: OuterProductStream, config: EngineConfig, upper_triangle_only: b
     report = LoadReport(kappa=config.kappa, workers=config.workers, rows=rows,
                         input_pair_total=prep.pair_total, per_product=per_product,
                         assignments=[(a.start, a.stop) for a in assignments])
+    return state, report
+
+
+def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triangle_only: bool = False,
+                  chunk_transactions: int | None = None) -> tuple[SketchState, LoadReport]:
+    """run() for pair mining with bounded summary memory: the transaction
+    stream is consumed in chunks; each chunk is counted exactly on the GPU
+    and merged into every bucket's Space-Saving summary of at most
+    config.ss_capacity records (kernels.StreamingSummaries, csrc/ss_stream.cu),
+    so the device state of an instance is kappa * l records of 16 B plus one
+    chunk's entries, whatever the stream's distinct-pair count. Records carry
+    the reference's (count, over) bounds (spacesaving.py:39-81): recorded
+    entries query as (count - over, count), unrecorded ones as (0, min) in a
+    full bucket. With chunk_transactions >= the stream length this is the
+    exact regime's top-l of run(). Takes 0/1 transaction streams
+    (mining.transactions_to_stream / TransactionStream); more than one
+    instance materialises host summaries per instance."""
+    import torch
+
+    from . import kernels
+
+    _check_stream(stream)
+    prep = prepare(stream)
+    if prep.kind != "pairs":
+        raise ConfigError("run_streaming takes 0/1 transaction streams (pair mining)")
+    dtx = prep.device
+    kappa = config.kappa
+    seeds = config.instance_seeds()
+    hashers = [make_hashes(HashConfig(kappa, s)) for s in seeds]
+    tables = [kernels.hash_tables(h, prep.n_items) for h in hashers]
+    signs = [h.sign_hash for h in hashers] if config.cs_enabled else None
+    n_tx = dtx.n_tx
+    host_off = dtx.offsets.cpu().numpy()
+    if chunk_transactions is None:
+        lens = np.diff(host_off)
+        terms = int((lens * (lens - 1) // 2).sum())
+        n_chunks = max(1, -(-terms // (1 << 30)))  # about 2^30 terms per chunk
+        chunk_transactions = max(1, -(-n_tx // n_chunks))
+    if chunk_transactions < 1:
+        raise ConfigError(f"chunk_transactions must be >= 1, got {chunk_transactions}")
+    summ = [kernels.StreamingSummaries(kappa, config.ss_capacity, tab) for tab in tables]
+    t = len(hashers)
+    loads = torch.zeros((t, kappa), dtype=torch.int64, device=dtx.offsets.device)
+    cs = torch.zeros((t, kappa), dtype=torch.int64, device=dtx.offsets.device) if signs else None
+    for t0 in range(0, max(n_tx, 1), chunk_transactions):
+        t1 = min(n_tx, t0 + chunk_transactions)
+        if t1 <= t0:
+            break
+        ent = kernels.count_pairs(dtx.slice(t0, t1, host_off), upper_triangle_only)
+        bl, _, c = kernels.entry_bucket_stats(ent, tables, kappa, prep.n_items, signs)
+        loads += bl
+        if cs is not None:
+            cs += c
+        for s in summ:
+            s.absorb(ent)
+        del ent
+    loads_h = loads.cpu().numpy()
+    cs_h = cs.cpu().numpy().astype(np.float64) if cs is not None else None
+    assignments = config.assignments()
+    rows = [_worker_rows(loads_h[i], assignments) for i in range(t)]
+    report = LoadReport(kappa=kappa, workers=config.workers, rows=rows, input_pair_total=prep.pair_total,
+                        assignments=[(a.start, a.stop) for a in assignments])
+    if t == 1:
+        s = summ[0]
+        ent = kernels.DeviceEntries(s.row, s.col, s.count, None, s.n, int(loads_h[0].sum()))
+        inst = _DeviceInstance(seeds[0], hashers[0], tables[0], loads_h[0],
+                               s.per_bucket.cpu().numpy().astype(np.int64),
+                               cs_h[0] if cs_h is not None else None)
+        inst.bucket_min = s.mu.to(torch.int64).bitwise_and(0xFFFFFFFF).cpu().numpy().astype(np.float64)
+        inst.bucket_weight = loads_h[0].astype(np.float64)
+        result = _DeviceResult(ent, True, [inst], config.ss_capacity, kappa, over=s.over)
+        state = SketchState._from_device(config, prep.n_rows, prep.n_cols, upper_triangle_only, result)
+        return state, report
+    # several instances: host summaries per instance
+    instances = []
+    for i, s in enumerate(summ):
+        row, col = kernels.u32_to_numpy(s.row), kernels.u32_to_numpy(s.col)
+        cnt, ovr = kernels.u32_to_numpy(s.count), kernels.u32_to_numpy(s.over)
+        b = (np.asarray(hashers[i].row_hash.values(row.tolist()), np.int64) +
+             np.asarray(hashers[i].col_hash.values(col.tolist()), np.int64)) % kappa if s.n else \
+            np.zeros(0, np.int64)
+        summaries = {}
+        for bucket in np.nonzero(loads_h[i])[0]:
+            summaries[int(bucket)] = SpaceSavingSummary(config.ss_capacity)
+            summaries[int(bucket)].total_weight = float(loads_h[i][bucket])
+        for x in np.lexsort((col, row, b)):
+            summaries[int(b[x])]._load_record((int(row[x]), int(col[x])), float(cnt[x]), float(ovr[x]))
+        sketch = CountSketch(hashers[i], [float(c) for c in cs_h[i]]) if cs_h is not None else None
+        instances.append(InstanceSketch(seeds[i], hashers[i], summaries, sketch))
+    state = SketchState(config, prep.n_rows, prep.n_cols, instances, upper_triangle_only)
+    state.frozen = True
     return state, report
 
 

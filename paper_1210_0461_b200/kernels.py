@@ -66,6 +66,18 @@ class DeviceTransactions:
     def to_host(self) -> tuple[np.ndarray, np.ndarray]:
         return self.offsets.cpu().numpy(), u32_to_numpy(self.items)
 
+    def slice(self, t0: int, t1: int, host_offsets: np.ndarray | None = None) -> "DeviceTransactions":
+        """Transactions [t0, t1) as their own stream (item ids shared, offsets
+        rebased); host_offsets (the host copy of offsets) avoids a read-back."""
+        if host_offsets is not None:
+            i0, i1 = int(host_offsets[t0]), int(host_offsets[t1])
+        else:
+            i0, i1 = (int(x) for x in self.offsets[[t0, t1]].tolist())
+        items = self.items[i0:i1]
+        if i0 % 4:
+            items = items.clone()  # the counting kernels read 16-byte aligned item vectors
+        return DeviceTransactions(self.offsets[t0:t1 + 1] - i0, items, self.n_items)
+
 
 @dataclass
 class DeviceOuterStream:
@@ -452,6 +464,76 @@ def bucket_topk(ent: DeviceEntries, h_row, h_col, kappa: int, capacity: int, wan
              nat.ptr(rec) if rec is not None else None, nat.ptr(bmin), nat.ptr(btot), nat.stream_ptr())
     mask = rec[: ent.n].to(torch.bool) if rec is not None else None
     return mask, bmin.to(torch.int64) & U32_MASK, btot.to(torch.int64) & U32_MASK
+
+
+# ------------------------------------------------------------------ streaming Space-Saving
+
+class StreamingSummaries:
+    """Per-bucket Space-Saving summaries of one instance with O(l) device
+    state (csrc/ss_stream.cu): flat records (row, col, count, over) of every
+    bucket, at most `capacity` per bucket, and mu[b] = the minimum count of a
+    full bucket (its upper bound for unrecorded keys). absorb() merges the
+    exact entries of one chunk of the stream (spacesaving.py:39-63 applied to
+    the chunk's aggregated weights; see the header of ss_stream.cu)."""
+
+    def __init__(self, kappa: int, capacity: int, tables):
+        dev = _dev()
+        self.kappa, self.capacity = int(kappa), int(capacity)
+        self.h_row, self.h_col = tables
+        self.row = torch.empty(0, dtype=torch.int32, device=dev)
+        self.col = torch.empty(0, dtype=torch.int32, device=dev)
+        self.count = torch.empty(0, dtype=torch.int32, device=dev)
+        self.over = torch.empty(0, dtype=torch.int32, device=dev)
+        self.mu = torch.zeros(kappa, dtype=torch.int32, device=dev)
+        self.per_bucket = torch.zeros(kappa, dtype=torch.int64, device=dev)
+
+    @property
+    def n(self) -> int:
+        return int(self.row.shape[0])
+
+    def state_bytes(self) -> int:
+        """Device bytes of the summaries themselves (16 B per record)."""
+        return 16 * self.n + 4 * self.kappa
+
+    def absorb(self, ent: DeviceEntries) -> None:
+        dev = self.mu.device
+        n_rec, n_e = self.n, int(ent.n)
+        if n_e == 0:
+            return
+        slots = 1024
+        while slots < 2 * n_rec:
+            slots <<= 1
+        keys = torch.empty(slots, dtype=torch.int64, device=dev)
+        idx = torch.empty(slots, dtype=torch.int32, device=dev)
+        nat.call("crop_ss_index", nat.ptr(self.row), nat.ptr(self.col), n_rec, nat.ptr(keys), nat.ptr(idx),
+                 slots, nat.stream_ptr())
+        m = n_rec + n_e
+        row = torch.empty(m, dtype=torch.int32, device=dev)
+        col = torch.empty(m, dtype=torch.int32, device=dev)
+        cnt = torch.empty(m, dtype=torch.int32, device=dev)
+        over = torch.empty(m, dtype=torch.int32, device=dev)
+        row[:n_rec], col[:n_rec], cnt[:n_rec], over[:n_rec] = self.row, self.col, self.count, self.over
+        n_out = torch.tensor([n_rec], dtype=torch.int64, device=dev)
+        sat = torch.zeros(1, dtype=torch.int32, device=dev)
+        n_dev = getattr(ent, "n_dev", None)
+        if n_dev is None:
+            n_dev = torch.tensor([n_e], dtype=torch.int64, device=dev)
+        nat.call("crop_ss_probe", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev), n_e,
+                 nat.ptr(keys), nat.ptr(idx), slots, nat.ptr(self.h_row), nat.ptr(self.h_col), self.kappa,
+                 nat.ptr(self.mu), nat.ptr(cnt), nat.ptr(row), nat.ptr(col), nat.ptr(cnt), nat.ptr(over),
+                 nat.ptr(n_out), nat.ptr(sat), nat.stream_ptr())
+        del keys, idx
+        n_tot, saturated = (int(x) for x in torch.cat([n_out, sat.to(torch.int64)]).tolist())
+        if saturated:
+            raise ResourceCapError("a Space-Saving count passed 2^32 - 1")
+        comb = DeviceEntries(row, col, cnt, None, n_tot, 0)
+        comb.n_dev = n_out
+        mask, bmin, per = bucket_topk(comb, self.h_row, self.h_col, self.kappa, self.capacity)
+        self.row, self.col = row[:n_tot][mask], col[:n_tot][mask]
+        self.count, self.over = cnt[:n_tot][mask], over[:n_tot][mask]
+        full = per >= self.capacity
+        self.per_bucket = torch.minimum(per, torch.full_like(per, self.capacity))
+        self.mu = torch.where(full, bmin, torch.zeros_like(bmin)).to(torch.int32)
 
 
 # ------------------------------------------------------------------ K5 outer

@@ -144,7 +144,8 @@ def config_dict(cfg, world):
                 "zipf_s": cfg.zipf_s, "length": list(cfg.length), "kappa": cfg.kappa,
                 "top_k": cfg.top_k, "ss_capacity": cfg.ss_capacity, "data_seed": cfg.seed,
                 "engine_seed": 0, "upper_triangle_only": True,
-                "parallelism": f"tiles{world}",
+                "parallelism": (f"stream-chunks{world}" if cfg.ss_capacity and world == 1
+                                else f"tiles{world}"),
                 "l2": "flushed (1 GiB write) before every timed step"}
     return {"workload": cfg.name, "n": cfg.n, "kappa": cfg.kappa, "data_seed": cfg.seed,
             "engine_seed": 0, "parallelism": f"buckets{world}",
@@ -198,6 +199,8 @@ def run_ours(args, rank, world):
         return run_product(args, rank, world)
     dev = torch.device("cuda", torch.cuda.current_device())
     dtx, bcast_s = load_workload(cfg, rank, world)
+    if cfg.ss_capacity and world == 1:
+        return run_streaming_summaries(args, cfg, dtx)
     config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
                                cs_enabled=False, seed=0)
     hasher = crop.make_hashes(crop.HashConfig(cfg.kappa, config.instance_seeds()[0]))
@@ -394,6 +397,150 @@ def run_ours(args, rank, world):
             "gpu_launches": int(launches), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+STREAM_CHUNK_TX = 5_000_000  # c3: transactions per chunk (2.25e9 terms, ~8e8 chunk entries)
+
+
+def run_streaming_summaries(args, cfg, dtx):
+    """c3 on one GPU: the bounded Space-Saving regime with O(l) summary
+    state (kernels.StreamingSummaries, the loop of crop.run_streaming). A
+    step counts every chunk of transactions exactly on chip and merges it
+    into the kappa per-bucket summaries of l records, then selects the
+    top-k records."""
+    import numpy as np
+    import torch
+
+    import paper_1210_0461_b200 as crop
+    from paper_1210_0461_b200 import kernels
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    hasher = crop.make_hashes(crop.HashConfig(cfg.kappa, crop.derive_seed(0, "instance:0")))
+    tables = kernels.hash_tables(hasher, cfg.n_items)
+    host_off = dtx.offsets.cpu().numpy()
+    flush = torch.empty(1 << 28, dtype=torch.int32, device=dev)
+    n_tx = dtx.n_tx
+    chunks = [(t0, min(n_tx, t0 + STREAM_CHUNK_TX)) for t0 in range(0, n_tx, STREAM_CHUNK_TX)]
+
+    def step(ev=None):
+        s = kernels.StreamingSummaries(cfg.kappa, cfg.ss_capacity, tables)
+        loads = torch.zeros(cfg.kappa, dtype=torch.int64, device=dev)
+        for k, (t0, t1) in enumerate(chunks):
+            if ev is not None:
+                ev[k][0].record()
+            ent = kernels.count_pairs(dtx.slice(t0, t1, host_off), True)
+            if ev is not None:
+                ev[k][1].record()
+            bl, _, _ = kernels.entry_bucket_stats(ent, [tables], cfg.kappa, cfg.n_items, None)
+            loads += bl[0]
+            s.absorb(ent)
+            del ent
+        rec = kernels.DeviceEntries(s.row, s.col, s.count, None, s.n, 0)
+        idx = kernels.topk_indices(rec, cfg.top_k)
+        return s, loads, (rec.row[idx], rec.col[idx], rec.count[idx])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = kernels.launch_counter()
+    times, count_ms = [], []
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in chunks]
+            e0.record()
+            s, loads, top = step(ev)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            count_ms.append(sum(a.elapsed_time(b) for a, b in ev))
+    launches = kernels.launch_counter() - launches0
+    ms = statistics.mean(times)
+    lens = (dtx.offsets[1:] - dtx.offsets[:-1])
+    terms = int((lens * (lens - 1) // 2).sum().item())
+    bucket_loads = [int(x) for x in loads.cpu().tolist()]
+    assert sum(bucket_loads) == terms
+    balance = {"partitions": cfg.kappa,
+               "max_mean": crop.LoadReport(kappa=cfg.kappa, workers=cfg.kappa, rows=[bucket_loads],
+                                           input_pair_total=0).max_avg_ratio(),
+               "max_terms": max(bucket_loads), "mean_terms": sum(bucket_loads) / cfg.kappa,
+               "source": "exact per-bucket term counts of the chunks (LoadReport.max_avg_ratio arithmetic)"}
+    in_bytes = 4 * int(dtx.items.numel()) + 8 * int(dtx.offsets.numel())
+    summary_bytes = s.state_bytes()
+    # B_alg (SURVEY.md §8d, c3): 8 B per term + input + the kappa * l * 16 B summaries
+    b_alg = 8 * terms + in_bytes + cfg.kappa * cfg.ss_capacity * 16
+    peak, peak_src = peaks()
+    achieved = b_alg / (ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "per chunk of 5e6 transactions: pair engine (k_item_terms, "
+                "k_plan_stream, k_stream_scatter, k_count_stream, k_reduce_slabs) -> crop_ss_index + "
+                "crop_ss_probe + crop_bucket_topk (summary merge)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": b_alg, "avg_launch_ms": round(ms, 3),
+                "phases": {"count": {"ms": round(statistics.mean(count_ms), 3),
+                                     "share_of_step": round(statistics.mean(count_ms) / ms, 4)},
+                           "merge": {"ms": round(ms - statistics.mean(count_ms), 3),
+                                     "share_of_step": round(1 - statistics.mean(count_ms) / ms, 4)}},
+                "mode": f"streaming summaries, {len(chunks)} chunks"}
+    e2e = None if args.no_e2e else run_e2e_streaming(args, cfg, dtx, terms)
+    cpu = None if args.no_cpu else cpu_baseline(args, cfg, dtx)
+    line = {
+        "metric": BASELINE_METRIC, "value": terms / (ms * 1e-3), "unit": "terms/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: seeded Zipf transactions (SURVEY.md §8d, data seed = config no.)",
+        "config": config_dict(cfg, 1),
+        "details": {"terms": terms, "chunks": len(chunks), "summary_records": s.n,
+                    "summary_bytes": summary_bytes, "summary_bound_bytes": cfg.kappa * cfg.ss_capacity * 16,
+                    "peak_device_bytes": int(torch.cuda.max_memory_allocated())},
+        "partition_balance": balance, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": sampler.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e_streaming(args, cfg, dtx, terms):
+    """Public API end to end: pinned host transactions -> crop.run_streaming
+    -> SketchState.top_entries(top_k) + every summary record to pinned host
+    memory (SketchState.entry_arrays)."""
+    import numpy as np
+    import torch
+
+    import paper_1210_0461_b200 as crop
+
+    off_h = dtx.offsets.cpu().pin_memory()
+    it_h = dtx.items.cpu().pin_memory()
+    off_np, it_np = off_h.numpy(), it_h.numpy().view(np.uint32)
+    config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=cfg.ss_capacity, workers=cfg.workers,
+                               cs_enabled=False, seed=0)
+    out = tuple(torch.empty(cfg.kappa * cfg.ss_capacity, dtype=torch.int32, pin_memory=True).numpy()
+                .view(np.uint32) for _ in range(3))
+    d2h = [0]
+
+    def once():
+        stream = crop.TransactionStream(cfg.n_items, off_np, it_np, validate=False)
+        state, report = crop.run_streaming(stream, config, upper_triangle_only=True,
+                                           chunk_transactions=STREAM_CHUNK_TX)
+        top = state.top_entries(cfg.top_k)
+        row, col, cnt = state.entry_arrays(out=out)
+        d2h[0] = cfg.kappa * 8 + cfg.top_k * 32 + 12 * int(row.shape[0])
+        torch.cuda.synchronize()
+        return top
+
+    once()
+    times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        once()
+        times.append(time.perf_counter() - t0)
+    tm = statistics.mean(times)
+    return {"value": terms / tm, "unit": "terms/s", "ms_per_step": tm * 1e3,
+            "h2d_bytes_per_step": off_h.numel() * 8 + it_h.numel() * 4, "d2h_bytes_per_step": d2h[0],
+            "api": "crop.run_streaming(TransactionStream) + SketchState.top_entries + "
+                   "SketchState.entry_arrays (every summary record to pinned host memory)"}
 
 
 def run_product(args, rank, world):

@@ -229,23 +229,30 @@ int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
  * records of every bucket as flat device arrays (row, col, count, over) and
  * merges each chunk's exact entries into them:
  *   crop_ss_index  builds an open-addressing index over the n record keys
- *                  (keys uint64[slots], idx uint32[slots]; slots a power of
- *                  two >= 2n)
- *   crop_ss_probe  for each chunk entry (row, col, e): a recorded key adds e
- *                  to rec_count; an unrecorded key is appended to out_* as a
- *                  candidate (mu[b] + e, over mu[b]) at position *d_n_out
- *                  (incremented), b = (h_row[row] + h_col[col]) mod kappa.
+ *                  (slots uint64[n_slots]: hash fingerprint << 32 | record;
+ *                  n_slots a power of two >= 2n)
+ *   crop_ss_merge  for each chunk entry (row, col, e): a recorded key adds e
+ *                  to its record's count; an unrecorded key becomes a
+ *                  candidate (mu[b] + e, over mu[b]), b = (h_row[row] +
+ *                  h_col[col]) mod kappa, appended behind the records at
+ *                  *d_n_out (in: the record count; out: records +
+ *                  candidates). The arrays hold records + max_entries.
  *                  *d_saturated is set when a count would pass 2^32 - 1.
- * The caller then keeps each bucket's l largest of records + candidates
- * (crop_bucket_topk) and sets mu[b] to the l-th count of full buckets. */
-int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t n, unsigned long long* keys,
-                  uint32_t* idx, uint64_t slots, void* stream);
-int crop_ss_probe(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
-                  const uint64_t* d_n_entries, uint64_t max_entries, const unsigned long long* keys,
-                  const uint32_t* idx, uint64_t slots, const uint32_t* h_row, const uint32_t* h_col,
-                  uint32_t kappa, const uint32_t* mu, uint32_t* rec_count, uint32_t* out_row,
-                  uint32_t* out_col, uint32_t* out_count, uint32_t* out_over, uint64_t* d_n_out,
-                  unsigned int* d_saturated, void* stream);
+ *   crop_ss_keep   the entries a selection marked (mask[e] != 0, e <
+ *                  *d_n) appended to the out arrays; *d_n_out = their number.
+ * The caller keeps each bucket's l largest of records + candidates
+ * (crop_bucket_topk, then crop_ss_keep) and sets mu[b] to the l-th count of
+ * full buckets. */
+int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t n, unsigned long long* slots,
+                  uint64_t n_slots, void* stream);
+int crop_ss_merge(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
+                  const uint64_t* d_n_entries, uint64_t max_entries, const unsigned long long* slots,
+                  uint64_t n_slots, const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
+                  const uint32_t* mu, uint32_t* row, uint32_t* col, uint32_t* count, uint32_t* over,
+                  uint64_t* d_n_out, unsigned int* d_saturated, void* stream);
+int crop_ss_keep(const uint8_t* mask, const uint64_t* d_n, uint64_t max_n, const uint32_t* row,
+                 const uint32_t* col, const uint32_t* count, const uint32_t* over, uint32_t* out_row,
+                 uint32_t* out_col, uint32_t* out_count, uint32_t* out_over, uint64_t* d_n_out, void* stream);
 
 /* K5 -- general outer-product stream (real values), restricted to buckets
  * [start, stop): the per-partition enumerate_interval + accumulate loop

@@ -503,10 +503,9 @@ class StreamingSummaries:
         slots = 1024
         while slots < 2 * n_rec:
             slots <<= 1
-        keys = torch.empty(slots, dtype=torch.int64, device=dev)
-        idx = torch.empty(slots, dtype=torch.int32, device=dev)
-        nat.call("crop_ss_index", nat.ptr(self.row), nat.ptr(self.col), n_rec, nat.ptr(keys), nat.ptr(idx),
-                 slots, nat.stream_ptr())
+        index = torch.empty(slots, dtype=torch.int64, device=dev)
+        nat.call("crop_ss_index", nat.ptr(self.row), nat.ptr(self.col), n_rec, nat.ptr(index), slots,
+                 nat.stream_ptr())
         m = n_rec + n_e
         row = torch.empty(m, dtype=torch.int32, device=dev)
         col = torch.empty(m, dtype=torch.int32, device=dev)
@@ -518,19 +517,32 @@ class StreamingSummaries:
         n_dev = getattr(ent, "n_dev", None)
         if n_dev is None:
             n_dev = torch.tensor([n_e], dtype=torch.int64, device=dev)
-        nat.call("crop_ss_probe", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev), n_e,
-                 nat.ptr(keys), nat.ptr(idx), slots, nat.ptr(self.h_row), nat.ptr(self.h_col), self.kappa,
-                 nat.ptr(self.mu), nat.ptr(cnt), nat.ptr(row), nat.ptr(col), nat.ptr(cnt), nat.ptr(over),
-                 nat.ptr(n_out), nat.ptr(sat), nat.stream_ptr())
-        del keys, idx
+        nat.call("crop_ss_merge", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev), n_e,
+                 nat.ptr(index), slots, nat.ptr(self.h_row), nat.ptr(self.h_col), self.kappa, nat.ptr(self.mu),
+                 nat.ptr(row), nat.ptr(col), nat.ptr(cnt), nat.ptr(over), nat.ptr(n_out), nat.ptr(sat),
+                 nat.stream_ptr())
+        del index
         n_tot, saturated = (int(x) for x in torch.cat([n_out, sat.to(torch.int64)]).tolist())
         if saturated:
             raise ResourceCapError("a Space-Saving count passed 2^32 - 1")
+        self.last_candidates = n_tot - n_rec
         comb = DeviceEntries(row, col, cnt, None, n_tot, 0)
         comb.n_dev = n_out
-        mask, bmin, per = bucket_topk(comb, self.h_row, self.h_col, self.kappa, self.capacity)
-        self.row, self.col = row[:n_tot][mask], col[:n_tot][mask]
-        self.count, self.over = cnt[:n_tot][mask], over[:n_tot][mask]
+        rec = torch.empty(max(n_tot, 1), dtype=torch.uint8, device=dev)
+        bmin = torch.empty(self.kappa, dtype=torch.int32, device=dev)
+        per = torch.empty(self.kappa, dtype=torch.int32, device=dev)
+        nat.call("crop_bucket_topk", nat.ptr(row), nat.ptr(col), nat.ptr(cnt), nat.ptr(n_out), m,
+                 nat.ptr(self.h_row), nat.ptr(self.h_col), self.kappa, min(self.capacity, 0xFFFFFFFF),
+                 nat.ptr(rec), nat.ptr(bmin), nat.ptr(per), nat.stream_ptr())
+        bmin = bmin.to(torch.int64) & U32_MASK
+        per = per.to(torch.int64) & U32_MASK
+        keep_n = int(torch.minimum(per, torch.full_like(per, self.capacity)).sum().item())
+        out = [torch.empty(max(keep_n, 1), dtype=torch.int32, device=dev) for _ in range(4)]
+        n_keep = torch.zeros(1, dtype=torch.int64, device=dev)
+        nat.call("crop_ss_keep", nat.ptr(rec), nat.ptr(n_out), n_tot, nat.ptr(row), nat.ptr(col), nat.ptr(cnt),
+                 nat.ptr(over), *[nat.ptr(o) for o in out], nat.ptr(n_keep), nat.stream_ptr())
+        del rec, row, col, cnt, over
+        self.row, self.col, self.count, self.over = (o[:keep_n] for o in out)
         full = per >= self.capacity
         self.per_bucket = torch.minimum(per, torch.full_like(per, self.capacity))
         self.mu = torch.where(full, bmin, torch.zeros_like(bmin)).to(torch.int32)

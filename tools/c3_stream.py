@@ -41,7 +41,7 @@ for rep in range(2):
         ta += c - b
         terms += ent.total_terms
         print(f"  chunk [{t0}, {t1}): {ent.n} entries, count {1e3 * (b - a):.1f} ms, absorb {1e3 * (c - b):.1f} ms, "
-              f"records {s.n}", flush=True)
+              f"records {s.n}, candidates {getattr(s, 'last_candidates', 0)}", flush=True)
         del ent
     tot = time.perf_counter() - t_all
     print(f"rep {rep}: total {tot:.2f} s (count {tc:.2f}, absorb {ta:.2f}) -> {terms / tot:.3e} terms/s; "

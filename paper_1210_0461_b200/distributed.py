@@ -103,10 +103,16 @@ def _stream_from_arrays(arr: dict):
 
 def run_distributed(stream, config, upper_triangle_only: bool = False, compute=None, src: int = 0):
     """SPMD body of run_parallel. Returns (state, report) on rank `src`,
-    (None, None) elsewhere. `compute(stream, config, w_lo, w_hi, upper)` returns
-    the payloads of a worker block (default: the GPU engine's worker_payloads)."""
+    (None, None) elsewhere. Without `compute` and with one instance the whole
+    path stays on the GPUs (run_distributed_device); otherwise
+    `compute(stream, config, w_lo, w_hi, upper)` returns the crop-partial/1
+    payloads of a worker block (default: the GPU engine's worker_payloads),
+    gathered to `src` and merged with merge_partials."""
     from .engine import merge_partials, worker_payloads
 
+    dist = _dist()
+    if compute is None and config.instances == 1 and config.workers >= dist.get_world_size():
+        return run_distributed_device(stream, config, upper_triangle_only, src)
     dist = _dist()
     me, world = dist.get_rank(), dist.get_world_size()
     local = _stream_from_arrays(broadcast_arrays(_stream_arrays(stream) if me == src else None,
@@ -119,6 +125,170 @@ def run_distributed(stream, config, upper_triangle_only: bool = False, compute=N
     if me != src:
         return None, None
     return merge_partials([p for part in gathered for p in part])
+
+
+def _send(t, dst: int):
+    """Point-to-point send on the group's device (host copy under gloo)."""
+    dist = _dist()
+    dist.send(t if dist.get_backend() == "nccl" or t.device.type == "cpu" else t.cpu(), dst)
+
+
+def _recv(t, src: int):
+    dist = _dist()
+    if dist.get_backend() == "nccl" or t.device.type == "cpu":
+        dist.recv(t, src)
+        return
+    h = torch_empty_like_cpu(t)
+    dist.recv(h, src)
+    t.copy_(h)
+
+
+def torch_empty_like_cpu(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype, device="cpu")
+
+
+def _gather_cat(t, sizes: list, src: int):
+    """Concatenate every rank's 1-D tensor `t` (rank r holds sizes[r]
+    elements) on `src`, in rank order; None elsewhere."""
+    import torch
+
+    dist = _dist()
+    me = dist.get_rank()
+    if me != src:
+        if sizes[me]:
+            _send(t[: sizes[me]].contiguous(), src)
+        return None
+    parts = []
+    for r, n in enumerate(sizes):
+        if r == me:
+            parts.append(t[:n])
+        elif n:
+            buf = torch.empty(n, dtype=t.dtype, device=t.device)
+            _recv(buf, r)
+            parts.append(buf)
+    return torch.cat(parts) if parts else t[:0]
+
+
+def run_distributed_device(stream, config, upper_triangle_only: bool = False, src: int = 0):
+    """run_parallel with the data path on the GPUs: rank
+    `src` moves the stream to its GPU and broadcasts the arrays once (NCCL
+    over NVLink; device to device), every rank counts the buckets of its
+    contiguous block of worker intervals (the own-bucket layout for pair
+    streams, the bucket-major partitions for real streams) and finalises
+    their summaries -- each bucket lives on one rank, so the per-bucket
+    top-l of the bounded regime is final there -- and the disjoint results
+    are gathered to `src` as device arrays (point-to-point), with per-bucket
+    loads, distinct counts, Count-Sketch cells and summary minima summed
+    (each is non-zero only on its bucket's rank). `src` returns a device-
+    backed (SketchState, LoadReport) equal to crop.run's; input_pair_total
+    is 0 after a merge, as in the reference (engine.py:531)."""
+    import torch
+
+    from . import kernels
+    from .engine import (LoadReport, SketchState, _check_positive_terms, _compute, _DeviceResult,
+                         _Prepared, _worker_rows, prepare)
+    from .errors import CropError, InputError
+
+    dist = _dist()
+    me, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    meta = torch.zeros(9, dtype=torch.int64, device=dev)
+    prep, failure = None, None
+    if me == src:
+        try:
+            prep = prepare(stream)
+            _check_positive_terms(prep, upper_triangle_only)
+        except CropError as exc:  # every rank must leave the broadcast
+            failure = exc
+        if failure is None:
+            d = prep.device
+            if prep.kind == "pairs":
+                meta[:8] = torch.tensor([0, prep.n_rows, prep.n_cols, prep.n_items, d.n_tx + 1, d.nnz, 0, 0])
+            else:
+                meta[:8] = torch.tensor([1, prep.n_rows, prep.n_cols, prep.n_items, d.n_products + 1,
+                                         int(d.a_idx.numel()), int(d.b_idx.numel()), 0])
+        else:
+            meta[8] = 1
+    _coll(dist.broadcast, meta, src)
+    kind, n_rows, n_cols, n_items, n_ptr, nnz_a, nnz_b, _, err = (int(v) for v in meta.tolist())
+    if err:
+        if failure is not None:
+            raise failure
+        raise InputError(f"rank {src} rejected the stream")
+    if kind == 0:
+        if me == src:
+            arrays = [prep.device.offsets, prep.device.items]
+        else:
+            arrays = [torch.empty(n_ptr, dtype=torch.int64, device=dev),
+                      torch.empty(nnz_a, dtype=torch.int32, device=dev)]
+        for t in arrays:
+            _coll(dist.broadcast, t, src)
+        if me != src:
+            dtx = kernels.DeviceTransactions(arrays[0], arrays[1], n_items)
+            prep = _Prepared("pairs", dtx, n_rows, n_cols, n_items, 0, None)
+    else:
+        if me == src:
+            d = prep.device
+            arrays = [d.a_ptr, d.a_idx, d.a_val, d.b_ptr, d.b_idx, d.b_val]
+        else:
+            arrays = [torch.empty(n_ptr, dtype=torch.int64, device=dev),
+                      torch.empty(nnz_a, dtype=torch.int32, device=dev),
+                      torch.empty(nnz_a, dtype=torch.float64, device=dev),
+                      torch.empty(n_ptr, dtype=torch.int64, device=dev),
+                      torch.empty(nnz_b, dtype=torch.int32, device=dev),
+                      torch.empty(nnz_b, dtype=torch.float64, device=dev)]
+        for t in arrays:
+            _coll(dist.broadcast, t, src)
+        if me != src:
+            ds = kernels.DeviceOuterStream(*arrays, n_rows, n_cols)
+            prep = _Prepared("outer", ds, n_rows, n_cols, n_items, 0, None)
+    kappa = config.kappa
+    asg = config.assignments()
+    lo, hi = rank_workers(config.workers, me, world)  # hi > lo: workers >= world
+    result, hashers = _compute(prep, config, upper_triangle_only, asg[lo].start, asg[hi - 1].stop)
+    result.finalize_summaries()
+    inst = result.instances[0]
+    e = result.entries
+    integer = result.integer
+    # per-bucket facts, non-zero only on the bucket's rank: summed
+    facts = torch.tensor(np.stack([inst.loads.astype(np.float64), inst.distinct.astype(np.float64),
+                                   inst.cs.astype(np.float64) if inst.cs is not None else np.zeros(kappa),
+                                   inst.bucket_min.astype(np.float64)]), dtype=torch.float64, device=dev)
+    _coll(dist.all_reduce, facts)
+    sizes_t = torch.zeros(world, dtype=torch.int64, device=dev)
+    sizes_t[me] = e.n
+    _coll(dist.all_reduce, sizes_t)
+    sizes = [int(v) for v in sizes_t.tolist()]
+    rec = inst.recorded
+    if rec is None:
+        rec = torch.ones(e.n, dtype=torch.bool, device=dev)
+    cols = [e.row[: e.n], e.col[: e.n], rec[: e.n].to(torch.uint8)]
+    cols += [e.count[: e.n]] if integer else [e.value[: e.n], e.bucket[: e.n]]
+    got = [_gather_cat(c.contiguous(), sizes, src) for c in cols]
+    if me != src:
+        return None, None
+    n = sum(sizes)
+    if integer:
+        row, col, rmask, cnt = got
+        ent = kernels.DeviceEntries(row, col, cnt, None, n, 0)
+    else:
+        row, col, rmask, val, buck = got
+        ent = kernels.DeviceEntries(row, col, None, val, n, 0, bucket=buck)
+    f = facts.cpu().numpy()
+    inst.loads = f[0].astype(np.int64)
+    inst.distinct = f[1].astype(np.int64)
+    inst.cs = f[2] if inst.cs is not None else None
+    inst.bucket_min = f[3]
+    inst.bucket_weight = None
+    rmask = rmask.to(torch.bool)
+    inst.recorded = None if bool(rmask.all().item()) else rmask
+    merged = _DeviceResult(ent, integer, [inst], config.ss_capacity, kappa)
+    state = SketchState._from_device(config, n_rows, n_cols, upper_triangle_only, merged)
+    report = LoadReport(kappa=kappa, workers=config.workers, rows=[_worker_rows(inst.loads, asg)],
+                        input_pair_total=0, assignments=[(a.start, a.stop) for a in asg])
+    return state, report
 
 
 def _coll(op, t, *args, **kw):

@@ -2,8 +2,10 @@
 GPU (the ranks never wait on each other's kernels -- collectives run on the
 host), compared with the single-process crop.run on the same stream.
 
-Covers distributed.run_distributed (worker_payloads on the device, pickled
-crop-partial/1 gather, merge_partials) and distributed.top_entries_distributed
+Covers distributed.run_distributed (one instance: the device path with device
+broadcast, per-rank bucket intervals and point-to-point gather of the device
+results; several instances: worker_payloads, pickled crop-partial/1 gather,
+merge_partials) and distributed.top_entries_distributed
 (bucket-interval counting per rank, loads / Count-Sketch all-reduce, top-k
 gather), including the bounded Space-Saving regime.
 """
@@ -165,3 +167,56 @@ def test_tile_shard_summaries_merge_across_ranks():
         assert loads == inst.loads.astype(np.int64).tolist()
     assert got_keys == whole_keys
     assert bmin.tolist() == inst.bucket_min.astype(np.int64).tolist()
+
+
+def _outer_worker(rank, world, port, arrays, cfg_dict, upper, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        config = crop.EngineConfig(**cfg_dict)
+        stream = crop.ColumnRowStream(*arrays) if rank == 0 else None
+        state, report = distributed.run_distributed(stream, config, upper)
+        out = {}
+        if rank == 0:
+            out["records"] = _records(state)
+            out["rows"] = report.rows
+            out["total"] = report.input_pair_total
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,workers,cap,upper", [(2, 4, 2 ** 31, False), (3, 6, 40, True)])
+def test_device_run_distributed_real_stream(world, workers, cap, upper):
+    """run_distributed's device path on a real-valued CSC/CSR stream (bucket-
+    major partitions per rank, device broadcast and point-to-point gather):
+    the merged summaries equal single-process crop.run's, in the exact and
+    the bounded regime."""
+    from paper_1210_0461_b200 import workloads
+
+    cfg4 = workloads.CONFIGS["c4"]
+    s = workloads.generate_product_workload(cfg4, n_products=3_000)
+    pos = (s.a_ptr, s.a_idx, abs(s.a_val) + 0.5, s.b_ptr, s.b_idx, abs(s.b_val) + 0.5)
+    arrays = (cfg4.n, cfg4.n) + pos
+    cfg = crop.EngineConfig(kappa=24, ss_capacity=cap, workers=workers, cs_enabled=True, seed=5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_outer_worker, args=(r, world, port, arrays, cfg.to_dict(), upper, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    got = res[0]
+    state, report = crop.run(crop.ColumnRowStream(*arrays), cfg, upper_triangle_only=upper)
+    assert got["rows"] == report.rows
+    assert got["total"] == 0
+    want = _records(state)
+    assert [r for r, _ in got["records"]] == [r for r, _ in want]
+    np_cells_got, np_cells_want = got["records"][0][1], want[0][1]
+    assert np_cells_got == pytest.approx(np_cells_want, rel=1e-12, abs=1e-9)

@@ -351,11 +351,23 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         uint32_t* seg = s_hs + b0;
         if (L <= 32) {
           // stable rank by class (the items ascend with the lane): one ballot
-          // per class bit, most significant first
+          // per class bit, most significant first. The same ballots give,
+          // for this lane's row i, the lanes whose class lies in its own
+          // window: its own partners (ids above i: later lanes) and, for a
+          // single-bucket interval, the first partner's sorted position --
+          // no binary search, no second walk over these positions.
           const bool v = (uint32_t)lane < L;
           const uint32_t k = v ? seg[lane] : 0u;
           const uint32_t cls = k >> O.idbits;
-          uint32_t eq = __ballot_sync(0xffffffffu, v), lt = 0;
+          const uint32_t hr = v ? s_hr[b0 + lane] : 0u;
+          const uint32_t c_lo = O.start >= hr ? O.start - hr : O.start + O.kappa - hr;
+          const uint64_t c_end = (uint64_t)c_lo + O.len;           // window [c_lo, c_end) mod kappa
+          const bool wraps = c_end > O.kappa;
+          const uint32_t c_hi = wraps ? (uint32_t)(c_end - O.kappa) : (uint32_t)c_end;
+          const uint32_t vm = __ballot_sync(0xffffffffu, v);
+          uint32_t eq = vm, lt = 0;
+          uint32_t e_lo = vm, m_lo = 0;  // lanes with class == / < c_lo (prefix so far)
+          uint32_t e_hi = vm, m_hi = 0;  // lanes with class == / < c_hi
           for (int bt = (int)O.cbits - 1; bt >= 0; --bt) {
             const bool bit = (cls >> bt) & 1u;
             const uint32_t B = __ballot_sync(0xffffffffu, v && bit);
@@ -365,10 +377,44 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             } else {
               eq &= ~B;
             }
+            if ((c_lo >> bt) & 1u) {
+              m_lo |= e_lo & ~B;
+              e_lo &= B;
+            } else {
+              e_lo &= ~B;
+            }
+            if ((c_hi >> bt) & 1u) {
+              m_hi |= e_hi & ~B;
+              e_hi &= B;
+            } else {
+              e_hi &= ~B;
+            }
           }
+          if (c_hi >= (1u << O.cbits)) m_hi = vm;  // c_hi == kappa == 2^cbits: every class is below
           const uint32_t r = lt + __popc(eq & ((1u << lane) - 1u));
           __syncwarp();
           if (v) seg[r] = k;
+          // own window: classes in [c_lo, c_hi) (or [c_lo, kappa) + [0, c_hi) when it wraps)
+          const uint32_t wmask = wraps ? ((vm & ~m_lo) | m_hi) : (m_hi & ~m_lo);
+          const uint32_t after = UPPER ? ~((2u << lane) - 1u) : vm;  // lanes 2u << 31 wraps to 0
+          const uint32_t cnt = __popc(wmask & after);
+          if (v) {
+            uint32_t src = 0xFFFFu;
+            if (O.len == 1) {  // first own partner: class c_lo's start + its items not after i
+              const uint32_t upto = UPPER ? ((2u << lane) - 1u) : 0u;
+              src = __popc(m_lo) + __popc(e_lo & upto);
+            }
+            O.pos_rec[g_lo + b0 + lane] = cnt | (src << 16);
+            const uint32_t i = k & idmask;
+            if (cnt) {
+              if (i < n_smem) {
+                atomicAdd(&s_terms[i], cnt);
+                atomicAdd(&s_occ[i], 1u);
+              } else {
+                atomicAdd(&stats[i], kOccOne | cnt);
+              }
+            }
+          }
         } else if (L <= kOwnSortMax) {
           uint32_t P = 64;
           while (P < L) P <<= 1;
@@ -421,25 +467,32 @@ __global__ void __launch_bounds__(kPassThreads, 1)
       }
       __syncthreads();
       for (uint32_t x = threadIdx.x; x < npos; x += blockDim.x) hs_out[g_lo + x] = s_hs[x];
-      walk_chunk<false>(s_off, ntx, items, (const uint32_t*)nullptr,
-                        [&](int64_t g, const Pos& q, uint32_t i, uint32_t) {
-        if (!q.valid) return;
-        if (UPPER && q.p + 1 >= q.L) {
-          O.pos_rec[g] = 0;
-          return;
+      // transactions of more than 32 items: own windows by binary search on
+      // the sorted keys, one warp per transaction (the short ones were done
+      // in the sort)
+      for (int t = warp; t < ntx; t += kPassThreads / 32) {
+        const uint32_t b0 = (uint32_t)(s_off[t] - g_lo), L = (uint32_t)(s_off[t + 1] - s_off[t]);
+        if (L <= 32) continue;
+        const uint32_t* seg = s_hs + b0;
+        for (uint32_t p = lane; p < L; p += 32) {
+          const int64_t g = g_lo + b0 + p;
+          if (UPPER && p + 1 >= L) {
+            O.pos_rec[g] = 0;
+            continue;
+          }
+          const uint32_t i = __ldg(items + g);
+          uint32_t src;
+          const uint32_t cnt = own_partners<UPPER>(seg, L, i, s_hr[b0 + p], O, idmask, src);
+          O.pos_rec[g] = cnt | (src << 16);  // src < 2^16 (kNone for general intervals: 0xFFFF)
+          if (cnt == 0) continue;
+          if (i < n_smem) {
+            atomicAdd(&s_terms[i], cnt);
+            atomicAdd(&s_occ[i], 1u);
+          } else {
+            atomicAdd(&stats[i], kOccOne | cnt);
+          }
         }
-        uint32_t src;
-        const uint32_t cnt = own_partners<UPPER>(s_hs + (q.base - g_lo), q.L, i, s_hr[g - g_lo], O,
-                                                 idmask, src);
-        O.pos_rec[g] = cnt | (src << 16);  // src < 2^16 (kNone for general intervals: 0xFFFF)
-        if (cnt == 0) return;
-        if (i < n_smem) {
-          atomicAdd(&s_terms[i], cnt);
-          atomicAdd(&s_occ[i], 1u);
-        } else {
-          atomicAdd(&stats[i], kOccOne | cnt);
-        }
-      });
+      }
     }
   }
   __syncthreads();

@@ -516,8 +516,7 @@ def run_e2e_streaming(args, cfg, dtx, terms):
     off_np, it_np = off_h.numpy(), it_h.numpy().view(np.uint32)
     config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=cfg.ss_capacity, workers=cfg.workers,
                                cs_enabled=False, seed=0)
-    out = tuple(torch.empty(cfg.kappa * cfg.ss_capacity, dtype=torch.int32, pin_memory=True).numpy()
-                .view(np.uint32) for _ in range(3))
+    out = [None]
     d2h = [0]
 
     def once():
@@ -525,8 +524,13 @@ def run_e2e_streaming(args, cfg, dtx, terms):
         state, report = crop.run_streaming(stream, config, upper_triangle_only=True,
                                            chunk_transactions=STREAM_CHUNK_TX)
         top = state.top_entries(cfg.top_k)
-        row, col, cnt = state.entry_arrays(out=out)
-        d2h[0] = cfg.kappa * 8 + cfg.top_k * 32 + 12 * int(row.shape[0])
+        if out[0] is None:
+            tdt = {np.uint16: torch.int16, np.uint32: torch.int32}
+            out[0] = tuple(torch.empty(cfg.kappa * cfg.ss_capacity, dtype=tdt[dt], pin_memory=True)
+                           .numpy().view(dt) for dt in (*state.entry_dtypes()[:1] * 2, state.entry_dtypes()[1]))
+        row, col, cnt = state.entry_arrays(out=out[0])
+        per = row.dtype.itemsize + col.dtype.itemsize + cnt.dtype.itemsize
+        d2h[0] = cfg.kappa * 8 + cfg.top_k * 32 + per * int(row.shape[0])
         torch.cuda.synchronize()
         return top
 
@@ -617,7 +621,7 @@ def run_product(args, rank, world):
                          "(bucket-major partitions sorted in shared memory, ordered fp64 run "
                          "sums, look-back output offsets)",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": b_alg,
                          "avg_launch_ms": round(statistics.mean(times), 4)},
             "cpu_baseline": (product_cpu_baseline(args, cfg, s) if world == 1 and not args.no_cpu
@@ -743,11 +747,14 @@ def run_e2e(args, cfg, dtx, rank, world):
             n = state.device_result.entries.n
             if out is None or out[0].shape[0] < n:
                 cap = int(n * 1.05) + 1024
-                out = tuple(torch.empty(cap, dtype=torch.int32, pin_memory=True).numpy()
-                            .view(np.uint32) for _ in range(3))
+                idt, wdt = state.entry_dtypes()
+                tdt = {np.uint16: torch.int16, np.uint32: torch.int32}
+                out = tuple(torch.empty(cap, dtype=tdt[dt], pin_memory=True).numpy().view(dt)
+                            for dt in (idt, idt, wdt))
             row, col, cnt = state.entry_arrays(out=out)
             # loads (kappa u64) + top-k + every entry's (row, col, count)
-            d2h[0] = cfg.kappa * 8 + cfg.top_k * 24 + 12 * int(row.shape[0])
+            per = row.dtype.itemsize + col.dtype.itemsize + cnt.dtype.itemsize
+            d2h[0] = cfg.kappa * 8 + cfg.top_k * 24 + per * int(row.shape[0])
         torch.cuda.synchronize()
         return report
 

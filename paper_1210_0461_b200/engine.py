@@ -467,21 +467,25 @@ class SketchState:
         return [TopEntry(Entry(int(r), int(c)), float(l), float(u), self._estimate(int(r), int(c)))
                 for r, c, u, l in zip(h[0], h[1], h[2], h[3])]
 
-    def entry_arrays(self, instance: int = 0, out=None):
+    def entry_arrays(self, instance: int = 0, out=None, compact: bool = True):
         """All recorded entries of one instance as columnar host arrays
-        (row uint32, col uint32, weight): the columnar form of
-        `instances[t].summaries` (the reference's per-bucket dicts,
-        engine.py:108-118) without building one Python object per entry.
-        0/1 streams give uint32 supports, real streams float64 weights.
-        A device-backed state copies them with one device->host transfer per
-        column into pinned buffers (`out` = reusable (row, col, weight) numpy
-        arrays of at least the entry count, e.g. from pinned torch tensors)."""
+        (row, col, weight): the columnar form of `instances[t].summaries` (the
+        reference's per-bucket dicts, engine.py:108-118) without building one
+        Python object per entry. Ids are uint32, or uint16 when `compact` and
+        both dimensions are at most 65,536 (lossless; a third less to copy
+        from the device); 0/1 streams give uint32 supports, real streams
+        float64 weights. A device-backed state copies them with one
+        device->host transfer per column into pinned buffers (`out` =
+        reusable (row, col, weight) numpy arrays of at least the entry count
+        and of the returned dtypes, e.g. from pinned torch tensors;
+        entry_dtypes() names them)."""
         self._require_frozen()
+        id_dt, w_dt = self.entry_dtypes(compact)
         if self._dev is None:
             recs = [(it[0], it[1], c) for s in self.instances[instance].summaries.values()
                     for it, c, _ in s.records()]
-            row = np.array([r[0] for r in recs], dtype=np.uint32)
-            col = np.array([r[1] for r in recs], dtype=np.uint32)
+            row = np.array([r[0] for r in recs], dtype=id_dt)
+            col = np.array([r[1] for r in recs], dtype=id_dt)
             return row, col, np.array([r[2] for r in recs], dtype=np.float64)
         import torch
 
@@ -493,18 +497,30 @@ class SketchState:
         if inst.recorded is not None:
             cols = [c[inst.recorded] for c in cols]
             n = int(cols[0].shape[0])
+        if id_dt == np.uint16:
+            # values < 2^16: the int32 -> int16 cast keeps the low 16 bits
+            cols[0], cols[1] = cols[0].to(torch.int16), cols[1].to(torch.int16)
         if out is None:
             host = [torch.empty(n, dtype=c.dtype, pin_memory=True) for c in cols]
         else:
-            host = [torch.from_numpy(o.view(np.int32) if o.dtype == np.uint32 else o)[:n]
-                    for o in out]
+            signed = {np.dtype(np.uint32): np.int32, np.dtype(np.uint16): np.int16}
+            for o, c in zip(out, cols):
+                if o.dtype.itemsize != c.element_size():
+                    raise InputError(f"out array of dtype {o.dtype} for a column of {c.dtype}")
+            host = [torch.from_numpy(o.view(signed.get(o.dtype, o.dtype)))[:n] for o in out]
         for h, c in zip(host, cols):
             h.copy_(c, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         row, col, w = (h.numpy() for h in host)
         if d.integer:
-            return row.view(np.uint32), col.view(np.uint32), w.view(np.uint32)
-        return row.view(np.uint32), col.view(np.uint32), w
+            return row.view(id_dt), col.view(id_dt), w.view(np.uint32)
+        return row.view(id_dt), col.view(id_dt), w
+
+    def entry_dtypes(self, compact: bool = True):
+        """(id dtype, weight dtype) of entry_arrays."""
+        small = compact and self.n_rows <= 65536 and self.n_cols <= 65536
+        integer = self._dev.integer if self._dev is not None else False
+        return (np.uint16 if small else np.uint32), (np.uint32 if integer else np.float64)
 
     def recorded_weight(self) -> float:
         if self._dev is not None:

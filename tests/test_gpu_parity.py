@@ -410,3 +410,30 @@ def test_host_generator_copy_matches_device_generator(name):
     d_off, d_items = dtx.to_host()
     assert np.array_equal(off, d_off)
     assert np.array_equal(items, d_items)
+
+
+@pytest.mark.parametrize("compact", [True, False])
+def test_entry_arrays_columns(compact):
+    """SketchState.entry_arrays: every counted entry with its support, as
+    uint16 ids when both dimensions fit (compact) or uint32, into caller
+    buffers of the named dtypes or fresh pinned arrays; equal to the oracle."""
+    cfg = workloads.CONFIGS["c1"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=3000)
+    off, items = dtx.to_host()
+    stream = crop.TransactionStream(cfg.n_items, off, items)
+    config = crop.EngineConfig(kappa=4, ss_capacity=2 ** 31, workers=4, cs_enabled=False, seed=0)
+    state, _ = crop.run(stream, config, upper_triangle_only=True)
+    idt, wdt = state.entry_dtypes(compact)
+    assert idt == (np.uint16 if compact else np.uint32) and wdt == np.uint32
+    row, col, w = state.entry_arrays(compact=compact)
+    assert row.dtype == idt and col.dtype == idt and w.dtype == np.uint32
+    er, ec, ew = oracle.pair_supports(off, items)
+    want = sorted(zip(er.tolist(), ec.tolist(), ew.astype(np.int64).tolist()))
+    assert sorted(zip(row.tolist(), col.tolist(), w.tolist())) == want
+    n = row.shape[0]
+    out = (np.empty(n + 5, idt), np.empty(n + 5, idt), np.empty(n + 5, wdt))
+    r2, c2, w2 = state.entry_arrays(out=out, compact=compact)
+    assert np.array_equal(r2, row) and np.array_equal(c2, col) and np.array_equal(w2, w)
+    with pytest.raises(crop.InputError):
+        state.entry_arrays(out=(np.empty(n, np.uint64), np.empty(n, np.uint64), np.empty(n, np.uint64)),
+                           compact=compact)

@@ -399,7 +399,7 @@ def run_ours(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
-STREAM_CHUNK_TX = 5_000_000  # c3: transactions per chunk (2.25e9 terms, ~8e8 chunk entries)
+STREAM_CHUNK_TX = 8_333_334  # c3: 6 chunks of ~3.75e9 terms (measured: 10 chunks 1.71 s, 6 chunks 1.50 s, 5 chunks 1.62 s)
 
 
 def run_streaming_summaries(args, cfg, dtx):
@@ -474,7 +474,7 @@ def run_streaming_summaries(args, cfg, dtx):
     b_alg = 8 * terms + in_bytes + cfg.kappa * cfg.ss_capacity * 16
     peak, peak_src = peaks()
     achieved = b_alg / (ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "per chunk of 5e6 transactions: pair engine (k_item_terms, "
+    roofline = {"bound": "hbm", "kernel": "per chunk of 8.3e6 transactions: pair engine (k_item_terms, "
                 "k_plan_stream, k_stream_scatter, k_count_stream, k_reduce_slabs) -> crop_ss_index + "
                 "crop_ss_probe + crop_bucket_topk (summary merge)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -843,7 +843,7 @@ def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triang
     if chunk_transactions is None:
         lens = np.diff(host_off)
         terms = int((lens * (lens - 1) // 2).sum())
-        n_chunks = max(1, -(-terms // (1 << 30)))  # about 2^30 terms per chunk
+        n_chunks = max(1, -(-terms // 4_000_000_000))  # about 4e9 terms per chunk (c3: 6)
         chunk_transactions = max(1, -(-n_tx // n_chunks))
     if chunk_transactions < 1:
         raise ConfigError(f"chunk_transactions must be >= 1, got {chunk_transactions}")

@@ -32,7 +32,12 @@ for r in rows[2:]:
     for m, k in want.items():
         if m not in d:
             continue
-        v = float(d[m].replace(",", ""))
+        try:
+            v = float(d[m].replace(",", ""))
+        except ValueError:
+            continue
+        if v != v:  # n/a
+            continue
         u = units[h.index(m)]
         if k == "ms":
             v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
@@ -48,7 +53,11 @@ path = 0.0
 print(f"{'kernel':32s} {'n':>2s} {'ms':>8s} {'share':>6s} {'DRAM rd GB':>10s} {'DRAM wr GB':>10s} {'L2 hit':>6s} {'issue%':>6s}")
 for name, v in sorted(kernels.items(), key=lambda kv: -sum(x["ms"] for x in kv[1])):
     n = len(v)
-    agg = {k: sum(x.get(k, 0.0) for x in v) / n for k in v[0]}
+    keys = set().union(*v)
+    agg = {k: sum(x.get(k, 0.0) for x in v) / n for k in keys}
+    agg.setdefault("dram_read", 0.0)
+    agg.setdefault("dram_write", 0.0)
+    agg.setdefault("ms", 0.0)
     summary[name] = {"launches": n, "ms_per_launch": round(agg["ms"], 4),
                      "dram_bytes_per_launch": int(agg["dram_read"] + agg["dram_write"]),
                      "dram_read_bytes": int(agg["dram_read"]), "dram_write_bytes": int(agg["dram_write"]),

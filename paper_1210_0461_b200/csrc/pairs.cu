@@ -38,6 +38,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 using namespace crop;
@@ -3279,6 +3281,543 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
   }
 }
 
+
+// Cooperative form of k_plan_stream: the same plan, computed by one CTA per
+// SM instead of one CTA (k_plan_stream walks every row and tile on one SM:
+// 0.24 ms on c2, 5 ms on a c3 chunk). Each CTA takes a contiguous range of at
+// most kPlanChunk rows (then of tiles); the sequential carries of the
+// single-CTA planner (weight prefix, last light bucket, tile ids, last light
+// tile and its first row, shard cost prefixes, unit bases) become grid-wide
+// prefixes of per-CTA aggregates published in PlanScratch between grid
+// syncs. Every decision is the single-CTA planner's, so the plans are
+// identical (tests compare them).
+constexpr uint32_t kMaxPlanCtas = 160;
+struct PlanScratch {
+  unsigned long long totals[2];  // T, O
+  unsigned int has_win, pad;
+  unsigned long long cw[kMaxPlanCtas];
+  long long lastb[kMaxPlanCtas];
+  unsigned long long ct[kMaxPlanCtas];
+  long long llt[kMaxPlanCtas], lrow[kMaxPlanCtas];
+  unsigned long long ssum[3][kMaxPlanCtas];
+  unsigned long long sow[3][kMaxShardCheck];
+  unsigned long long u8[kMaxPlanCtas][8];
+  unsigned int bins[72];
+  unsigned int cur[72];
+};
+
+__global__ void __launch_bounds__(kPlanThreads, 1) k_plan_coop(PlanArgs P, PlanScratch* S) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long s_u64[33];
+  __shared__ long long s_i64[33];
+  __shared__ unsigned long long s_bc[8];
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_rec = s_dyn;               // per staged row: class | weight << 3
+  uint32_t* s_t = s_dyn + kPlanChunk;    // per staged row: terms
+  const uint32_t n = P.n, tid = threadIdx.x, nb = gridDim.x, cb = blockIdx.x;
+  auto add = [](unsigned long long a, unsigned long long b) { return a + b; };
+  auto mx = [](long long a, long long b) { return a > b ? a : b; };
+  long long totl;
+  // 1. totals and the mode decision
+  {
+    unsigned long long T = 0, O = 0;
+    for (uint32_t i = cb * kPlanThreads + tid; i < n; i += nb * kPlanThreads) {
+      const unsigned long long x = P.stats[i];
+      T += x & (kOccOne - 1);
+      O += x >> kOccShift;
+    }
+    plan_block_scan<unsigned long long>(T, s_u64, 0ull, add, T);
+    plan_block_scan<unsigned long long>(O, s_u64, 0ull, add, O);
+    if (tid == 0) {
+      atomicAdd(&S->totals[0], T);
+      atomicAdd(&S->totals[1], O);
+    }
+  }
+  grid.sync();
+  const unsigned long long T = S->totals[0], O = S->totals[1];
+  const bool fits = P.shard_world > 1 || T + 2 * O + 2ull * n + 2 < (1ull << 32);
+  const bool short_rows = O > 0 && T <= (unsigned long long)kStreamMeanMax * O;
+  bool sm = fits && short_rows;
+  if (P.force == 1) sm = false;
+  if (P.force == 2) sm = fits;
+  if (cb == 0 && tid == 0) {
+    P.out->total_terms = T;
+    P.out->occ_sum = O;
+    P.out->stream_mode = sm;
+    P.out->overflow = (!fits && short_rows && P.force == 0) ? 2u : 0u;
+  }
+  if (!sm) return;
+  const uint64_t unit_terms = P.unit_terms ? P.unit_terms : max(1ull << 16, T / ((uint64_t)kNumSMs * 8));
+  const double inv_ut = (double)kPlanS / (double)unit_terms;
+  const uint32_t rows_max = P.col_bits >= 32 ? 1u : ((1u << (32 - P.col_bits)) - 1u);
+  const uint64_t y = (kPlanS + rows_max - 1) / rows_max;
+  const uint64_t step = kPlanS - kPlanS / 4 - y - 1024;
+  const double inv_step = 1.0 / (double)step;
+  auto bucket = [inv_step](unsigned long long p) { return (long long)((double)p * inv_step); };
+  const uint64_t dense_cap = kStreamDenseCap, hash_cap = kStreamHashCap;
+  auto units_of = [&](uint64_t t, uint64_t occ) -> uint32_t {
+    uint64_t u = (t + unit_terms - 1) / unit_terms;
+    const uint64_t uo = (occ + kStreamUnitOcc - 1) / kStreamUnitOcc;
+    if (uo > u) u = uo;
+    return (uint32_t)(u < 1 ? 1 : (u > 65535 ? 65535 : u));
+  };
+  // sum / max of the per-CTA values before this CTA (thread 0 -> s_bc)
+  auto before_sum = [&](const unsigned long long* a, unsigned long long& all) -> unsigned long long {
+    if (tid == 0) {
+      unsigned long long s = 0, t = 0;
+      for (uint32_t k = 0; k < nb; ++k) {
+        if (k == cb) s = t;
+        t += a[k];
+      }
+      s_bc[0] = s;
+      s_bc[1] = t;
+    }
+    __syncthreads();
+    const unsigned long long r = s_bc[0];
+    all = s_bc[1];
+    __syncthreads();
+    return r;
+  };
+  auto before_max = [&](const long long* a) -> long long {
+    if (tid == 0) {
+      long long m = -1;
+      for (uint32_t k = 0; k < cb; ++k) m = a[k] > m ? a[k] : m;
+      s_bc[2] = (unsigned long long)m;
+    }
+    __syncthreads();
+    const long long r = (long long)s_bc[2];
+    __syncthreads();
+    return r;
+  };
+  // 2. rows [r0, r1) of this CTA
+  const uint32_t r0 = (uint32_t)((uint64_t)n * cb / nb), r1 = (uint32_t)((uint64_t)n * (cb + 1) / nb);
+  const uint32_t base = r0, cn = r1 - r0;
+  for (uint32_t qb = 0; qb < kPlanRowsPerThread; qb += 8) {
+    unsigned long long st8[8];
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) {
+      const uint32_t k = tid + (qb + q) * kPlanThreads;
+      st8[q] = k < cn ? P.stats[base + k] : 0ull;
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) {
+      const uint32_t k = tid + (qb + q) * kPlanThreads;
+      if (k >= cn) break;
+      const uint32_t i = base + k;
+      const uint64_t t = st8[q] & (kOccOne - 1);
+      const uint64_t w = P.upper ? (uint64_t)(n - 1 - i) : (uint64_t)n;
+      s_t[k] = (uint32_t)t;
+      uint32_t rec = 0;
+      if (t) {
+        const uint64_t b = t < w ? t : w;
+        const bool hfit = b <= hash_cap && t <= unit_terms;
+        if (w <= dense_cap && ((8 * t >= w && w >= kMinDenseWidth) || !hfit)) {
+          rec = 1;
+        } else if (!hfit) {
+          rec = 2 | (uint32_t)((w + dense_cap - 1) / dense_cap) << 3;
+          atomicOr(&S->has_win, 1u);
+        } else {
+          const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
+          const uint64_t xt = (uint64_t)((double)t * inv_ut) + 1;
+          const uint64_t x = xb > xt ? xb : xt;
+          rec = x > kPlanS / 4 ? 3u : (4u | (uint32_t)x << 3);
+        }
+      }
+      s_rec[k] = rec;
+    }
+  }
+  __syncthreads();
+  const uint32_t lo = min(cn, tid * kPlanRowsPerThread), hi = min(cn, lo + kPlanRowsPerThread);
+  unsigned long long pw = 0;
+  for (uint32_t k = lo; k < hi; ++k) {
+    const uint32_t r = s_rec[k];
+    pw += ((r & 7) == 4 ? (r >> 3) : 0) + y;
+  }
+  unsigned long long chunk_w;
+  const unsigned long long pw_ex = plan_block_scan<unsigned long long>(pw, s_u64, 0ull, add, chunk_w);
+  if (tid == 0) S->cw[cb] = chunk_w;
+  grid.sync();
+  unsigned long long all_w;
+  const unsigned long long c_p = before_sum(S->cw, all_w);
+  const unsigned long long pbase = c_p + pw_ex;
+  long long lastb = -1;
+  {
+    unsigned long long p = pbase;
+    for (uint32_t k = lo; k < hi; ++k) {
+      const uint32_t r = s_rec[k];
+      if ((r & 7) == 4) lastb = bucket(p);
+      p += ((r & 7) == 4 ? (r >> 3) : 0) + y;
+    }
+  }
+  long long carryb = plan_block_scan<long long>(lastb, s_i64, -1ll, mx, totl);
+  if (tid == 0) S->lastb[cb] = totl;
+  grid.sync();
+  const long long c_bucket = before_max(S->lastb);
+  carryb = carryb > c_bucket ? carryb : c_bucket;
+  unsigned long long cnt = 0;
+  {
+    unsigned long long p = pbase;
+    long long lb = carryb;
+    for (uint32_t k = lo; k < hi; ++k) {
+      const uint32_t r = s_rec[k], c = r & 7;
+      if (c == 1 || c == 3) cnt += 1;
+      else if (c == 2) cnt += r >> 3;
+      else if (c == 4) {
+        const long long bk = bucket(p);
+        if (bk != lb) cnt += 1;
+        lb = bk;
+      }
+      p += (c == 4 ? (r >> 3) : 0) + y;
+    }
+  }
+  unsigned long long chunk_tiles;
+  const unsigned long long t_ex = plan_block_scan<unsigned long long>(cnt, s_u64, 0ull, add, chunk_tiles);
+  if (tid == 0) S->ct[cb] = chunk_tiles;
+  grid.sync();
+  unsigned long long all_tiles;
+  const unsigned long long c_tiles = before_sum(S->ct, all_tiles);
+  if (all_tiles > P.tile_cap) {
+    if (cb == 0 && tid == 0) P.out->overflow = 1;
+    return;
+  }
+  const unsigned long long tbase = c_tiles + t_ex;
+  long long last_lt = -1, last_row0 = -1;
+  {
+    unsigned long long p = pbase;
+    long long lb = carryb;
+    uint32_t id = (uint32_t)tbase;
+    for (uint32_t k = lo; k < hi; ++k) {
+      const uint32_t r = s_rec[k], c = r & 7, i = base + k;
+      if (c == 1 || c == 3) {
+        const uint64_t t = s_t[k];
+        Tile tl{};
+        tl.row0 = i;
+        tl.row1 = i + 1;
+        tl.c1 = n;
+        tl.terms = t;
+        if (c == 1) {
+          tl.c0 = P.upper ? i + 1 : 0;
+          tl.mode = P.filter ? 0 : 2;
+          tl.width = P.upper ? n - 1 - i : n;
+          const uint64_t occ = P.stats[i] >> kOccShift;
+          tl.n_units = units_of(t, (P.safe && tl.mode == 0 && t > occ) ? t : occ);
+        } else {
+          tl.mode = 1;
+          tl.n_units = 1;
+        }
+        P.tiles[id] = tl;
+        P.item_info[i] = make_uint2(id | (tl.mode == 2 ? kEntFlag : 0u),
+                                    stream_base(tl, i, n, P.col_bits, P.upper != 0));
+        ++id;
+      } else if (c == 2) {
+        const uint64_t t = s_t[k];
+        const uint32_t col_lo = P.upper ? i + 1 : 0;
+        const uint32_t nwin = r >> 3;
+        for (uint32_t q = 0; q < nwin; ++q) {
+          Tile tl{};
+          tl.row0 = i;
+          tl.row1 = i + 1;
+          tl.c0 = col_lo + q * (uint32_t)dense_cap;
+          tl.c1 = (uint32_t)min((uint64_t)n, (uint64_t)tl.c0 + dense_cap);
+          tl.mode = 0;
+          tl.nwin = q == 0 ? nwin : 0;
+          tl.width = tl.c1 - tl.c0;
+          tl.terms = t / nwin + 1;
+          const uint64_t occ = P.stats[i] >> kOccShift;
+          tl.n_units = units_of(tl.terms, (P.safe && tl.terms > occ) ? tl.terms : occ);
+          P.tiles[id + q] = tl;
+        }
+        P.item_info[i] = make_uint2(id | kWinFlag, 0u);
+        id += nwin;
+      } else if (c == 4) {
+        const long long bk = bucket(p);
+        if (bk != lb) {
+          Tile tl{};
+          tl.row0 = i;
+          tl.row1 = i + 1;
+          tl.c1 = n;
+          tl.mode = 1;
+          tl.n_units = 1;
+          P.tiles[id] = tl;
+          last_lt = id;
+          last_row0 = i;
+          ++id;
+        }
+        lb = bk;
+      } else {
+        P.item_info[i] = make_uint2(kNone, 0u);
+      }
+      p += (c == 4 ? (r >> 3) : 0) + y;
+    }
+  }
+  long long carry_lt = plan_block_scan<long long>(last_lt, s_i64, -1ll, mx, totl);
+  if (tid == 0) S->llt[cb] = totl;
+  long long carry_row0 = plan_block_scan<long long>(last_row0, s_i64, -1ll, mx, totl);
+  if (tid == 0) S->lrow[cb] = totl;
+  grid.sync();
+  {
+    const long long c_lt = before_max(S->llt), c_lrow0 = before_max(S->lrow);
+    carry_lt = carry_lt > c_lt ? carry_lt : c_lt;
+    carry_row0 = carry_row0 > c_lrow0 ? carry_row0 : c_lrow0;
+  }
+  {
+    unsigned long long p = pbase;
+    long long lb = carryb, cur = carry_lt, row0 = carry_row0;
+    uint32_t id = (uint32_t)tbase;
+    long long acc_tile = -1;
+    unsigned long long acc_terms = 0;
+    uint32_t acc_row1 = 0;
+    auto flush = [&]() {
+      if (acc_tile >= 0) {
+        Tile* tl = P.tiles + acc_tile;
+        atomicMax(&tl->row1, acc_row1);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&tl->terms), acc_terms);
+      }
+    };
+    for (uint32_t k = lo; k < hi; ++k) {
+      const uint32_t r = s_rec[k], c = r & 7, i = base + k;
+      if (c == 1 || c == 3) ++id;
+      else if (c == 2) id += r >> 3;
+      else if (c == 4) {
+        const long long bk = bucket(p);
+        if (bk != lb) {
+          cur = id++;
+          row0 = i;
+        }
+        lb = bk;
+        if (cur != acc_tile) {
+          flush();
+          acc_tile = cur;
+          acc_terms = 0;
+        }
+        acc_terms += s_t[k];
+        acc_row1 = i + 1;
+        P.item_info[i] = make_uint2((uint32_t)cur, (i - (uint32_t)row0) << P.col_bits);
+      }
+      p += (c == 4 ? (r >> 3) : 0) + y;
+    }
+    flush();
+  }
+  grid.sync();
+  const uint32_t nt = (uint32_t)all_tiles;
+  const uint32_t ta = (uint32_t)((uint64_t)nt * cb / nb), tb = (uint32_t)((uint64_t)nt * (cb + 1) / nb);
+  const uint32_t tseg = (tb - ta + kPlanThreads - 1) / kPlanThreads;
+  const uint32_t tlo = min(tb, ta + tid * tseg), thi = min(tb, tlo + tseg);
+  if (P.shard_world > 1) {
+    auto is_window = [&](const Tile& tl) {
+      return tl.mode == 0 && tl.row1 - tl.row0 == 1 && tl.width < (P.upper ? n - 1 - tl.row0 : n);
+    };
+    auto words_of = [&](const Tile& tl) -> unsigned long long {
+      if (is_window(tl)) return 2 + (tl.nwin ? (P.stats[tl.row0] & (kOccOne - 1)) : 0ull);
+      return 2 + (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms);
+    };
+    auto cost = [&](const Tile& tl) -> unsigned long long {
+      if (is_window(tl) && tl.n_units == 1 && tl.terms <= kSparseWindowWords) {
+        Tile h = tl;
+        h.mode = 1;
+        return tile_cost(h, stream_hash_slots(tl.terms));
+      }
+      return tile_cost(tl, stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap));
+    };
+    bool done = false;
+    for (int pass = 0; pass < 3 && !done; ++pass) {
+      auto metric = [&](const Tile& tl) -> unsigned long long {
+        if (pass == 0) return cost(tl);
+        return words_of(tl) + (pass == 1 ? 2048ull * (tl.n_units ? tl.n_units : 1) : 0ull);
+      };
+      unsigned long long tsum = 0, ctot;
+      for (uint32_t t = tlo; t < thi; ++t) tsum += metric(P.tiles[t]);
+      const unsigned long long pre_l = plan_block_scan<unsigned long long>(tsum, s_u64, 0ull, add, ctot);
+      if (tid == 0) S->ssum[pass][cb] = ctot;
+      grid.sync();
+      unsigned long long all;
+      unsigned long long pre = before_sum(S->ssum[pass], all) + pre_l;
+      for (uint32_t t = tlo; t < thi; ++t) {
+        const unsigned long long c = metric(P.tiles[t]);
+        const unsigned long long ow = all ? (pre + c / 2) * P.shard_world / all : 0;
+        P.tiles[t].slab_base = ow < P.shard_world - 1 ? ow : P.shard_world - 1;
+        pre += c;
+      }
+      grid.sync();
+      {
+        uint32_t cur = kNone;
+        unsigned long long acc = 0;
+        for (uint32_t t = tlo; t < thi; ++t) {
+          const Tile& tl = P.tiles[t];
+          uint32_t ow;
+          if (is_window(tl) && tl.nwin == 0 && t > tlo) {
+            ow = cur;
+          } else {
+            uint32_t f = t;
+            if (is_window(tl))
+              while (P.tiles[f].nwin == 0 && f > 0) --f;
+            ow = (uint32_t)P.tiles[f].slab_base;
+          }
+          if (ow != cur) {
+            if (cur != kNone) atomicAdd(&S->sow[pass][cur < kMaxShardCheck ? cur : kMaxShardCheck - 1], acc);
+            cur = ow;
+            acc = 0;
+          }
+          acc += words_of(tl);
+        }
+        if (cur != kNone) atomicAdd(&S->sow[pass][cur < kMaxShardCheck ? cur : kMaxShardCheck - 1], acc);
+      }
+      grid.sync();
+      unsigned long long mxw = 0;
+      for (uint32_t k = tid; k < kMaxShardCheck; k += kPlanThreads)
+        mxw = S->sow[pass][k] > mxw ? S->sow[pass][k] : mxw;
+      plan_block_scan<long long>((long long)mxw, s_i64, 0ll, mx, totl);
+      if (totl + 2 < (1ll << 32)) {
+        done = true;
+      } else if (pass == 2) {
+        if (cb == 0 && tid == 0) P.out->overflow = 2;
+        return;
+      }
+    }
+    {
+      uint32_t cur = kNone;
+      for (uint32_t t = tlo; t < thi; ++t) {
+        Tile& tl = P.tiles[t];
+        if (!(is_window(tl) && tl.nwin == 0 && t > tlo)) {
+          uint32_t f = t;
+          if (is_window(tl))
+            while (P.tiles[f].nwin == 0 && f > 0) --f;
+          cur = (uint32_t)P.tiles[f].slab_base;
+        }
+        if (cur != P.shard_rank) tl.n_units = 0;
+      }
+    }
+    grid.sync();
+    for (uint32_t t = tlo; t < thi; ++t) P.tiles[t].slab_base = 0;
+    for (uint32_t i = cb * kPlanThreads + tid; i < n; i += nb * kPlanThreads) {
+      const uint2 tv = P.item_info[i];
+      if (tv.x != kNone && P.tiles[tv.x & kTileMask].n_units == 0) P.item_info[i] = make_uint2(kNone, 0u);
+    }
+    grid.sync();
+  }
+  // 4. units, slabs, split list, reduce chunks, output capacity
+  for (uint32_t t = tlo; t < thi; ++t) {
+    Tile& tl = P.tiles[t];
+    if (tl.mode == 1) tl.width = stream_hash_slots(tl.terms < hash_cap ? tl.terms : hash_cap);
+  }
+  auto nu_of = [&](uint32_t t) { return P.tiles[t].n_units; };
+  auto wd_of = [&](uint32_t t) { return P.tiles[t].mode != 1 ? P.tiles[t].width : 0xFFFFFFFFu; };
+  unsigned long long a[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // slab, split, single, rc, cap, units, words, terms
+  for (uint32_t t = tlo; t < thi; ++t) {
+    const uint32_t nu_t = nu_of(t), wd = wd_of(t);
+    if (nu_t == 0) continue;
+    {
+      const Tile& tl = P.tiles[t];
+      const bool win = tl.mode == 0 && tl.row1 - tl.row0 == 1 &&
+                       tl.width < (P.upper ? n - 1 - tl.row0 : n);
+      if (win) a[6] += tl.nwin ? (P.stats[tl.row0] & (kOccOne - 1)) : 0ull;
+      else a[6] += tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms;
+      a[6] += 2;
+      a[7] += tl.terms;
+    }
+    a[4] += tile_out_cap(P.tiles[t], kStreamHashCap, n, P.upper != 0);
+    a[5] += nu_t;
+    if (nu_t > 1) {
+      a[0] += nu_t;
+      a[1] += 1;
+      a[3] += ((wd < kSHalf ? wd : kSHalf) + kReduceSlots - 1) / kReduceSlots;
+    } else {
+      a[2] += 1;
+    }
+  }
+  unsigned long long b_l[8], c_tot[8];
+  for (int q = 0; q < 8; ++q) {
+    b_l[q] = plan_block_scan<unsigned long long>(a[q], s_u64, 0ull, add, c_tot[q]);
+    if (tid == 0) S->u8[cb][q] = c_tot[q];
+  }
+  grid.sync();
+  unsigned long long b_c[8], tot[8];
+  if (tid < 8) {
+    unsigned long long s = 0, t = 0;
+    for (uint32_t k = 0; k < nb; ++k) {
+      if (k == cb) s = t;
+      t += S->u8[k][tid];
+    }
+    s_u64[tid] = s;
+    s_u64[8 + tid] = t;
+  }
+  __syncthreads();
+  for (int q = 0; q < 8; ++q) {
+    b_c[q] = s_u64[q];
+    tot[q] = s_u64[8 + q];
+  }
+  __syncthreads();
+  const unsigned long long n_slabs = tot[0], n_split = tot[1], n_rc = tot[3], cap = tot[4], nu = tot[5];
+  const unsigned long long own_words = tot[6], own_terms = tot[7];
+  if (nu > P.unit_cap || n_rc > P.rc_cap || own_words + 2 >= (1ull << 32)) {
+    if (cb == 0 && tid == 0) P.out->overflow = 1;
+    return;
+  }
+  constexpr int kFracBins = 64;
+  {
+    uint64_t sb = b_c[0] + b_l[0], sp = b_c[1] + b_l[1], rc = b_c[3] + b_l[3];
+    for (uint32_t t = tlo; t < thi; ++t) {
+      const uint32_t nu_t = nu_of(t), width = wd_of(t);
+      if (nu_t > 1) {
+        P.tiles[t].slab_base = sb;
+        sb += nu_t;
+        P.split[sp++] = t;
+        const uint32_t dw = width < kSHalf ? width : kSHalf;
+        for (uint32_t c0 = 0; c0 < dw; c0 += kReduceSlots) P.reduce_chunks[rc++] = make_uint2(t, c0);
+      }
+    }
+  }
+  for (uint32_t t = tlo; t < thi; ++t) {
+    const uint32_t nu_t = nu_of(t);
+    if (nu_t > 1)
+      for (uint32_t u = 0; u < nu_t; ++u) atomicAdd(&S->bins[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
+  }
+  grid.sync();
+  if (cb == 0 && tid == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < kFracBins; ++k) {
+      S->cur[k] = run;
+      run += S->bins[k];
+    }
+    S->cur[kFracBins] = run;
+  }
+  grid.sync();
+  for (uint32_t t = tlo; t < thi; ++t) {
+    const uint32_t nu_t = nu_of(t);
+    if (nu_t > 1) {
+      for (uint32_t u = 0; u < nu_t; ++u) {
+        const uint32_t pos = atomicAdd(&S->cur[(uint64_t)(2 * u + 1) * kFracBins / (2 * nu_t)], 1u);
+        P.units[pos] = Unit{t, u};
+      }
+    }
+  }
+  {
+    uint64_t pos = S->cur[kFracBins] + b_c[2] + b_l[2];  // unchanged by the placements above: bins < 64
+    for (uint32_t t = tlo; t < thi; ++t)
+      if (nu_of(t) == 1) P.units[pos++] = Unit{t, 0};
+  }
+  const bool known = (!P.filter || P.own) && !S->has_win;
+  if (known)
+    for (uint32_t t = tlo; t < thi; ++t) {
+      const Tile& tl = P.tiles[t];
+      P.tile_words[t] = tl.n_units == 0 ? 0ull : (tl.mode == 2 ? 2 * (P.stats[tl.row0] >> kOccShift) : tl.terms);
+    }
+  if (cb == 0 && tid == 0) {
+    P.out->words_known = known;
+    P.out->pad0 = 0;
+    P.out->pad1 = 0;
+    P.out->max_entries = cap;
+    P.out->own_words = own_words + 2;
+    P.out->own_terms = own_terms;
+    P.out->n_slabs = n_slabs;
+    P.out->n_tiles = nt;
+    P.out->n_units = (uint32_t)nu;
+    P.out->n_split = (uint32_t)n_split;
+    P.out->n_reduce_chunks = (uint32_t)n_rc;
+  }
+}
+
 }  // namespace
 
 // =============================================================== host side
@@ -3969,10 +4508,23 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
       PA.shard_world = J->shard_world;
       PA.out = reinterpret_cast<PlanOut*>(db + o_out);
       JCUDA(cudaMemsetAsync(db + o_misc, 0, 32, st));
-      JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kPlanChunk * 8)));
       if (dbg_t) JCUDA(cudaEventRecord(dbg_ev[1], st));
-      k_plan_stream<<<1, kPlanThreads, kPlanChunk * 8, st>>>(PA);
+      PlanScratch* d_ps = nullptr;
+      if (n_items <= (uint64_t)kNumSMs * kPlanChunk && !getenv("CROP_PLAN_SINGLE_CTA")) {
+        // one CTA per SM (cooperative launch: all resident, grid-wide syncs)
+        JCUDA(cudaMallocAsync(&d_ps, sizeof(PlanScratch), st));
+        JCUDA(cudaMemsetAsync(d_ps, 0, sizeof(PlanScratch), st));
+        JCUDA(cudaFuncSetAttribute(k_plan_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kPlanChunk * 8)));
+        void* args[] = {(void*)&PA, (void*)&d_ps};
+        JCUDA(cudaLaunchCooperativeKernel((void*)k_plan_coop, dim3(kNumSMs), dim3(kPlanThreads), args,
+                                          kPlanChunk * 8, st));
+        JCUDA(cudaFreeAsync(d_ps, st));
+      } else {
+        JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kPlanChunk * 8)));
+        k_plan_stream<<<1, kPlanThreads, kPlanChunk * 8, st>>>(PA);
+      }
       JCUDA(cudaGetLastError());
       crop_count_launches(1);
       if (dbg_t) JCUDA(cudaEventRecord(dbg_ev[2], st));

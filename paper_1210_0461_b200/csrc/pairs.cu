@@ -1811,10 +1811,10 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 2)
     k_stream_scatter(StreamRouteArgs A, const uint32_t* __restrict__ bounds, uint32_t n_chunks) {
   extern __shared__ __align__(16) unsigned char smem[];
   int64_t* s_off = reinterpret_cast<int64_t*>(smem);                          // MAXTX + 1
-  uint32_t* s_tile = reinterpret_cast<uint32_t*>(s_off + MAXTX + 1);     // parked rows
-  uint32_t* s_rank = s_tile + PARK;
-  uint32_t* s_meta = s_rank + PARK;                                      // n | entry << 31
-  uint32_t* s_bp = s_meta + PARK;                                        // word rows: base
+  // parked rows: entry << 31 | n << 16 | (absolute rank ? 0x8000 : shared tile id), or kNone
+  uint32_t* s_tm = reinterpret_cast<uint32_t*>(s_off + MAXTX + 1);
+  uint32_t* s_rank = s_tm + PARK;
+  uint32_t* s_bp = s_rank + PARK;                                        // word rows: base
   uint32_t* s_job = s_bp + PARK;                                         // per warp 128 words
   uint32_t* s_misc = s_job + THREADS / 32 * 128;
   const uint32_t ns = min(A.n_tiles, A.scat_ns);
@@ -1837,25 +1837,26 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 2)
                        [&](int64_t g, const Pos& q, uint32_t, uint2 tv) {
         if (!q.valid) return;
         const uint32_t x = (uint32_t)(g - g_lo);
-        uint32_t tile = kNone;
+        uint32_t tm = kNone;
         if (tv.x != kNone && (UPPER ? q.p + 1 < q.L : q.L > 0)) {
-          const uint32_t n = UPPER ? q.L - 1 - q.p : q.L;
+          const uint32_t n = UPPER ? q.L - 1 - q.p : q.L;  // < 2^15 (kMaxLen)
           const bool ent = (tv.x & kEntFlag) != 0;
-          tile = tv.x & kTileMask;
+          const uint32_t tile = tv.x & kTileMask;
           const uint32_t units = ent ? 2u : n;
           uint32_t r;
-          if (tile < ns) {
+          if (tile < ns) {  // ns < 2^15
             r = atomicAdd(&s_cnt[tile], units);
             if (r == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = (uint16_t)tile;
+            tm = tile;
           } else {
             r = (uint32_t)atomicAdd(&A.tile_cursor[tile], (unsigned long long)units);
-            tile |= kWinFlag;  // rank is already absolute
+            tm = 0x8000u;  // rank is already absolute
           }
+          tm |= n << 16 | (ent ? 0x80000000u : 0u);
           s_rank[x] = r;
-          s_meta[x] = n | (ent ? 0x80000000u : 0u);
           s_bp[x] = tv.y;
         }
-        s_tile[x] = tile;
+        s_tm[x] = tm;
       });
       __syncthreads();
       const uint32_t n_touch = s_misc[0];
@@ -1877,10 +1878,11 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : 2)
           const uint32_t x = x0 + lane;
           uint32_t tile = kNone, pos = 0, meta = 0;
           if (x < npos) {
-            tile = s_tile[x];
-            if (tile != kNone) {
-              pos = (tile & kWinFlag) ? s_rank[x] : s_cnt[tile] + s_rank[x];
-              meta = s_meta[x];
+            const uint32_t tm = s_tm[x];
+            if (tm != kNone) {
+              tile = tm & 0xFFFFu;
+              pos = (tm & 0x8000u) ? s_rank[x] : s_cnt[tm & 0x7FFFu] + s_rank[x];
+              meta = (tm >> 16 & 0x7FFFu) | (tm & 0x80000000u);
             }
           }
           const uint64_t g = (uint64_t)g_lo + x;
@@ -4009,7 +4011,7 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
           J->offsets, J->n_tx, n_chunks, band, bounds);
       CROP_LAUNCH_CHECK();
       if (two) {
-        const size_t fixed = (size_t)(kScatMaxTx2 + 1) * 8 + (size_t)kScatPark2 * 16 + 16 + 512 / 32 * 128 * 4;
+        const size_t fixed = (size_t)(kScatMaxTx2 + 1) * 8 + (size_t)kScatPark2 * 12 + 16 + 512 / 32 * 128 * 4;
         const size_t budget = 112 * 1024 - fixed;
         R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
         const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;
@@ -4021,7 +4023,7 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
         CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(112 * 1024)));
         kern<<<(int)std::min<uint32_t>(2 * kNumSMs, n_chunks), 512, smem, st>>>(R, bounds, n_chunks);
       } else {
-        const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 16 + 16 + kPassThreads / 32 * 128 * 4;
+        const size_t fixed = (size_t)(kScatMaxTx + 1) * 8 + (size_t)kScatPark * 12 + 16 + kPassThreads / 32 * 128 * 4;
         const size_t budget = 227 * 1024 - fixed;
         R.scat_ns = (uint32_t)std::min<size_t>(std::min<size_t>(nt, kTileSmem), budget / 6 - 2);
         const size_t smem = fixed + (((size_t)R.scat_ns + 1) & ~(size_t)1) * 6;

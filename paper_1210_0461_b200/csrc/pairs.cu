@@ -4519,8 +4519,11 @@ extern "C" int crop_pairs_create_ex(const int64_t* offsets, const uint32_t* item
         JCUDA(cudaFuncSetAttribute(k_plan_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(kPlanChunk * 8)));
         void* args[] = {(void*)&PA, (void*)&d_ps};
-        JCUDA(cudaLaunchCooperativeKernel((void*)k_plan_coop, dim3(kNumSMs), dim3(kPlanThreads), args,
-                                          kPlanChunk * 8, st));
+        // as few CTAs as the row ranges allow: the grid syncs dominate a
+        // small plan (c2: 16 CTAs of 3,125 rows; c3 chunks: 123 CTAs)
+        const uint32_t pb = (uint32_t)std::max<uint64_t>(16, ((uint64_t)n_items + kPlanChunk - 1) / kPlanChunk);
+        JCUDA(cudaLaunchCooperativeKernel((void*)k_plan_coop, dim3(std::min<uint32_t>(pb, kNumSMs)),
+                                          dim3(kPlanThreads), args, kPlanChunk * 8, st));
         JCUDA(cudaFreeAsync(d_ps, st));
       } else {
         JCUDA(cudaFuncSetAttribute(k_plan_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,

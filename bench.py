@@ -359,9 +359,12 @@ def run_ours(args, rank, world):
         mode_name = f"entry, {stats[5]} sub-shards per GPU"
     else:
         mode_name = "stream" if stream_mode else "entry"
-    kern = {"plan": "k_item_terms + host tile plan + uploads",
-            "route": "k_stream_count + k_scan_u64" if stream_mode else "k_route",
-            "write": "k_stream_write" if stream_mode else "k_tile_entries",
+    kern = {"plan": ("k_item_terms + k_plan_coop (device planner) + plan read-back" if stream_mode
+                     else "k_item_terms + host tile plan + uploads"),
+            "route": "k_scan_u64 (+ k_stream_count when word totals are unknown)" if stream_mode
+                     else "k_route",
+            "write": "k_chunk_bounds + k_stream_scatter (or k_stream_write)" if stream_mode
+                     else "k_tile_entries",
             "count": "k_count_stream + k_reduce_slabs" if stream_mode else "k_count"}
     roofline = {"bound": "hbm", "kernel": "counting path: " + " -> ".join(kern[k] for k in
                                                                           ("plan", "route", "write", "count")),

@@ -230,26 +230,45 @@ int crop_topk(const uint32_t* row, const uint32_t* col, const uint32_t* count,
  * merges each chunk's exact entries into them:
  *   crop_ss_index  builds an open-addressing index over the n record keys
  *                  (slots uint64[n_slots]: hash fingerprint << 32 | record;
- *                  n_slots a power of two >= 2n)
- *   crop_ss_merge  for each chunk entry (row, col, e): a recorded key adds e
- *                  to its record's count; an unrecorded key becomes a
- *                  candidate (mu[b] + e, over mu[b]), b = (h_row[row] +
- *                  h_col[col]) mod kappa, appended behind the records at
- *                  *d_n_out (in: the record count; out: records +
- *                  candidates). The arrays hold records + max_entries.
- *                  *d_saturated is set when a count would pass 2^32 - 1.
+ *                  n_slots a power of two >= 2n) and, when bloom is not
+ *                  NULL, a Bloom filter over the same keys (bloom_words
+ *                  64-bit words, a power of two; four bits of one word per
+ *                  key) that answers most misses from L2
+ *   crop_ss_probe  pass 1 over the chunk entries (row, col, e): a recorded
+ *                  key adds e to its record's count (rec_count, in place); an
+ *                  unrecorded key (a miss) sets bit e of missbits and counts
+ *                  in hist[b * 16 + min(e, 15)], b = (h_row[row] + h_col[col])
+ *                  mod kappa. Then per bucket the cut: cut[b] = the largest
+ *                  weight with at least `capacity` misses at or above it (0:
+ *                  keep every miss) -- a miss below it cannot be among the
+ *                  bucket's `capacity` largest. d_meta[0] = misses at or
+ *                  above their cut (the candidates), d_meta[1] = the
+ *                  smallest cut. hist: uint32[kappa * 16], cut: uint32[kappa],
+ *                  missbits: uint32[ceil(max_entries / 32)].
+ *   crop_ss_append pass 2: every miss at or above its bucket's cut becomes a
+ *                  candidate (mu[b] + e, over mu[b]) appended behind the
+ *                  records at *d_n_out (in: the record count; out: records +
+ *                  candidates). *d_saturated is set when a count would pass
+ *                  2^32 - 1.
  *   crop_ss_keep   the entries a selection marked (mask[e] != 0, e <
  *                  *d_n) appended to the out arrays; *d_n_out = their number.
  * The caller keeps each bucket's l largest of records + candidates
  * (crop_bucket_topk, then crop_ss_keep) and sets mu[b] to the l-th count of
  * full buckets. */
 int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t n, unsigned long long* slots,
-                  uint64_t n_slots, void* stream);
-int crop_ss_merge(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
+                  uint64_t n_slots, unsigned long long* bloom, uint64_t bloom_words, void* stream);
+int crop_ss_probe(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
                   const uint64_t* d_n_entries, uint64_t max_entries, const unsigned long long* slots,
-                  uint64_t n_slots, const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
-                  const uint32_t* mu, uint32_t* row, uint32_t* col, uint32_t* count, uint32_t* over,
-                  uint64_t* d_n_out, unsigned int* d_saturated, void* stream);
+                  uint64_t n_slots, const unsigned long long* bloom, uint64_t bloom_words,
+                  const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
+                  uint32_t capacity, const uint32_t* rec_row, const uint32_t* rec_col, uint32_t* rec_count,
+                  uint32_t* missbits, uint32_t* hist, uint32_t* cut, uint64_t* d_meta,
+                  unsigned int* d_saturated, void* stream);
+int crop_ss_append(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
+                   const uint64_t* d_n_entries, uint64_t max_entries, const uint32_t* missbits,
+                   const uint32_t* cut, const uint64_t* d_meta, const uint32_t* h_row, const uint32_t* h_col,
+                   uint32_t kappa, const uint32_t* mu, uint32_t* row, uint32_t* col, uint32_t* count,
+                   uint32_t* over, uint64_t* d_n_out, unsigned int* d_saturated, void* stream);
 int crop_ss_keep(const uint8_t* mask, const uint64_t* d_n, uint64_t max_n, const uint32_t* row,
                  const uint32_t* col, const uint32_t* count, const uint32_t* over, uint32_t* out_row,
                  uint32_t* out_col, uint32_t* out_count, uint32_t* out_over, uint64_t* d_n_out, void* stream);

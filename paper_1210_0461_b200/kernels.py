@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .errors import ConfigError, InputError, ResourceCapError
+from .errors import ConfigError, DeviceError, InputError, ResourceCapError
 
 TOPK_EXACT_BINS = 2048       # topk histogram: exact below, 2^-10 relative above
 TOPK_BINS = 2048 + 21 * 1024  # common.cuh kTopkBins
@@ -504,28 +504,53 @@ class StreamingSummaries:
         while slots < 2 * n_rec:
             slots <<= 1
         index = torch.empty(slots, dtype=torch.int64, device=dev)
+        # Bloom filter over the record keys: at most 4 keys per 64-bit word up
+        # to 2^23 words (64 MB, L2-resident; c3: 9 keys per word); none for a
+        # handful of records
+        bloom_words = 0
+        if n_rec >= 4096:
+            bloom_words = 1024
+            while bloom_words < n_rec // 4 and bloom_words < (1 << 23):
+                bloom_words <<= 1
+        bloom = torch.empty(bloom_words, dtype=torch.int64, device=dev) if bloom_words else None
         nat.call("crop_ss_index", nat.ptr(self.row), nat.ptr(self.col), n_rec, nat.ptr(index), slots,
-                 nat.stream_ptr())
-        m = n_rec + n_e
+                 nat.ptr(bloom), bloom_words, nat.stream_ptr())
+        n_dev = getattr(ent, "n_dev", None)
+        if n_dev is None:
+            n_dev = torch.tensor([n_e], dtype=torch.int64, device=dev)
+        # pass 1: hits add to their records; misses are flagged and counted per
+        # bucket and chunk weight, which gives every bucket its cut
+        missbits = torch.empty((n_e + 31) // 32, dtype=torch.int32, device=dev)
+        hist = torch.empty(self.kappa * 16, dtype=torch.int32, device=dev)
+        cut = torch.empty(self.kappa, dtype=torch.int32, device=dev)
+        meta = torch.empty(2, dtype=torch.int64, device=dev)
+        sat = torch.zeros(1, dtype=torch.int32, device=dev)
+        nat.call("crop_ss_probe", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev), n_e,
+                 nat.ptr(index), slots, nat.ptr(bloom), bloom_words,
+                 nat.ptr(self.h_row), nat.ptr(self.h_col), self.kappa,
+                 min(self.capacity, 0xFFFFFFFF), nat.ptr(self.row), nat.ptr(self.col), nat.ptr(self.count),
+                 nat.ptr(missbits), nat.ptr(hist), nat.ptr(cut), nat.ptr(meta), nat.ptr(sat), nat.stream_ptr())
+        del index, bloom
+        n_cand = int(meta[0].item())
+        # pass 2: the misses at or above their bucket's cut, behind the records
+        m = n_rec + n_cand
         row = torch.empty(m, dtype=torch.int32, device=dev)
         col = torch.empty(m, dtype=torch.int32, device=dev)
         cnt = torch.empty(m, dtype=torch.int32, device=dev)
         over = torch.empty(m, dtype=torch.int32, device=dev)
         row[:n_rec], col[:n_rec], cnt[:n_rec], over[:n_rec] = self.row, self.col, self.count, self.over
         n_out = torch.tensor([n_rec], dtype=torch.int64, device=dev)
-        sat = torch.zeros(1, dtype=torch.int32, device=dev)
-        n_dev = getattr(ent, "n_dev", None)
-        if n_dev is None:
-            n_dev = torch.tensor([n_e], dtype=torch.int64, device=dev)
-        nat.call("crop_ss_merge", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev), n_e,
-                 nat.ptr(index), slots, nat.ptr(self.h_row), nat.ptr(self.h_col), self.kappa, nat.ptr(self.mu),
-                 nat.ptr(row), nat.ptr(col), nat.ptr(cnt), nat.ptr(over), nat.ptr(n_out), nat.ptr(sat),
-                 nat.stream_ptr())
-        del index
+        nat.call("crop_ss_append", nat.ptr(ent.row), nat.ptr(ent.col), nat.ptr(ent.count), nat.ptr(n_dev), n_e,
+                 nat.ptr(missbits), nat.ptr(cut), nat.ptr(meta), nat.ptr(self.h_row), nat.ptr(self.h_col),
+                 self.kappa, nat.ptr(self.mu), nat.ptr(row), nat.ptr(col), nat.ptr(cnt), nat.ptr(over),
+                 nat.ptr(n_out), nat.ptr(sat), nat.stream_ptr())
+        del missbits
         n_tot, saturated = (int(x) for x in torch.cat([n_out, sat.to(torch.int64)]).tolist())
         if saturated:
             raise ResourceCapError("a Space-Saving count passed 2^32 - 1")
-        self.last_candidates = n_tot - n_rec
+        if n_tot != m:
+            raise DeviceError(f"summary merge: {n_tot - n_rec} candidates appended, {n_cand} counted")
+        self.last_candidates = n_cand
         comb = DeviceEntries(row, col, cnt, None, n_tot, 0)
         comb.n_dev = n_out
         rec = torch.empty(max(n_tot, 1), dtype=torch.uint8, device=dev)

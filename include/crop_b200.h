@@ -260,7 +260,7 @@ int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t n, unsigned
 int crop_ss_probe(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
                   const uint64_t* d_n_entries, uint64_t max_entries, const unsigned long long* slots,
                   uint64_t n_slots, const unsigned long long* bloom, uint64_t bloom_words,
-                  const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
+                  uint64_t n_records, const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
                   uint32_t capacity, const uint32_t* rec_row, const uint32_t* rec_col, uint32_t* rec_count,
                   uint32_t* missbits, uint32_t* hist, uint32_t* cut, uint64_t* d_meta,
                   unsigned int* d_saturated, void* stream);

@@ -83,7 +83,7 @@ _SIGS = {
     "crop_outer_destroy": (None, [P]),
     "crop_ss_index": (i32, [P, P, u64, P, u64, P, u64, P]),
     "crop_ss_keep": (i32, [P, P, u64, P, P, P, P, P, P, P, P, P, P]),
-    "crop_ss_probe": (i32, [P, P, P, P, u64, P, u64, P, u64, P, P, u32, u32, P, P, P, P, P, P, P, P, P]),
+    "crop_ss_probe": (i32, [P, P, P, P, u64, P, u64, P, u64, u64, P, P, u32, u32, P, P, P, P, P, P, P, P, P]),
     "crop_ss_append": (i32, [P, P, P, P, u64, P, P, P, P, P, u32, P, P, P, P, P, P, P, P]),
     "crop_gen_lengths": (i32, [i64, u64, P, u32, u32, P, P]),
     "crop_gen_items": (i32, [i64, u64, u32, P, P, P, P, P]),

@@ -58,9 +58,10 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t k, uint64_t mask, uint64_t&
 // <= 0.5) is not: a chunk's misses -- 9 in 10 of its entries on c3 -- are
 // answered by one L2 sector instead of a DRAM access.
 __device__ __forceinline__ void bloom_of(uint64_t x, uint64_t wmask, uint64_t& word, unsigned long long& bits) {
-  word = (x >> 20) & wmask;
+  word = (x >> 20) & (wmask & 0x7FFFFFFFFFFFFFFFull);
   const uint32_t y = (uint32_t)(x >> 32) * 0x9E3779B1u;
-  bits = (1ull << (y & 63)) | (1ull << ((y >> 6) & 63)) | (1ull << ((y >> 12) & 63)) | (1ull << ((y >> 18) & 63));
+  bits = (1ull << (y & 63)) | (1ull << ((y >> 6) & 63));
+  if (!(wmask >> 63)) bits |= (1ull << ((y >> 12) & 63)) | (1ull << ((y >> 18) & 63));
 }
 // filter words are read with an L2 evict-last policy (the entry streams are
 // read evict-first), so the streamed chunk does not push the filter out
@@ -349,6 +350,12 @@ __global__ void __launch_bounds__(256) k_ss_keep(const uint8_t* __restrict__ mas
   }
 }
 
+// word mask of the filter; bit 63 set = two bits per key (more than 12 keys
+// per word: four bits each would fill the words)
+uint64_t bloom_wmask(uint64_t words, uint64_t n_keys) {
+  return (words - 1) | (n_keys > 12 * words ? (1ull << 63) : 0ull);
+}
+
 }  // namespace
 
 extern "C" int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t n, unsigned long long* slots,
@@ -370,7 +377,8 @@ extern "C" int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t 
   CROP_LAUNCH_CHECK();
   if (bloom) CROP_CUDA(cudaMemsetAsync(bloom, 0, bloom_words * 8, st));
   if (n) {
-    k_ss_insert<<<8 * kNumSMs, 256, 0, st>>>(row, col, n, slots, n_slots - 1, bloom, bloom ? bloom_words - 1 : 0);
+    k_ss_insert<<<8 * kNumSMs, 256, 0, st>>>(row, col, n, slots, n_slots - 1, bloom,
+                                             bloom ? bloom_wmask(bloom_words, n) : 0);
     CROP_LAUNCH_CHECK();
   }
   crop_count_launches(n ? 2 : 1);
@@ -380,7 +388,7 @@ extern "C" int crop_ss_index(const uint32_t* row, const uint32_t* col, uint64_t 
 extern "C" int crop_ss_probe(const uint32_t* erow, const uint32_t* ecol, const uint32_t* ecnt,
                              const uint64_t* d_n_entries, uint64_t max_entries, const unsigned long long* slots,
                              uint64_t n_slots, const unsigned long long* bloom, uint64_t bloom_words,
-                             const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
+                             uint64_t n_records, const uint32_t* h_row, const uint32_t* h_col, uint32_t kappa,
                              uint32_t capacity, const uint32_t* rec_row, const uint32_t* rec_col,
                              uint32_t* rec_count, uint32_t* missbits, uint32_t* hist, uint32_t* cut,
                              uint64_t* d_meta, unsigned int* d_saturated, void* stream) {
@@ -401,11 +409,13 @@ extern "C" int crop_ss_probe(const uint32_t* erow, const uint32_t* ecol, const u
       CROP_CUDA(cudaFuncSetAttribute(k_ss_probe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
       k_ss_probe<true><<<(unsigned)blocks, kProbeThreads, hist_bytes, st>>>(
           erow, ecol, ecnt, (const unsigned long long*)d_n_entries, slots, n_slots - 1, bloom,
-          bloom ? bloom_words - 1 : 0, h_row, h_col, kappa, rec_row, rec_col, rec_count, missbits, hist, d_saturated);
+          bloom ? bloom_wmask(bloom_words, n_records) : 0, h_row, h_col, kappa, rec_row, rec_col, rec_count, missbits, hist,
+          d_saturated);
     } else {
       k_ss_probe<false><<<(unsigned)blocks, kProbeThreads, 0, st>>>(
           erow, ecol, ecnt, (const unsigned long long*)d_n_entries, slots, n_slots - 1, bloom,
-          bloom ? bloom_words - 1 : 0, h_row, h_col, kappa, rec_row, rec_col, rec_count, missbits, hist, d_saturated);
+          bloom ? bloom_wmask(bloom_words, n_records) : 0, h_row, h_col, kappa, rec_row, rec_col, rec_count, missbits, hist,
+          d_saturated);
     }
     CROP_LAUNCH_CHECK();
     ++launches;

@@ -1446,6 +1446,21 @@ __device__ __forceinline__ void split_row_dest(const StreamRouteArgs& A, uint32_
   }
 }
 
+// Runs of equal destination among adjacent lanes (the windows of a sorted
+// suffix are contiguous, so a run is a window's group; a filter may cut a
+// window into several runs): the run's first lane, this lane's rank in it
+// and, for the first lane, the run's length. Replaces __match_any_sync.
+__device__ __forceinline__ void lane_runs(uint32_t dst, int& lead, uint32_t& rank, uint32_t& len) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, dst, 1);
+  const uint32_t heads = __ballot_sync(0xffffffffu, lane == 0 || prev != dst);
+  const uint32_t upto = 0xFFFFFFFFu >> (31 - lane);  // lanes <= lane
+  lead = 31 - __clz(heads & upto);
+  const uint32_t above = heads & ~upto;
+  len = (above ? (uint32_t)__ffs(above) - 1u : 32u) - (uint32_t)lead;
+  rank = (uint32_t)(lane - lead);
+}
+
 // B1: words per tile (shared counters per CTA, flushed once)
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArgs A) {
@@ -1492,10 +1507,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
           const uint32_t k = k0 + lane;
           uint32_t dst = kNone, word = 0;
           if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
-          const uint32_t grp = __match_any_sync(0xffffffffu, dst);
-          if (dst != kNone && lane == __ffs(grp) - 1) {
-            if (dst < ns) atomicAdd(&s_cnt[dst], (uint32_t)__popc(grp));
-            else atomicAdd(&A.tile_words[dst], (unsigned long long)__popc(grp));
+          int lead;
+          uint32_t rank, len;
+          lane_runs(dst, lead, rank, len);
+          if (dst != kNone && rank == 0) {
+            if (dst < ns) atomicAdd(&s_cnt[dst], len);
+            else atomicAdd(&A.tile_words[dst], (unsigned long long)len);
           }
         }
       }
@@ -1569,9 +1586,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
           uint32_t dst = kNone, word = 0;
           if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
           if (dst >= ns) dst = kNone;
-          const uint32_t grp = __match_any_sync(0xffffffffu, dst);
-          if (dst != kNone && lane == __ffs(grp) - 1)
-            if (atomicAdd(&s_cnt[dst], (uint32_t)__popc(grp)) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = dst;
+          int lead;
+          uint32_t rank, len;
+          lane_runs(dst, lead, rank, len);
+          if (dst != kNone && rank == 0)
+            if (atomicAdd(&s_cnt[dst], len) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = dst;
         }
       }
     });
@@ -1645,18 +1664,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
             const uint32_t k = k0 + lane;
             uint32_t dst = kNone, word = 0;
             if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
-            const uint32_t grp = __match_any_sync(0xffffffffu, dst);
-            if (dst != kNone) {
-              const int lead = __ffs(grp) - 1;
-              uint32_t p0 = 0;
-              if (lane == lead) {
-                const uint32_t cnt = __popc(grp);
-                p0 = dst < ns ? atomicAdd(&s_cnt[dst], cnt)
-                              : (uint32_t)atomicAdd(&A.tile_cursor[dst], (unsigned long long)cnt);
-              }
-              p0 = __shfl_sync(grp, p0, lead);
-              A.words[p0 + __popc(grp & ((1u << lane) - 1u))] = word;
-            }
+            int lead;
+            uint32_t rank, len;
+            lane_runs(dst, lead, rank, len);
+            uint32_t p0 = 0;
+            if (dst != kNone && rank == 0)
+              p0 = dst < ns ? atomicAdd(&s_cnt[dst], len)
+                            : (uint32_t)atomicAdd(&A.tile_cursor[dst], (unsigned long long)len);
+            p0 = __shfl_sync(0xffffffffu, p0, lead);
+            if (dst != kNone) A.words[p0 + rank] = word;
           }
         }
         return __ballot_sync(0xffffffffu, fast);

@@ -1461,6 +1461,55 @@ __device__ __forceinline__ void lane_runs(uint32_t dst, int& lead, uint32_t& ran
   rank = (uint32_t)(lane - lead);
 }
 
+// The suffix columns of the warp's split (column-window) / filtered rows,
+// flattened across the warp: lane state = one row occurrence (slow: it is such
+// a row; first, n = position and length of its column run), fn(dst, word) is
+// called warp-wide once per 32 columns with each lane's destination tile and
+// word (dst = kNone: none). The owner of flattened column t is found by a
+// binary search over the inclusive lengths (zero-length lanes in between);
+// every lane of a step is busy whatever the rows' lengths, where one row at
+// a time across the warp left half the lanes idle (c3: 11 warp instructions
+// per term in k_stream_write).
+template <typename Fn>
+__device__ __forceinline__ void for_slow_columns(const StreamRouteArgs& A, bool slow, uint32_t ir,
+                                                 uint32_t tx, uint32_t ty, uint32_t first, uint32_t n,
+                                                 Fn&& fn) {
+  if (!__any_sync(0xffffffffu, slow)) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t c0 = 0, nwin = 1, hr = 0;
+  if (slow) {
+    if (tx & kWinFlag) {
+      const Tile T0 = A.tiles[tx & kTileMask];
+      c0 = T0.c0;
+      nwin = T0.nwin;
+    }
+    if (A.filter) hr = A.h_row[ir];
+  }
+  const uint32_t my_n = slow ? n : 0u;
+  const uint32_t incl = warp_incl_scan(my_n);
+  const uint32_t S = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t start = first - (incl - my_n);  // position of flattened column t: t + start
+  for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+    const uint32_t t = t0 + lane;
+    int o = 0;  // lanes whose run ends at or before t
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, o + d - 1);
+      if (v <= t) o += d;
+    }
+    o &= 31;
+    const uint32_t o_start = __shfl_sync(0xffffffffu, start, o);
+    const uint32_t o_tx = __shfl_sync(0xffffffffu, tx, o);
+    const uint32_t o_ty = __shfl_sync(0xffffffffu, ty, o);
+    const uint32_t o_c0 = __shfl_sync(0xffffffffu, c0, o);
+    const uint32_t o_nwin = __shfl_sync(0xffffffffu, nwin, o);
+    const uint32_t o_hr = __shfl_sync(0xffffffffu, hr, o);
+    uint32_t dst = kNone, word = 0;
+    if (t < S) split_row_dest(A, o_tx, o_ty, o_c0, o_nwin, o_hr, A.items[t + o_start], dst, word);
+    fn(dst, word);
+  }
+}
+
 // B1: words per tile (shared counters per CTA, flushed once)
 template <bool UPPER>
 __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArgs A) {
@@ -1485,37 +1534,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
         if (t < ns) atomicAdd(&s_cnt[t], n);
         else atomicAdd(&A.tile_words[t], (unsigned long long)n);
       }
-      // split / filtered rows one at a time across the warp (as k_stream_write)
-      uint32_t sm = __ballot_sync(0xffffffffu, slow);
-      while (sm) {
-        const int r = __ffs(sm) - 1;
-        sm &= sm - 1;
-        const uint32_t ir = __shfl_sync(0xffffffffu, i, r);
-        const uint32_t tx = __shfl_sync(0xffffffffu, tv.x, r);
-        const uint32_t ty = __shfl_sync(0xffffffffu, tv.y, r);
-        const int64_t tb = __shfl_sync(0xffffffffu, q.base, r);
-        const uint32_t pr = __shfl_sync(0xffffffffu, q.p, r);
-        const uint32_t L = __shfl_sync(0xffffffffu, q.L, r);
-        uint32_t c0 = 0, nwin = 1;
-        if (tx & kWinFlag) {
-          const Tile T0 = A.tiles[tx & kTileMask];
-          c0 = T0.c0;
-          nwin = T0.nwin;
+      // split / filtered rows: their columns flattened across the warp
+      const uint32_t skip = UPPER ? q.p + 1 : 0u;
+      for_slow_columns(A, slow, i, tv.x, tv.y, (uint32_t)q.base + skip, q.L - skip,
+                       [&](uint32_t dst, uint32_t) {
+        int lead;
+        uint32_t rank, len;
+        lane_runs(dst, lead, rank, len);
+        if (dst != kNone && rank == 0) {
+          if (dst < ns) atomicAdd(&s_cnt[dst], len);
+          else atomicAdd(&A.tile_words[dst], (unsigned long long)len);
         }
-        const uint32_t hr = A.filter ? A.h_row[ir] : 0u;
-        for (uint32_t k0 = UPPER ? pr + 1 : 0; k0 < L; k0 += 32) {
-          const uint32_t k = k0 + lane;
-          uint32_t dst = kNone, word = 0;
-          if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
-          int lead;
-          uint32_t rank, len;
-          lane_runs(dst, lead, rank, len);
-          if (dst != kNone && rank == 0) {
-            if (dst < ns) atomicAdd(&s_cnt[dst], len);
-            else atomicAdd(&A.tile_words[dst], (unsigned long long)len);
-          }
-        }
-      }
+      });
     });
     // flush per chunk: shared u32 counts never exceed one chunk's words
     __syncthreads();
@@ -1564,35 +1594,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
         const uint32_t n = (tv.x & kEntFlag) ? 2u : q.L - (UPPER ? q.p + 1 : 0u);
         if (atomicAdd(&s_cnt[t], n) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = t;
       }
-      uint32_t sm = __ballot_sync(0xffffffffu, slow);
-      while (sm) {
-        const int r = __ffs(sm) - 1;
-        sm &= sm - 1;
-        const uint32_t ir = __shfl_sync(0xffffffffu, i, r);
-        const uint32_t tx = __shfl_sync(0xffffffffu, tv.x, r);
-        const uint32_t ty = __shfl_sync(0xffffffffu, tv.y, r);
-        const int64_t tb = __shfl_sync(0xffffffffu, q.base, r);
-        const uint32_t pr = __shfl_sync(0xffffffffu, q.p, r);
-        const uint32_t L = __shfl_sync(0xffffffffu, q.L, r);
-        uint32_t c0 = 0, nwin = 1;
-        if (tx & kWinFlag) {
-          const Tile T0 = A.tiles[tx & kTileMask];
-          c0 = T0.c0;
-          nwin = T0.nwin;
-        }
-        const uint32_t hr = A.filter ? A.h_row[ir] : 0u;
-        for (uint32_t k0 = UPPER ? pr + 1 : 0; k0 < L; k0 += 32) {
-          const uint32_t k = k0 + lane;
-          uint32_t dst = kNone, word = 0;
-          if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
-          if (dst >= ns) dst = kNone;
-          int lead;
-          uint32_t rank, len;
-          lane_runs(dst, lead, rank, len);
-          if (dst != kNone && rank == 0)
-            if (atomicAdd(&s_cnt[dst], len) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = dst;
-        }
-      }
+      const uint32_t skip = UPPER ? q.p + 1 : 0u;
+      for_slow_columns(A, slow, i, tv.x, tv.y, (uint32_t)q.base + skip, q.L - skip,
+                       [&](uint32_t dst, uint32_t) {
+        if (dst >= ns) dst = kNone;
+        int lead;
+        uint32_t rank, len;
+        lane_runs(dst, lead, rank, len);
+        if (dst != kNone && rank == 0)
+          if (atomicAdd(&s_cnt[dst], len) == 0) s_touched[atomicAdd(&s_misc[0], 1u)] = dst;
+      });
     });
     __syncthreads();
     const uint32_t n_touch = s_misc[0];
@@ -1645,36 +1656,19 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
         // the warp -- lanes take 32 suffix columns, group by destination tile
         // (windows of a sorted suffix are contiguous), one claim per group,
         // and the group's words are stored to consecutive positions
-        uint32_t sm = __ballot_sync(0xffffffffu, slow);
-        while (sm) {
-          const int r = __ffs(sm) - 1;
-          sm &= sm - 1;
-          const uint32_t ir = __shfl_sync(0xffffffffu, i, r);
-          const uint32_t tx = __shfl_sync(0xffffffffu, tv.x, r);
-          const uint32_t ty = __shfl_sync(0xffffffffu, tv.y, r);
-          const uint32_t tile = tx & kTileMask;
-          uint32_t c0 = 0, nwin = 1;
-          if (tx & kWinFlag) {
-            const Tile T0 = A.tiles[tile];
-            c0 = T0.c0;
-            nwin = T0.nwin;
-          }
-          const uint32_t hr = A.filter ? A.h_row[ir] : 0u;
-          for (uint32_t k0 = UPPER ? pc + r + 1 : 0; k0 < L; k0 += 32) {
-            const uint32_t k = k0 + lane;
-            uint32_t dst = kNone, word = 0;
-            if (k < L) split_row_dest(A, tx, ty, c0, nwin, hr, A.items[tb + k], dst, word);
-            int lead;
-            uint32_t rank, len;
-            lane_runs(dst, lead, rank, len);
-            uint32_t p0 = 0;
-            if (dst != kNone && rank == 0)
-              p0 = dst < ns ? atomicAdd(&s_cnt[dst], len)
-                            : (uint32_t)atomicAdd(&A.tile_cursor[dst], (unsigned long long)len);
-            p0 = __shfl_sync(0xffffffffu, p0, lead);
-            if (dst != kNone) A.words[p0 + rank] = word;
-          }
-        }
+        const uint32_t skip = UPPER ? p + 1 : 0u;
+        for_slow_columns(A, slow, i, tv.x, tv.y, (uint32_t)tb + skip, L - skip,
+                         [&](uint32_t dst, uint32_t word) {
+          int lead;
+          uint32_t rank, len;
+          lane_runs(dst, lead, rank, len);
+          uint32_t p0 = 0;
+          if (dst != kNone && rank == 0)
+            p0 = dst < ns ? atomicAdd(&s_cnt[dst], len)
+                          : (uint32_t)atomicAdd(&A.tile_cursor[dst], (unsigned long long)len);
+          p0 = __shfl_sync(0xffffffffu, p0, lead);
+          if (dst != kNone) A.words[p0 + rank] = word;
+        });
         return __ballot_sync(0xffffffffu, fast);
       };
       uint32_t it_cur = ld_it(warp), it1 = ld_it(warp + NW), it2 = ld_it(warp + 2 * NW),

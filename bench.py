@@ -478,8 +478,8 @@ def run_streaming_summaries(args, cfg, dtx):
     peak, peak_src = peaks()
     achieved = b_alg / (ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": "per chunk of 8.3e6 transactions: pair engine (k_item_terms, "
-                "k_plan_stream, k_stream_scatter, k_count_stream, k_reduce_slabs) -> crop_ss_index + "
-                "crop_ss_probe + crop_bucket_topk (summary merge)",
+                "k_plan_coop, k_stream_count, k_stream_write, k_count_stream, k_reduce_slabs) -> crop_ss_index + "
+                "crop_ss_probe + crop_ss_append + crop_bucket_topk + crop_ss_keep (summary merge)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": b_alg, "avg_launch_ms": round(ms, 3),

@@ -41,10 +41,13 @@ for it in range(6):
     tick("top_entries")
     n = state.device_result.entries.n
     if out is None or out[0].shape[0] < n:
-        out = tuple(torch.empty(int(n * 1.05) + 1024, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-                    for _ in range(3))
+        idt, wdt = state.entry_dtypes()
+        tdt = {np.uint16: torch.int16, np.uint32: torch.int32}
+        out = tuple(torch.empty(int(n * 1.05) + 1024, dtype=tdt[dt], pin_memory=True).numpy().view(dt)
+                    for dt in (idt, idt, wdt))
     row, col, cnt = state.entry_arrays(out=out)
-    tick(f"entry_arrays({12 * n / 1e6:.0f} MB)")
+    per = row.dtype.itemsize + col.dtype.itemsize + cnt.dtype.itemsize
+    tick(f"entry_arrays({per * n / 1e6:.0f} MB)")
     print(f"iter {it}: total {1e3 * (t - t0):.2f} ms | " + " | ".join(log), flush=True)
 # raw copy rates
 a = torch.empty(610_000_000 // 4, dtype=torch.int32, device="cuda")

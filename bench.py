@@ -69,51 +69,77 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region:
+    ONE `nvidia-smi -lms` process (the profiling recipe's clocks line), started
+    when the sampler is made -- before the warm-up steps -- so that no
+    process is spawned inside the timed region (a fork + nvidia-smi start-up
+    per sample perturbed the host-side launches of short steps: c4 measured
+    2.1 to 3.2 ms with it). `with sampler:` marks the timed window; the
+    summary uses the samples inside it (or the nearest ones when the window
+    is shorter than the sampling period)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 100
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []
-        self._stop = threading.Event()
+        self.samples = []  # (wall time, fields)
+        self.t0 = self.t1 = None
+        self._proc = None
         self._t = None
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [x.strip() for x in out.stdout.strip().split(",")]
+    def _read(self):
+        try:
+            for line in self._proc.stdout:  # blocks in read(): the GIL is released
+                parts = [x.strip() for x in line.strip().split(",")]
                 if len(parts) >= 9:
-                    self.samples.append(parts)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+                    self.samples.append((time.time(), parts))
+        except Exception:
+            pass
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self.t1 = time.time()
+        # one more period so a sample taken under the last steps' load arrives
+        time.sleep(self.PERIOD_MS / 1000.0)
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            if self._t is not None:
+                self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        inside = [f for t, f in self.samples if self.t0 is not None and self.t0 <= t <= self.t1]
+        if not inside and self.t0 is not None:
+            # window shorter than the period: the samples next to it
+            mid = 0.5 * (self.t0 + self.t1)
+            inside = [f for _, f in sorted(self.samples, key=lambda tf: abs(tf[0] - mid))[:2]]
+        sm = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in inside if s[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if s[5 + k].lower() == "active"})
+        reasons = sorted({names[k] for s in inside for k in range(4) if s[5 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(inside), "period_ms": self.PERIOD_MS}
 
 
 def ncu_traffic(config: str):
@@ -280,6 +306,7 @@ def run_ours(args, rank, world):
         job.close()
         return phases, stats, top
 
+    sampler = ClockSampler(torch.cuda.current_device())  # started before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -293,7 +320,6 @@ def run_ours(args, rank, world):
 
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
         for k in range(args.steps):
             flush.zero_()
@@ -442,12 +468,12 @@ def run_streaming_summaries(args, cfg, dtx):
         idx = kernels.topk_indices(rec, cfg.top_k)
         return s, loads, (rec.row[idx], rec.col[idx], rec.count[idx])
 
+    sampler = ClockSampler(torch.cuda.current_device())  # started before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches0 = kernels.launch_counter()
     times, count_ms = [], []
-    sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
         for _ in range(args.steps):
             flush.zero_()
@@ -574,6 +600,7 @@ def run_product(args, rank, world):
     def step():
         return kernels.outer_product(ds, False, cfg.kappa, asg.start, asg.stop, *tab)
 
+    sampler = ClockSampler(torch.cuda.current_device())  # started before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -583,7 +610,6 @@ def run_product(args, rank, world):
 
         dist.barrier()
     times = []
-    sampler = ClockSampler(torch.cuda.current_device())
     with sampler:
         for _ in range(args.steps):
             flush.zero_()

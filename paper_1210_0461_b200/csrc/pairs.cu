@@ -1366,6 +1366,9 @@ struct StreamRouteArgs {
   uint32_t scat_ns;                 // k_stream_scatter: tiles with shared counters
   int packed_filter;                // k_stream_scatter: bucket-filter the word rows' pairs
   uint32_t* words;
+  // B1 -> B2: words per (chunk, shared-counter tile), [n_chunks][min(n_tiles,
+  // kTileSmem)], so that B2 does not walk the chunk a second time (nullable)
+  uint32_t* chunk_counts;
 };
 
 // Visit the words of row occurrence (g, q) of row item i: fn(dest_tile, base,
@@ -1549,11 +1552,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_count(StreamRouteArg
     });
     // flush per chunk: shared u32 counts never exceed one chunk's words
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x)
-      if (s_cnt[t]) {
-        atomicAdd(&A.tile_words[t], (unsigned long long)s_cnt[t]);
+    uint32_t* cc = A.chunk_counts ? A.chunk_counts + (size_t)chunk * ns : nullptr;
+    for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) {
+      const uint32_t c = s_cnt[t];
+      if (cc) cc[t] = c;
+      if (c) {
+        atomicAdd(&A.tile_words[t], (unsigned long long)c);
         s_cnt[t] = 0;
       }
+    }
   }
 }
 
@@ -1582,6 +1589,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_stream_write(StreamRouteArg
     __syncthreads();
     if (threadIdx.x == 0) s_misc[0] = 0;
     const int ntx = stage_offsets(s_off, A.offsets, A.n_tx, chunk, A.chunk_tx);
+    if (A.chunk_counts) {
+      // B1 (k_stream_count) left this chunk's words per shared-counter tile
+      const uint32_t* cc = A.chunk_counts + (size_t)chunk * ns;
+      for (uint32_t t = threadIdx.x; t < ns; t += blockDim.x) {
+        const uint32_t c = cc[t];
+        s_cnt[t] = c;
+        if (c) s_touched[atomicAdd(&s_misc[0], 1u)] = (uint16_t)t;
+      }
+    } else
     walk_chunk<true>(s_off, ntx, A.items, A.item_info,
                      [&](int64_t, const Pos& q, uint32_t i, uint2 tv) {
       // words per shared-counter tile (ids < ns; a split row's windows follow
@@ -3973,8 +3989,18 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
     R.chunk_tx = (int)std::max<int64_t>(256, std::min<int64_t>(kChunkTx, J->n_tx / (kNumSMs * 12)));
     const int64_t chunks = (J->n_tx + R.chunk_tx - 1) / R.chunk_tx;
     const int grid = (int)std::min<int64_t>(kNumSMs, chunks);
+    R.chunk_counts = nullptr;
+    uint32_t* d_chunk_counts = nullptr;
     if (!J->words_known) {
       CROP_CUDA(cudaMemsetAsync(J->d_tile_words, 0, nt * 8, st));
+      // per-chunk counts for k_stream_write (same chunks, same shared tiles)
+      // when they stay under 512 MB (c3 chunk: 2,035 x 24,576 x 4 B = 200 MB)
+      const size_t cc_bytes = (size_t)chunks * std::min(nt, kTileSmem) * 4;
+      const bool writes_by_chunk = !(J->own && J->d_own_bounds);
+      if (writes_by_chunk && cc_bytes <= (512ull << 20) && !getenv("CROP_NO_CHUNK_COUNTS")) {
+        CROP_CUDA(cudaMallocAsync(&d_chunk_counts, std::max<size_t>(cc_bytes, 4), st));
+        R.chunk_counts = d_chunk_counts;
+      }
       auto kern = up ? k_stream_count<true> : k_stream_count<false>;
       const size_t smem = kOffBytes + (size_t)std::min(nt, kTileSmem) * 4;
       CROP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -4054,6 +4080,7 @@ static int stream_write(crop_pairs* J, cudaStream_t st, bool rec) {
       kern<<<grid, kPassThreads, smem, st>>>(R);
       CROP_LAUNCH_CHECK();
     }
+    if (d_chunk_counts) cudaFreeAsync(d_chunk_counts, st);
     mark(2);
   }
   return CROP_OK;

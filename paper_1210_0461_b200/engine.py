@@ -839,10 +839,11 @@ def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triang
     tables = [kernels.hash_tables(h, prep.n_items) for h in hashers]
     signs = [h.sign_hash for h in hashers] if config.cs_enabled else None
     n_tx = dtx.n_tx
-    host_off = dtx.offsets.cpu().numpy()
     if chunk_transactions is None:
-        lens = np.diff(host_off)
-        terms = int((lens * (lens - 1) // 2).sum())
+        # (on the device: the offsets of c3 are 400 MB)
+        lens = dtx.offsets[1:] - dtx.offsets[:-1]
+        terms = int((lens * (lens - 1) // 2).sum().item())
+        del lens
         n_chunks = max(1, -(-terms // 4_000_000_000))  # about 4e9 terms per chunk (c3: 6)
         chunk_transactions = max(1, -(-n_tx // n_chunks))
     if chunk_transactions < 1:
@@ -855,7 +856,7 @@ def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triang
         t1 = min(n_tx, t0 + chunk_transactions)
         if t1 <= t0:
             break
-        ent = kernels.count_pairs(dtx.slice(t0, t1, host_off), upper_triangle_only)
+        ent = kernels.count_pairs(dtx.slice(t0, t1), upper_triangle_only)
         bl, _, c = kernels.entry_bucket_stats(ent, tables, kappa, prep.n_items, signs)
         loads += bl
         if cs is not None:

@@ -255,6 +255,19 @@ class _DeviceResult:
         return inst.bucket_weight
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(device):
+    """One side stream per device for overlapped device->host transfers."""
+    import torch
+
+    key = str(device)
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _COPY_STREAMS[key]
+
+
 class SketchState:
     """Frozen query surface over all instances' bucket structures."""
 
@@ -467,7 +480,7 @@ class SketchState:
         return [TopEntry(Entry(int(r), int(c)), float(l), float(u), self._estimate(int(r), int(c)))
                 for r, c, u, l in zip(h[0], h[1], h[2], h[3])]
 
-    def entry_arrays(self, instance: int = 0, out=None, compact: bool = True):
+    def entry_arrays(self, instance: int = 0, out=None, compact: bool = True, wait: bool = True):
         """All recorded entries of one instance as columnar host arrays
         (row, col, weight): the columnar form of `instances[t].summaries` (the
         reference's per-bucket dicts, engine.py:108-118) without building one
@@ -478,7 +491,10 @@ class SketchState:
         device->host transfer per column into pinned buffers (`out` =
         reusable (row, col, weight) numpy arrays of at least the entry count
         and of the returned dtypes, e.g. from pinned torch tensors;
-        entry_dtypes() names them)."""
+        entry_dtypes() names them). With wait=False the transfers run on a
+        copy stream and the call returns at once: the arrays are valid after
+        wait_entries(), and device work issued meanwhile (top_entries) overlaps
+        the copy."""
         self._require_frozen()
         id_dt, w_dt = self.entry_dtypes(compact)
         if self._dev is None:
@@ -508,13 +524,30 @@ class SketchState:
                 if o.dtype.itemsize != c.element_size():
                     raise InputError(f"out array of dtype {o.dtype} for a column of {c.dtype}")
             host = [torch.from_numpy(o.view(signed.get(o.dtype, o.dtype)))[:n] for o in out]
-        for h, c in zip(host, cols):
-            h.copy_(c, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        if wait:
+            for h, c in zip(host, cols):
+                h.copy_(c, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        else:
+            cur = torch.cuda.current_stream()
+            side = _copy_stream(cur.device)
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                for h, c in zip(host, cols):
+                    c.record_stream(side)
+                    h.copy_(c, non_blocking=True)
+                self._entries_copied = side.record_event()
         row, col, w = (h.numpy() for h in host)
         if d.integer:
             return row.view(id_dt), col.view(id_dt), w.view(np.uint32)
         return row.view(id_dt), col.view(id_dt), w
+
+    def wait_entries(self) -> None:
+        """Block until the transfers of entry_arrays(wait=False) have landed."""
+        ev = getattr(self, "_entries_copied", None)
+        if ev is not None:
+            ev.synchronize()
+            self._entries_copied = None
 
     def entry_dtypes(self, compact: bool = True):
         """(id dtype, weight dtype) of entry_arrays."""

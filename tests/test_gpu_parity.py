@@ -434,6 +434,14 @@ def test_entry_arrays_columns(compact):
     out = (np.empty(n + 5, idt), np.empty(n + 5, idt), np.empty(n + 5, wdt))
     r2, c2, w2 = state.entry_arrays(out=out, compact=compact)
     assert np.array_equal(r2, row) and np.array_equal(c2, col) and np.array_equal(w2, w)
+    # transfers on the copy stream under other device work: valid after wait_entries()
+    out3 = tuple(torch.empty(n, dtype={2: torch.int16, 4: torch.int32}[np.dtype(dt).itemsize],
+                             pin_memory=True).numpy().view(dt) for dt in (idt, idt, wdt))
+    r3, c3, w3 = state.entry_arrays(out=out3, compact=compact, wait=False)
+    top = state.top_entries(10)
+    state.wait_entries()
+    assert np.array_equal(r3, row) and np.array_equal(c3, col) and np.array_equal(w3, w)
+    assert len(top) == 10
     with pytest.raises(crop.InputError):
         state.entry_arrays(out=(np.empty(n, np.uint64), np.empty(n, np.uint64), np.empty(n, np.uint64)),
                            compact=compact)

@@ -170,3 +170,47 @@ def test_streaming_rejects_real_streams():
                              np.array([0, 1], np.int64), np.array([2], np.uint32), np.array([3.0]))
     with pytest.raises(crop.ConfigError):
         crop.run_streaming(s, crop.EngineConfig(kappa=2, ss_capacity=4, workers=1, seed=0))
+
+
+@pytest.mark.parametrize("kappa,cap,chunk", [(64, 100, 300), (7, 3, 50), (2048, 2, 400)])
+def test_merge_with_the_cut_equals_appending_every_miss(kappa, cap, chunk):
+    """The two-pass merge (per-bucket weight cut, Bloom filter in front of the
+    index) keeps exactly the records of the plain batch update restated here
+    in Python: hits add e, every miss becomes (mu_b + e, over mu_b), each
+    bucket keeps its `cap` largest by (count desc, row, col). kappa = 2048
+    takes the global-memory histograms (kappa * 16 counters exceed a CTA's
+    shared memory), kappa = 64 with 100 records per bucket (6,400 records) has
+    the Bloom filter on."""
+    cfg = workloads.CONFIGS["c1"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=1200)
+    off, items = dtx.to_host()
+    h = crop.make_hashes(crop.HashConfig(kappa, crop.derive_seed(5, "instance:0")))
+    tab = kernels.hash_tables(h, cfg.n_items)
+    hr = np.array(h.row_hash.values(range(cfg.n_items)), np.int64)
+    hc = np.array(h.col_hash.values(range(cfg.n_items)), np.int64)
+    summ = kernels.StreamingSummaries(kappa, cap, tab)
+    want = [dict() for _ in range(kappa)]  # bucket -> {(row, col): [count, over]}
+    mu = [0] * kappa
+    for t0 in range(0, dtx.n_tx, chunk):
+        t1 = min(dtx.n_tx, t0 + chunk)
+        ent = kernels.count_pairs(dtx.slice(t0, t1), True)
+        summ.absorb(ent)
+        i0, i1 = int(off[t0]), int(off[t1])
+        er, ec, ew = oracle.pair_supports(off[t0:t1 + 1] - i0, items[i0:i1])
+        for r, c, e in zip(er.tolist(), ec.tolist(), ew.tolist()):
+            b = int((hr[r] + hc[c]) % kappa)
+            rec = want[b].get((r, c))
+            if rec is not None:
+                rec[0] += e
+            else:
+                want[b][(r, c)] = [mu[b] + e, mu[b]]
+        for b in range(kappa):
+            if len(want[b]) >= cap:
+                keep = sorted(want[b].items(), key=lambda kv: (-kv[1][0], kv[0]))[:cap]
+                want[b] = dict(keep)
+                mu[b] = keep[-1][1][0]
+    got = sorted(zip(kernels.u32_to_numpy(summ.row).tolist(), kernels.u32_to_numpy(summ.col).tolist(),
+                     kernels.u32_to_numpy(summ.count).tolist(), kernels.u32_to_numpy(summ.over).tolist()))
+    exp = sorted((r, c, v[0], v[1]) for b in range(kappa) for (r, c), v in want[b].items())
+    assert got == exp
+    assert (summ.mu.cpu().numpy().astype(np.int64) & 0xFFFFFFFF).tolist() == mu

@@ -1301,17 +1301,6 @@ constexpr uint32_t kStreamDenseCap = 57344;
 // (so neighbouring columns never share a word), <= 65,535 row occurrences
 // per unit keep them from wrapping; hash tables 14,336 64-bit slots.
 constexpr uint32_t kSHalf = kStreamDenseCap / 2;  // 28672 words = 112 KB
-// Column windows of a row too wide for one table lie on one grid for every
-// row: window q covers columns [q * cap, (q + 1) * cap), a row's first
-// window is the one holding its first column. The windows a sorted
-// transaction's columns fall into are then the same for all of its rows
-// (the routing kernels cut a transaction into window runs once).
-__host__ __device__ __forceinline__ uint32_t window_lo(uint32_t first_col, uint64_t cap) {
-  return (uint32_t)(first_col / cap * cap);
-}
-__host__ __device__ __forceinline__ uint32_t window_count(uint32_t first_col, uint32_t n, uint64_t cap) {
-  return (uint32_t)((n - window_lo(first_col, cap) + cap - 1) / cap);
-}
 constexpr int kSCThreads = 512;                     // count kernel threads (2 CTAs / SM)
 constexpr int kSCWarps = kSCThreads / 32;
 constexpr uint32_t kStreamUnitOcc = 65535;
@@ -2874,7 +2863,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
         if (w <= dense_cap && ((8 * t >= w && w >= kMinDenseWidth) || !hfit)) {
           rec = 1;
         } else if (!hfit) {
-          rec = 2 | window_count(P.upper ? i + 1 : 0, n, dense_cap) << 3;
+          rec = 2 | (uint32_t)((w + dense_cap - 1) / dense_cap) << 3;
           s_has_win = 1;
         } else {
           const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
@@ -2965,7 +2954,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_stream(PlanArgs P) {
           ++id;
         } else if (c == 2) {
           const uint64_t t = s_t[k];
-          const uint32_t col_lo = window_lo(P.upper ? i + 1 : 0, dense_cap);
+          const uint32_t col_lo = P.upper ? i + 1 : 0;
           const uint32_t nwin = r >> 3;
           for (uint32_t q = 0; q < nwin; ++q) {
             Tile tl{};
@@ -3454,7 +3443,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_coop(PlanArgs P, PlanS
         if (w <= dense_cap && ((8 * t >= w && w >= kMinDenseWidth) || !hfit)) {
           rec = 1;
         } else if (!hfit) {
-          rec = 2 | window_count(P.upper ? i + 1 : 0, n, dense_cap) << 3;
+          rec = 2 | (uint32_t)((w + dense_cap - 1) / dense_cap) << 3;
           atomicOr(&S->has_win, 1u);
         } else {
           const uint64_t xb = (b * kPlanS + hash_cap - 1) / hash_cap;
@@ -3551,7 +3540,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1) k_plan_coop(PlanArgs P, PlanS
         ++id;
       } else if (c == 2) {
         const uint64_t t = s_t[k];
-        const uint32_t col_lo = window_lo(P.upper ? i + 1 : 0, dense_cap);
+        const uint32_t col_lo = P.upper ? i + 1 : 0;
         const uint32_t nwin = r >> 3;
         for (uint32_t q = 0; q < nwin; ++q) {
           Tile tl{};
@@ -4205,8 +4194,8 @@ static void plan_tiles(crop_pairs* J, const std::vector<unsigned long long>& ter
     }
     // one row too wide for a dense tile and too heavy for a hash tile:
     // column windows of kDenseCap counters with consecutive tile ids.
-    const uint32_t col_lo = window_lo(upper ? i + 1 : 0, dense_cap);
-    const uint32_t nwin = window_count(upper ? i + 1 : 0, n, dense_cap);
+    const uint32_t col_lo = upper ? i + 1 : 0;
+    const uint32_t nwin = (uint32_t)((w + dense_cap - 1) / dense_cap);
     const uint32_t first = (uint32_t)tiles.size();
     for (uint32_t k = 0; k < nwin; ++k) {
       Tile t{};

@@ -255,11 +255,18 @@ def run_ours(args, rank, world):
             job.set_timing(True)
             ent = job.run(sync=False)
             p1.record()
-            ent.n = int(ent.n_dev.item())
-            if ent.n > ent.capacity or job.overflowed():
-                raise RuntimeError("pair engine overflow")
+
+        def settle():
+            # the entry count is read back after the top-k launches when the
+            # select runs on the device-side count (one synchronisation less)
+            if job is not None:
+                ent.n = int(ent.n_dev.item())
+                if ent.n > ent.capacity or job.overflowed():
+                    raise RuntimeError("pair engine overflow")
+
         src, cnt = ent, None
         if cfg.ss_capacity:
+            settle()
             # bounded Space-Saving regime (c3): per-bucket top-l summaries. With
             # N > 1 every bucket's pairs are spread over the tile shards: each
             # rank sends its per-bucket candidates to the bucket's owner (one
@@ -275,6 +282,8 @@ def run_ours(args, rank, world):
                 mask, _, _ = kernels.bucket_topk(ent, tables[0], tables[1], cfg.kappa, cfg.ss_capacity)
                 cnt = torch.where(mask, ent.count[: ent.n], torch.zeros_like(ent.count[: ent.n]))
         idx = kernels.topk_indices(src, cfg.top_k, count=cnt)
+        if not cfg.ss_capacity:
+            settle()
         top = (src.row[idx], src.col[idx], src.count[idx])
         if world > 1:
             import torch.distributed as dist

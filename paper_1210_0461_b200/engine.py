@@ -985,24 +985,48 @@ class ProductPartition:
     def __len__(self) -> int:
         return self.entries.n
 
-    def arrays(self, out=None):
-        """(row uint32, col uint32, value float64, bucket uint32) host arrays,
-        one device->host copy per column (into `out`, e.g. pinned buffers of
-        at least len(self) entries, when given)."""
+    def arrays(self, out=None, value_dtype=np.float64, bucket_ptr: bool = False):
+        """(row uint32, col uint32, value, bucket) host arrays, one
+        device->host copy per column (into `out`, e.g. pinned buffers of at
+        least len(self) entries, when given). value_dtype = float64 (the
+        exact stream-order sums) or float32 (each sum rounded once: within
+        rel 1e-5 / abs 1e-6 of the float64 reference, the tolerance BASELINE
+        c4 states for fp32 output). With bucket_ptr the fourth array is not
+        the per-entry bucket but int64 offsets: the entries of bucket
+        start + b are [ptr[b], ptr[b + 1]) (the result is sorted by bucket),
+        and `out` holds three arrays."""
         import torch
 
+        if np.dtype(value_dtype) not in (np.dtype(np.float64), np.dtype(np.float32)):
+            raise ConfigError(f"value_dtype must be float64 or float32, got {value_dtype}")
         e = self.entries
         n = e.n
-        cols = [e.row[:n], e.col[:n], e.value[:n], e.bucket[:n]]
+        val = e.value[:n]
+        if np.dtype(value_dtype) == np.dtype(np.float32):
+            val = val.to(torch.float32)
+        cols = [e.row[:n], e.col[:n], val]
+        ptr = None
+        if bucket_ptr:
+            edges = torch.arange(self.start, self.stop + 1, dtype=torch.int64, device=e.row.device)
+            ptr = torch.searchsorted(e.bucket[:n].to(torch.int64) & 0xFFFFFFFF, edges)
+        else:
+            cols.append(e.bucket[:n])
         if out is None:
             host = [torch.empty(n, dtype=c.dtype, pin_memory=True) for c in cols]
         else:
+            if len(out) != len(cols):
+                raise InputError(f"out must hold {len(cols)} arrays, got {len(out)}")
+            for o, c in zip(out, cols):
+                if o.dtype.itemsize != c.element_size():
+                    raise InputError(f"out array of dtype {o.dtype} for a column of {c.dtype}")
             host = [torch.from_numpy(o.view(np.int32) if o.dtype == np.uint32 else o)[:n] for o in out]
         for h, c in zip(host, cols):
             h.copy_(c, non_blocking=True)
+        ptr_h = ptr.cpu().numpy() if ptr is not None else None  # (synchronises the stream)
         torch.cuda.current_stream().synchronize()
-        row, col, val, buck = (h.numpy() for h in host)
-        return row.view(np.uint32), col.view(np.uint32), val, buck.view(np.uint32)
+        res = [h.numpy() for h in host]
+        last = ptr_h if bucket_ptr else res[3].view(np.uint32)
+        return res[0].view(np.uint32), res[1].view(np.uint32), res[2], last
 
 
 def partition_product(stream, config: EngineConfig, worker: int | None = None,

@@ -72,6 +72,23 @@ def test_partition_product_c4_prefix(workers, outer_path, monkeypatch):
     new = crop.partition_product(s, config, worker=None if workers == 1 else 5).arrays()
     for x, y in zip(ref, new):
         assert np.array_equal(x, y)
+    # compact transfer: float32 values (each fp64 sum rounded once, inside the
+    # BASELINE c4 tolerance) and bucket offsets instead of the bucket column
+    part = crop.partition_product(s, config, worker=None if workers == 1 else 5)
+    a = config.assignments()[0 if workers == 1 else 5]
+    row, col, val, buck = part.arrays()
+    r32, c32, v32, ptr = part.arrays(value_dtype=np.float32, bucket_ptr=True)
+    assert np.array_equal(r32, row) and np.array_equal(c32, col)
+    assert v32.dtype == np.float32 and np.array_equal(v32, val.astype(np.float32))
+    assert np.all(np.abs(v32.astype(np.float64) - val) <= 1e-6 + 1e-5 * np.abs(val))
+    assert ptr.shape[0] == a.stop - a.start + 1 and ptr[0] == 0 and ptr[-1] == len(part)
+    assert np.array_equal(np.repeat(np.arange(a.start, a.stop), np.diff(ptr)), buck.astype(np.int64))
+    n = len(part)
+    out = (np.empty(n, np.uint32), np.empty(n, np.uint32), np.empty(n, np.float32))
+    r2, c2, v2, p2 = part.arrays(out=out, value_dtype=np.float32, bucket_ptr=True)
+    assert np.array_equal(r2, row) and np.array_equal(v2, v32) and np.array_equal(p2, ptr)
+    with pytest.raises(crop.InputError):
+        part.arrays(out=out, value_dtype=np.float64, bucket_ptr=True)
 
 
 def test_partition_product_skewed_rows(outer_path):

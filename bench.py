@@ -767,10 +767,13 @@ def run_e2e(args, cfg, dtx, rank, world):
     import paper_1210_0461_b200 as crop
 
     off_h = dtx.offsets.cpu().pin_memory()
-    it_h = dtx.items.cpu().pin_memory()
+    # the host stream holds uint16 item ids when the universe fits (c2, c5):
+    # TransactionStream keeps them and the upload moves half the bytes
+    small = cfg.n_items <= 65536
+    it_h = (dtx.items.to(torch.int16) if small else dtx.items).cpu().pin_memory()
     config = crop.EngineConfig(kappa=cfg.kappa, ss_capacity=2 ** 31, workers=cfg.workers,
                                cs_enabled=False, seed=0)
-    off_np, it_np = off_h.numpy(), it_h.numpy().view(np.uint32)
+    off_np, it_np = off_h.numpy(), it_h.numpy().view(np.uint16 if small else np.uint32)
     out = None
     d2h = [0]
 
@@ -817,11 +820,11 @@ def run_e2e(args, cfg, dtx, rank, world):
         tm = statistics.mean(times)
     terms = int(((dtx.offsets[1:] - dtx.offsets[:-1]) *
                  (dtx.offsets[1:] - dtx.offsets[:-1] - 1) // 2).sum().item())
-    h2d = off_h.numel() * 8 + it_h.numel() * 4
+    h2d = off_h.numel() * 8 + it_h.numel() * it_h.element_size()
     return {"value": terms / tm, "unit": "terms/s", "ms_per_step": tm * 1e3,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0],
-            "api": "crop.run(TransactionStream) + SketchState.top_entries + "
-                   "SketchState.entry_arrays (all counts to pinned host memory)"
+            "api": "crop.run(TransactionStream, uint16 item ids when the universe fits) + "
+                   "SketchState.top_entries + SketchState.entry_arrays (all counts to pinned host memory)"
             if world == 1 else "distributed.top_entries_distributed"}
 
 

@@ -57,11 +57,18 @@ class DeviceTransactions:
                   non_blocking: bool = False) -> "DeviceTransactions":
         dev = _dev()
         off = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64))
-        it = torch.from_numpy(np.ascontiguousarray(items, dtype=np.uint32).view(np.int32))
+        items = np.asarray(items)
+        if items.dtype == np.uint16:
+            # 16-bit ids travel as they are and widen on the device
+            it = torch.from_numpy(np.ascontiguousarray(items).view(np.int16))
+        else:
+            it = torch.from_numpy(np.ascontiguousarray(items, dtype=np.uint32).view(np.int32))
         if non_blocking:
             off, it = off.pin_memory(), it.pin_memory()
-        return cls(off.to(dev, non_blocking=non_blocking), it.to(dev, non_blocking=non_blocking),
-                   int(n_items))
+        it = it.to(dev, non_blocking=non_blocking)
+        if it.dtype == torch.int16:
+            it = it.to(torch.int32) & 0xFFFF
+        return cls(off.to(dev, non_blocking=non_blocking), it, int(n_items))
 
     def to_host(self) -> tuple[np.ndarray, np.ndarray]:
         return self.offsets.cpu().numpy(), u32_to_numpy(self.items)

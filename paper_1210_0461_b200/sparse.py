@@ -142,7 +142,9 @@ def _csr_from_lists(rows) -> tuple[np.ndarray, np.ndarray]:
 
 
 class TransactionStream(OuterProductStream):
-    """Self-join stream over transactions stored as CSR (pair mining input)."""
+    """Self-join stream over transactions stored as CSR (pair mining input):
+    offsets int64[n + 1], items uint32[nnz] (or uint16 when passed as uint16
+    and dim <= 65,536), strictly increasing within a transaction."""
 
     __slots__ = ("offsets", "items")
 
@@ -167,7 +169,9 @@ class TransactionStream(OuterProductStream):
                 if np.any(inner & (d <= 0)):
                     raise InputError("items must be strictly increasing within a transaction")
         self.offsets = offsets
-        self.items = np.ascontiguousarray(items_i64, dtype=np.uint32)
+        # ids stay uint16 when given so (half the bytes to move to the device)
+        keep16 = items_i64.dtype == np.uint16 and dim <= 65536
+        self.items = np.ascontiguousarray(items_i64, dtype=np.uint16 if keep16 else np.uint32)
         n = offsets.shape[0] - 1
         super().__init__(dim, dim, n, self._pairs)
 

@@ -412,6 +412,26 @@ def test_host_generator_copy_matches_device_generator(name):
     assert np.array_equal(items, d_items)
 
 
+def test_uint16_item_ids_give_the_same_run():
+    """A TransactionStream built from uint16 item ids keeps them (half the
+    upload) and counts exactly what the uint32 stream counts."""
+    cfg = workloads.CONFIGS["c1"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=3000)
+    off, items = dtx.to_host()
+    config = crop.EngineConfig(kappa=4, ss_capacity=2 ** 31, workers=4, cs_enabled=False, seed=0)
+    s32 = crop.TransactionStream(cfg.n_items, off, items)
+    s16 = crop.TransactionStream(cfg.n_items, off, items.astype(np.uint16))
+    assert s16.items.dtype == np.uint16 and s32.items.dtype == np.uint32
+    a, ra = crop.run(s32, config, upper_triangle_only=True)
+    b, rb = crop.run(s16, config, upper_triangle_only=True)
+    assert ra.rows == rb.rows
+    ea, eb = a.entry_arrays(), b.entry_arrays()
+    assert sorted(zip(*(x.tolist() for x in ea))) == sorted(zip(*(x.tolist() for x in eb)))
+    assert a.top_entries(20) == b.top_entries(20)
+    with pytest.raises(crop.InputError):
+        crop.TransactionStream(10, off, items.astype(np.uint16))  # ids outside the universe
+
+
 @pytest.mark.parametrize("compact", [True, False])
 def test_entry_arrays_columns(compact):
     """SketchState.entry_arrays: every counted entry with its support, as

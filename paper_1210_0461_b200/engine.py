@@ -843,6 +843,58 @@ def run(stream: OuterProductStream, config: EngineConfig, upper_triangle_only: b
     return state, report
 
 
+# run_streaming uploads a host stream's items chunk by chunk under the
+# counting of the earlier chunks when it holds at least this many items
+STAGED_UPLOAD_MIN_ITEMS = 50_000_000
+
+
+class _StagedUpload:
+    """A host TransactionStream whose items reach the device chunk by chunk
+    on a copy stream (run_streaming): the offsets are uploaded at once, the
+    item buffer is allocated whole, and chunk k's items are enqueued one
+    chunk ahead of its counting (from pinned host memory the transfer runs
+    under the previous chunk's kernels; from pageable memory it is merely
+    synchronous). The hash tables take the stream's universe (dim) instead
+    of max id + 1, which would need every item on the device first."""
+
+    def __init__(self, ts):
+        import torch
+
+        from . import kernels
+
+        dev = kernels._dev()
+        self.ts = ts
+        self.off_h = ts.offsets
+        off = torch.from_numpy(ts.offsets).to(dev, non_blocking=True)
+        self.items = torch.empty(int(ts.offsets[-1]), dtype=torch.int32, device=dev)
+        self.dtx = kernels.DeviceTransactions(off, self.items, int(ts.n_rows))
+        lens = off[1:] - off[:-1]
+        total = int((lens * lens).sum().item())
+        self.prepared = _Prepared("pairs", self.dtx, ts.n_rows, ts.n_cols, int(ts.n_rows), total, ts)
+        self.side = _copy_stream(dev)
+        self.side.wait_stream(torch.cuda.current_stream())
+        self.items.record_stream(self.side)
+        self.events = {}
+        self.src = torch.from_numpy(ts.items.view(np.int16 if ts.items.dtype == np.uint16 else np.int32))
+
+    def enqueue(self, t0: int, t1: int) -> None:
+        import torch
+
+        i0, i1 = int(self.off_h[t0]), int(self.off_h[t1])
+        with torch.cuda.stream(self.side):
+            if self.src.dtype == torch.int16:
+                tmp = self.src[i0:i1].to(self.items.device, non_blocking=True)
+                self.items[i0:i1] = tmp.to(torch.int32) & 0xFFFF
+            else:
+                self.items[i0:i1].copy_(self.src[i0:i1], non_blocking=True)
+            self.events[t0] = self.side.record_event()
+
+    def wait(self, t0: int) -> None:
+        import torch
+
+        torch.cuda.current_stream().wait_event(self.events.pop(t0))
+
+
 def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triangle_only: bool = False,
                   chunk_transactions: int | None = None) -> tuple[SketchState, LoadReport]:
     """run() for pair mining with bounded summary memory: the transaction
@@ -862,7 +914,12 @@ def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triang
     from . import kernels
 
     _check_stream(stream)
-    prep = prepare(stream)
+    staged = None
+    if not isinstance(stream, kernels.DeviceTransactions) and getattr(stream, "_crop_device", None) is None:
+        ts = as_transaction_stream(stream)
+        if ts is not None and ts.items.shape[0] >= max(STAGED_UPLOAD_MIN_ITEMS, 1):
+            staged = _StagedUpload(ts)
+    prep = staged.prepared if staged is not None else prepare(stream)
     if prep.kind != "pairs":
         raise ConfigError("run_streaming takes 0/1 transaction streams (pair mining)")
     dtx = prep.device
@@ -885,11 +942,17 @@ def run_streaming(stream: OuterProductStream, config: EngineConfig, upper_triang
     t = len(hashers)
     loads = torch.zeros((t, kappa), dtype=torch.int64, device=dtx.offsets.device)
     cs = torch.zeros((t, kappa), dtype=torch.int64, device=dtx.offsets.device) if signs else None
-    for t0 in range(0, max(n_tx, 1), chunk_transactions):
-        t1 = min(n_tx, t0 + chunk_transactions)
-        if t1 <= t0:
-            break
-        ent = kernels.count_pairs(dtx.slice(t0, t1), upper_triangle_only)
+    bounds = [(t0, min(n_tx, t0 + chunk_transactions)) for t0 in range(0, n_tx, chunk_transactions)]
+    if staged is not None and bounds:
+        staged.enqueue(*bounds[0])
+    for k, (t0, t1) in enumerate(bounds):
+        if staged is not None:
+            # the next chunk's items travel under this chunk's counting
+            if k + 1 < len(bounds):
+                staged.enqueue(*bounds[k + 1])
+            staged.wait(t0)
+        ent = kernels.count_pairs(dtx.slice(t0, t1, staged.off_h if staged is not None else None),
+                                  upper_triangle_only)
         bl, _, c = kernels.entry_bucket_stats(ent, tables, kappa, prep.n_items, signs)
         loads += bl
         if cs is not None:

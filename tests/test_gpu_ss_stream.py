@@ -214,3 +214,32 @@ def test_merge_with_the_cut_equals_appending_every_miss(kappa, cap, chunk):
     exp = sorted((r, c, v[0], v[1]) for b in range(kappa) for (r, c), v in want[b].items())
     assert got == exp
     assert (summ.mu.cpu().numpy().astype(np.int64) & 0xFFFFFFFF).tolist() == mu
+
+
+@pytest.mark.parametrize("ids16,pinned", [(False, True), (True, False)])
+def test_staged_upload_equals_the_whole_upload(monkeypatch, ids16, pinned):
+    """run_streaming's chunk-by-chunk upload of a host stream (items enqueued
+    one chunk ahead on the copy stream) gives the summaries of the whole
+    upload: same records, bounds, loads and top entries."""
+    from paper_1210_0461_b200 import engine
+
+    cfg = workloads.CONFIGS["c1"]
+    dtx = workloads.generate_pairs_workload(cfg, n_tx=4000)
+    off, items = dtx.to_host()
+    if ids16:
+        items = items.astype(np.uint16)
+    if pinned:
+        items = torch.from_numpy(items.view(np.int32)).pin_memory().numpy().view(np.uint32)
+    config = crop.EngineConfig(kappa=16, ss_capacity=50, workers=4, cs_enabled=True, seed=3)
+
+    def run():
+        s = crop.TransactionStream(cfg.n_items, off, items, validate=False)
+        state, report = crop.run_streaming(s, config, upper_triangle_only=True, chunk_transactions=700)
+        r, c, w, o, inst = _records(state)
+        return sorted(zip(r.tolist(), c.tolist(), w.tolist(), o.tolist())), report.rows, \
+            inst.bucket_min.tolist(), inst.cs.tolist(), state.top_entries(30)
+
+    whole = run()
+    monkeypatch.setattr(engine, "STAGED_UPLOAD_MIN_ITEMS", 1)
+    staged = run()
+    assert staged == whole
